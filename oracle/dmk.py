@@ -1,0 +1,161 @@
+"""The discrete DMK algorithm for the 3D Laplace kernel  (oracle; test infrastructure).
+
+Follows "The full DMK algorithm for discrete sources", Sec. 3.5, PAPER.md:1414-1623,
+step by step and in the paper's order, with the PSWF kernel split of Sec. 3.6
+(oracle/kernels.py) and the Table 1 parameters (oracle/params.py):
+
+  Step 0  tree + flags
+  Step 1  precomputation of T_c2p, T_p2c, T_prox2pw, T_pw2poly,
+          T_pwshift (1D factors)
+  Step 2  upward pass: leaf proxy charges (Eq. 2.8), then c2p
+  Step 3  downward pass per level: outgoing Phi_l (Eq. 3.42),
+          incoming Psi_l (Eq. 3.39), local Lambda_l (Eqs. 3.43-3.44),
+          split to children (T_p2c, Eq. 3.46), evaluate at
+          leaf targets
+  Step 4  direct residual interactions over the lists
+  Step 5  self-interaction corrections
+
+Readings: R2 Fourier spacing, R4 root window M_1 = W_0 + D_0,
+R5-R8 tree conventions, R9 coincident pairs, R10 root-leaf case (N <= n_s: plain
+direct sum).  No blocking, fusion or reordering beyond the paper's; 1D factor
+matrices are applied axis by axis (separation of variables, which the paper's
+Step 1 prescribes).  Sources = targets; the potential at a source excludes the
+source itself.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import cheb
+from .kernels import LaplaceSplit, trapezoid_weights_3d, r_level
+from .params import for_eps
+from .tree import Tree
+
+
+def _octant_sides(code: int):
+    """Child octant -> side (+-1) per axis; bit 2 = x, bit 1 = y, bit 0 = z."""
+    o = int(code) & 7
+    return [1 if (o >> (2 - d)) & 1 else -1 for d in range(3)]
+
+
+def dmk_laplace3d(points, charges, eps: float, ns: int, return_stages: bool = False):
+    """u_i = sum_{j != i} rho_j / |x_i - x_j| by DMK.  points (N,3), charges (N,)."""
+    prm = for_eps(eps)
+    split = LaplaceSplit(prm.c)
+    T = Tree(points, ns)                                   # Step 0
+    rho = np.asarray(charges, dtype=np.float64)[T.perm]
+    X = T.xs
+    N = T.N
+    st = {"tree": T, "params": prm}
+    if T.box_leaf[0]:                                      # reading R10: root is a leaf
+        d = X[:, None, :] - X[None, :, :]
+        r = np.sqrt(np.einsum("ijk,ijk->ij", d, d))
+        with np.errstate(divide="ignore"):
+            inv = np.where(r > 0.0, 1.0 / r, 0.0)
+        us = inv @ rho
+        u = np.empty(N)
+        u[T.perm] = us / T.side
+        st.update(u_far=np.zeros(N), u_near=us, u_self=np.zeros(N))
+        return (u, st) if return_stages else u
+
+    p = prm.p
+    # ---- Step 1: precomputation -------------------------------------------
+    xn = cheb.nodes(p)
+    Vi = cheb.Vinv(p)
+    C2P = {s: cheb.c2p_1d(p, s) for s in (-1, 1)}
+    P2C = {s: cheb.p2c_1d(p, s) for s in (-1, 1)}
+    lev = {}
+    for l in range(T.nlevels):
+        h, nf = prm.h(l), prm.nfl(l)
+        if l == 0:
+            w = trapezoid_weights_3d(lambda k: split.What_root(k, prm.RT), h, nf)
+        else:
+            w = trapezoid_weights_3d(lambda k, l=l: split.Dhat(l, k), h, nf)
+        m = np.arange(-nf, nf + 1, dtype=np.float64)
+        s = r_level(l)
+        E_out = np.exp(-1j * h * np.outer(m, xn * s / 2.0))     # T_prox2pw 1D factor (N1, p)
+        E_in = np.exp(1j * h * np.outer(xn * s / 2.0, m))       # T_pw2poly 1D factor (p, N1)
+        shift = {dd: np.exp(1j * h * m * dd * s) for dd in (-1, 0, 1)}   # T_pwshift factors
+        lev[l] = dict(h=h, nf=nf, w=w, E_out=E_out, E_in=E_in, shift=shift)
+
+    # ---- Step 2: upward pass -----------------------------------------------
+    proxy = {}
+    for i in np.nonzero(T.box_leaf & (T.box_npts > 0))[0]:
+        a, b = T.box_start[i], T.box_end[i]
+        c, s = T.center(i), r_level(T.box_level[i])
+        U = [cheb.interp_matrix(2.0 * (X[a:b, d] - c[d]) / s, p) for d in range(3)]
+        proxy[i] = np.einsum("ja,jb,jc,j->abc", U[0], U[1], U[2], rho[a:b], optimize=True)
+    for l in range(T.nlevels - 2, -1, -1):
+        for i in range(T.level_offset[l], T.level_offset[l + 1]):
+            if T.box_leaf[i] or T.box_npts[i] == 0:
+                continue
+            acc = np.zeros((p, p, p))
+            for ch in T.box_children[i]:
+                if ch >= 0 and ch in proxy:
+                    sd = _octant_sides(T.box_code[ch])
+                    acc += cheb.apply3([C2P[sd[0]], C2P[sd[1]], C2P[sd[2]]], proxy[ch])
+            proxy[i] = acc
+    st["proxy"] = proxy
+
+    # ---- Step 3: downward pass ---------------------------------------------
+    Phi, Psi, local = {}, {}, {}
+    u_far = np.zeros(N)
+    for l in range(T.nlevels):
+        L = lev[l]
+        rng_ = range(T.level_offset[l], T.level_offset[l + 1])
+        for i in rng_:                                    # outgoing expansions
+            if T.fout[i]:
+                Phi[i] = cheb.apply3([L["E_out"]] * 3, proxy[i])
+        for i in rng_:                                    # incoming expansions
+            if T.fin[i]:
+                acc = np.zeros_like(L["w"], dtype=np.complex128)
+                for sb in T.pwlist[i]:
+                    dd = T.box_coords[i] - T.box_coords[sb]
+                    sh = (L["shift"][dd[0]][:, None, None] * L["shift"][dd[1]][None, :, None]
+                          * L["shift"][dd[2]][None, None, :])
+                    acc += L["w"] * sh * Phi[sb]
+                Psi[i] = acc
+        for i in rng_:                                    # local expansions
+            if T.box_npts[i] == 0:
+                continue
+            lam = np.zeros((p, p, p))
+            if T.fin[i]:
+                vals = cheb.apply3([L["E_in"]] * 3, Psi[i]).real
+                lam += cheb.apply3([Vi, Vi, Vi], vals)
+            par = T.box_parent[i]                         # split from parent (Eq. 3.46)
+            if par >= 0 and par in local:
+                sd = _octant_sides(T.box_code[i])
+                lam += cheb.apply3([P2C[sd[0]], P2C[sd[1]], P2C[sd[2]]], local[par])
+            local[i] = lam
+        for i in rng_:                                    # evaluate at leaf targets
+            if T.box_leaf[i] and T.box_npts[i] > 0:
+                a, b = T.box_start[i], T.box_end[i]
+                c, s = T.center(i), r_level(l)
+                E = [cheb.vander(2.0 * (X[a:b, d] - c[d]) / s, p) for d in range(3)]
+                u_far[a:b] = np.einsum("ja,jb,jc,abc->j", E[0], E[1], E[2], local[i], optimize=True)
+    st.update(Phi=Phi, Psi=Psi, local=local)
+
+    # ---- Step 4: direct interactions (residual kernel of the SOURCE level) ----
+    u_near = np.zeros(N)
+    for i in np.nonzero(T.box_leaf & (T.box_npts > 0))[0]:
+        a, b = T.box_start[i], T.box_end[i]
+        for sb in T.dlist[i]:
+            sa, se = T.box_start[sb], T.box_end[sb]
+            d = X[a:b, None, :] - X[None, sa:se, :]
+            r = np.sqrt(np.einsum("ijk,ijk->ij", d, d))
+            R = np.where(r > 0.0, split.R(int(T.box_level[sb]), np.where(r > 0, r, 1.0)), 0.0)
+            u_near[a:b] += R @ rho[sa:se]
+
+    # ---- Step 5: self-interaction corrections --------------------------------
+    u_self = np.zeros(N)
+    for i in np.nonzero(T.box_leaf & (T.box_npts > 0))[0]:
+        a, b = T.box_start[i], T.box_end[i]
+        d = X[a:b, None, :] - X[None, a:b, :]
+        coinc = np.all(d == 0.0, axis=2)
+        u_self[a:b] -= split.M0_at_zero(int(T.box_level[i])) * (coinc @ rho[a:b])
+
+    us = u_far + u_near + u_self
+    u = np.empty(N)
+    u[T.perm] = us / T.side
+    st.update(u_far=u_far, u_near=u_near, u_self=u_self)
+    return (u, st) if return_stages else u
