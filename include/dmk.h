@@ -1,0 +1,181 @@
+/*
+ * dmk.h -- C ABI of the B200-native DMK library (libdmk.so, built for sm_100a).
+ *
+ * The library evaluates the discrete sum of arXiv 2308.00292 (Jiang & Greengard,
+ * "A dual-space multilevel kernel-splitting framework"),
+ *
+ *     u_i = sum_{j : x_j != x_i} K(x_i - x_j) rho_j ,   i = 1..N      (Eq. 1.1)
+ *
+ * with sources = targets, for K(r) = 1/r in 3D (Eq. 3.1), by the
+ * discrete DMK algorithm of Sec. 3.5 with the PSWF kernel split
+ * of Sec. 3.6 (Eq. 3.66) and the parameters of Table 1
+ * (PAPER.md:2010-2035).  Coincident pairs (x_j == x_i, including j == i) are omitted,
+ * as the paper's self-interaction rule prescribes.
+ *
+ * Conventions for every entry point
+ *   - Return value: DMK_OK (0) on success, a negative DMK_ERR_* code otherwise.  The
+ *     message of the last failure on the calling thread is returned by dmk_last_error().
+ *     On failure no output buffer is partially meaningful.
+ *   - Memory: `mem` says where a caller pointer lives: DMK_MEM_DEVICE (CUDA device
+ *     memory on the plan's device) or DMK_MEM_HOST (pageable or pinned host memory).
+ *     The library never takes ownership of caller buffers.  A plan owns its device
+ *     memory until dmk_destroy().
+ *   - Streams: all device work of a plan is ordered on the stream given at plan time
+ *     (0 = legacy default stream).  dmk_plan() synchronises that stream before it
+ *     returns.  dmk_eval() with DMK_MEM_DEVICE buffers is asynchronous with respect
+ *     to the host; with DMK_MEM_HOST buffers it returns after the result is in host
+ *     memory.
+ *   - Precision: all arithmetic is IEEE fp64.
+ *   - There is no CPU fallback: without a usable CUDA device every call fails with
+ *     DMK_ERR_CUDA.
+ */
+#ifndef DMK_H
+#define DMK_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DMK_OK 0
+#define DMK_ERR_ARG (-1)          /* invalid argument (null pointer, bad size, bad enum) */
+#define DMK_ERR_UNSUPPORTED (-2)  /* valid but not implemented (dim, kernel, precision) */
+#define DMK_ERR_CUDA (-3)         /* CUDA runtime / launch failure, or no device */
+#define DMK_ERR_STATE (-4)        /* call out of order (e.g. stage query before eval) */
+
+#define DMK_MEM_DEVICE 0
+#define DMK_MEM_HOST 1
+
+/* Kernels.  DMK_KERNEL_LAPLACE: K(r) = 1/r in 3D (Eq. 3.1).  Others are reserved
+ * (2D log, 3D Yukawa: Sec. 4.6, Eqs. 4.17-4.18) and return DMK_ERR_UNSUPPORTED. */
+#define DMK_KERNEL_LAPLACE 0
+#define DMK_KERNEL_YUKAWA 1
+#define DMK_KERNEL_LOG 2
+
+typedef struct dmk_plan_s* dmk_plan_t;
+
+/* Optional plan parameters; pass NULL for defaults. */
+typedef struct dmk_options {
+  int32_t leaf_capacity;   /* n_s: a box holding more than n_s points is refined
+                              (PAPER.md:804-806); default 200 */
+  int32_t reserved0;
+  double lambda;           /* Yukawa parameter (reserved) */
+  void* stream;            /* cudaStream_t for all device work; NULL = default stream */
+} dmk_options;
+
+/* dmk_plan: build the plan for N points in `dim` dimensions.
+ *   dim      must be 3.
+ *   kernel   DMK_KERNEL_*.
+ *   eps      requested precision; snapped to the next tighter Table 1 row among
+ *            {1e-3, 1e-6, 1e-9}.  eps < 1e-9: DMK_ERR_UNSUPPORTED.
+ *   n        number of points, 1 <= n < 2^31.
+ *   points   n x dim row-major fp64 (point i at points[dim*i .. dim*i+dim-1]), in `mem`.
+ *   opt      see dmk_options (may be NULL).
+ *   out      receives the plan handle.
+ * Work done (Sec. 3.5 Step 0 and Step 1): bounding cube, Morton keys, stable sort,
+ * adaptive 2:1-balanced octree, colleague / plane-wave / direct interaction lists --
+ * all in CUDA kernels on the device -- plus the per-precision tables of Step 1
+ * (computed once on the host per precision and cached).  */
+int dmk_plan(int dim, int kernel, double eps, int64_t n, const double* points, int mem,
+             const dmk_options* opt, dmk_plan_t* out);
+
+/* dmk_eval: potentials for one charge vector (Sec. 3.5 Steps 2-5).
+ *   charges     n fp64 (caller's point order), in `mem`.
+ *   potentials  n fp64 output (caller's point order), in `mem`; may not alias charges. */
+int dmk_eval(dmk_plan_t plan, const double* charges, double* potentials, int mem);
+
+/* dmk_destroy: free the plan (NULL is a no-op). */
+int dmk_destroy(dmk_plan_t plan);
+
+/* Last error message of the calling thread ("" if none). */
+const char* dmk_last_error(void);
+
+/* Library version string. */
+const char* dmk_version(void);
+
+/* ---------------------------------------------------------------------------
+ * Introspection (used by the stage-by-stage parity tests).  All outputs are host
+ * buffers the caller sized from dmk_plan_info().
+ * ------------------------------------------------------------------------- */
+typedef struct dmk_plan_info {
+  int64_t n;          /* points */
+  int64_t nbox;       /* boxes kept: all non-leaf boxes + non-empty leaves */
+  int32_t nlevels;    /* levels 0..nlevels-1 */
+  int32_t p;          /* Chebyshev order (Table 1) */
+  int32_t nf;         /* difference-kernel Fourier half-width, N_1 = 2 nf + 1 */
+  int32_t nf0;        /* root-window Fourier half-width */
+  int64_t nfout;      /* boxes with an outgoing expansion (F_out) */
+  int64_t nexp;       /* boxes with a local expansion */
+  int64_t ndlist;     /* total entries of the direct lists */
+  double lo[3];       /* root cube corner */
+  double side;        /* root cube side */
+  double c;           /* PSWF parameter (Table 1) */
+  int32_t respoly_degree; /* degree of the residual-kernel polynomial */
+  int32_t reserved;
+} dmk_plan_info;
+
+int dmk_plan_info_get(dmk_plan_t plan, dmk_plan_info* info);
+
+/* Tree arrays, copied to host.  `which` selects the array; element types/sizes:
+ *   DMK_TREE_PERM        int64[n]        sorted position -> caller index
+ *   DMK_TREE_BOX_LEVEL   int64[nbox]
+ *   DMK_TREE_BOX_CODE    int64[nbox]     Morton code of the box at its level
+ *   DMK_TREE_BOX_START   int64[nbox]     first sorted point of the box
+ *   DMK_TREE_BOX_END     int64[nbox]     one past the last
+ *   DMK_TREE_BOX_LEAF    int64[nbox]     1 = leaf
+ *   DMK_TREE_BOX_PARENT  int64[nbox]     -1 for the root
+ *   DMK_TREE_COLLEAGUES  int64[27*nbox]  slot (dx+1)*9+(dy+1)*3+(dz+1), -1 if absent
+ *   DMK_TREE_DLIST_OFF   int64[nbox+1]   CSR offsets of the direct lists (empty for
+ *                                         boxes that are not non-empty leaves)
+ *   DMK_TREE_DLIST       int64[ndlist]   source leaves of each target leaf (any order)
+ *   DMK_TREE_FOUT        int64[nbox]     rank among F_out boxes, -1 if not F_out
+ *   DMK_TREE_EXP         int64[nbox]     rank among local-expansion boxes, -1 if none */
+#define DMK_TREE_PERM 0
+#define DMK_TREE_BOX_LEVEL 1
+#define DMK_TREE_BOX_CODE 2
+#define DMK_TREE_BOX_START 3
+#define DMK_TREE_BOX_END 4
+#define DMK_TREE_BOX_LEAF 5
+#define DMK_TREE_BOX_PARENT 6
+#define DMK_TREE_COLLEAGUES 7
+#define DMK_TREE_DLIST_OFF 8
+#define DMK_TREE_DLIST 9
+#define DMK_TREE_FOUT 10
+#define DMK_TREE_EXP 11
+int dmk_tree_copy(dmk_plan_t plan, int which, int64_t* host_out);
+
+/* Intermediate results of the last dmk_eval, copied to host (fp64):
+ *   DMK_STAGE_MOMENTS  [nfout][p][p][p]     Chebyshev moments mu_n = sum_j rho_j T_n(xi_j)
+ *                                            of each F_out box (proxy charges = V^{-T} mu,
+ *                                            Def. 2.1)
+ *   DMK_STAGE_OUTGOING outgoing plane waves Phi_l(B) (Eq. 3.42) of the F_out boxes in
+ *                                            rank order; the root (rank 0) first with
+ *                                            [nf0+1][2nf0+1][2nf0+1][2] values, then every
+ *                                            other box with [nf+1][2nf+1][2nf+1][2]: half
+ *                                            space m3 >= 0 (Hermitian symmetry), axes
+ *                                            (m3, m1, m2), m1, m2 in [-nf_l, nf_l], (re, im)
+ *   DMK_STAGE_LOCAL    [nexp][p][p][p]      Chebyshev coefficients of the local expansion
+ *                                            Lambda (Eq. 3.43) incl. parent contributions
+ *   DMK_STAGE_UFAR     [n]                  far-field potential, sorted order, unit cube
+ *   DMK_STAGE_UNEAR    [n]                  residual + self terms, sorted order, unit cube */
+#define DMK_STAGE_MOMENTS 0
+#define DMK_STAGE_OUTGOING 1
+#define DMK_STAGE_LOCAL 2
+#define DMK_STAGE_UFAR 3
+#define DMK_STAGE_UNEAR 4
+int dmk_stage_copy(dmk_plan_t plan, int which, double* host_out, int64_t count);
+
+/* Number of fp64 values dmk_stage_copy(plan, which, ...) expects (>= 0), or < 0 on error. */
+int64_t dmk_stage_size(dmk_plan_t plan, int which);
+
+/* Per-kernel timing of the last dmk_eval (milliseconds, CUDA events on the plan
+ * stream); fills up to `cap` entries, returns the number of timed phases or < 0.
+ * Names: "gather","anterp","c2p","prox2pw","pwlocal","p2c","eval","p2p".
+ * Enabled only when the plan was created with env DMK_PROFILE=1. */
+int dmk_eval_timings(dmk_plan_t plan, double* ms, const char** names, int cap);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DMK_H */

@@ -1,0 +1,192 @@
+"""paper_2308_00292_b200 -- B200-native DMK (arXiv 2308.00292) for 3D Laplace.
+
+Thin ctypes binding over the C ABI in ``include/dmk.h`` (libdmk.so, built in-tree
+for sm_100a by ``paper_2308_00292_b200/build.py``).  Argument marshalling only:
+every step of the computation runs in the library's CUDA kernels.  There is no
+CPU path -- if the library or a CUDA device is missing, calls raise.
+
+    plan = dmk_plan(points, eps=1e-6, leaf_capacity=200)   # torch.cuda (n,3) f64 or numpy (n,3)
+    u = plan.eval(charges)                                  # same placement as `charges`
+    plan.close()
+
+Function names mirror the C entry points (dmk_plan, dmk_eval, dmk_destroy,
+dmk_plan_info_get, dmk_tree_copy, dmk_stage_copy).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libdmk.so")
+
+DMK_OK = 0
+DMK_MEM_DEVICE, DMK_MEM_HOST = 0, 1
+DMK_KERNEL_LAPLACE, DMK_KERNEL_YUKAWA, DMK_KERNEL_LOG = 0, 1, 2
+KERNELS = {"laplace": DMK_KERNEL_LAPLACE, "yukawa": DMK_KERNEL_YUKAWA, "log": DMK_KERNEL_LOG}
+TREE = {name: i for i, name in enumerate(
+    ["perm", "box_level", "box_code", "box_start", "box_end", "box_leaf", "box_parent",
+     "colleagues", "dlist_off", "dlist", "fout", "exp"])}
+STAGE = {"moments": 0, "outgoing": 1, "local": 2, "ufar": 3, "unear": 4}
+
+
+class DmkError(RuntimeError):
+    pass
+
+
+class _Options(ctypes.Structure):
+    _fields_ = [("leaf_capacity", ctypes.c_int32), ("reserved0", ctypes.c_int32),
+                ("lam", ctypes.c_double), ("stream", ctypes.c_void_p)]
+
+
+class PlanInfo(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int64), ("nbox", ctypes.c_int64), ("nlevels", ctypes.c_int32),
+                ("p", ctypes.c_int32), ("nf", ctypes.c_int32), ("nf0", ctypes.c_int32),
+                ("nfout", ctypes.c_int64), ("nexp", ctypes.c_int64), ("ndlist", ctypes.c_int64),
+                ("lo", ctypes.c_double * 3), ("side", ctypes.c_double), ("c", ctypes.c_double),
+                ("respoly_degree", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libdmk.so (built in-tree); raise if it is missing."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise DmkError(f"{LIB_PATH} not built; run __graft_entry__.build() or "
+                           "python paper_2308_00292_b200/build.py")
+        L = ctypes.CDLL(LIB_PATH)
+        vp, i64, dbl, ci = ctypes.c_void_p, ctypes.c_int64, ctypes.c_double, ctypes.c_int
+        L.dmk_plan.argtypes = [ci, ci, dbl, i64, vp, ci, ctypes.POINTER(_Options), ctypes.POINTER(vp)]
+        L.dmk_eval.argtypes = [vp, vp, vp, ci]
+        L.dmk_destroy.argtypes = [vp]
+        L.dmk_last_error.restype = ctypes.c_char_p
+        L.dmk_version.restype = ctypes.c_char_p
+        L.dmk_plan_info_get.argtypes = [vp, ctypes.POINTER(PlanInfo)]
+        L.dmk_tree_copy.argtypes = [vp, ci, vp]
+        L.dmk_stage_copy.argtypes = [vp, ci, vp, i64]
+        L.dmk_stage_size.argtypes = [vp, ci]
+        L.dmk_stage_size.restype = i64
+        L.dmk_eval_timings.argtypes = [vp, ctypes.POINTER(dbl), ctypes.POINTER(ctypes.c_char_p), ci]
+        for f in ("dmk_plan", "dmk_eval", "dmk_destroy", "dmk_plan_info_get", "dmk_tree_copy",
+                  "dmk_stage_copy", "dmk_eval_timings"):
+            getattr(L, f).restype = ci
+        _lib = L
+    return _lib
+
+
+def _check(rc: int, what: str):
+    if rc != DMK_OK:
+        raise DmkError(f"{what} failed ({rc}): {lib().dmk_last_error().decode()}")
+
+
+def _placement(a):
+    """(pointer, mem, keepalive) for a torch tensor or numpy array of float64."""
+    try:
+        import torch
+        if isinstance(a, torch.Tensor):
+            if a.dtype != torch.float64:
+                raise DmkError("expected float64")
+            a = a.contiguous()
+            return a.data_ptr(), (DMK_MEM_DEVICE if a.is_cuda else DMK_MEM_HOST), a
+    except ImportError:
+        pass
+    arr = np.ascontiguousarray(a, dtype=np.float64)
+    return arr.ctypes.data, DMK_MEM_HOST, arr
+
+
+class Plan:
+    """A dmk_plan_t: tree, lists and tables for one point set (sources = targets)."""
+
+    def __init__(self, points, eps: float = 1e-6, leaf_capacity: int = 200, kernel: str = "laplace",
+                 stream=None):
+        ptr, mem, keep = _placement(points)
+        n = keep.shape[0]
+        if keep.ndim != 2 or keep.shape[1] != 3:
+            raise DmkError("points must have shape (n, 3)")
+        opt = _Options(int(leaf_capacity), 0, 0.0, stream)
+        h = ctypes.c_void_p()
+        _check(lib().dmk_plan(3, KERNELS[kernel], float(eps), int(n), ptr, mem, ctypes.byref(opt),
+                              ctypes.byref(h)), "dmk_plan")
+        self._h = h
+        self.n = int(n)
+
+    def eval(self, charges, out=None):
+        """Potentials u_i = sum_{j: x_j != x_i} rho_j / |x_i - x_j| (caller order)."""
+        qptr, mem, qkeep = _placement(charges)
+        if qkeep.shape != (self.n,):
+            raise DmkError("charges must have shape (n,)")
+        if out is None:
+            if mem == DMK_MEM_DEVICE:
+                import torch
+                out = torch.empty(self.n, dtype=torch.float64, device=qkeep.device)
+            else:
+                out = np.empty(self.n, dtype=np.float64)
+        optr, omem, okeep = _placement(out)
+        if omem != mem:
+            raise DmkError("charges and output must live in the same memory")
+        _check(lib().dmk_eval(self._h, qptr, optr, mem), "dmk_eval")
+        return okeep
+
+    def info(self) -> PlanInfo:
+        inf = PlanInfo()
+        _check(lib().dmk_plan_info_get(self._h, ctypes.byref(inf)), "dmk_plan_info_get")
+        return inf
+
+    def tree(self, which: str) -> np.ndarray:
+        inf = self.info()
+        size = {"perm": inf.n, "colleagues": 27 * inf.nbox, "dlist_off": inf.nbox + 1,
+                "dlist": inf.ndlist}.get(which, inf.nbox)
+        out = np.empty(size, dtype=np.int64)
+        _check(lib().dmk_tree_copy(self._h, TREE[which], out.ctypes.data), "dmk_tree_copy")
+        return out
+
+    def stage(self, which: str) -> np.ndarray:
+        k = STAGE[which]
+        size = int(lib().dmk_stage_size(self._h, k))
+        out = np.empty(size, dtype=np.float64)
+        _check(lib().dmk_stage_copy(self._h, k, out.ctypes.data, size), "dmk_stage_copy")
+        return out
+
+    def timings(self) -> dict:
+        ms = (ctypes.c_double * 32)()
+        names = (ctypes.c_char_p * 32)()
+        k = lib().dmk_eval_timings(self._h, ms, names, 32)
+        return {names[i].decode(): ms[i] for i in range(max(k, 0))}
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().dmk_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+
+def dmk_plan(points, eps: float = 1e-6, leaf_capacity: int = 200, kernel: str = "laplace", stream=None) -> Plan:
+    return Plan(points, eps=eps, leaf_capacity=leaf_capacity, kernel=kernel, stream=stream)
+
+
+def dmk_eval(plan: Plan, charges, out=None):
+    return plan.eval(charges, out)
+
+
+def dmk_destroy(plan: Plan):
+    plan.close()
+
+
+def version() -> str:
+    return lib().dmk_version().decode()

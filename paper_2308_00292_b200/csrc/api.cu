@@ -1,0 +1,243 @@
+// api.cu -- the C ABI of libdmk (include/dmk.h): argument checking, memory
+// placement (host <-> device), plan lifetime, introspection.
+#include <cstdlib>
+#include <cstring>
+#include <exception>
+
+#include "common.cuh"
+
+namespace dmk {
+void build_tree(dmk_plan_s* P, const double* dpts);
+void eval_plan(dmk_plan_s* P, const double* dcharges, double* dout);
+
+static thread_local std::string g_err;
+void set_error(const std::string& m) { g_err = m; }
+void fail(int code, const std::string& m) { throw Error{code, m}; }
+
+template <class F>
+static int guard(F f) {
+  try {
+    f();
+    g_err.clear();
+    return DMK_OK;
+  } catch (const Error& e) {
+    g_err = e.msg;
+    return e.code;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return DMK_ERR_CUDA;
+  }
+}
+
+static void require_device() {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0) fail(DMK_ERR_CUDA, "no CUDA device available (libdmk has no CPU path)");
+}
+
+static void alloc_eval_buffers(dmk_plan_s* P) {
+  const Tables& T = *P->tab;
+  cudaStream_t s = P->stream;
+  const int64_t p3 = (int64_t)T.p * T.p * T.p;
+  P->q.alloc(P->n, s);
+  P->ufar.alloc(P->n, s);
+  P->unear.alloc(P->n, s);
+  P->phi_size0 = (int64_t)2 * (T.nf0 + 1) * (2 * T.nf0 + 1) * (2 * T.nf0 + 1);
+  P->phi_size1 = (int64_t)2 * (T.nf + 1) * (2 * T.nf + 1) * (2 * T.nf + 1);
+  if (P->th.nlevels > 1) {
+    P->mom.alloc(P->nfout * p3, s);
+    P->phi.alloc(P->phi_size0 + (P->nfout - 1) * P->phi_size1, s);
+    P->lam.alloc(P->nexp * p3, s);
+  }
+}
+
+}  // namespace dmk
+
+using namespace dmk;
+
+extern "C" {
+
+const char* dmk_last_error(void) { return g_err.c_str(); }
+const char* dmk_version(void) { return "libdmk 0.1 (sm_100a, fp64, 3D Laplace PSWF split)"; }
+
+int dmk_plan(int dim, int kernel, double eps, int64_t n, const double* points, int mem, const dmk_options* opt,
+             dmk_plan_t* out) {
+  return guard([&] {
+    if (!out) fail(DMK_ERR_ARG, "out is NULL");
+    *out = nullptr;
+    if (!points) fail(DMK_ERR_ARG, "points is NULL");
+    if (n < 1 || n >= (int64_t)1 << 31) fail(DMK_ERR_ARG, "n must be in [1, 2^31)");
+    if (mem != DMK_MEM_DEVICE && mem != DMK_MEM_HOST) fail(DMK_ERR_ARG, "bad mem");
+    if (!(eps > 0)) fail(DMK_ERR_ARG, "eps must be > 0");
+    if (dim != 3) fail(DMK_ERR_UNSUPPORTED, "only dim = 3 is implemented");
+    if (kernel != DMK_KERNEL_LAPLACE) fail(DMK_ERR_UNSUPPORTED, "only DMK_KERNEL_LAPLACE is implemented");
+    require_device();
+    dmk_plan_s* P = new dmk_plan_s();
+    try {
+      P->dim = dim;
+      P->kernel = kernel;
+      P->eps = eps;
+      P->n = n;
+      if (opt) {
+        if (opt->leaf_capacity < 1) fail(DMK_ERR_ARG, "leaf_capacity must be >= 1");
+        P->ns = opt->leaf_capacity;
+        P->stream = (cudaStream_t)opt->stream;
+      }
+      const char* pe = std::getenv("DMK_PROFILE");
+      P->profile = pe && pe[0] == '1';
+      P->tab = &get_tables(kernel, eps);
+      const double* dpts = points;
+      DevBuf<double> tmp;
+      if (mem == DMK_MEM_HOST) {
+        tmp.alloc(3 * n, P->stream);
+        DMK_CUDA(cudaMemcpyAsync(tmp.p, points, 3 * n * sizeof(double), cudaMemcpyHostToDevice, P->stream));
+        dpts = tmp.p;
+      }
+      build_tree(P, dpts);
+      alloc_eval_buffers(P);
+      DMK_CUDA(cudaStreamSynchronize(P->stream));
+    } catch (...) {
+      delete P;
+      throw;
+    }
+    *out = P;
+  });
+}
+
+int dmk_eval(dmk_plan_t P, const double* charges, double* potentials, int mem) {
+  return guard([&] {
+    if (!P) fail(DMK_ERR_ARG, "plan is NULL");
+    if (!charges || !potentials) fail(DMK_ERR_ARG, "null buffer");
+    if (mem != DMK_MEM_DEVICE && mem != DMK_MEM_HOST) fail(DMK_ERR_ARG, "bad mem");
+    cudaStream_t s = P->stream;
+    if (mem == DMK_MEM_HOST) {
+      DevBuf<double> dq, du;
+      dq.alloc(P->n, s);
+      du.alloc(P->n, s);
+      DMK_CUDA(cudaMemcpyAsync(dq.p, charges, P->n * sizeof(double), cudaMemcpyHostToDevice, s));
+      eval_plan(P, dq.p, du.p);
+      DMK_CUDA(cudaMemcpyAsync(potentials, du.p, P->n * sizeof(double), cudaMemcpyDeviceToHost, s));
+      DMK_CUDA(cudaStreamSynchronize(s));
+    } else {
+      eval_plan(P, charges, potentials);
+    }
+    P->evaluated = true;
+  });
+}
+
+int dmk_destroy(dmk_plan_t P) {
+  return guard([&] {
+    if (!P) return;
+    cudaStream_t s = P->stream;
+    delete P;   // DevBuf destructors enqueue cudaFreeAsync on the plan stream
+    cudaStreamSynchronize(s);
+  });
+}
+
+int dmk_plan_info_get(dmk_plan_t P, dmk_plan_info* info) {
+  return guard([&] {
+    if (!P || !info) fail(DMK_ERR_ARG, "null argument");
+    std::memset(info, 0, sizeof(*info));
+    info->n = P->n;
+    info->nbox = P->nbox;
+    info->nlevels = P->th.nlevels;
+    info->p = P->tab->p;
+    info->nf = P->tab->nf;
+    info->nf0 = P->tab->nf0;
+    info->nfout = P->nfout;
+    info->nexp = P->nexp;
+    info->ndlist = P->ndlist;
+    for (int d = 0; d < 3; ++d) info->lo[d] = P->lo[d];
+    info->side = P->side;
+    info->c = P->tab->c;
+    info->respoly_degree = (int32_t)P->tab->respoly.size() - 1;
+  });
+}
+
+}  // extern "C"
+
+namespace dmk {
+template <class T>
+static void copy_widen(cudaStream_t s, const T* d, int64_t cnt, int64_t* out) {
+  std::vector<T> h(cnt);
+  if (cnt) DMK_CUDA(cudaMemcpyAsync(h.data(), d, cnt * sizeof(T), cudaMemcpyDeviceToHost, s));
+  DMK_CUDA(cudaStreamSynchronize(s));
+  for (int64_t i = 0; i < cnt; ++i) out[i] = (int64_t)h[i];
+}
+}  // namespace dmk
+
+extern "C" {
+
+int dmk_tree_copy(dmk_plan_t P, int which, int64_t* out) {
+  return guard([&] {
+    if (!P || !out) fail(DMK_ERR_ARG, "null argument");
+    cudaStream_t s = P->stream;
+    const int64_t nb = P->nbox;
+    switch (which) {
+      case DMK_TREE_PERM: copy_widen(s, P->perm.p, P->n, out); break;
+      case DMK_TREE_BOX_LEVEL: copy_widen(s, P->box_level.p, nb, out); break;
+      case DMK_TREE_BOX_CODE: copy_widen(s, P->box_code.p, nb, out); break;
+      case DMK_TREE_BOX_START: copy_widen(s, P->box_start.p, nb, out); break;
+      case DMK_TREE_BOX_END: copy_widen(s, P->box_end.p, nb, out); break;
+      case DMK_TREE_BOX_LEAF: {
+        copy_widen(s, P->box_flags.p, nb, out);
+        for (int64_t i = 0; i < nb; ++i) out[i] &= 1;
+        break;
+      }
+      case DMK_TREE_BOX_PARENT: copy_widen(s, P->box_parent.p, nb, out); break;
+      case DMK_TREE_COLLEAGUES: copy_widen(s, P->box_coll.p, 27 * nb, out); break;
+      case DMK_TREE_DLIST_OFF: copy_widen(s, P->dlist_off.p, nb + 1, out); break;
+      case DMK_TREE_DLIST: copy_widen(s, P->dlist.p, P->ndlist, out); break;
+      case DMK_TREE_FOUT: copy_widen(s, P->fout_rank.p, nb, out); break;
+      case DMK_TREE_EXP: copy_widen(s, P->exp_rank.p, nb, out); break;
+      default: fail(DMK_ERR_ARG, "unknown tree array");
+    }
+  });
+}
+
+int dmk_stage_copy(dmk_plan_t P, int which, double* out, int64_t count) {
+  return guard([&] {
+    if (!P || !out) fail(DMK_ERR_ARG, "null argument");
+    if (!P->evaluated) fail(DMK_ERR_STATE, "no dmk_eval has run on this plan");
+    const DevBuf<double>* b = nullptr;
+    switch (which) {
+      case DMK_STAGE_MOMENTS: b = &P->mom; break;
+      case DMK_STAGE_OUTGOING: b = &P->phi; break;
+      case DMK_STAGE_LOCAL: b = &P->lam; break;
+      case DMK_STAGE_UFAR: b = &P->ufar; break;
+      case DMK_STAGE_UNEAR: b = &P->unear; break;
+      default: fail(DMK_ERR_ARG, "unknown stage");
+    }
+    if (count != (int64_t)b->n) fail(DMK_ERR_ARG, "count must equal the stage size " + std::to_string(b->n));
+    DMK_CUDA(cudaMemcpyAsync(out, b->p, count * sizeof(double), cudaMemcpyDeviceToHost, P->stream));
+    DMK_CUDA(cudaStreamSynchronize(P->stream));
+  });
+}
+
+int64_t dmk_stage_size(dmk_plan_t P, int which) {
+  if (!P) return DMK_ERR_ARG;
+  switch (which) {
+    case DMK_STAGE_MOMENTS: return (int64_t)P->mom.n;
+    case DMK_STAGE_OUTGOING: return (int64_t)P->phi.n;
+    case DMK_STAGE_LOCAL: return (int64_t)P->lam.n;
+    case DMK_STAGE_UFAR: return (int64_t)P->ufar.n;
+    case DMK_STAGE_UNEAR: return (int64_t)P->unear.n;
+    default: return DMK_ERR_ARG;
+  }
+}
+
+int dmk_eval_timings(dmk_plan_t P, double* ms, const char** names, int cap) {
+  if (!P) return DMK_ERR_ARG;
+  int k = 0;
+  std::vector<std::pair<const char*, double>> all(P->tree_timings);
+  all.insert(all.end(), P->timings.begin(), P->timings.end());
+  for (auto& pr : all) {
+    if (k >= cap) break;
+    if (ms) ms[k] = pr.second;
+    if (names) names[k] = pr.first;
+    ++k;
+  }
+  return k;
+}
+
+}  // extern "C"

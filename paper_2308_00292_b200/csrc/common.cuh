@@ -1,0 +1,133 @@
+// common.cuh -- internal types of libdmk (not part of the ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/dmk.h"
+
+namespace dmk {
+
+constexpr int NBITS = 21;  // bits per coordinate of the 63-bit Morton key
+constexpr int LMAX = 20;   // deepest level a box may be refined into
+
+// ---------------------------------------------------------------- errors
+struct Error {
+  int code;
+  std::string msg;
+};
+void set_error(const std::string& m);
+[[noreturn]] void fail(int code, const std::string& m);
+
+#define DMK_CUDA(call)                                                                  \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess)                                                              \
+      ::dmk::fail(DMK_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_) +   \
+                                    " (" + __FILE__ + ":" + std::to_string(__LINE__) + ")"); \
+  } while (0)
+#define DMK_LAUNCH_CHECK() DMK_CUDA(cudaGetLastError())
+
+// ---------------------------------------------------------------- device buffer
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  cudaStream_t s = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { release(); }
+  void alloc(size_t count, cudaStream_t st) {
+    release();
+    s = st;
+    n = count;
+    if (count) DMK_CUDA(cudaMallocAsync((void**)&p, count * sizeof(T), st));
+  }
+  void release() {
+    if (p) cudaFreeAsync(p, s);
+    p = nullptr;
+    n = 0;
+  }
+  T* get() const { return p; }
+  size_t bytes() const { return n * sizeof(T); }
+};
+
+// ---------------------------------------------------------------- tables (Step 1)
+// Per-precision tables, computed on the host once and kept on the device.
+struct Tables {
+  double eps = 0, c = 0;
+  int p = 0, nf = 0, nf0 = 0;
+  double RT = 0, P0 = 0;   // root window truncation radius and Fourier period
+  // host copies
+  std::vector<double> Q1, Q0;   // [n1][p] complex (re,im): moments -> plane waves, levels>=1 / root
+  std::vector<double> A;        // [2][p][p]: A_s[n][k], T_n(x/2 + s/2) = sum_k A_s[n][k] T_k(x), s=-1,+1
+  std::vector<double> W;        // [LMAX+1][nh][n1][n1] difference-kernel weights, level l at l*stride
+  std::vector<double> W0;       // [nh0][n10][n10] root window weights
+  std::vector<double> respoly;  // residual: M_L(r) r_L ~= sum_k a_k s^k, s = 2 r^2/r_L^2 - 1
+  double m0 = 0;                // psi(0)/c0 = r_L M_L(0)
+  // device copies
+  double *dQ1 = nullptr, *dQ0 = nullptr, *dA = nullptr, *dW = nullptr, *dW0 = nullptr;
+  size_t wstride = 0;
+};
+const Tables& get_tables(int kernel, double eps);  // cached; throws via fail()
+
+// ---------------------------------------------------------------- plan
+struct TreeHost {
+  int nlevels = 0;
+  std::vector<int64_t> level_off;   // boxes of level l: [level_off[l], level_off[l+1])
+  std::vector<int64_t> fout_off;    // F_out boxes (ranked by box index) per level
+  std::vector<int64_t> exp_off;     // local-expansion boxes per level
+};
+
+}  // namespace dmk
+
+struct dmk_plan_s {
+  int dim = 3, kernel = 0, ns = 200;
+  double eps = 0;
+  int64_t n = 0;
+  cudaStream_t stream = 0;
+  const dmk::Tables* tab = nullptr;
+  bool profile = false;
+  bool evaluated = false;
+
+  // root cube
+  double lo[3] = {0, 0, 0};
+  double side = 1;
+
+  // sorted points (normalised coordinates in [0,1]^3) and permutation
+  dmk::DevBuf<uint64_t> keys;
+  dmk::DevBuf<int32_t> perm;        // sorted -> caller index
+  dmk::DevBuf<double> xs, ys, zs;
+
+  // boxes
+  int64_t nbox = 0;
+  dmk::TreeHost th;
+  dmk::DevBuf<uint64_t> box_code;
+  dmk::DevBuf<int32_t> box_level, box_start, box_end, box_parent, box_child /*8*nbox*/,
+      box_coll /*27*nbox*/;
+  dmk::DevBuf<uint8_t> box_flags;   // bit0 leaf, bit1 F_out, bit2 F_in, bit3 local expansion
+  dmk::DevBuf<int32_t> fout_rank, exp_rank;      // per box, -1 if none
+  dmk::DevBuf<int32_t> fout_list, exp_list;      // box ids, ordered by box id (=> by level)
+  int64_t nfout = 0, nexp = 0;
+  // direct lists (CSR over boxes)
+  dmk::DevBuf<int32_t> dlist_off, dlist;
+  int64_t ndlist = 0;
+  // work list for the P2P kernel: (leaf box, first target) items of <= 32 targets
+  dmk::DevBuf<int32_t> p2p_items;
+  int64_t np2p = 0;
+  // anterpolation / evaluation work: box ids
+  dmk::DevBuf<int32_t> anterp_list, eval_list;
+  int64_t nanterp = 0, neval = 0;
+  std::vector<int64_t> c2p_off, p2c_off;   // per-level ranges into fout_list / exp_list
+
+  // eval buffers
+  dmk::DevBuf<double> q, mom, phi, lam, ufar, unear;
+  int64_t phi_size0 = 0, phi_size1 = 0;   // doubles per root / per other box
+
+  // profiling
+  std::vector<std::pair<const char*, double>> timings;
+  std::vector<std::pair<const char*, double>> tree_timings;
+};

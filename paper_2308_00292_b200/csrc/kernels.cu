@@ -1,0 +1,752 @@
+// kernels.cu -- the DMK hot path on the device (Sec. 3.5 Steps 2-5).
+//
+// Representation: the upward pass carries Chebyshev *moments*
+// mu_n(B) = sum_j rho_j T_n(xi_j) instead of the proxy charges rho~ = V^{-T} mu of
+// Def. 2.1 -- a fixed linear bijection, folded into the plane-wave matrix
+// Q = E V^{-T} (so Phi_l(B) of Eq. 3.42 is bit-for-bit the same quantity), and
+// c2p (Lemma 2.2) becomes the exact re-expansion mu^P = (A (x) A (x) A) mu^C.
+// The downward pass carries Chebyshev coefficients Lambda (Eq. 3.43) and splits
+// them with T_p2c = A^T (Lemma 2.3).  Plane-wave expansions are stored for m3 >= 0
+// only (Hermitian symmetry of real sources).
+//
+// Kernels (one CTA per box unless noted):
+//   k_gather_q     charges into Morton order
+//   k_anterp<P>    moments of each F_out box from the points of its leaf children
+//                  (register-tiled rank-CH updates: a small fp64 GEMM per box)
+//   k_c2p<P>       child -> parent moments, one tree level per launch
+//   k_prox2pw<P,NF>   Phi_l(B) = (Q (x) Q (x) Q) mu(B), m3-sliced (T_prox2pw)
+//   k_pwlocal<P,NF>   Psi_l(B) = w_l sum_S shift(B,S) Phi_l(S) (Eq. 3.39) fused with
+//                  Lambda_own(B) = (G (x) G (x) G) Psi_l(B), G = conj(Q)^T (T_pw2poly)
+//   k_p2c<P>       Lambda(B) += (A^T)^{(x)3} Lambda(parent), one level per launch
+//   k_eval<P>      far field at targets from Lambda (Chebyshev sums)
+//   k_p2p<K>       residual kernel R_{L_S} over the direct lists (warp per 32
+//                  targets), self terms, final combine and scatter to caller order
+#include <cstring>
+
+#include "common.cuh"
+
+namespace dmk {
+
+// ---------------------------------------------------------------- tiling configs
+template <int P>
+struct Cfg;
+template <>
+struct Cfg<9> {
+  static constexpr int TB = 3, RB = 3, TA = 27, RA = 3, CH = 32, ECH = 16;
+};
+template <>
+struct Cfg<18> {
+  static constexpr int TB = 3, RB = 6, TA = 54, RA = 6, CH = 32, ECH = 16;
+};
+template <>
+struct Cfg<28> {
+  static constexpr int TB = 4, RB = 7, TA = 98, RA = 8, CH = 16, ECH = 8;
+};
+
+struct DevTree {
+  const uint64_t* code;
+  const int32_t* level;
+  const int32_t* start;
+  const int32_t* end;
+  const int32_t* parent;
+  const int32_t* child;
+  const int32_t* coll;
+  const uint8_t* flags;
+  const int32_t* fout_rank;
+  const int32_t* exp_rank;
+  const double* xs;
+  const double* ys;
+  const double* zs;
+};
+constexpr uint8_t F_LEAF = 1, F_OUT = 2, F_IN = 4, F_EXP = 8;
+
+__device__ __forceinline__ uint32_t compact3d(uint64_t x) {
+  x &= 0x1249249249249249ULL;
+  x = (x ^ (x >> 2)) & 0x10c30c30c30c30c3ULL;
+  x = (x ^ (x >> 4)) & 0x100f00f00f00f00fULL;
+  x = (x ^ (x >> 8)) & 0x1f0000ff0000ffULL;
+  x = (x ^ (x >> 16)) & 0x1f00000000ffffULL;
+  x = (x ^ (x >> 32)) & 0x1fffffULL;
+  return (uint32_t)x;
+}
+// centre of box (code, level) and the scale 2/side
+__device__ __forceinline__ void box_geom(uint64_t code, int l, double c[3], double& inv_half) {
+  double s = ldexp(1.0, -l);
+  c[0] = ((double)compact3d(code >> 2) + 0.5) * s;
+  c[1] = ((double)compact3d(code >> 1) + 0.5) * s;
+  c[2] = ((double)compact3d(code) + 0.5) * s;
+  inv_half = ldexp(1.0, l + 1);
+}
+
+__device__ __forceinline__ void cheb_vec(double x, double* T, int P, double scale0) {
+  // T[n] = scale0 * T_n(x)
+  double t0 = 1.0, t1 = x;
+  T[0] = scale0;
+  if (P > 1) T[1] = scale0 * x;
+  for (int n = 2; n < P; ++n) {
+    double t2 = 2.0 * x * t1 - t0;
+    T[n] = scale0 * t2;
+    t0 = t1;
+    t1 = t2;
+  }
+}
+
+// ---------------------------------------------------------------- gather
+__global__ void k_gather_q(const double* __restrict__ charges, const int32_t* __restrict__ perm, int64_t n,
+                           double* q) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) q[i] = charges[perm[i]];
+}
+
+// collect the point ranges a box works on:
+//   ANTERP: leaf children with points (F_out box)
+//   EVAL:   own points if the box is a leaf, else leaf children without F_in
+template <bool EVAL>
+__device__ int box_ranges(const DevTree& t, int b, int2* rg) {
+  int nr = 0;
+  uint8_t f = t.flags[b];
+  if (EVAL && (f & F_LEAF)) {
+    rg[nr++] = make_int2(t.start[b], t.end[b]);
+    return nr;
+  }
+  for (int o = 0; o < 8; ++o) {
+    int ch = t.child[8 * (int64_t)b + o];
+    if (ch < 0) continue;
+    uint8_t fc = t.flags[ch];
+    if (!(fc & F_LEAF) || t.end[ch] <= t.start[ch]) continue;
+    if (EVAL && (fc & F_IN)) continue;
+    rg[nr++] = make_int2(t.start[ch], t.end[ch]);
+  }
+  return nr;
+}
+__device__ __forceinline__ int range_point(const int2* rg, int nr, int idx) {
+  for (int r = 0; r < nr; ++r) {
+    int len = rg[r].y - rg[r].x;
+    if (idx < len) return rg[r].x + idx;
+    idx -= len;
+  }
+  return -1;
+}
+
+// ---------------------------------------------------------------- anterpolation
+// mu[a=(n1,n2)][b=n3] += sum_j (rho_j Tx_j[n1] Ty_j[n2]) Tz_j[n3]
+template <int P>
+__global__ void __launch_bounds__(Cfg<P>::TA * Cfg<P>::TB)
+    k_anterp(DevTree t, const int32_t* __restrict__ boxes, const double* __restrict__ q, double* __restrict__ mom) {
+  using C = Cfg<P>;
+  constexpr int NT = C::TA * C::TB, P2 = P * P, CH = C::CH;
+  extern __shared__ double sm[];
+  double* sU = sm;                 // [CH][P2]
+  double* sV = sU + CH * P2;       // [CH][P]
+  double* sT = sV + CH * P;        // [CH][2][P] (rho Tx, Ty)
+  __shared__ int2 rg[8];
+  __shared__ int nr_s, tot_s;
+  const int b = boxes[blockIdx.x];
+  if (threadIdx.x == 0) {
+    nr_s = box_ranges<false>(t, b, rg);
+    int tot = 0;
+    for (int r = 0; r < nr_s; ++r) tot += rg[r].y - rg[r].x;
+    tot_s = tot;
+  }
+  __syncthreads();
+  const int nr = nr_s, tot = tot_s;
+  if (tot == 0) return;   // moments were zeroed by the caller
+  double cen[3], ih;
+  box_geom(t.code[b], t.level[b], cen, ih);
+  const int tid = threadIdx.x, tb = tid % C::TB, ta = tid / C::TB;
+  double acc[C::RA][C::RB];
+#pragma unroll
+  for (int i = 0; i < C::RA; ++i)
+#pragma unroll
+    for (int k = 0; k < C::RB; ++k) acc[i][k] = 0.0;
+
+  for (int c0 = 0; c0 < tot; c0 += CH) {
+    const int nc = min(CH, tot - c0);
+    for (int w = tid; w < CH * 3; w += NT) {   // Chebyshev vectors
+      int j = w / 3, d = w % 3;
+      double T[P];
+      if (j < nc) {
+        int pi = range_point(rg, nr, c0 + j);
+        double x = (d == 0 ? t.xs[pi] : d == 1 ? t.ys[pi] : t.zs[pi]);
+        cheb_vec((x - cen[d]) * ih, T, P, d == 0 ? q[pi] : 1.0);
+      } else {
+        for (int n = 0; n < P; ++n) T[n] = 0.0;
+      }
+      double* dst = (d == 2) ? (sV + j * P) : (sT + (j * 2 + d) * P);
+      for (int n = 0; n < P; ++n) dst[n] = T[n];
+    }
+    __syncthreads();
+    for (int w = tid; w < CH * P2; w += NT) {
+      int j = w / P2, a = w % P2;
+      sU[w] = sT[(j * 2) * P + a / P] * sT[(j * 2 + 1) * P + a % P];
+    }
+    __syncthreads();
+    for (int j = 0; j < nc; ++j) {
+      double u[C::RA], v[C::RB];
+#pragma unroll
+      for (int i = 0; i < C::RA; ++i) u[i] = sU[j * P2 + ta + i * C::TA];
+#pragma unroll
+      for (int k = 0; k < C::RB; ++k) v[k] = sV[j * P + tb + k * C::TB];
+#pragma unroll
+      for (int i = 0; i < C::RA; ++i)
+#pragma unroll
+        for (int k = 0; k < C::RB; ++k) acc[i][k] = fma(u[i], v[k], acc[i][k]);
+    }
+    __syncthreads();
+  }
+  double* out = mom + (size_t)t.fout_rank[b] * P * P2;
+#pragma unroll
+  for (int i = 0; i < C::RA; ++i)
+#pragma unroll
+    for (int k = 0; k < C::RB; ++k) out[(ta + i * C::TA) * P + tb + k * C::TB] = acc[i][k];
+}
+
+// ---------------------------------------------------------------- line transforms
+// In-place 1D transform of a P^3 smem cube along axis `ax` (0: n1, 1: n2, 2: n3):
+//   out[n] = sum_k M[n][k] in[k]   (TRANS: out[n] = sum_k M[k][n] in[k])
+template <int P, bool TRANS>
+__device__ __forceinline__ void line_apply(double* cube, const double* M, int ax, int tid, int nt) {
+  for (int line = tid; line < P * P; line += nt) {
+    int u = line / P, v = line % P;
+    size_t base, stride;
+    if (ax == 2) { base = ((size_t)u * P + v) * P; stride = 1; }
+    else if (ax == 1) { base = (size_t)u * P * P + v; stride = P; }
+    else { base = (size_t)u * P + v; stride = (size_t)P * P; }
+    double in[P];
+#pragma unroll
+    for (int k = 0; k < P; ++k) in[k] = cube[base + k * stride];
+#pragma unroll 1
+    for (int nn = 0; nn < P; ++nn) {
+      double s = 0.0;
+#pragma unroll
+      for (int k = 0; k < P; ++k) s = fma(TRANS ? M[k * P + nn] : M[nn * P + k], in[k], s);
+      cube[base + nn * stride] = s;
+    }
+  }
+}
+
+// c2p: mu(P) += sum over non-leaf children C of (A_sx (x) A_sy (x) A_sz) mu(C)
+template <int P>
+__global__ void __launch_bounds__(P* P) k_c2p(DevTree t, const int32_t* __restrict__ boxes, const double* __restrict__ A,
+                                              double* __restrict__ mom) {
+  constexpr int P2 = P * P, P3 = P2 * P, NT = P2;
+  extern __shared__ double sm[];
+  double* cube = sm;          // P3
+  double* sA = cube + P3;     // [2][P][P]
+  const int b = boxes[blockIdx.x], tid = threadIdx.x;
+  for (int i = tid; i < 2 * P2; i += NT) sA[i] = A[i];
+  double* dst = mom + (size_t)t.fout_rank[b] * P3 + (size_t)tid * P;
+  for (int o = 0; o < 8; ++o) {
+    int ch = t.child[8 * (int64_t)b + o];
+    if (ch < 0 || !(t.flags[ch] & F_OUT)) continue;
+    const double* src = mom + (size_t)t.fout_rank[ch] * P3;
+    __syncthreads();
+    for (int i = tid; i < P3; i += NT) cube[i] = src[i];
+    __syncthreads();
+    // child octant bits: bit2 = x (axis n1), bit1 = y (n2), bit0 = z (n3); side +1 if set
+    line_apply<P, false>(cube, sA + ((o >> 0) & 1) * P2, 2, tid, NT);
+    __syncthreads();
+    line_apply<P, false>(cube, sA + ((o >> 1) & 1) * P2, 1, tid, NT);
+    __syncthreads();
+    line_apply<P, false>(cube, sA + ((o >> 2) & 1) * P2, 0, tid, NT);
+    __syncthreads();
+    for (int k = 0; k < P; ++k) dst[k] += cube[(size_t)tid * P + k];   // this CTA owns mu(P)
+  }
+}
+
+// p2c: Lambda(B) += (A_sx^T (x) A_sy^T (x) A_sz^T) Lambda(parent)
+template <int P>
+__global__ void __launch_bounds__(P* P) k_p2c(DevTree t, const int32_t* __restrict__ boxes, const double* __restrict__ A,
+                                              double* __restrict__ lam) {
+  constexpr int P2 = P * P, P3 = P2 * P, NT = P2;
+  extern __shared__ double sm[];
+  double* cube = sm;
+  double* sA = cube + P3;
+  const int b = boxes[blockIdx.x], tid = threadIdx.x;
+  const int par = t.parent[b];
+  const int o = (int)(t.code[b] & 7);
+  for (int i = tid; i < 2 * P2; i += NT) sA[i] = A[i];
+  const double* src = lam + (size_t)t.exp_rank[par] * P3;
+  for (int i = tid; i < P3; i += NT) cube[i] = src[i];
+  __syncthreads();
+  line_apply<P, true>(cube, sA + ((o >> 0) & 1) * P2, 2, tid, NT);
+  __syncthreads();
+  line_apply<P, true>(cube, sA + ((o >> 1) & 1) * P2, 1, tid, NT);
+  __syncthreads();
+  line_apply<P, true>(cube, sA + ((o >> 2) & 1) * P2, 0, tid, NT);
+  __syncthreads();
+  double* dst = lam + (size_t)t.exp_rank[b] * P3 + (size_t)tid * P;
+#pragma unroll
+  for (int k = 0; k < P; ++k) dst[k] += cube[(size_t)tid * P + k];
+}
+
+// ---------------------------------------------------------------- plane waves
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ double2 cfma(double2 a, double2 b, double2 c) {   // a*b + c
+  return make_double2(fma(a.x, b.x, fma(-a.y, b.y, c.x)), fma(a.x, b.y, fma(a.y, b.x, c.y)));
+}
+__device__ __forceinline__ double2 rcfma(double a, double2 b, double2 c) {
+  return make_double2(fma(a, b.x, c.x), fma(a, b.y, c.y));
+}
+
+__host__ __device__ constexpr size_t phi_doubles(int nf) { return (size_t)2 * (nf + 1) * (2 * nf + 1) * (2 * nf + 1); }
+
+template <int P, int NF, bool MU_SMEM>
+__global__ void __launch_bounds__(256) k_prox2pw(DevTree t, const int32_t* __restrict__ boxes,
+                                                 const double* __restrict__ Qg, const double* __restrict__ mom,
+                                                 double* __restrict__ phi, size_t phi_base, size_t phi_stride) {
+  constexpr int N1 = 2 * NF + 1, NH = NF + 1, P2 = P * P, P3 = P2 * P, NT = 256;
+  extern __shared__ double sm[];
+  double2* sQ = (double2*)sm;               // [N1][P]
+  double2* X1 = sQ + N1 * P;                // [P2]
+  double2* X2 = X1 + P2;                    // [P][N1]
+  double* smu = (double*)(X2 + P * N1);     // [P3] if MU_SMEM
+  const int b = boxes[blockIdx.x], tid = threadIdx.x;
+  const int r = t.fout_rank[b];
+  const double* mu = mom + (size_t)r * P3;
+  double2* out = (double2*)(phi + phi_base + (size_t)(r == 0 ? 0 : r - 1) * phi_stride);
+  for (int i = tid; i < N1 * P; i += NT) sQ[i] = ((const double2*)Qg)[i];
+  if (MU_SMEM)
+    for (int i = tid; i < P3; i += NT) smu[i] = mu[i];
+  __syncthreads();
+  const double* M = MU_SMEM ? smu : mu;
+  for (int m3 = 0; m3 < NH; ++m3) {
+    const double2* q3 = sQ + (m3 + NF) * P;
+    for (int a = tid; a < P2; a += NT) {        // X1[n1 n2] = sum_n3 mu Q[m3][n3]
+      double2 s = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int k = 0; k < P; ++k) s = rcfma(M[(size_t)a * P + k], q3[k], s);
+      X1[a] = s;
+    }
+    __syncthreads();
+    for (int w = tid; w < P * N1; w += NT) {    // X2[n1][m2] = sum_n2 Q[m2][n2] X1[n1 n2]
+      int n1 = w / N1, m2 = w % N1;
+      double2 s = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int k = 0; k < P; ++k) s = cfma(sQ[m2 * P + k], X1[n1 * P + k], s);
+      X2[w] = s;
+    }
+    __syncthreads();
+    double2* o3 = out + (size_t)m3 * N1 * N1;
+    for (int w = tid; w < N1 * N1; w += NT) {   // Phi[m3][m1][m2] = sum_n1 Q[m1][n1] X2[n1][m2]
+      int m1 = w / N1, m2 = w % N1;
+      double2 s = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int k = 0; k < P; ++k) s = cfma(sQ[m1 * P + k], X2[k * N1 + m2], s);
+      o3[w] = s;
+    }
+  }
+}
+
+// Incoming expansion + conversion to Chebyshev coefficients, fused per m3 slice.
+// ROOT: the root box with the window weights W0 (only colleague: itself).
+template <int P, int NF, bool ROOT>
+__global__ void __launch_bounds__(P* P) k_pwlocal(DevTree t, const int32_t* __restrict__ boxes,
+                                                  const double* __restrict__ Qg, const double* __restrict__ Wall,
+                                                  size_t wstride, const double* __restrict__ phi, size_t phi_base,
+                                                  size_t phi_stride, double* __restrict__ lam) {
+  constexpr int N1 = 2 * NF + 1, NH = NF + 1, P2 = P * P, NT = P2;
+  extern __shared__ double sm[];
+  double2* G = (double2*)sm;        // [P][N1]  G[n][m] = conj(Q[m][n])
+  double2* Ps = G + P * N1;         // [N1][N1]
+  double2* Y1 = Ps + N1 * N1;       // [P][N1]
+  __shared__ const double2* src[27];
+  __shared__ int dl[27][3];
+  __shared__ int nsrc;
+  const int b = boxes[blockIdx.x], tid = threadIdx.x;
+  if (!(t.flags[b] & F_IN)) return;   // leaf without incoming: Lambda = 0 before p2c
+  const int l = t.level[b];
+  const double* W = Wall + (ROOT ? 0 : (size_t)l * wstride);
+  for (int i = tid; i < P * N1; i += NT) {
+    int n = i / N1, m = i % N1;
+    double2 qv = ((const double2*)Qg)[m * P + n];
+    G[i] = make_double2(qv.x, -qv.y);
+  }
+  if (tid == 0) {
+    int k2 = 0;
+    for (int k = 0; k < 27; ++k) {
+      int s = t.coll[27 * (int64_t)b + k];
+      if (s < 0 || !(t.flags[s] & F_OUT)) continue;
+      int r = t.fout_rank[s];
+      src[k2] = (const double2*)(phi + phi_base + (size_t)(r == 0 ? 0 : r - 1) * phi_stride);
+      // delta = coords(B) - coords(S) = -(dx, dy, dz) of the colleague slot
+      dl[k2][0] = -(k / 9 - 1);
+      dl[k2][1] = -((k / 3) % 3 - 1);
+      dl[k2][2] = -(k % 3 - 1);
+      ++k2;
+    }
+    nsrc = k2;
+  }
+  __syncthreads();
+  const int ns = nsrc;
+  const int n1 = tid / P, n2 = tid % P;
+  double acc[P];
+#pragma unroll
+  for (int k = 0; k < P; ++k) acc[k] = 0.0;
+  // omega^k, omega = exp(2 pi i / 3): the colleague shift exp(i h_l m.(c_B - c_S)), h_l r_l = 2 pi/3
+  const double2 om[3] = {make_double2(1.0, 0.0), make_double2(-0.5, 0.86602540378443864676),
+                         make_double2(-0.5, -0.86602540378443864676)};
+  for (int m3 = 0; m3 < NH; ++m3) {
+    for (int w = tid; w < N1 * N1; w += NT) {   // Psi slice
+      int m1 = w / N1 - NF, m2 = w % N1 - NF;
+      double2 s = make_double2(0.0, 0.0);
+      for (int k = 0; k < ns; ++k) {
+        double2 v = src[k][(size_t)m3 * N1 * N1 + w];
+        if (ROOT) {
+          s.x += v.x;
+          s.y += v.y;
+        } else {
+          int e = (m1 * dl[k][0] + m2 * dl[k][1] + m3 * dl[k][2]) % 3;
+          e = (e + 3) % 3;
+          s = cfma(v, om[e], s);
+        }
+      }
+      double wt = W[(size_t)m3 * N1 * N1 + w];
+      Ps[w] = make_double2(wt * s.x, wt * s.y);
+    }
+    __syncthreads();
+    for (int w = tid; w < P * N1; w += NT) {    // Y1[n1][m2] = sum_m1 G[n1][m1] Psi[m1][m2]
+      int a = w / N1, m2 = w % N1;
+      double2 s = make_double2(0.0, 0.0);
+#pragma unroll 5
+      for (int k = 0; k < N1; ++k) s = cfma(G[a * N1 + k], Ps[k * N1 + m2], s);
+      Y1[w] = s;
+    }
+    __syncthreads();
+    double2 y = make_double2(0.0, 0.0);          // Y2[n1][n2] = sum_m2 G[n2][m2] Y1[n1][m2]
+#pragma unroll 5
+    for (int k = 0; k < N1; ++k) y = cfma(G[n2 * N1 + k], Y1[n1 * N1 + k], y);
+    const double cw = (m3 == 0) ? 1.0 : 2.0;     // Hermitian half space
+#pragma unroll
+    for (int k = 0; k < P; ++k) {
+      double2 g = G[k * N1 + m3 + NF];
+      acc[k] = fma(cw, y.x * g.x - y.y * g.y, acc[k]);
+    }
+    __syncthreads();
+  }
+  double* dst = lam + (size_t)t.exp_rank[b] * P * P2 + (size_t)tid * P;
+#pragma unroll
+  for (int k = 0; k < P; ++k) dst[k] = acc[k];
+}
+
+// ---------------------------------------------------------------- evaluation
+template <int P>
+__global__ void __launch_bounds__(Cfg<P>::TA * Cfg<P>::TB)
+    k_eval(DevTree t, const int32_t* __restrict__ boxes, const double* __restrict__ lam, double* __restrict__ ufar) {
+  using C = Cfg<P>;
+  constexpr int NT = C::TA * C::TB, P2 = P * P, CH = C::ECH;
+  extern __shared__ double sm[];
+  double* sU = sm;                 // [CH][P2]
+  double* sV = sU + CH * P2;       // [CH][P]
+  double* sT = sV + CH * P;        // [CH][2][P]
+  double* red = sT + CH * 2 * P;   // [NT][CH]
+  __shared__ int2 rg[8];
+  __shared__ int nr_s, tot_s;
+  const int b = boxes[blockIdx.x];
+  if (threadIdx.x == 0) {
+    nr_s = box_ranges<true>(t, b, rg);
+    int tot = 0;
+    for (int r = 0; r < nr_s; ++r) tot += rg[r].y - rg[r].x;
+    tot_s = tot;
+  }
+  __syncthreads();
+  const int nr = nr_s, tot = tot_s;
+  if (tot == 0) return;
+  double cen[3], ih;
+  box_geom(t.code[b], t.level[b], cen, ih);
+  const int tid = threadIdx.x, tb = tid % C::TB, ta = tid / C::TB;
+  double L[C::RA][C::RB];
+  const double* src = lam + (size_t)t.exp_rank[b] * P * P2;
+#pragma unroll
+  for (int i = 0; i < C::RA; ++i)
+#pragma unroll
+    for (int k = 0; k < C::RB; ++k) L[i][k] = src[(ta + i * C::TA) * P + tb + k * C::TB];
+  // reduction uses only complete warps (NT need not be a multiple of 32)
+  const int lane = tid & 31, warp = tid >> 5, nwarp = NT / 32;
+  for (int c0 = 0; c0 < tot; c0 += CH) {
+    const int nc = min(CH, tot - c0);
+    for (int w = tid; w < CH * 3; w += NT) {
+      int j = w / 3, d = w % 3;
+      double T[P];
+      if (j < nc) {
+        int pi = range_point(rg, nr, c0 + j);
+        double x = (d == 0 ? t.xs[pi] : d == 1 ? t.ys[pi] : t.zs[pi]);
+        cheb_vec((x - cen[d]) * ih, T, P, 1.0);
+      } else {
+        for (int n = 0; n < P; ++n) T[n] = 0.0;
+      }
+      double* dst = (d == 2) ? (sV + j * P) : (sT + (j * 2 + d) * P);
+      for (int n = 0; n < P; ++n) dst[n] = T[n];
+    }
+    __syncthreads();
+    for (int w = tid; w < CH * P2; w += NT) {
+      int j = w / P2, a = w % P2;
+      sU[w] = sT[(j * 2) * P + a / P] * sT[(j * 2 + 1) * P + a % P];
+    }
+    __syncthreads();
+    for (int j = 0; j < CH; ++j) {
+      double part = 0.0;
+      if (j < nc) {
+#pragma unroll
+        for (int i = 0; i < C::RA; ++i) {
+          double g = 0.0;
+#pragma unroll
+          for (int k = 0; k < C::RB; ++k) g = fma(L[i][k], sV[j * P + tb + k * C::TB], g);
+          part = fma(g, sU[j * P2 + ta + i * C::TA], part);
+        }
+      }
+      red[tid * CH + j] = part;
+    }
+    __syncthreads();
+    for (int j = warp; j < nc && warp < nwarp; j += nwarp) {
+      double s = 0.0;
+      for (int i = lane; i < NT; i += 32) s += red[i * CH + j];
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+      if (lane == 0) ufar[range_point(rg, nr, c0 + j)] = s;
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------- P2P
+struct ResPoly {
+  double a[25];   // monomial coefficients in s = 2 r^2/r_L^2 - 1
+};
+
+// FULL: root is a leaf -> plain 1/r (no far field).  Otherwise R_L(r) =
+// 1/r - m(r/r_L)/r_L for r < r_L, and the r = 0 (self / coincident) term is
+// -m(0)/r_L = -M_L(0) (Step 5 folded in).
+template <int K, bool FULL>
+__global__ void __launch_bounds__(128) k_p2p(DevTree t, const int32_t* __restrict__ items, int64_t nitems,
+                                             const int32_t* __restrict__ doff, const int32_t* __restrict__ dlist,
+                                             const double* __restrict__ q, const double* __restrict__ ufar,
+                                             const int32_t* __restrict__ perm, double inv_side, ResPoly rp,
+                                             double* __restrict__ unear, double* __restrict__ out) {
+  __shared__ double4 ssrc[4][32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t it = (int64_t)blockIdx.x * 4 + warp;
+  if (it >= nitems) return;
+  const int B = items[2 * it], t0 = items[2 * it + 1];
+  const int nt = min(32, t.end[B] - t0);
+  const int ti = t0 + min(lane, nt - 1);
+  const double xt = t.xs[ti], yt = t.ys[ti], zt = t.zs[ti];
+  double acc = 0.0;
+  for (int e = doff[B]; e < doff[B + 1]; ++e) {
+    const int S = dlist[e];
+    const int L = t.level[S];
+    const double irl = ldexp(1.0, L), two_irl2 = ldexp(2.0, 2 * L), rl2 = ldexp(1.0, -2 * L);
+    for (int s0 = t.start[S]; s0 < t.end[S]; s0 += 32) {
+      const int ns = min(32, t.end[S] - s0);
+      if (lane < ns) {
+        int j = s0 + lane;
+        ssrc[warp][lane] = make_double4(t.xs[j], t.ys[j], t.zs[j], q[j]);
+      }
+      __syncwarp();
+      for (int k = 0; k < ns; ++k) {
+        const double4 sp = ssrc[warp][k];
+        const double dx = xt - sp.x, dy = yt - sp.y, dz = zt - sp.z;
+        const double r2 = fma(dx, dx, fma(dy, dy, dz * dz));
+        if (FULL) {
+          acc += r2 > 0.0 ? sp.w * rsqrt(r2) : 0.0;
+        } else if (r2 < rl2) {
+          const double s = fma(r2, two_irl2, -1.0);
+          double pv = rp.a[K];
+#pragma unroll
+          for (int j = K - 1; j >= 0; --j) pv = fma(pv, s, rp.a[j]);
+          const double rinv = r2 > 0.0 ? rsqrt(r2) : 0.0;
+          acc = fma(sp.w, fma(-pv, irl, rinv), acc);
+        }
+      }
+      __syncwarp();
+    }
+  }
+  if (lane < nt) {
+    const int i = t0 + lane;
+    unear[i] = acc;
+    out[perm[i]] = (ufar[i] + acc) * inv_side;
+  }
+}
+
+// ---------------------------------------------------------------- host launchers
+static DevTree dev_tree(const dmk_plan_s* P) {
+  return DevTree{P->box_code.p, P->box_level.p, P->box_start.p, P->box_end.p, P->box_parent.p,
+                 P->box_child.p, P->box_coll.p, P->box_flags.p, P->fout_rank.p, P->exp_rank.p,
+                 P->xs.p,        P->ys.p,      P->zs.p};
+}
+
+template <class Kern>
+static void set_smem(Kern k, size_t bytes) {
+  if (bytes > 48 * 1024) DMK_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+}
+
+struct Timer {
+  dmk_plan_s* P;
+  cudaEvent_t e0 = nullptr;
+  const char* name = nullptr;
+  Timer(dmk_plan_s* p) : P(p) {}
+  void begin(const char* nm) {
+    if (!P->profile) return;
+    name = nm;
+    DMK_CUDA(cudaEventCreate(&e0));
+    DMK_CUDA(cudaEventRecord(e0, P->stream));
+  }
+  void end() {
+    if (!P->profile) return;
+    cudaEvent_t e1;
+    DMK_CUDA(cudaEventCreate(&e1));
+    DMK_CUDA(cudaEventRecord(e1, P->stream));
+    DMK_CUDA(cudaEventSynchronize(e1));
+    float ms = 0;
+    DMK_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    bool found = false;
+    for (auto& pr : P->timings)
+      if (std::strcmp(pr.first, name) == 0) { pr.second += ms; found = true; }
+    if (!found) P->timings.push_back({name, (double)ms});
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+  }
+};
+
+template <int P, int NF, int NF0>
+static void run_eval(dmk_plan_s* PL) {
+  using C = Cfg<P>;
+  cudaStream_t s = PL->stream;
+  const Tables& T = *PL->tab;
+  DevTree dt = dev_tree(PL);
+  const auto& th = PL->th;
+  const int nl = th.nlevels;
+  constexpr int P3 = P * P * P;
+  Timer tm(PL);
+  const int64_t n = PL->n;
+  if (nl > 1) {
+    // ---- Step 2: upward pass
+    tm.begin("anterp");
+    DMK_CUDA(cudaMemsetAsync(PL->mom.p, 0, PL->mom.bytes(), s));
+    {
+      constexpr int NT = C::TA * C::TB;
+      size_t sm = sizeof(double) * (C::CH * P * P + C::CH * P + C::CH * 2 * P);
+      set_smem(k_anterp<P>, sm);
+      if (PL->nfout) k_anterp<P><<<(int)PL->nfout, NT, sm, s>>>(dt, PL->fout_list.p, PL->q.p, PL->mom.p);
+      DMK_LAUNCH_CHECK();
+    }
+    tm.end();
+    tm.begin("c2p");
+    {
+      size_t sm = sizeof(double) * (P3 + 2 * P * P);
+      set_smem(k_c2p<P>, sm);
+      for (int l = nl - 2; l >= 0; --l) {
+        int64_t a = th.fout_off[l], b = th.fout_off[l + 1];
+        if (b > a) k_c2p<P><<<(int)(b - a), P * P, sm, s>>>(dt, PL->fout_list.p + a, T.dA, PL->mom.p);
+        DMK_LAUNCH_CHECK();
+      }
+    }
+    tm.end();
+    // ---- Step 3: downward pass
+    tm.begin("prox2pw");
+    {
+      constexpr size_t base_sm1 = sizeof(double2) * ((2 * NF + 1) * P + P * P + P * (2 * NF + 1));
+      constexpr bool MU1 = base_sm1 + sizeof(double) * P3 <= 200 * 1024;
+      size_t sm1 = base_sm1 + (MU1 ? sizeof(double) * P3 : 0);
+      constexpr size_t base_sm0 = sizeof(double2) * ((2 * NF0 + 1) * P + P * P + P * (2 * NF0 + 1));
+      constexpr bool MU0 = base_sm0 + sizeof(double) * P3 <= 200 * 1024;
+      size_t sm0 = base_sm0 + (MU0 ? sizeof(double) * P3 : 0);
+      set_smem(k_prox2pw<P, NF0, MU0>, sm0);
+      set_smem(k_prox2pw<P, NF, MU1>, sm1);
+      k_prox2pw<P, NF0, MU0><<<1, 256, sm0, s>>>(dt, PL->fout_list.p, T.dQ0, PL->mom.p, PL->phi.p, 0, 0);
+      DMK_LAUNCH_CHECK();
+      if (PL->nfout > 1)
+        k_prox2pw<P, NF, MU1><<<(int)(PL->nfout - 1), 256, sm1, s>>>(dt, PL->fout_list.p + 1, T.dQ1, PL->mom.p,
+                                                                    PL->phi.p, PL->phi_size0, PL->phi_size1);
+      DMK_LAUNCH_CHECK();
+    }
+    tm.end();
+    tm.begin("pwlocal");
+    {
+      size_t sm0 = sizeof(double2) * (2 * P * (2 * NF0 + 1) + (2 * NF0 + 1) * (2 * NF0 + 1));
+      size_t sm1 = sizeof(double2) * (2 * P * (2 * NF + 1) + (2 * NF + 1) * (2 * NF + 1));
+      set_smem(k_pwlocal<P, NF0, true>, sm0);
+      set_smem(k_pwlocal<P, NF, false>, sm1);
+      // root: exp rank 0, F_out rank 0
+      k_pwlocal<P, NF0, true><<<1, P * P, sm0, s>>>(dt, PL->exp_list.p, T.dQ0, T.dW0, 0, PL->phi.p, 0, 0,
+                                                    PL->lam.p);
+      DMK_LAUNCH_CHECK();
+      if (PL->nexp > 1)
+        k_pwlocal<P, NF, false><<<(int)(PL->nexp - 1), P * P, sm1, s>>>(
+            dt, PL->exp_list.p + 1, T.dQ1, T.dW, T.wstride, PL->phi.p, PL->phi_size0, PL->phi_size1, PL->lam.p);
+      DMK_LAUNCH_CHECK();
+    }
+    tm.end();
+    tm.begin("p2c");
+    {
+      size_t sm = sizeof(double) * (P3 + 2 * P * P);
+      set_smem(k_p2c<P>, sm);
+      for (int l = 1; l < nl; ++l) {
+        int64_t a = th.exp_off[l], b = th.exp_off[l + 1];
+        if (b > a) k_p2c<P><<<(int)(b - a), P * P, sm, s>>>(dt, PL->exp_list.p + a, T.dA, PL->lam.p);
+        DMK_LAUNCH_CHECK();
+      }
+    }
+    tm.end();
+    tm.begin("eval");
+    {
+      constexpr int NT = C::TA * C::TB;
+      size_t sm = sizeof(double) * (C::ECH * P * P + C::ECH * P + C::ECH * 2 * P + NT * C::ECH);
+      set_smem(k_eval<P>, sm);
+      if (PL->nexp) k_eval<P><<<(int)PL->nexp, NT, sm, s>>>(dt, PL->exp_list.p, PL->lam.p, PL->ufar.p);
+      DMK_LAUNCH_CHECK();
+    }
+    tm.end();
+  } else {
+    DMK_CUDA(cudaMemsetAsync(PL->ufar.p, 0, n * sizeof(double), s));
+  }
+}
+
+// P2P dispatch on the residual-polynomial degree
+template <bool FULL>
+static void run_p2p_deg(dmk_plan_s* PL, double* out, const ResPoly& rp, int K) {
+  DevTree dt = dev_tree(PL);
+  int nb = (int)((PL->np2p + 3) / 4);
+  if (nb == 0) return;
+#define DMK_P2P_CASE(KK)                                                                                    \
+  case KK:                                                                                                  \
+    k_p2p<KK, FULL><<<nb, 128, 0, PL->stream>>>(dt, PL->p2p_items.p, PL->np2p, PL->dlist_off.p, PL->dlist.p, \
+                                                 PL->q.p, PL->ufar.p, PL->perm.p, 1.0 / PL->side, rp,       \
+                                                 PL->unear.p, out);                                         \
+    break;
+  switch (K) {
+    DMK_P2P_CASE(4) DMK_P2P_CASE(6) DMK_P2P_CASE(8) DMK_P2P_CASE(10) DMK_P2P_CASE(12) DMK_P2P_CASE(14)
+    DMK_P2P_CASE(16) DMK_P2P_CASE(18) DMK_P2P_CASE(20) DMK_P2P_CASE(22) DMK_P2P_CASE(24)
+    default: fail(DMK_ERR_UNSUPPORTED, "residual polynomial degree out of range");
+  }
+#undef DMK_P2P_CASE
+  DMK_LAUNCH_CHECK();
+}
+
+void eval_plan(dmk_plan_s* PL, const double* dcharges, double* dout) {
+  cudaStream_t s = PL->stream;
+  PL->timings.clear();
+  Timer tm(PL);
+  tm.begin("gather");
+  k_gather_q<<<(int)((PL->n + 255) / 256), 256, 0, s>>>(dcharges, PL->perm.p, PL->n, PL->q.p);
+  DMK_LAUNCH_CHECK();
+  tm.end();
+  switch (PL->tab->p) {
+    case 9: run_eval<9, 6, 10>(PL); break;
+    case 18: run_eval<18, 12, 19>(PL); break;
+    case 28: run_eval<28, 19, 28>(PL); break;
+    default: fail(DMK_ERR_UNSUPPORTED, "unsupported Chebyshev order");
+  }
+  ResPoly rp{};
+  const auto& poly = PL->tab->respoly;
+  int K = (int)poly.size() - 1;
+  for (int k = 0; k <= K && k < 25; ++k) rp.a[k] = poly[k];
+  tm.begin("p2p");
+  if (PL->th.nlevels == 1) run_p2p_deg<true>(PL, dout, rp, K);
+  else run_p2p_deg<false>(PL, dout, rp, K);
+  tm.end();
+}
+
+}  // namespace dmk

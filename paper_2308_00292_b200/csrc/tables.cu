@@ -1,0 +1,352 @@
+// tables.cu -- Step 1 of the DMK algorithm ("Precomputation"):
+// the per-precision constants and 1D operator matrices the device kernels use.
+// Host code, computed once per precision and cached.  This is an independent
+// implementation (it shares nothing with oracle/); the parity tests compare the
+// device results against the oracle.
+//
+//   PSWF psi_0^c (App. A.5, Eq. A.15): lowest eigenvector of the prolate
+//     differential operator in the normalised Legendre basis (symmetric
+//     tridiagonal), solved with cyclic Jacobi rotations.
+//   Difference-kernel weights w_{l,m} = (h_l/2pi)^3 Dhat_l(h_l |m|)  (Eqs. 3.37, 3.68)
+//   Root window weights (W_0 + D_0 = M_1 windowed by the truncated kernel, Sec. 4.7)
+//   Q = E V^{-T}: Chebyshev moments -> outgoing plane waves (T_prox2pw, Eq. 3.42)
+//     and conj(Q)^T = V^{-1} E: incoming plane waves -> Chebyshev coefficients
+//     (T_pw2poly, Eqs. 3.43-3.44)
+//   A_s: Chebyshev re-expansion T_n(x/2 + s/2) = sum_k A_s[n][k] T_k(x) which gives
+//     both T_c2p in moment form (Lemma 2.2) and T_p2c = A_s^T (Lemma 2.3)
+//   Residual polynomial: r_L M_L(r) = m(r/r_L), m(t) = Phi(t)/t, fitted as a
+//     polynomial in s = 2 t^2 - 1 ("piecewise polynomial approximation ... Estrin",
+//     PAPER.md:2002-2008), so R_L(r) = 1/r - m(r/r_L)/r_L for r < r_L (Eq. 3.66).
+#include <cmath>
+#include <map>
+#include <mutex>
+
+#include "common.cuh"
+
+namespace dmk {
+namespace {
+
+constexpr double PI = 3.14159265358979323846;
+
+// Table 1: eps, c, N_1, p
+struct Row {
+  double eps, c;
+  int N1, p;
+};
+const Row TABLE1[] = {
+    {1e-3, 7.2462000846862793, 13, 9},
+    {1e-6, 13.739999771118164, 25, 18},
+    {1e-9, 20.736000061035156, 39, 28},
+};
+
+// ---------------------------------------------------------------- PSWF
+struct Pswf {
+  double c = 0;
+  std::vector<double> a;  // plain Legendre coefficients, degree 0..nmax
+  double psi0 = 0, c0 = 0, c2 = 0;
+
+  static void legendre_all(double x, int nmax, std::vector<double>& P) {
+    P.resize(nmax + 2);
+    P[0] = 1.0;
+    P[1] = x;
+    for (int n = 1; n <= nmax; ++n) P[n + 1] = ((2.0 * n + 1.0) * x * P[n] - n * P[n - 1]) / (n + 1.0);
+  }
+  double eval(double x) const {  // truncated to 0 outside [-1, 1]
+    if (std::fabs(x) > 1.0) return 0.0;
+    std::vector<double> P;
+    legendre_all(x, (int)a.size(), P);
+    double s = 0;
+    for (size_t n = 0; n < a.size(); n += 2) s += a[n] * P[n];
+    return s;
+  }
+  double integral0(double t) const {  // int_0^t psi, t in [0,1]
+    std::vector<double> P;
+    legendre_all(t, (int)a.size(), P);
+    double s = a[0] * t;
+    for (size_t n = 2; n < a.size(); n += 2) s += a[n] * (P[n + 1] - P[n - 1]) / (2.0 * n + 1.0);
+    return s;
+  }
+  double Phi(double t) const { return t >= 1.0 ? 1.0 : integral0(t) / c0; }
+};
+
+void jacobi_lowest(int m, std::vector<double>& A, std::vector<double>& vec) {
+  // cyclic Jacobi on a dense symmetric m x m matrix; returns the eigenvector of the
+  // smallest eigenvalue.
+  std::vector<double> V(m * m, 0.0);
+  for (int i = 0; i < m; ++i) V[i * m + i] = 1.0;
+  for (int sweep = 0; sweep < 100; ++sweep) {
+    double off = 0, tot = 0;
+    for (int i = 0; i < m; ++i)
+      for (int j = 0; j < m; ++j) {
+        tot += A[i * m + j] * A[i * m + j];
+        if (i != j) off += A[i * m + j] * A[i * m + j];
+      }
+    if (off <= 1e-32 * tot) break;
+    for (int p = 0; p < m - 1; ++p)
+      for (int q = p + 1; q < m; ++q) {
+        double apq = A[p * m + q];
+        if (std::fabs(apq) < 1e-300) continue;
+        double app = A[p * m + p], aqq = A[q * m + q];
+        double theta = (aqq - app) / (2.0 * apq);
+        double t = (theta >= 0 ? 1.0 : -1.0) / (std::fabs(theta) + std::sqrt(theta * theta + 1.0));
+        double cs = 1.0 / std::sqrt(t * t + 1.0), sn = t * cs;
+        for (int k = 0; k < m; ++k) {  // A <- J^T A J
+          double akp = A[k * m + p], akq = A[k * m + q];
+          A[k * m + p] = cs * akp - sn * akq;
+          A[k * m + q] = sn * akp + cs * akq;
+        }
+        for (int k = 0; k < m; ++k) {
+          double apk = A[p * m + k], aqk = A[q * m + k];
+          A[p * m + k] = cs * apk - sn * aqk;
+          A[q * m + k] = sn * apk + cs * aqk;
+        }
+        for (int k = 0; k < m; ++k) {
+          double vkp = V[k * m + p], vkq = V[k * m + q];
+          V[k * m + p] = cs * vkp - sn * vkq;
+          V[k * m + q] = sn * vkp + cs * vkq;
+        }
+      }
+  }
+  int best = 0;
+  for (int i = 1; i < m; ++i)
+    if (A[i * m + i] < A[best * m + best]) best = i;
+  vec.resize(m);
+  for (int k = 0; k < m; ++k) vec[k] = V[k * m + best];
+}
+
+void gauss_legendre(int n, std::vector<double>& x, std::vector<double>& w) {
+  x.resize(n);
+  w.resize(n);
+  for (int i = 0; i < n; ++i) {
+    double z = std::cos(PI * (i + 0.75) / (n + 0.5)), pp = 0;
+    for (int it = 0; it < 100; ++it) {
+      double p1 = 1, p2 = 0;
+      for (int j = 1; j <= n; ++j) {
+        double p3 = p2;
+        p2 = p1;
+        p1 = ((2.0 * j - 1.0) * z * p2 - (j - 1.0) * p3) / j;
+      }
+      pp = n * (z * p1 - p2) / (z * z - 1.0);
+      double z1 = z;
+      z = z1 - p1 / pp;
+      if (std::fabs(z - z1) < 1e-16) break;
+    }
+    x[i] = z;
+    w[i] = 2.0 / ((1.0 - z * z) * pp * pp);
+  }
+}
+
+Pswf make_pswf(double c) {
+  Pswf P;
+  P.c = c;
+  int nmax = 2 * (int)std::ceil(c) + 60;
+  if (nmax % 2) ++nmax;
+  int m = nmax / 2 + 1;
+  std::vector<double> A(m * m, 0.0);
+  for (int k = 0; k < m; ++k) {
+    double n = 2.0 * k;
+    double b = (2 * n * (n + 1) - 1) / ((2 * n + 3) * (2 * n - 1));   // <Pbar_n, x^2 Pbar_n>
+    A[k * m + k] = n * (n + 1) + c * c * b;
+    if (k + 1 < m) {
+      double a = (n + 1) * (n + 2) / ((2 * n + 3) * std::sqrt((2 * n + 1) * (2 * n + 5)));
+      A[k * m + k + 1] = A[(k + 1) * m + k] = c * c * a;
+    }
+  }
+  std::vector<double> v;
+  jacobi_lowest(m, A, v);
+  P.a.assign(nmax + 1, 0.0);
+  for (int k = 0; k < m; ++k) P.a[2 * k] = v[k] * std::sqrt(2.0 * k + 0.5);   // Pbar -> P
+  if (P.eval(0.0) < 0)
+    for (auto& x : P.a) x = -x;
+  P.psi0 = P.eval(0.0);
+  P.c0 = P.a[0];   // int_0^1 P_n = 0 for even n >= 2
+  std::vector<double> gx, gw;
+  gauss_legendre(120, gx, gw);
+  double s2 = 0;
+  for (int i = 0; i < 120; ++i) {
+    double x = 0.5 * (gx[i] + 1.0);
+    s2 += 0.5 * gw[i] * x * x * P.eval(x);
+  }
+  P.c2 = s2;
+  return P;
+}
+
+// ---------------------------------------------------------------- Chebyshev helpers
+inline double cheb_node(int i, int p) { return std::cos(PI * (i + 0.5) / p); }
+inline double vinv(int n, int i, int p) {   // V^{-1}[n][i] by discrete orthogonality
+  return (n == 0 ? 1.0 : 2.0) / p * std::cos(n * PI * (i + 0.5) / p);
+}
+void cheb_T(double x, int p, std::vector<double>& T) {
+  T.resize(p);
+  T[0] = 1.0;
+  if (p > 1) T[1] = x;
+  for (int n = 2; n < p; ++n) T[n] = 2.0 * x * T[n - 1] - T[n - 2];
+}
+
+// Q[m'][n] = sum_i exp(-i a m x_i) V^{-1}[n][i],  m = m' - nf, a = h s / 2
+void make_Q(int p, int nf, double a, std::vector<double>& Q) {
+  int n1 = 2 * nf + 1;
+  Q.assign((size_t)n1 * p * 2, 0.0);
+  for (int mp = 0; mp < n1; ++mp) {
+    double m = mp - nf;
+    for (int n = 0; n < p; ++n) {
+      double re = 0, im = 0;
+      for (int i = 0; i < p; ++i) {
+        double x = cheb_node(i, p), v = vinv(n, i, p);
+        re += std::cos(a * m * x) * v;
+        im -= std::sin(a * m * x) * v;
+      }
+      Q[(mp * p + n) * 2 + 0] = re;
+      Q[(mp * p + n) * 2 + 1] = im;
+    }
+  }
+}
+
+template <class F>
+void make_weights(int nf, double h, F fhat, double* W) {   // layout [m3'][m1'][m2'], m3' >= 0
+  int n1 = 2 * nf + 1, nh = nf + 1;
+  double scale = std::pow(h / (2.0 * PI), 3);
+  for (int a3 = 0; a3 < nh; ++a3)
+    for (int a1 = 0; a1 < n1; ++a1)
+      for (int a2 = 0; a2 < n1; ++a2) {
+        double m1 = a1 - nf, m2 = a2 - nf, m3 = a3;
+        double k = h * std::sqrt(m1 * m1 + m2 * m2 + m3 * m3);
+        W[((size_t)a3 * n1 + a1) * n1 + a2] = scale * fhat(k);
+      }
+}
+
+void upload(const std::vector<double>& h, double** d) {
+  DMK_CUDA(cudaMalloc((void**)d, h.size() * sizeof(double)));
+  DMK_CUDA(cudaMemcpy(*d, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice));
+}
+
+Tables* build_tables(int kernel, double eps) {
+  if (kernel != DMK_KERNEL_LAPLACE) fail(DMK_ERR_UNSUPPORTED, "only DMK_KERNEL_LAPLACE is implemented");
+  const Row* row = nullptr;
+  for (const Row& r : TABLE1)
+    if (r.eps >= eps * (1 - 1e-9)) row = &r;
+  if (!row) fail(DMK_ERR_UNSUPPORTED, "eps tighter than 1e-9 is not supported");
+  Tables* T = new Tables();
+  T->eps = row->eps;
+  T->c = row->c;
+  T->p = row->p;
+  T->nf = (row->N1 - 1) / 2;
+  T->RT = 1.0 + std::sqrt(3.0);
+  T->P0 = 1.0 + T->RT + 0.5;
+  T->nf0 = (int)std::ceil(2.0 * T->c * T->P0 / (2.0 * PI));
+  const int p = T->p, nf = T->nf, nf0 = T->nf0;
+  Pswf P = make_pswf(T->c);
+  const double c = T->c;
+
+  // plane-wave <-> Chebyshev matrices: h_l r_l = 2 pi / 3 for every l >= 1 (reading R2)
+  make_Q(p, nf, PI / 3.0, T->Q1);
+  make_Q(p, nf0, PI / T->P0, T->Q0);
+
+  // Chebyshev re-expansion A_s
+  T->A.assign(2 * p * p, 0.0);
+  std::vector<double> Tn;
+  for (int si = 0; si < 2; ++si) {
+    double s = si ? 1.0 : -1.0;
+    for (int i = 0; i < p; ++i) {
+      cheb_T(cheb_node(i, p) / 2.0 + s / 2.0, p, Tn);
+      for (int n = 0; n < p; ++n)
+        for (int k = 0; k < p; ++k) T->A[(si * p + n) * p + k] += vinv(k, i, p) * Tn[n];
+    }
+  }
+
+  // difference-kernel weights per level (Eq. 3.68)
+  int n1 = 2 * nf + 1, nh = nf + 1;
+  T->wstride = (size_t)nh * n1 * n1;
+  T->W.assign((LMAX + 1) * T->wstride, 0.0);
+  for (int l = 1; l <= LMAX; ++l) {
+    double rl = std::ldexp(1.0, -l), rl1 = std::ldexp(1.0, -l - 1);
+    double h = 2.0 * PI / (3.0 * rl);
+    auto Dhat = [&](double k) {
+      if (k == 0.0) return 2.0 * PI * P.c2 / P.c0 * (rl * rl - rl1 * rl1);
+      return 4.0 * PI / P.psi0 * (P.eval(k * rl1 / c) - P.eval(k * rl / c)) / (k * k);
+    };
+    make_weights(nf, h, Dhat, &T->W[l * T->wstride]);
+  }
+  // root window: psi(k r_1/c)/psi(0) * 8 pi sin^2(k R_T/2)/k^2
+  {
+    int n10 = 2 * nf0 + 1, nh0 = nf0 + 1;
+    T->W0.assign((size_t)nh0 * n10 * n10, 0.0);
+    double h0 = 2.0 * PI / T->P0, RT = T->RT;
+    auto What = [&](double k) {
+      double G = P.eval(k * 0.5 / c) / P.psi0;
+      if (k == 0.0) return 2.0 * PI * RT * RT;
+      double sn = std::sin(k * RT / 2.0);
+      return G * 8.0 * PI * sn * sn / (k * k);
+    };
+    make_weights(nf0, h0, What, T->W0.data());
+  }
+
+  // residual polynomial in s = 2u - 1, u = t^2:  g(u) = m(sqrt u), m(t) = Phi(t)/t
+  T->m0 = P.psi0 / P.c0;
+  auto g = [&](double u) {
+    if (u <= 0.0) return T->m0;
+    double t = std::sqrt(u);
+    return P.Phi(t) / t;
+  };
+  for (int K = 4; K <= 24; K += 2) {
+    std::vector<double> cc(K + 1, 0.0);   // Chebyshev coefficients in s
+    for (int k = 0; k <= K; ++k) {
+      double sum = 0;
+      for (int j = 0; j <= K; ++j) {
+        double th = PI * (j + 0.5) / (K + 1);
+        sum += g((std::cos(th) + 1.0) / 2.0) * std::cos(k * th);
+      }
+      cc[k] = (k == 0 ? 1.0 : 2.0) / (K + 1) * sum;
+    }
+    // Chebyshev -> monomial in s
+    std::vector<double> mono(K + 1, 0.0), t0(K + 1, 0.0), t1(K + 1, 0.0), t2(K + 1, 0.0);
+    t0[0] = 1.0;
+    t1[1] = 1.0;
+    for (int k = 0; k <= K; ++k) {
+      const std::vector<double>& tk = (k == 0) ? t0 : t1;
+      for (int j = 0; j <= K; ++j) mono[j] += cc[k] * tk[j];
+      if (k >= 1) {   // t2 = 2 s t1 - t0, then shift
+        std::fill(t2.begin(), t2.end(), 0.0);
+        for (int j = 0; j < K; ++j) t2[j + 1] += 2.0 * t1[j];
+        for (int j = 0; j <= K; ++j) t2[j] -= t0[j];
+        t0 = t1;
+        t1 = t2;
+      }
+    }
+    double err = 0;
+    for (int i = 0; i <= 4000; ++i) {
+      double u = i / 4000.0, s = 2.0 * u - 1.0, v = 0;
+      for (int j = K; j >= 0; --j) v = v * s + mono[j];
+      err = std::fmax(err, std::fabs(v - g(u)));
+    }
+    T->respoly = mono;
+    if (err <= 1e-2 * T->eps * T->m0) break;
+  }
+
+  upload(T->Q1, &T->dQ1);
+  upload(T->Q0, &T->dQ0);
+  upload(T->A, &T->dA);
+  upload(T->W, &T->dW);
+  upload(T->W0, &T->dW0);
+  return T;
+}
+
+std::mutex g_mu;
+std::map<std::pair<int, double>, Tables*> g_cache;
+
+}  // namespace
+
+const Tables& get_tables(int kernel, double eps) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  double key_eps = 0;
+  for (const Row& r : TABLE1)
+    if (r.eps >= eps * (1 - 1e-9)) key_eps = r.eps;
+  auto key = std::make_pair(kernel, key_eps);
+  auto it = g_cache.find(key);
+  if (it != g_cache.end()) return *it->second;
+  Tables* T = build_tables(kernel, eps);
+  g_cache[key] = T;
+  return *T;
+}
+
+}  // namespace dmk

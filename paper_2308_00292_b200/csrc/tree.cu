@@ -1,0 +1,660 @@
+// tree.cu -- device-resident adaptive octree and interaction lists
+// (Sec. 3.5 Step 0; Sec. 3.2; lists of
+// Sec. 3.3 / Fig. 7).
+//
+// Everything point- or box-sized runs in CUDA kernels; the host only reads back
+// counts to size the next level's arrays.  Conventions (readings R5-R8 of
+// DESIGN.md) are identical to the oracle's, so the integer structure must match it
+// bit for bit:
+//   root cube lo = per-axis min, side = max extent; q = floor((x - lo) * (2^21/side))
+//   (IEEE-rounded subtract, then multiply: no FMA contraction), 63-bit Morton keys
+//   (x most significant), stable sort; refine a box iff it holds > n_s points and its
+//   level is < LMAX; 2:1 balance over closed-box contact, built bottom-up; keep all
+//   non-leaf boxes and all non-empty leaves, numbered by (level, Morton code).
+#include <chrono>
+
+#include <cub/cub.cuh>
+
+#include "common.cuh"
+
+namespace dmk {
+namespace {
+
+constexpr int TPB = 256;
+inline int nblk(int64_t n, int t = TPB) { return (int)((n + t - 1) / t); }
+
+template <class F>
+void cub_run(cudaStream_t s, F f) {
+  size_t bytes = 0;
+  DMK_CUDA(f(nullptr, bytes));
+  DevBuf<char> tmp;
+  tmp.alloc(bytes ? bytes : 1, s);
+  DMK_CUDA(f(tmp.p, bytes));
+}
+
+__device__ __forceinline__ uint64_t spread3(uint64_t x) {
+  x &= 0x1fffffULL;
+  x = (x | x << 32) & 0x1f00000000ffffULL;
+  x = (x | x << 16) & 0x1f0000ff0000ffULL;
+  x = (x | x << 8) & 0x100f00f00f00f00fULL;
+  x = (x | x << 4) & 0x10c30c30c30c30c3ULL;
+  x = (x | x << 2) & 0x1249249249249249ULL;
+  return x;
+}
+__device__ __forceinline__ uint32_t compact3(uint64_t x) {
+  x &= 0x1249249249249249ULL;
+  x = (x ^ (x >> 2)) & 0x10c30c30c30c30c3ULL;
+  x = (x ^ (x >> 4)) & 0x100f00f00f00f00fULL;
+  x = (x ^ (x >> 8)) & 0x1f0000ff0000ffULL;
+  x = (x ^ (x >> 16)) & 0x1f00000000ffffULL;
+  x = (x ^ (x >> 32)) & 0x1fffffULL;
+  return (uint32_t)x;
+}
+__device__ __forceinline__ uint64_t encode(uint32_t x, uint32_t y, uint32_t z) {
+  return (spread3(x) << 2) | (spread3(y) << 1) | spread3(z);
+}
+__device__ __forceinline__ void decode(uint64_t c, int& x, int& y, int& z) {
+  x = (int)compact3(c >> 2);
+  y = (int)compact3(c >> 1);
+  z = (int)compact3(c);
+}
+
+// binary search for `v` in sorted a[0..n); returns index or -1
+__device__ __forceinline__ int64_t bsearch_u64(const uint64_t* a, int64_t n, uint64_t v) {
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if (a[mid] < v) lo = mid + 1; else hi = mid;
+  }
+  return (lo < n && a[lo] == v) ? lo : -1;
+}
+__device__ __forceinline__ int64_t lower_bound_u64(const uint64_t* a, int64_t n, uint64_t v) {
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if (a[mid] < v) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// ---------------------------------------------------------------- kernels
+__global__ void k_bbox_partial(const double* __restrict__ pts, int64_t n, double* out) {
+  double mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    for (int d = 0; d < 3; ++d) {
+      double v = pts[3 * i + d];
+      mn[d] = fmin(mn[d], v);
+      mx[d] = fmax(mx[d], v);
+    }
+  __shared__ double s[6][TPB];
+  for (int d = 0; d < 3; ++d) {
+    s[d][threadIdx.x] = mn[d];
+    s[3 + d][threadIdx.x] = mx[d];
+  }
+  __syncthreads();
+  for (int w = TPB / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w)
+      for (int d = 0; d < 3; ++d) {
+        s[d][threadIdx.x] = fmin(s[d][threadIdx.x], s[d][threadIdx.x + w]);
+        s[3 + d][threadIdx.x] = fmax(s[3 + d][threadIdx.x], s[3 + d][threadIdx.x + w]);
+      }
+    __syncthreads();
+  }
+  if (threadIdx.x < 6) out[blockIdx.x * 6 + threadIdx.x] = s[threadIdx.x][0];
+}
+
+__global__ void k_keys(const double* __restrict__ pts, int64_t n, double lo0, double lo1, double lo2,
+                       double scale, uint64_t* keys, int32_t* idx) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double lo[3] = {lo0, lo1, lo2};
+  uint32_t q[3];
+  for (int d = 0; d < 3; ++d) {
+    double t = floor(__dmul_rn(__dsub_rn(pts[3 * i + d], lo[d]), scale));
+    t = fmin(fmax(t, 0.0), (double)((1 << NBITS) - 1));
+    q[d] = (uint32_t)t;
+  }
+  keys[i] = encode(q[0], q[1], q[2]);
+  idx[i] = (int32_t)i;
+}
+
+__global__ void k_gather_pts(const double* __restrict__ pts, const int32_t* __restrict__ perm, int64_t n,
+                             double lo0, double lo1, double lo2, double side, double* xs, double* ys,
+                             double* zs) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int64_t j = perm[i];
+  xs[i] = __ddiv_rn(__dsub_rn(pts[3 * j + 0], lo0), side);
+  ys[i] = __ddiv_rn(__dsub_rn(pts[3 * j + 1], lo1), side);
+  zs[i] = __ddiv_rn(__dsub_rn(pts[3 * j + 2], lo2), side);
+}
+
+// level-l box of point a is "big" (> ns points) and a is its first point
+__global__ void k_big(const uint64_t* __restrict__ keys, int64_t n, int l, int ns, uint64_t* codes,
+                      uint8_t* flags) {
+  int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (a >= n) return;
+  int sh = 3 * (NBITS - l);
+  uint64_t c = (sh >= 64) ? 0 : (keys[a] >> sh);
+  bool start = (a == 0) || (((sh >= 64) ? 0 : (keys[a - 1] >> sh)) != c);
+  bool big = (a + ns < n) && ((((sh >= 64) ? 0 : (keys[a + ns] >> sh))) == c);
+  codes[a] = c;
+  flags[a] = (start && big) ? 1 : 0;
+}
+
+// the level-l boxes touching each level-(l+1) box q (8 candidates, clipped)
+__global__ void k_touch(const uint64_t* __restrict__ Bq, int64_t nq, int l, uint64_t* out, uint8_t* flags) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= nq * 8) return;
+  int64_t i = t >> 3;
+  int o = (int)(t & 7);
+  int qx, qy, qz;
+  decode(Bq[i], qx, qy, qz);
+  int q[3] = {qx, qy, qz}, c[3];
+  int n1 = 1 << l;
+  bool ok = true;
+  for (int d = 0; d < 3; ++d) {
+    int lo = (q[d] % 2 == 0) ? q[d] / 2 - 1 : q[d] / 2;
+    c[d] = lo + ((o >> (2 - d)) & 1);
+    ok = ok && c[d] >= 0 && c[d] < n1;
+  }
+  out[t] = ok ? encode(c[0], c[1], c[2]) : 0;
+  flags[t] = ok ? 1 : 0;
+}
+
+// non-empty level-l boxes whose parent is non-leaf
+__global__ void k_nonempty(const uint64_t* __restrict__ keys, int64_t n, int l, const uint64_t* __restrict__ Bp,
+                           int64_t nBp, uint64_t* codes, uint8_t* flags) {
+  int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (a >= n) return;
+  int sh = 3 * (NBITS - l);
+  uint64_t c = keys[a] >> sh;
+  bool start = (a == 0) || ((keys[a - 1] >> sh) != c);
+  codes[a] = c;
+  flags[a] = (start && bsearch_u64(Bp, nBp, c >> 3) >= 0) ? 1 : 0;
+}
+
+__global__ void k_fill_level(int32_t* lev, int64_t a, int64_t b, int l) {
+  int64_t i = a + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < b) lev[i] = l;
+}
+
+struct BoxCtx {
+  const uint64_t* code;
+  const int32_t* level;
+  const int64_t* loff;      // device level offsets [nlevels+1]
+  const uint64_t* B;        // concatenated non-leaf sets
+  const int64_t* boff;      // offsets of B per level [nlevels+1]
+  int nlevels;
+  const uint64_t* keys;
+  int64_t n;
+};
+
+__global__ void k_box_attrs(BoxCtx c, int64_t nbox, int32_t* start, int32_t* end, int32_t* parent,
+                            int32_t* coll, uint8_t* flags) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= nbox) return;
+  int l = c.level[i];
+  uint64_t code = c.code[i];
+  int sh = 3 * (NBITS - l);
+  uint64_t lo = (sh >= 64) ? 0 : (code << sh);
+  uint64_t hiv = (sh >= 64) ? ~0ULL : ((code + 1) << sh);
+  int64_t s = lower_bound_u64(c.keys, c.n, lo);
+  int64_t e = (l == 0) ? c.n : lower_bound_u64(c.keys, c.n, hiv);
+  start[i] = (int32_t)s;
+  end[i] = (int32_t)e;
+  bool leaf = bsearch_u64(c.B + c.boff[l], c.boff[l + 1] - c.boff[l], code) < 0;
+  flags[i] = leaf ? 1 : 0;
+  if (l > 0) {
+    int64_t j = bsearch_u64(c.code + c.loff[l - 1], c.loff[l] - c.loff[l - 1], code >> 3);
+    parent[i] = (int32_t)(j < 0 ? -1 : c.loff[l - 1] + j);
+  } else {
+    parent[i] = -1;
+  }
+  int x, y, z;
+  decode(code, x, y, z);
+  int n1 = 1 << l, k = 0;
+  const uint64_t* lv = c.code + c.loff[l];
+  int64_t nl = c.loff[l + 1] - c.loff[l];
+  for (int dx = -1; dx <= 1; ++dx)
+    for (int dy = -1; dy <= 1; ++dy)
+      for (int dz = -1; dz <= 1; ++dz, ++k) {
+        int xx = x + dx, yy = y + dy, zz = z + dz;
+        int32_t r = -1;
+        if (xx >= 0 && yy >= 0 && zz >= 0 && xx < n1 && yy < n1 && zz < n1) {
+          int64_t j = bsearch_u64(lv, nl, encode(xx, yy, zz));
+          if (j >= 0) r = (int32_t)(c.loff[l] + j);
+        }
+        coll[27 * i + k] = r;
+      }
+}
+
+__global__ void k_children(const uint64_t* code, const int32_t* parent, int64_t nbox, int32_t* child) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= nbox) return;
+  int32_t p = parent[i];
+  if (p >= 0) child[8 * (int64_t)p + (code[i] & 7)] = (int32_t)i;
+}
+
+// flags: bit0 leaf, bit1 F_out, bit2 F_in, bit3 has local expansion
+__global__ void k_flags_out(const int32_t* start, const int32_t* end, int64_t nbox, uint8_t* flags,
+                            uint8_t* fout) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= nbox) return;
+  bool leaf = flags[i] & 1;
+  bool f = !leaf && end[i] > start[i];
+  flags[i] = (uint8_t)((leaf ? 1 : 0) | (f ? 2 : 0));
+  fout[i] = f ? 1 : 0;
+}
+__global__ void k_flags_in(const int32_t* start, const int32_t* end, const int32_t* coll, int64_t nbox,
+                           uint8_t* flags, uint8_t* exp) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= nbox) return;
+  uint8_t f = flags[i];
+  bool nonempty = end[i] > start[i];
+  bool fin = false;
+  if (nonempty)
+    for (int k = 0; k < 27; ++k) {
+      int32_t s = coll[27 * i + k];
+      if (s >= 0 && (flags[s] & 2)) fin = true;
+    }
+  bool e = nonempty && (!(f & 1) || fin);
+  // other threads only read bit 1 (F_out), which this write leaves unchanged
+  flags[i] = (uint8_t)(f | (fin ? 4 : 0) | (e ? 8 : 0));
+  exp[i] = e ? 1 : 0;
+}
+
+__global__ void k_rank(const int32_t* scan, const uint8_t* sel, int64_t nbox, int32_t* rank) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= nbox) return;
+  rank[i] = sel[i] ? scan[i] : -1;
+}
+
+// direct lists: pass 0 counts, pass 1 fills
+template <bool FILL>
+__global__ void k_dlist(const int32_t* start, const int32_t* end, const int32_t* parent, const int32_t* child,
+                        const int32_t* coll, const uint8_t* flags, const uint64_t* code, const int32_t* level,
+                        int64_t nbox, int32_t* cnt, const int32_t* off, int32_t* items) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= nbox) return;
+  int n_ = 0;
+  int64_t base = FILL ? off[i] : 0;
+  bool is_target = (flags[i] & 1) && end[i] > start[i];
+  if (is_target) {
+    int64_t a = i;
+    while (a >= 0) {   // B and its ancestors: leaf colleagues at that level
+      for (int k = 0; k < 27; ++k) {
+        int32_t s = coll[27 * a + k];
+        if (s >= 0 && (flags[s] & 1) && end[s] > start[s]) {
+          if (FILL) items[base + n_] = s;
+          ++n_;
+        }
+      }
+      a = parent[a];
+    }
+    int bx, by, bz;
+    decode(code[i], bx, by, bz);
+    for (int k = 0; k < 27; ++k) {   // fine neighbours: leaves one level down touching B
+      int32_t s = coll[27 * i + k];
+      if (s < 0 || (flags[s] & 1)) continue;
+      for (int o = 0; o < 8; ++o) {
+        int32_t ch = child[8 * (int64_t)s + o];
+        if (ch < 0 || !(flags[ch] & 1) || end[ch] <= start[ch]) continue;
+        int cx, cy, cz;
+        decode(code[ch], cx, cy, cz);
+        if (cx >= 2 * bx - 1 && cx <= 2 * bx + 2 && cy >= 2 * by - 1 && cy <= 2 * by + 2 &&
+            cz >= 2 * bz - 1 && cz <= 2 * bz + 2) {
+          if (FILL) items[base + n_] = ch;
+          ++n_;
+        }
+      }
+    }
+  }
+  if (!FILL) cnt[i] = n_;
+}
+
+// P2P work items: (leaf, first target) for every chunk of 32 targets
+__global__ void k_p2p_count(const int32_t* start, const int32_t* end, const uint8_t* flags, int64_t nbox,
+                            int32_t* cnt) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= nbox) return;
+  int n_ = end[i] - start[i];
+  cnt[i] = ((flags[i] & 1) && n_ > 0) ? (n_ + 31) / 32 : 0;
+}
+__global__ void k_p2p_fill(const int32_t* start, const int32_t* cnt, const int32_t* off, int64_t nbox,
+                           int32_t* items) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= nbox) return;
+  for (int k = 0; k < cnt[i]; ++k) {
+    items[2 * (off[i] + k)] = (int32_t)i;
+    items[2 * (off[i] + k) + 1] = start[i] + 32 * k;
+  }
+}
+
+// ---------------------------------------------------------------- host helpers
+int64_t select_flagged(cudaStream_t s, const uint64_t* in, const uint8_t* flags, int64_t n,
+                       DevBuf<uint64_t>& out) {
+  DevBuf<uint64_t> tmp;
+  tmp.alloc(n ? n : 1, s);
+  DevBuf<int64_t> cnt;
+  cnt.alloc(1, s);
+  cub_run(s, [&](void* t, size_t& b) {
+    return cub::DeviceSelect::Flagged(t, b, in, flags, tmp.p, cnt.p, n, s);
+  });
+  int64_t h = 0;
+  DMK_CUDA(cudaMemcpyAsync(&h, cnt.p, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  DMK_CUDA(cudaStreamSynchronize(s));
+  out.alloc(h ? h : 1, s);
+  if (h) DMK_CUDA(cudaMemcpyAsync(out.p, tmp.p, h * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
+  return h;
+}
+
+// sort + unique of n codes with `bits` significant bits
+int64_t sort_unique(cudaStream_t s, const uint64_t* in, int64_t n, int bits, DevBuf<uint64_t>& out) {
+  if (n == 0) {
+    out.alloc(1, s);
+    return 0;
+  }
+  DevBuf<uint64_t> sorted;
+  sorted.alloc(n, s);
+  cub_run(s, [&](void* t, size_t& b) {
+    return cub::DeviceRadixSort::SortKeys(t, b, in, sorted.p, (int64_t)n, 0, bits > 0 ? bits : 1, s);
+  });
+  DevBuf<uint64_t> tmp;
+  tmp.alloc(n, s);
+  DevBuf<int64_t> cnt;
+  cnt.alloc(1, s);
+  cub_run(s, [&](void* t, size_t& b) {
+    return cub::DeviceSelect::Unique(t, b, sorted.p, tmp.p, cnt.p, (int64_t)n, s);
+  });
+  int64_t h = 0;
+  DMK_CUDA(cudaMemcpyAsync(&h, cnt.p, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  DMK_CUDA(cudaStreamSynchronize(s));
+  out.alloc(h, s);
+  DMK_CUDA(cudaMemcpyAsync(out.p, tmp.p, h * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
+  return h;
+}
+
+void exclusive_scan(cudaStream_t s, const int32_t* in, int32_t* out, int64_t n) {
+  cub_run(s, [&](void* t, size_t& b) { return cub::DeviceScan::ExclusiveSum(t, b, in, out, n, s); });
+}
+void exclusive_scan_u8(cudaStream_t s, const uint8_t* in, int32_t* out, int64_t n) {
+  cub::TransformInputIterator<int32_t, cub::CastOp<int32_t>, const uint8_t*> it(in, cub::CastOp<int32_t>());
+  cub_run(s, [&](void* t, size_t& b) { return cub::DeviceScan::ExclusiveSum(t, b, it, out, n, s); });
+}
+
+template <class T>
+T d2h_at(cudaStream_t s, const T* p) {
+  T h;
+  DMK_CUDA(cudaMemcpyAsync(&h, p, sizeof(T), cudaMemcpyDeviceToHost, s));
+  DMK_CUDA(cudaStreamSynchronize(s));
+  return h;
+}
+
+}  // namespace
+
+// Build the tree of plan P from n points (device pointer, row-major n x 3).
+void build_tree(dmk_plan_s* P, const double* dpts) {
+  cudaStream_t s = P->stream;
+  const int64_t n = P->n;
+  const int ns = P->ns;
+  // phase timing (DMK_PROFILE=1): synchronising wall-clock marks, plan time only
+  auto t_last = std::chrono::steady_clock::now();
+  auto mark = [&](const char* name) {
+    if (!P->profile) return;
+    cudaStreamSynchronize(s);
+    auto now = std::chrono::steady_clock::now();
+    P->tree_timings.push_back({name, std::chrono::duration<double, std::milli>(now - t_last).count()});
+    t_last = now;
+  };
+
+  // ---- root cube (reading R5)
+  {
+    int nb = std::min(nblk(n), 1024);
+    DevBuf<double> part;
+    part.alloc(6 * nb, s);
+    k_bbox_partial<<<nb, TPB, 0, s>>>(dpts, n, part.p);
+    DMK_LAUNCH_CHECK();
+    std::vector<double> h(6 * nb);
+    DMK_CUDA(cudaMemcpyAsync(h.data(), part.p, h.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+    DMK_CUDA(cudaStreamSynchronize(s));
+    double mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (int b = 0; b < nb; ++b)
+      for (int d = 0; d < 3; ++d) {
+        mn[d] = std::fmin(mn[d], h[6 * b + d]);
+        mx[d] = std::fmax(mx[d], h[6 * b + 3 + d]);
+      }
+    double ext = 0;
+    for (int d = 0; d < 3; ++d) {
+      P->lo[d] = mn[d];
+      ext = std::fmax(ext, mx[d] - mn[d]);
+    }
+    if (!std::isfinite(ext)) fail(DMK_ERR_ARG, "points contain non-finite coordinates");
+    P->side = ext > 0 ? ext : 1.0;
+  }
+  const double scale = (double)(1 << NBITS) / P->side;
+  mark("bbox");
+
+  // ---- Morton keys, stable sort, sorted normalised coordinates
+  {
+    DevBuf<uint64_t> k0;
+    DevBuf<int32_t> i0;
+    k0.alloc(n, s);
+    i0.alloc(n, s);
+    k_keys<<<nblk(n), TPB, 0, s>>>(dpts, n, P->lo[0], P->lo[1], P->lo[2], scale, k0.p, i0.p);
+    DMK_LAUNCH_CHECK();
+    P->keys.alloc(n, s);
+    P->perm.alloc(n, s);
+    cub_run(s, [&](void* t, size_t& b) {
+      return cub::DeviceRadixSort::SortPairs(t, b, k0.p, P->keys.p, i0.p, P->perm.p, (int64_t)n, 0, 3 * NBITS, s);
+    });
+    P->xs.alloc(n, s);
+    P->ys.alloc(n, s);
+    P->zs.alloc(n, s);
+    k_gather_pts<<<nblk(n), TPB, 0, s>>>(dpts, P->perm.p, n, P->lo[0], P->lo[1], P->lo[2], P->side, P->xs.p,
+                                         P->ys.p, P->zs.p);
+    DMK_LAUNCH_CHECK();
+  }
+
+  mark("sort");
+  // ---- unbalanced refinement: U[l] = level-l boxes with > ns points
+  std::vector<DevBuf<uint64_t>> U(LMAX);
+  std::vector<int64_t> nU(LMAX, 0);
+  int ltop = -1;
+  {
+    DevBuf<uint64_t> codes;
+    DevBuf<uint8_t> flags;
+    codes.alloc(n, s);
+    flags.alloc(n, s);
+    for (int l = 0; l < LMAX; ++l) {
+      k_big<<<nblk(n), TPB, 0, s>>>(P->keys.p, n, l, ns, codes.p, flags.p);
+      DMK_LAUNCH_CHECK();
+      nU[l] = select_flagged(s, codes.p, flags.p, n, U[l]);
+      if (nU[l] == 0) break;
+      ltop = l;
+    }
+  }
+
+  mark("refine");
+  // ---- 2:1 balance, bottom-up: B[l] = U[l] + level-l boxes touching B[l+1]
+  std::vector<DevBuf<uint64_t>> B(ltop + 1);
+  std::vector<int64_t> nB(ltop + 1, 0);
+  if (ltop >= 0) {
+    B[ltop].alloc(nU[ltop], s);
+    DMK_CUDA(cudaMemcpyAsync(B[ltop].p, U[ltop].p, nU[ltop] * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
+    nB[ltop] = nU[ltop];
+    for (int l = ltop - 1; l >= 0; --l) {
+      int64_t nc = nU[l] + 8 * nB[l + 1];
+      DevBuf<uint64_t> cand;
+      DevBuf<uint8_t> cf;
+      cand.alloc(nc, s);
+      cf.alloc(nc, s);
+      if (nU[l]) {
+        DMK_CUDA(cudaMemcpyAsync(cand.p, U[l].p, nU[l] * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
+        DMK_CUDA(cudaMemsetAsync(cf.p, 1, nU[l], s));
+      }
+      k_touch<<<nblk(8 * nB[l + 1]), TPB, 0, s>>>(B[l + 1].p, nB[l + 1], l, cand.p + nU[l], cf.p + nU[l]);
+      DMK_LAUNCH_CHECK();
+      DevBuf<uint64_t> valid;
+      int64_t nv = select_flagged(s, cand.p, cf.p, nc, valid);
+      nB[l] = sort_unique(s, valid.p, nv, 3 * l, B[l]);
+    }
+  }
+  const int nlevels = ltop + 2;
+  mark("balance");
+  P->th.nlevels = nlevels;
+
+  // ---- box sets per level: E_l = B_l + non-empty children of B_{l-1}
+  std::vector<DevBuf<uint64_t>> E(nlevels);
+  std::vector<int64_t> nE(nlevels, 0);
+  E[0].alloc(1, s);
+  DMK_CUDA(cudaMemsetAsync(E[0].p, 0, sizeof(uint64_t), s));
+  nE[0] = 1;
+  {
+    DevBuf<uint64_t> codes;
+    DevBuf<uint8_t> flags;
+    codes.alloc(n, s);
+    flags.alloc(n, s);
+    for (int l = 1; l < nlevels; ++l) {
+      k_nonempty<<<nblk(n), TPB, 0, s>>>(P->keys.p, n, l, B[l - 1].p, nB[l - 1], codes.p, flags.p);
+      DMK_LAUNCH_CHECK();
+      DevBuf<uint64_t> ne;
+      int64_t nne = select_flagged(s, codes.p, flags.p, n, ne);
+      int64_t nb_l = (l <= ltop) ? nB[l] : 0;
+      DevBuf<uint64_t> cat;
+      cat.alloc(nne + nb_l, s);
+      if (nne) DMK_CUDA(cudaMemcpyAsync(cat.p, ne.p, nne * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
+      if (nb_l) DMK_CUDA(cudaMemcpyAsync(cat.p + nne, B[l].p, nb_l * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
+      nE[l] = sort_unique(s, cat.p, nne + nb_l, 3 * l, E[l]);
+    }
+  }
+
+  mark("boxsets");
+  // ---- global box arrays
+  auto& th = P->th;
+  th.level_off.assign(nlevels + 1, 0);
+  for (int l = 0; l < nlevels; ++l) th.level_off[l + 1] = th.level_off[l] + nE[l];
+  const int64_t nbox = P->nbox = th.level_off[nlevels];
+  P->box_code.alloc(nbox, s);
+  P->box_level.alloc(nbox, s);
+  for (int l = 0; l < nlevels; ++l) {
+    DMK_CUDA(cudaMemcpyAsync(P->box_code.p + th.level_off[l], E[l].p, nE[l] * sizeof(uint64_t),
+                             cudaMemcpyDeviceToDevice, s));
+    k_fill_level<<<nblk(nE[l]), TPB, 0, s>>>(P->box_level.p, th.level_off[l], th.level_off[l + 1], l);
+    DMK_LAUNCH_CHECK();
+  }
+  std::vector<int64_t> boff(nlevels + 1, 0);
+  for (int l = 0; l < nlevels; ++l) boff[l + 1] = boff[l] + ((l <= ltop) ? nB[l] : 0);
+  DevBuf<uint64_t> Bcat;
+  Bcat.alloc(boff[nlevels] ? boff[nlevels] : 1, s);
+  for (int l = 0; l <= ltop; ++l)
+    if (nB[l])
+      DMK_CUDA(cudaMemcpyAsync(Bcat.p + boff[l], B[l].p, nB[l] * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
+  DevBuf<int64_t> dloff, dboff;
+  dloff.alloc(nlevels + 1, s);
+  dboff.alloc(nlevels + 1, s);
+  DMK_CUDA(cudaMemcpyAsync(dloff.p, th.level_off.data(), (nlevels + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+  DMK_CUDA(cudaMemcpyAsync(dboff.p, boff.data(), (nlevels + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+
+  P->box_start.alloc(nbox, s);
+  P->box_end.alloc(nbox, s);
+  P->box_parent.alloc(nbox, s);
+  P->box_coll.alloc(27 * nbox, s);
+  P->box_child.alloc(8 * nbox, s);
+  P->box_flags.alloc(nbox, s);
+  BoxCtx ctx{P->box_code.p, P->box_level.p, dloff.p, Bcat.p, dboff.p, nlevels, P->keys.p, n};
+  k_box_attrs<<<nblk(nbox), TPB, 0, s>>>(ctx, nbox, P->box_start.p, P->box_end.p, P->box_parent.p,
+                                         P->box_coll.p, P->box_flags.p);
+  DMK_LAUNCH_CHECK();
+  DMK_CUDA(cudaMemsetAsync(P->box_child.p, 0xff, 8 * nbox * sizeof(int32_t), s));
+  k_children<<<nblk(nbox), TPB, 0, s>>>(P->box_code.p, P->box_parent.p, nbox, P->box_child.p);
+  DMK_LAUNCH_CHECK();
+
+  mark("boxattrs");
+  // ---- flags, ranks, compact lists
+  DevBuf<uint8_t> fsel, esel;
+  fsel.alloc(nbox, s);
+  esel.alloc(nbox, s);
+  k_flags_out<<<nblk(nbox), TPB, 0, s>>>(P->box_start.p, P->box_end.p, nbox, P->box_flags.p, fsel.p);
+  DMK_LAUNCH_CHECK();
+  k_flags_in<<<nblk(nbox), TPB, 0, s>>>(P->box_start.p, P->box_end.p, P->box_coll.p, nbox, P->box_flags.p,
+                                        esel.p);
+  DMK_LAUNCH_CHECK();
+  DevBuf<int32_t> fscan, escan;
+  fscan.alloc(nbox + 1, s);
+  escan.alloc(nbox + 1, s);
+  exclusive_scan_u8(s, fsel.p, fscan.p, nbox);
+  exclusive_scan_u8(s, esel.p, escan.p, nbox);
+  P->fout_rank.alloc(nbox, s);
+  P->exp_rank.alloc(nbox, s);
+  k_rank<<<nblk(nbox), TPB, 0, s>>>(fscan.p, fsel.p, nbox, P->fout_rank.p);
+  k_rank<<<nblk(nbox), TPB, 0, s>>>(escan.p, esel.p, nbox, P->exp_rank.p);
+  DMK_LAUNCH_CHECK();
+  {
+    std::vector<int32_t> fs(nlevels + 1), es(nlevels + 1);
+    int32_t lastf = d2h_at(s, fscan.p + nbox - 1), laste = d2h_at(s, escan.p + nbox - 1);
+    uint8_t lf = d2h_at(s, fsel.p + nbox - 1), le = d2h_at(s, esel.p + nbox - 1);
+    P->nfout = lastf + lf;
+    P->nexp = laste + le;
+    th.fout_off.assign(nlevels + 1, 0);
+    th.exp_off.assign(nlevels + 1, 0);
+    for (int l = 1; l < nlevels; ++l) {
+      th.fout_off[l] = d2h_at(s, fscan.p + th.level_off[l]);
+      th.exp_off[l] = d2h_at(s, escan.p + th.level_off[l]);
+    }
+    th.fout_off[nlevels] = P->nfout;
+    th.exp_off[nlevels] = P->nexp;
+  }
+  {
+    cub::CountingInputIterator<int32_t> cnt_it(0);
+    DevBuf<int64_t> nsel;
+    nsel.alloc(1, s);
+    P->fout_list.alloc(P->nfout ? P->nfout : 1, s);
+    P->exp_list.alloc(P->nexp ? P->nexp : 1, s);
+    cub_run(s, [&](void* t, size_t& b) {
+      return cub::DeviceSelect::Flagged(t, b, cnt_it, fsel.p, P->fout_list.p, nsel.p, nbox, s);
+    });
+    cub_run(s, [&](void* t, size_t& b) {
+      return cub::DeviceSelect::Flagged(t, b, cnt_it, esel.p, P->exp_list.p, nsel.p, nbox, s);
+    });
+  }
+
+  mark("flags");
+  // ---- direct lists (CSR over boxes)
+  {
+    DevBuf<int32_t> cnt;
+    cnt.alloc(nbox + 1, s);
+    DMK_CUDA(cudaMemsetAsync(cnt.p, 0, (nbox + 1) * sizeof(int32_t), s));
+    k_dlist<false><<<nblk(nbox), TPB, 0, s>>>(P->box_start.p, P->box_end.p, P->box_parent.p, P->box_child.p,
+                                              P->box_coll.p, P->box_flags.p, P->box_code.p, P->box_level.p, nbox,
+                                              cnt.p, nullptr, nullptr);
+    DMK_LAUNCH_CHECK();
+    P->dlist_off.alloc(nbox + 1, s);
+    exclusive_scan(s, cnt.p, P->dlist_off.p, nbox + 1);
+    P->ndlist = d2h_at(s, P->dlist_off.p + nbox);
+    P->dlist.alloc(P->ndlist ? P->ndlist : 1, s);
+    k_dlist<true><<<nblk(nbox), TPB, 0, s>>>(P->box_start.p, P->box_end.p, P->box_parent.p, P->box_child.p,
+                                             P->box_coll.p, P->box_flags.p, P->box_code.p, P->box_level.p, nbox,
+                                             nullptr, P->dlist_off.p, P->dlist.p);
+    DMK_LAUNCH_CHECK();
+  }
+  mark("dlists");
+  // ---- P2P work items
+  {
+    DevBuf<int32_t> cnt, off;
+    cnt.alloc(nbox + 1, s);
+    off.alloc(nbox + 1, s);
+    DMK_CUDA(cudaMemsetAsync(cnt.p, 0, (nbox + 1) * sizeof(int32_t), s));
+    k_p2p_count<<<nblk(nbox), TPB, 0, s>>>(P->box_start.p, P->box_end.p, P->box_flags.p, nbox, cnt.p);
+    DMK_LAUNCH_CHECK();
+    exclusive_scan(s, cnt.p, off.p, nbox + 1);
+    P->np2p = d2h_at(s, off.p + nbox);
+    P->p2p_items.alloc(2 * (P->np2p ? P->np2p : 1), s);
+    k_p2p_fill<<<nblk(nbox), TPB, 0, s>>>(P->box_start.p, cnt.p, off.p, nbox, P->p2p_items.p);
+    DMK_LAUNCH_CHECK();
+  }
+  DMK_CUDA(cudaStreamSynchronize(s));
+  mark("p2pitems");
+}
+
+}  // namespace dmk
