@@ -1,0 +1,342 @@
+#!/usr/bin/env python
+"""bench.py -- DMK throughput on BASELINE.json config 1 (3D Laplace, N = 1e6 uniform
+points in [0,1]^3, charges U[-1,1], eps = 1e-6, leaf capacity 200).
+
+One step = the whole hot path on device-resident inputs: dmk_plan (bounding cube,
+Morton sort, adaptive tree, interaction lists) + dmk_eval (Steps 2-5 of Sec. 3.5).
+Timed with CUDA events on the plan stream, L2 flushed (256 MiB write) between steps,
+max over ranks.  Prints ONE JSON line (rank 0).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+--impl reference times the CPU oracle (oracle/dmk.py, fp64 numpy, as it stands) on a
+bounded sample of the same workload on the host cores; under torchrun only rank 0
+runs it.  N > 1 runs independent replicas (one problem per GPU, weak scaling): the
+partitioned multi-GPU DMK is not built yet (DESIGN.md §8 row "multi-GPU").
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "points/sec, 3D Laplace DMK, eps=1e-6, 1/2/4/8 B200; rel ℓ2 err vs direct"
+WORKLOAD = ("config1: 3D Laplace K=1/r, N=1e6 uniform iid in [0,1]^3, charges U[-1,1], "
+            "eps=1e-6, leaf capacity 200, single B200 per rank")
+FP64_FMA_PER_CLK_SM = 64
+N_SM = 148
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--n", type=int, default=1_000_000)
+    ap.add_argument("--eps", type=float, default=1e-6)
+    ap.add_argument("--ns", type=int, default=200)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=20000)
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0, "fallback": True}
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index, self.rows, self.proc = index, [], None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm = [float(r[1]) for r in self.rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) >= 9 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows if len(r) >= 9 for k in range(4)
+                          if r[5 + k].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(sm)}
+
+
+def stage_models(info, n, pairs, K):
+    """Algorithmic work per phase: (bound, amount, unit)."""
+    P, nf, nf0 = info.p, info.nf, info.nf0
+    n1, nh, n10, nh0 = 2 * nf + 1, nf + 1, 2 * nf0 + 1, nf0 + 1
+    p3 = P ** 3
+    phi_bytes = 16 * (nh0 * n10 * n10 + (info.nfout - 1) * nh * n1 * n1)
+    return {
+        "anterp": ("alu", 2.0 * p3 * n, "flop"),
+        "c2p": ("alu", 2.0 * 3 * P ** 4 * (info.nfout - 1), "flop"),
+        "prox2pw": ("hbm", 8.0 * p3 * info.nfout + phi_bytes, "byte"),
+        "pwlocal": ("hbm", phi_bytes + 8.0 * p3 * info.nexp, "byte"),
+        "p2c": ("alu", 2.0 * 3 * P ** 4 * (info.nexp - 1), "flop"),
+        "eval": ("alu", 2.0 * p3 * n, "flop"),
+        "p2p": ("alu", float(pairs) * (2 * K + 16), "flop"),
+    }
+
+
+def list_pairs(plan):
+    import numpy as np
+    off, items = plan.tree("dlist_off"), plan.tree("dlist")
+    st, en = plan.tree("box_start"), plan.tree("box_end")
+    cnt = en - st
+    per_box_src = np.add.reduceat(cnt[items], off[:-1]) if items.size else np.zeros(len(cnt))
+    has = off[1:] > off[:-1]
+    return int(np.sum(np.where(has, cnt * per_box_src, 0)))
+
+
+def cpu_baseline(n_sample, eps, ns):
+    import numpy as np
+
+    import dmk_inputs
+    from oracle.dmk import dmk_laplace3d
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max([d.get("num_threads", 1) for d in threadpool_info()] + [1])
+    except Exception:
+        cores = os.cpu_count()
+    x, q = dmk_inputs.uniform(n_sample, seed=1)
+    t0 = time.perf_counter()
+    dmk_laplace3d(x, q, eps, ns)
+    dt = time.perf_counter() - t0
+    return {"value": n_sample / dt, "unit": "points/s", "cores": cores, "kind": "oracle",
+            "sample": f"oracle DMK (oracle/dmk.py, fp64 numpy) on {n_sample} points drawn from the "
+                      f"config-1 distribution (uniform [0,1]^3, U[-1,1] charges), eps={eps}, "
+                      f"leaf capacity {ns}; {dt:.1f} s"}
+
+
+def run_reference(a):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import numpy as np
+
+    import dmk_inputs
+    from oracle.dmk import dmk_laplace3d
+    n_s = 10000
+    x, q = dmk_inputs.uniform(n_s, seed=1)
+    for _ in range(a.warmup):
+        dmk_laplace3d(x, q, a.eps, a.ns)
+    ts = []
+    for _ in range(a.steps):
+        t0 = time.perf_counter()
+        dmk_laplace3d(x, q, a.eps, a.ns)
+        ts.append(time.perf_counter() - t0)
+    dt = float(np.mean(ts))
+    value = n_s / dt
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max([d.get("num_threads", 1) for d in threadpool_info()] + [1])
+    except Exception:
+        cores = os.cpu_count()
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "points/s", "n_gpus": a.gpus,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "sample_points": n_s, "eps": a.eps, "leaf_capacity": a.ns},
+            "cpu_baseline": {"value": value, "unit": "points/s", "cores": cores, "kind": "oracle",
+                             "sample": f"each step: oracle DMK on {n_s} points of the config-1 distribution"},
+            "e2e": {"value": value, "unit": "points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        return run_reference(a)
+    os.environ.setdefault("DMK_PROFILE", "1")
+    import numpy as np
+    import torch
+
+    import dmk_inputs
+    import paper_2308_00292_b200 as dmk
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    x, q = dmk_inputs.uniform(a.n, seed=1 + rank)
+    X = torch.as_tensor(x, device=dev)
+    Q = torch.as_tensor(q, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    sptr = stream.cuda_stream
+    flush = torch.empty(256 * 2 ** 20 // 4, dtype=torch.float32, device=dev)
+
+    def step():
+        plan = dmk.dmk_plan(X, eps=a.eps, leaf_capacity=a.ns, stream=sptr)
+        u = plan.eval(Q)
+        return plan, u
+
+    for _ in range(a.warmup):
+        p_, u_ = step()
+        p_.close()
+    torch.cuda.synchronize(dev)
+
+    L = dmk.lib()
+    import ctypes
+    L.dmk_kernel_launches.restype = ctypes.c_int64
+    L.dmk_kernel_launches.argtypes = [ctypes.c_void_p]
+    clk = Clocks(local)
+    clk.start()
+    times, stage_ms = [], {}
+    launches0 = L.dmk_kernel_launches(None)
+    info = pairs = None
+    for k in range(a.steps):
+        flush.zero_()
+        torch.cuda.synchronize(dev)
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        plan, u = step()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        barrier()
+        times.append(e0.elapsed_time(e1))
+        for name, ms in plan.timings().items():
+            stage_ms[name] = stage_ms.get(name, 0.0) + ms / a.steps
+        if k == a.steps - 1:
+            info = plan.info()
+            pairs = list_pairs(plan)
+            u_last = u.cpu().numpy()
+        plan.close()
+    launches = (L.dmk_kernel_launches(None) - launches0) // a.steps
+    clocks = clk.stop()
+    t_step = float(np.mean(times))
+    if dist is not None:
+        t = torch.tensor([t_step], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_step = float(t.item())
+    value = a.n * world / (t_step * 1e-3)
+
+    # ---- end to end through the public API, pinned host buffers
+    Xh = torch.as_tensor(x).pin_memory()
+    Qh = torch.as_tensor(q).pin_memory()
+    Uh = torch.empty(a.n, dtype=torch.float64).pin_memory()
+    e2e_times = []
+    for k in range(a.warmup + a.steps):
+        flush.zero_()
+        torch.cuda.synchronize(dev)
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        plan = dmk.dmk_plan(Xh, eps=a.eps, leaf_capacity=a.ns, stream=sptr)
+        plan.eval(Qh, out=Uh)            # H2D of charges, D2H of potentials inside
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        plan.close()
+        if k >= a.warmup:
+            e2e_times.append(e0.elapsed_time(e1))
+    t_e2e = float(np.mean(e2e_times))
+    if dist is not None:
+        t = torch.tensor([t_e2e], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_e2e = float(t.item())
+
+    if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return
+
+    # ---- accuracy on this run's output: direct sum at 200 sampled targets
+    idx = np.random.default_rng(7).choice(a.n, 200, replace=False)
+    ref = np.array([np.sum(np.delete(q, i) / np.linalg.norm(np.delete(x, i, axis=0) - x[i], axis=1)) for i in idx])
+    rel = float(np.linalg.norm(u_last[idx] - ref) / np.linalg.norm(ref))
+
+    pk = peaks()
+    fp64_peak = N_SM * FP64_FMA_PER_CLK_SM * 2 * pk.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+    models = stage_models(info, a.n, pairs, info.respoly_degree)
+    stages = {}
+    for name, (bound, amount, unit) in models.items():
+        ms = stage_ms.get(name)
+        if not ms:
+            continue
+        if bound == "hbm":
+            ach, peak, u_ = amount / (ms * 1e-3) / 1e9, pk["hbm_gbs"], "GB/s"
+        else:
+            ach, peak, u_ = amount / (ms * 1e-3) / 1e12, fp64_peak, "TFLOP/s"
+        stages[name] = {"ms": round(ms, 4), "bound": bound, "achieved": round(ach, 3), "peak": round(peak, 1),
+                        "unit": u_, "frac": round(ach / peak, 4)}
+    tree_ms = t_step - sum(stage_ms.get(s, 0.0) for s in ["gather", *models.keys()])
+    dom = max(stages, key=lambda s: stages[s]["ms"])
+    roof = dict(stages[dom])
+    roof.pop("ms")
+    roof.update({"kernel": dom, "traffic": None,
+                 "peak_source": ("MEASURED_PEAKS.json hbm_gbs" if roof["bound"] == "hbm" else
+                                 "derived: 148 SM x 64 fp64 FMA/clk x 2 x sm_max_mhz (DESIGN.md §6)")})
+    line = {
+        "metric": METRIC, "value": value, "unit": "points/s", "n_gpus": world, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": t_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "N_per_gpu": a.n, "eps": a.eps, "leaf_capacity": a.ns,
+                   "step": "dmk_plan (tree+lists) + dmk_eval, device-resident inputs",
+                   "l2": "flushed by a 256 MiB write between timed steps",
+                   "parallelism": "single" if world == 1 else f"replicas x{world} (independent problems)"},
+        "rel_l2_err_sampled": rel,
+        "clocks": clocks,
+        "e2e": {"value": a.n * world / (t_e2e * 1e-3), "unit": "points/s",
+                "h2d_bytes_per_step": a.n * 4 * 8, "d2h_bytes_per_step": a.n * 8,
+                "api": "paper_2308_00292_b200.dmk_plan(host points) + Plan.eval(host charges -> host potentials)"},
+        "gpu_launches": int(launches),
+        "roofline": roof,
+        "stages_ms": {**{k: round(v, 4) for k, v in stage_ms.items()}, "tree_and_lists": round(tree_ms, 4)},
+        "stages": stages,
+        "tree": {"nbox": info.nbox, "nlevels": info.nlevels, "nfout": info.nfout, "nexp": info.nexp,
+                 "p2p_pairs": pairs},
+    }
+    if world == 1 and not a.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(a.cpu_sample, a.eps, a.ns)
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -175,6 +175,11 @@ int64_t dmk_stage_size(dmk_plan_t plan, int which);
  * Enabled only when the plan was created with env DMK_PROFILE=1. */
 int dmk_eval_timings(dmk_plan_t plan, double* ms, const char** names, int cap);
 
+/* Cumulative count of kernel launches issued by libdmk since the library was
+ * loaded: its own kernels (return value) and CUB device-algorithm calls
+ * (sort / scan / select, each one or more CUB kernels) in *cub_calls (may be NULL). */
+int64_t dmk_kernel_launches(int64_t* cub_calls);
+
 #ifdef __cplusplus
 }
 #endif

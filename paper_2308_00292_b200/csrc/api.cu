@@ -11,6 +11,7 @@ void build_tree(dmk_plan_s* P, const double* dpts);
 void eval_plan(dmk_plan_s* P, const double* dcharges, double* dout);
 
 static thread_local std::string g_err;
+int64_t g_launches = 0, g_cub_launches = 0;
 void set_error(const std::string& m) { g_err = m; }
 void fail(int code, const std::string& m) { throw Error{code, m}; }
 
@@ -85,6 +86,8 @@ int dmk_plan(int dim, int kernel, double eps, int64_t n, const double* points, i
       }
       const char* pe = std::getenv("DMK_PROFILE");
       P->profile = pe && pe[0] == '1';
+      const char* pt = std::getenv("DMK_PROFILE_TREE");
+      P->profile_tree = pt && pt[0] == '1';
       P->tab = &get_tables(kernel, eps);
       const double* dpts = points;
       DevBuf<double> tmp;
@@ -228,6 +231,8 @@ int64_t dmk_stage_size(dmk_plan_t P, int which) {
 
 int dmk_eval_timings(dmk_plan_t P, double* ms, const char** names, int cap) {
   if (!P) return DMK_ERR_ARG;
+  int rc = guard([&] { resolve_timings(P); });
+  if (rc != DMK_OK) return rc;
   int k = 0;
   std::vector<std::pair<const char*, double>> all(P->tree_timings);
   all.insert(all.end(), P->timings.begin(), P->timings.end());
@@ -238,6 +243,11 @@ int dmk_eval_timings(dmk_plan_t P, double* ms, const char** names, int cap) {
     ++k;
   }
   return k;
+}
+
+int64_t dmk_kernel_launches(int64_t* cub_calls) {
+  if (cub_calls) *cub_calls = g_cub_launches;
+  return g_launches;
 }
 
 }  // extern "C"

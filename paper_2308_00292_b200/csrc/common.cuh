@@ -9,6 +9,7 @@
 #include "../../include/dmk.h"
 
 namespace dmk {
+extern int64_t g_launches, g_cub_launches;
 
 constexpr int NBITS = 21;  // bits per coordinate of the 63-bit Morton key
 constexpr int LMAX = 20;   // deepest level a box may be refined into
@@ -28,7 +29,12 @@ void set_error(const std::string& m);
       ::dmk::fail(DMK_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_) +   \
                                     " (" + __FILE__ + ":" + std::to_string(__LINE__) + ")"); \
   } while (0)
-#define DMK_LAUNCH_CHECK() DMK_CUDA(cudaGetLastError())
+// placed directly after each of libdmk's own kernel launches: counts it, checks it
+#define DMK_LAUNCH_CHECK()     \
+  do {                         \
+    ++::dmk::g_launches;       \
+    DMK_CUDA(cudaGetLastError()); \
+  } while (0)
 
 // ---------------------------------------------------------------- device buffer
 template <class T>
@@ -90,7 +96,8 @@ struct dmk_plan_s {
   int64_t n = 0;
   cudaStream_t stream = 0;
   const dmk::Tables* tab = nullptr;
-  bool profile = false;
+  bool profile = false;        // DMK_PROFILE=1: per-phase CUDA events in dmk_eval (no host syncs)
+  bool profile_tree = false;   // DMK_PROFILE_TREE=1: synchronising phase marks in dmk_plan
   bool evaluated = false;
 
   // root cube
@@ -130,4 +137,21 @@ struct dmk_plan_s {
   // profiling
   std::vector<std::pair<const char*, double>> timings;
   std::vector<std::pair<const char*, double>> tree_timings;
+  struct Mark {
+    const char* name;
+    cudaEvent_t e0, e1;
+  };
+  std::vector<Mark> ev_marks;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  ~dmk_plan_s() {
+    for (auto e : ev_pool) cudaEventDestroy(e);
+  }
 };
+
+namespace dmk {
+void resolve_timings(dmk_plan_s* P);
+// cumulative number of libdmk kernel launches (this library's own kernels; the
+// CUB sort/scan/select kernels compiled into the library are counted separately)
+extern int64_t g_launches, g_cub_launches;
+}  // namespace dmk

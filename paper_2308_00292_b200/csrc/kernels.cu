@@ -582,33 +582,46 @@ static void set_smem(Kern k, size_t bytes) {
   if (bytes > 48 * 1024) DMK_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
 }
 
+// Phase timing (DMK_PROFILE=1): CUDA events recorded on the plan stream around each
+// phase, no host synchronisation; resolved when dmk_eval_timings() is called.
 struct Timer {
   dmk_plan_s* P;
-  cudaEvent_t e0 = nullptr;
-  const char* name = nullptr;
   Timer(dmk_plan_s* p) : P(p) {}
+  cudaEvent_t ev() {
+    if (P->ev_used == P->ev_pool.size()) {
+      cudaEvent_t e;
+      DMK_CUDA(cudaEventCreate(&e));
+      P->ev_pool.push_back(e);
+    }
+    return P->ev_pool[P->ev_used++];
+  }
   void begin(const char* nm) {
     if (!P->profile) return;
-    name = nm;
-    DMK_CUDA(cudaEventCreate(&e0));
-    DMK_CUDA(cudaEventRecord(e0, P->stream));
+    cudaEvent_t e = ev();
+    DMK_CUDA(cudaEventRecord(e, P->stream));
+    P->ev_marks.push_back({nm, e, nullptr});
   }
   void end() {
     if (!P->profile) return;
-    cudaEvent_t e1;
-    DMK_CUDA(cudaEventCreate(&e1));
-    DMK_CUDA(cudaEventRecord(e1, P->stream));
-    DMK_CUDA(cudaEventSynchronize(e1));
-    float ms = 0;
-    DMK_CUDA(cudaEventElapsedTime(&ms, e0, e1));
-    bool found = false;
-    for (auto& pr : P->timings)
-      if (std::strcmp(pr.first, name) == 0) { pr.second += ms; found = true; }
-    if (!found) P->timings.push_back({name, (double)ms});
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
+    cudaEvent_t e = ev();
+    DMK_CUDA(cudaEventRecord(e, P->stream));
+    P->ev_marks.back().e1 = e;
   }
 };
+
+void resolve_timings(dmk_plan_s* P) {
+  if (P->ev_marks.empty()) return;
+  DMK_CUDA(cudaEventSynchronize(P->ev_marks.back().e1));
+  for (auto& m : P->ev_marks) {
+    float ms = 0;
+    DMK_CUDA(cudaEventElapsedTime(&ms, m.e0, m.e1));
+    bool found = false;
+    for (auto& pr : P->timings)
+      if (std::strcmp(pr.first, m.name) == 0) { pr.second += ms; found = true; }
+    if (!found) P->timings.push_back({m.name, (double)ms});
+  }
+  P->ev_marks.clear();
+}
 
 template <int P, int NF, int NF0>
 static void run_eval(dmk_plan_s* PL) {
@@ -629,8 +642,7 @@ static void run_eval(dmk_plan_s* PL) {
       constexpr int NT = C::TA * C::TB;
       size_t sm = sizeof(double) * (C::CH * P * P + C::CH * P + C::CH * 2 * P);
       set_smem(k_anterp<P>, sm);
-      if (PL->nfout) k_anterp<P><<<(int)PL->nfout, NT, sm, s>>>(dt, PL->fout_list.p, PL->q.p, PL->mom.p);
-      DMK_LAUNCH_CHECK();
+      if (PL->nfout) { k_anterp<P><<<(int)PL->nfout, NT, sm, s>>>(dt, PL->fout_list.p, PL->q.p, PL->mom.p); DMK_LAUNCH_CHECK(); }
     }
     tm.end();
     tm.begin("c2p");
@@ -639,8 +651,7 @@ static void run_eval(dmk_plan_s* PL) {
       set_smem(k_c2p<P>, sm);
       for (int l = nl - 2; l >= 0; --l) {
         int64_t a = th.fout_off[l], b = th.fout_off[l + 1];
-        if (b > a) k_c2p<P><<<(int)(b - a), P * P, sm, s>>>(dt, PL->fout_list.p + a, T.dA, PL->mom.p);
-        DMK_LAUNCH_CHECK();
+        if (b > a) { k_c2p<P><<<(int)(b - a), P * P, sm, s>>>(dt, PL->fout_list.p + a, T.dA, PL->mom.p); DMK_LAUNCH_CHECK(); }
       }
     }
     tm.end();
@@ -658,9 +669,8 @@ static void run_eval(dmk_plan_s* PL) {
       k_prox2pw<P, NF0, MU0><<<1, 256, sm0, s>>>(dt, PL->fout_list.p, T.dQ0, PL->mom.p, PL->phi.p, 0, 0);
       DMK_LAUNCH_CHECK();
       if (PL->nfout > 1)
-        k_prox2pw<P, NF, MU1><<<(int)(PL->nfout - 1), 256, sm1, s>>>(dt, PL->fout_list.p + 1, T.dQ1, PL->mom.p,
-                                                                    PL->phi.p, PL->phi_size0, PL->phi_size1);
-      DMK_LAUNCH_CHECK();
+        { k_prox2pw<P, NF, MU1><<<(int)(PL->nfout - 1), 256, sm1, s>>>(dt, PL->fout_list.p + 1, T.dQ1, PL->mom.p,
+                                                                    PL->phi.p, PL->phi_size0, PL->phi_size1); DMK_LAUNCH_CHECK(); }
     }
     tm.end();
     tm.begin("pwlocal");
@@ -674,9 +684,8 @@ static void run_eval(dmk_plan_s* PL) {
                                                     PL->lam.p);
       DMK_LAUNCH_CHECK();
       if (PL->nexp > 1)
-        k_pwlocal<P, NF, false><<<(int)(PL->nexp - 1), P * P, sm1, s>>>(
-            dt, PL->exp_list.p + 1, T.dQ1, T.dW, T.wstride, PL->phi.p, PL->phi_size0, PL->phi_size1, PL->lam.p);
-      DMK_LAUNCH_CHECK();
+        { k_pwlocal<P, NF, false><<<(int)(PL->nexp - 1), P * P, sm1, s>>>(
+            dt, PL->exp_list.p + 1, T.dQ1, T.dW, T.wstride, PL->phi.p, PL->phi_size0, PL->phi_size1, PL->lam.p); DMK_LAUNCH_CHECK(); }
     }
     tm.end();
     tm.begin("p2c");
@@ -685,8 +694,7 @@ static void run_eval(dmk_plan_s* PL) {
       set_smem(k_p2c<P>, sm);
       for (int l = 1; l < nl; ++l) {
         int64_t a = th.exp_off[l], b = th.exp_off[l + 1];
-        if (b > a) k_p2c<P><<<(int)(b - a), P * P, sm, s>>>(dt, PL->exp_list.p + a, T.dA, PL->lam.p);
-        DMK_LAUNCH_CHECK();
+        if (b > a) { k_p2c<P><<<(int)(b - a), P * P, sm, s>>>(dt, PL->exp_list.p + a, T.dA, PL->lam.p); DMK_LAUNCH_CHECK(); }
       }
     }
     tm.end();
@@ -695,8 +703,7 @@ static void run_eval(dmk_plan_s* PL) {
       constexpr int NT = C::TA * C::TB;
       size_t sm = sizeof(double) * (C::ECH * P * P + C::ECH * P + C::ECH * 2 * P + NT * C::ECH);
       set_smem(k_eval<P>, sm);
-      if (PL->nexp) k_eval<P><<<(int)PL->nexp, NT, sm, s>>>(dt, PL->exp_list.p, PL->lam.p, PL->ufar.p);
-      DMK_LAUNCH_CHECK();
+      if (PL->nexp) { k_eval<P><<<(int)PL->nexp, NT, sm, s>>>(dt, PL->exp_list.p, PL->lam.p, PL->ufar.p); DMK_LAUNCH_CHECK(); }
     }
     tm.end();
   } else {
@@ -728,6 +735,8 @@ static void run_p2p_deg(dmk_plan_s* PL, double* out, const ResPoly& rp, int K) {
 void eval_plan(dmk_plan_s* PL, const double* dcharges, double* dout) {
   cudaStream_t s = PL->stream;
   PL->timings.clear();
+  PL->ev_marks.clear();
+  PL->ev_used = 0;
   Timer tm(PL);
   tm.begin("gather");
   k_gather_q<<<(int)((PL->n + 255) / 256), 256, 0, s>>>(dcharges, PL->perm.p, PL->n, PL->q.p);

