@@ -34,6 +34,15 @@ static void require_device() {
   int n = 0;
   cudaError_t e = cudaGetDeviceCount(&n);
   if (e != cudaSuccess || n == 0) fail(DMK_ERR_CUDA, "no CUDA device available (libdmk has no CPU path)");
+  // Plans allocate and free ~1 GB per evaluation cycle through the stream-ordered
+  // allocator; keep freed memory in the device pool instead of returning it to the
+  // driver at every synchronisation (which would re-map pages on every plan).
+  int dev = 0;
+  DMK_CUDA(cudaGetDevice(&dev));
+  cudaMemPool_t pool;
+  DMK_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+  uint64_t thr = UINT64_MAX;
+  DMK_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
 }
 
 static void alloc_eval_buffers(dmk_plan_s* P) {
