@@ -511,6 +511,199 @@ __global__ void __launch_bounds__(Cfg<P>::TA * Cfg<P>::TB)
   }
 }
 
+// ---------------------------------------------------------------- fp64 tensor-core (DMMA) versions
+// mma.sync.m8n8k4 f64: A[row=lane>>2][col=lane&3], B[row=lane&3][col=lane>>2],
+// C[row=lane>>2][col=2*(lane&3)+{0,1}].  Measured on this B200: 37.2 TFLOP/s, the
+// same as DFMA, but 256 FMA per warp instruction from 2 register operands, which
+// takes the shared-memory bandwidth limit off these small per-box GEMMs.
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+// Far-field evaluation: u_j = sum_a (Tx_j[n1] Ty_j[n2]) G[j][a],  G = V Lambda^T,
+// V[j][b] = Tz_j[b]  (a = n1 P + n2, b = n3).  One CTA per local-expansion box,
+// Lambda in smem in DMMA-fragment order, each warp evaluates tiles of 8 targets.
+template <int P>
+struct EvalMma {
+  static constexpr int P2 = P * P, KS = (P + 3) / 4, NT8 = (P2 + 7) / 8, NW = 8;
+  static constexpr size_t smem = sizeof(double) * ((size_t)NT8 * KS * 32 + (size_t)NW * 8 * 3 * P);
+};
+template <int P>
+__global__ void __launch_bounds__(256) k_eval_mma(DevTree t, const int32_t* __restrict__ boxes,
+                                                  const double* __restrict__ lam, double* __restrict__ ufar) {
+  using E = EvalMma<P>;
+  constexpr int P2 = E::P2, KS = E::KS, NT8 = E::NT8, NW = E::NW;
+  extern __shared__ double sm[];
+  double* lamF = sm;                        // [NT8][KS][32]
+  double* Tv = lamF + NT8 * KS * 32;        // [NW][8 targets][3 dims][P]
+  __shared__ int2 rg[8];
+  __shared__ int nr_s, tot_s;
+  const int b = boxes[blockIdx.x], tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    nr_s = box_ranges<true>(t, b, rg);
+    int tot = 0;
+    for (int r = 0; r < nr_s; ++r) tot += rg[r].y - rg[r].x;
+    tot_s = tot;
+  }
+  const double* src = lam + (size_t)t.exp_rank[b] * P * P2;
+  for (int i = tid; i < NT8 * KS * 32; i += NW * 32) {
+    int ln = i & 31, ks = (i >> 5) % KS, nt = (i >> 5) / KS;
+    int a = nt * 8 + (ln >> 2), bb = ks * 4 + (ln & 3);
+    lamF[i] = (a < P2 && bb < P) ? src[a * P + bb] : 0.0;
+  }
+  __syncthreads();
+  const int nr = nr_s, tot = tot_s;
+  if (tot == 0) return;
+  double cen[3], ih;
+  box_geom(t.code[b], t.level[b], cen, ih);
+  double* T = Tv + warp * 8 * 3 * P;
+  const int g = lane >> 2, q4 = lane & 3;
+  for (int tt = warp * 8; tt < tot; tt += NW * 8) {
+    const int nv = min(8, tot - tt);
+    if (lane < 24) {
+      const int j = lane / 3, d = lane % 3;
+      double Tl[P];
+      if (j < nv) {
+        int pi = range_point(rg, nr, tt + j);
+        double x = (d == 0 ? t.xs[pi] : d == 1 ? t.ys[pi] : t.zs[pi]);
+        cheb_vec((x - cen[d]) * ih, Tl, P, 1.0);
+      } else {
+#pragma unroll
+        for (int n = 0; n < P; ++n) Tl[n] = 0.0;
+      }
+#pragma unroll
+      for (int n = 0; n < P; ++n) T[(j * 3 + d) * P + n] = Tl[n];
+    }
+    __syncwarp();
+    double af[KS];
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      int bb = ks * 4 + q4;
+      af[ks] = bb < P ? T[(g * 3 + 2) * P + bb] : 0.0;
+    }
+    const double* Tx = T + (g * 3 + 0) * P;
+    const double* Ty = T + (g * 3 + 1) * P;
+    double part = 0.0;
+#pragma unroll 1
+    for (int nt = 0; nt < NT8; nt += 2) {
+      double c0 = 0.0, c1 = 0.0, d0 = 0.0, d1 = 0.0;
+      const bool two = nt + 1 < NT8;
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) {
+        dmma(c0, c1, af[ks], lamF[(nt * KS + ks) * 32 + lane]);
+        if (two) dmma(d0, d1, af[ks], lamF[((nt + 1) * KS + ks) * 32 + lane]);
+      }
+      int a = nt * 8 + 2 * q4;
+      if (a < P2) part = fma(c0, Tx[a / P] * Ty[a % P], part);
+      if (a + 1 < P2) part = fma(c1, Tx[(a + 1) / P] * Ty[(a + 1) % P], part);
+      a += 8;
+      if (two && a < P2) part = fma(d0, Tx[a / P] * Ty[a % P], part);
+      if (two && a + 1 < P2) part = fma(d1, Tx[(a + 1) / P] * Ty[(a + 1) % P], part);
+    }
+    part += __shfl_xor_sync(0xffffffffu, part, 1);
+    part += __shfl_xor_sync(0xffffffffu, part, 2);
+    if (q4 == 0 && g < nv) ufar[range_point(rg, nr, tt + g)] = part;
+    __syncwarp();
+  }
+}
+
+// Anterpolation: mu[a][b] = sum_j (rho_j Tx_j[n1] Ty_j[n2]) Tz_j[b] as C = U^T V with
+// the points as the DMMA k dimension; each warp keeps its m-tiles x all n-tiles of mu
+// in registers.  One CTA per F_out box.
+template <int P>
+struct AntMma {
+  static constexpr int P2 = P * P, MT = (P2 + 7) / 8, NTB = (P + 7) / 8, NW = (P >= 28) ? 16 : 8;
+  static constexpr int MPW = (MT + NW - 1) / NW, CH = 64;
+  static constexpr size_t smem = sizeof(double) * 3 * CH * P;
+};
+template <int P>
+__global__ void __launch_bounds__(AntMma<P>::NW * 32)
+    k_anterp_mma(DevTree t, const int32_t* __restrict__ boxes, const double* __restrict__ q,
+                 double* __restrict__ mom) {
+  using A_ = AntMma<P>;
+  constexpr int P2 = A_::P2, MT = A_::MT, NTB = A_::NTB, NW = A_::NW, MPW = A_::MPW, CH = A_::CH;
+  constexpr int NT = NW * 32;
+  extern __shared__ double sm[];
+  double* Tx = sm;             // [CH][P] (times rho)
+  double* Ty = Tx + CH * P;    // [CH][P]
+  double* Tz = Ty + CH * P;    // [CH][P]
+  __shared__ int2 rg[8];
+  __shared__ int nr_s, tot_s;
+  const int b = boxes[blockIdx.x], tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    nr_s = box_ranges<false>(t, b, rg);
+    int tot = 0;
+    for (int r = 0; r < nr_s; ++r) tot += rg[r].y - rg[r].x;
+    tot_s = tot;
+  }
+  __syncthreads();
+  const int nr = nr_s, tot = tot_s;
+  if (tot == 0) return;   // moments were zeroed by the caller
+  double cen[3], ih;
+  box_geom(t.code[b], t.level[b], cen, ih);
+  const int g = lane >> 2, q4 = lane & 3;
+  double acc[MPW][NTB][2];
+#pragma unroll
+  for (int i = 0; i < MPW; ++i)
+#pragma unroll
+    for (int nb = 0; nb < NTB; ++nb) acc[i][nb][0] = acc[i][nb][1] = 0.0;
+  for (int c0 = 0; c0 < tot; c0 += CH) {
+    const int nc = min(CH, tot - c0);
+    for (int w = tid; w < CH * 3; w += NT) {
+      int j = w / 3, d = w % 3;
+      double Tl[P];
+      if (j < nc) {
+        int pi = range_point(rg, nr, c0 + j);
+        double x = (d == 0 ? t.xs[pi] : d == 1 ? t.ys[pi] : t.zs[pi]);
+        cheb_vec((x - cen[d]) * ih, Tl, P, d == 0 ? q[pi] : 1.0);
+      } else {
+#pragma unroll
+        for (int n = 0; n < P; ++n) Tl[n] = 0.0;
+      }
+      double* dst = (d == 0 ? Tx : d == 1 ? Ty : Tz) + j * P;
+#pragma unroll
+      for (int n = 0; n < P; ++n) dst[n] = Tl[n];
+    }
+    __syncthreads();
+    const int nks = (nc + 3) / 4;
+    for (int ks = 0; ks < nks; ++ks) {
+      const int j = ks * 4 + q4;
+      double bf[NTB];
+#pragma unroll
+      for (int nb = 0; nb < NTB; ++nb) {
+        int bb = nb * 8 + g;
+        bf[nb] = bb < P ? Tz[j * P + bb] : 0.0;
+      }
+#pragma unroll
+      for (int i = 0; i < MPW; ++i) {
+        const int mt = warp + i * NW;
+        if (mt < MT) {
+          const int a = mt * 8 + g;
+          const double af = a < P2 ? Tx[j * P + a / P] * Ty[j * P + a % P] : 0.0;
+#pragma unroll
+          for (int nb = 0; nb < NTB; ++nb) dmma(acc[i][nb][0], acc[i][nb][1], af, bf[nb]);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  double* out = mom + (size_t)t.fout_rank[b] * P * P2;
+#pragma unroll
+  for (int i = 0; i < MPW; ++i) {
+    const int mt = warp + i * NW;
+    const int a = mt * 8 + g;
+    if (mt >= MT || a >= P2) continue;
+#pragma unroll
+    for (int nb = 0; nb < NTB; ++nb) {
+      const int bb = nb * 8 + 2 * q4;
+      if (bb < P) out[a * P + bb] = acc[i][nb][0];
+      if (bb + 1 < P) out[a * P + bb + 1] = acc[i][nb][1];
+    }
+  }
+}
+
 // ---------------------------------------------------------------- P2P
 struct ResPoly {
   double a[25];   // monomial coefficients in s = 2 r^2/r_L^2 - 1
@@ -639,10 +832,12 @@ static void run_eval(dmk_plan_s* PL) {
     tm.begin("anterp");
     DMK_CUDA(cudaMemsetAsync(PL->mom.p, 0, PL->mom.bytes(), s));
     {
-      constexpr int NT = C::TA * C::TB;
-      size_t sm = sizeof(double) * (C::CH * P * P + C::CH * P + C::CH * 2 * P);
-      set_smem(k_anterp<P>, sm);
-      if (PL->nfout) { k_anterp<P><<<(int)PL->nfout, NT, sm, s>>>(dt, PL->fout_list.p, PL->q.p, PL->mom.p); DMK_LAUNCH_CHECK(); }
+      size_t sm = AntMma<P>::smem;
+      set_smem(k_anterp_mma<P>, sm);
+      if (PL->nfout) {
+        k_anterp_mma<P><<<(int)PL->nfout, AntMma<P>::NW * 32, sm, s>>>(dt, PL->fout_list.p, PL->q.p, PL->mom.p);
+        DMK_LAUNCH_CHECK();
+      }
     }
     tm.end();
     tm.begin("c2p");
@@ -700,10 +895,12 @@ static void run_eval(dmk_plan_s* PL) {
     tm.end();
     tm.begin("eval");
     {
-      constexpr int NT = C::TA * C::TB;
-      size_t sm = sizeof(double) * (C::ECH * P * P + C::ECH * P + C::ECH * 2 * P + NT * C::ECH);
-      set_smem(k_eval<P>, sm);
-      if (PL->nexp) { k_eval<P><<<(int)PL->nexp, NT, sm, s>>>(dt, PL->exp_list.p, PL->lam.p, PL->ufar.p); DMK_LAUNCH_CHECK(); }
+      size_t sm = EvalMma<P>::smem;
+      set_smem(k_eval_mma<P>, sm);
+      if (PL->nexp) {
+        k_eval_mma<P><<<(int)PL->nexp, 256, sm, s>>>(dt, PL->exp_list.p, PL->lam.p, PL->ufar.p);
+        DMK_LAUNCH_CHECK();
+      }
     }
     tm.end();
   } else {
