@@ -150,11 +150,13 @@ int dmk_tree_copy(dmk_plan_t plan, int which, int64_t* host_out);
  *                                            of each F_out box (proxy charges = V^{-T} mu,
  *                                            Def. 2.1)
  *   DMK_STAGE_OUTGOING outgoing plane waves Phi_l(B) (Eq. 3.42) of the F_out boxes in
- *                                            rank order; the root (rank 0) first with
- *                                            [nf0+1][2nf0+1][2nf0+1][2] values, then every
- *                                            other box with [nf+1][2nf+1][2nf+1][2]: half
- *                                            space m3 >= 0 (Hermitian symmetry), axes
- *                                            (m3, m1, m2), m1, m2 in [-nf_l, nf_l], (re, im)
+ *                                            rank order, in the real parity-split form: the
+ *                                            root (rank 0) first with [nf0+1][8][nf0+1][nf0+1]
+ *                                            values, then every other box with
+ *                                            [nf+1][8][nf+1][nf+1]: F[a][pi][b][c], a,b,c =
+ *                                            |m1|,|m2|,|m3|, pi = 4 pi1 + 2 pi2 + pi3, and
+ *                                            Phi(m) = sum_pi i^(pi1+pi2+pi3) sgn(m1)^pi1
+ *                                            sgn(m2)^pi2 sgn(m3)^pi3 F[|m1|][pi][|m2|][|m3|]
  *   DMK_STAGE_LOCAL    [nexp][p][p][p]      Chebyshev coefficients of the local expansion
  *                                            Lambda (Eq. 3.43) incl. parent contributions
  *   DMK_STAGE_UFAR     [n]                  far-field potential, sorted order, unit cube

@@ -52,8 +52,9 @@ static void alloc_eval_buffers(dmk_plan_s* P) {
   P->q.alloc(P->n, s);
   P->ufar.alloc(P->n, s);
   P->unear.alloc(P->n, s);
-  P->phi_size0 = (int64_t)2 * (T.nf0 + 1) * (2 * T.nf0 + 1) * (2 * T.nf0 + 1);
-  P->phi_size1 = (int64_t)2 * (T.nf + 1) * (2 * T.nf + 1) * (2 * T.nf + 1);
+  // outgoing expansions in the real parity-split layout [a][pi][b][c] (kernels.cu)
+  P->phi_size0 = (int64_t)8 * (T.nf0 + 1) * (T.nf0 + 1) * (T.nf0 + 1);
+  P->phi_size1 = (int64_t)8 * (T.nf + 1) * (T.nf + 1) * (T.nf + 1);
   if (P->th.nlevels > 1) {
     P->mom.alloc(P->nfout * p3, s);
     P->phi.alloc(P->phi_size0 + (P->nfout - 1) * P->phi_size1, s);

@@ -68,14 +68,17 @@ struct Tables {
   int p = 0, nf = 0, nf0 = 0;
   double RT = 0, P0 = 0;   // root window truncation radius and Fourier period
   // host copies
-  std::vector<double> Q1, Q0;   // [n1][p] complex (re,im): moments -> plane waves, levels>=1 / root
+  int pp = 0;                   // p rounded up to even (row length of Qr)
+  std::vector<double> Qr1, Qr0; // [nf+1][pp] real parity-split plane-wave matrix, levels>=1 / root
+  std::vector<double> Gr1, Gr0; // [p][hh] back transform, hh = nf+1 rounded up to even
   std::vector<double> A;        // [2][p][p]: A_s[n][k], T_n(x/2 + s/2) = sum_k A_s[n][k] T_k(x), s=-1,+1
-  std::vector<double> W;        // [LMAX+1][nh][n1][n1] difference-kernel weights, level l at l*stride
-  std::vector<double> W0;       // [nh0][n10][n10] root window weights
+  std::vector<double> W;        // [LMAX+1][nh][nh][nh] difference-kernel weights (|m1|,|m2|,|m3|)
+  std::vector<double> W0;       // [nh0][nh0][nh0] root window weights
   std::vector<double> respoly;  // residual: M_L(r) r_L ~= sum_k a_k s^k, s = 2 r^2/r_L^2 - 1
   double m0 = 0;                // psi(0)/c0 = r_L M_L(0)
   // device copies
-  double *dQ1 = nullptr, *dQ0 = nullptr, *dA = nullptr, *dW = nullptr, *dW0 = nullptr;
+  double *dQr1 = nullptr, *dQr0 = nullptr, *dGr1 = nullptr, *dGr0 = nullptr, *dA = nullptr, *dW = nullptr,
+         *dW0 = nullptr;
   size_t wstride = 0;
 };
 const Tables& get_tables(int kernel, double eps);  // cached; throws via fail()

@@ -281,154 +281,293 @@ __global__ void __launch_bounds__(P* P) k_p2c(DevTree t, const int32_t* __restri
 }
 
 // ---------------------------------------------------------------- plane waves
-__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
-  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
-}
-__device__ __forceinline__ double2 cfma(double2 a, double2 b, double2 c) {   // a*b + c
-  return make_double2(fma(a.x, b.x, fma(-a.y, b.y, c.x)), fma(a.x, b.y, fma(a.y, b.x, c.y)));
-}
-__device__ __forceinline__ double2 rcfma(double a, double2 b, double2 c) {
-  return make_double2(fma(a, b.x, c.x), fma(a, b.y, c.y));
+// Real parity-split representation of the plane-wave expansions.  With Qr (tables.cu:
+// Q[m][n] = Qr[|m|][n] i^{n mod 2} sgn(m)^{n mod 2}) the outgoing expansion of Eq. 3.42,
+//   Phi(m1,m2,m3) = sum_n Q[m1][n1] Q[m2][n2] Q[m3][n3] mu[n1 n2 n3],
+// splits by the index parities pi_d = n_d mod 2 into eight REAL arrays on the octant
+// a, b, c in [0, nf]:
+//   F_pi[a][b][c] = sum_{n_d = pi_d (mod 2)} Qr[a][n1] Qr[b][n2] Qr[c][n3] mu[n1 n2 n3],
+//   Phi(m) = sum_pi i^{|pi|} sgn(m1)^pi1 sgn(m2)^pi2 sgn(m3)^pi3 F_pi[|m1|][|m2|][|m3|].
+// The colleague shift exp(i h_l m_d delta_d r_l) of Eq. 3.39 (h_l r_l = 2 pi/3) acts on
+// each parity pair (F_{pi_d=0}, F_{pi_d=1}) of axis d as a rotation by 2 pi |m_d| delta_d/3;
+// the weights w_l(|m|) act diagonally; and T_pw2poly (Eqs. 3.43-3.44: sum over all m,
+// real part) collapses to
+//   Lambda[n1 n2 n3] = sum_{abc} Gr[n1][a] Gr[n2][b] Gr[n3][c] Psi_{(n1,n2,n3) mod 2}[a][b][c]
+// with Gr[n][a] = c_a Qr[a][n], c_0 = 1, c_a = 2.  Everything is real and each 1D factor
+// has half of p columns: 4x fewer flops than the complex form.
+// Per-box layout F[a][pi][b][c], pi = 4 pi1 + 2 pi2 + pi3: one slab a is contiguous.
+template <int P, int H>
+struct PwGeom {
+  static constexpr int PP = (P + 1) & ~1, HH = (H + 1) & ~1, P2 = P * P, HSQ = H * H;
+  static constexpr int SLAB = 8 * H * H;            // doubles per slab a
+  static constexpr size_t BOX = (size_t)H * SLAB;   // doubles per box
+};
+
+// 1D transform of P values held in registers by the p-row of an smem matrix (row
+// length even, double2 loads), restricted to one parity class of n.
+template <int P, int PAR>
+__device__ __forceinline__ double dot_par(const double* __restrict__ row, const double* v) {
+  double s = 0.0;
+#pragma unroll
+  for (int n = 0; n < P; n += 2) {
+    const double2 q = *(const double2*)(row + n);
+    if (PAR == 0) s = fma(q.x, v[n], s);
+    else if (n + 1 < P) s = fma(q.y, v[n + 1], s);
+  }
+  return s;
 }
 
-__host__ __device__ constexpr size_t phi_doubles(int nf) { return (size_t)2 * (nf + 1) * (2 * nf + 1) * (2 * nf + 1); }
-
-template <int P, int NF, bool MU_SMEM>
+// Outgoing expansion F(B) of an F_out box from its moments (T_prox2pw, Eq. 3.42): three
+// axis transforms on chunks of AC output slabs a, all in shared memory.
+template <int P, int H, int AC>
+struct Prox2pw {
+  using G = PwGeom<P, H>;
+  static constexpr int NT = 256;
+  static constexpr size_t smem =
+      sizeof(double) * ((size_t)H * G::PP + (size_t)AC * 2 * G::P2 + (size_t)AC * 4 * H * P + (size_t)AC * G::SLAB);
+};
+template <int P, int H, int AC>
 __global__ void __launch_bounds__(256) k_prox2pw(DevTree t, const int32_t* __restrict__ boxes,
-                                                 const double* __restrict__ Qg, const double* __restrict__ mom,
-                                                 double* __restrict__ phi, size_t phi_base, size_t phi_stride) {
-  constexpr int N1 = 2 * NF + 1, NH = NF + 1, P2 = P * P, P3 = P2 * P, NT = 256;
+                                                 const double* __restrict__ Qr, const double* __restrict__ mom,
+                                                 double* __restrict__ F, size_t base, size_t stride) {
+  using G = PwGeom<P, H>;
+  constexpr int NT = 256, P2 = G::P2, PP = G::PP, PH = (P + 1) / 2;
   extern __shared__ double sm[];
-  double2* sQ = (double2*)sm;               // [N1][P]
-  double2* X1 = sQ + N1 * P;                // [P2]
-  double2* X2 = X1 + P2;                    // [P][N1]
-  double* smu = (double*)(X2 + P * N1);     // [P3] if MU_SMEM
+  double* sQ = sm;                   // [H][PP]
+  double* Z = sQ + H * PP;           // [AC][2][P2]      axis 1 done
+  double* Z2 = Z + AC * 2 * P2;      // [AC][4][H][P]    axes 1, 2 done
+  double* Fs = Z2 + AC * 4 * H * P;  // [AC][8][H][H]    all axes
   const int b = boxes[blockIdx.x], tid = threadIdx.x;
   const int r = t.fout_rank[b];
-  const double* mu = mom + (size_t)r * P3;
-  double2* out = (double2*)(phi + phi_base + (size_t)(r == 0 ? 0 : r - 1) * phi_stride);
-  for (int i = tid; i < N1 * P; i += NT) sQ[i] = ((const double2*)Qg)[i];
-  if (MU_SMEM)
-    for (int i = tid; i < P3; i += NT) smu[i] = mu[i];
+  const double* mu = mom + (size_t)r * P * P2;
+  double* out = F + base + (size_t)(r == 0 ? 0 : r - 1) * stride;
+  for (int i = tid; i < H * PP; i += NT) sQ[i] = Qr[i];
   __syncthreads();
-  const double* M = MU_SMEM ? smu : mu;
-  for (int m3 = 0; m3 < NH; ++m3) {
-    const double2* q3 = sQ + (m3 + NF) * P;
-    for (int a = tid; a < P2; a += NT) {        // X1[n1 n2] = sum_n3 mu Q[m3][n3]
-      double2 s = make_double2(0.0, 0.0);
+  for (int a0 = 0; a0 < H; a0 += AC) {
+    const int nac = min(AC, H - a0);
+    // axis 1: Z[ac][pi1][n2 n3] = sum_{n1 = pi1} Qr[a0+ac][n1] mu[n1][n2 n3]
+    for (int w = tid; w < 2 * P2; w += NT) {
+      const int col = w % P2, par = w / P2;
+      double m[P];
 #pragma unroll
-      for (int k = 0; k < P; ++k) s = rcfma(M[(size_t)a * P + k], q3[k], s);
-      X1[a] = s;
+      for (int n = 0; n < P; ++n) m[n] = ((n & 1) == par) ? __ldg(mu + (size_t)n * P2 + col) : 0.0;
+      for (int ac = 0; ac < nac; ++ac) {
+        const double* q = sQ + (a0 + ac) * PP;
+        Z[(ac * 2 + par) * P2 + col] = par ? dot_par<P, 1>(q, m) : dot_par<P, 0>(q, m);
+      }
     }
     __syncthreads();
-    for (int w = tid; w < P * N1; w += NT) {    // X2[n1][m2] = sum_n2 Q[m2][n2] X1[n1 n2]
-      int n1 = w / N1, m2 = w % N1;
-      double2 s = make_double2(0.0, 0.0);
+    // axis 2: Z2[ac][pi1 pi2][b][n3] = sum_{n2 = pi2} Qr[b][n2] Z[ac][pi1][n2][n3]
+    for (int w = tid; w < nac * 2 * P * 2; w += NT) {
+      const int par = w & 1, n3 = (w >> 1) % P, g = (w >> 1) / P;   // g = ac*2 + pi1
+      double z[P];
 #pragma unroll
-      for (int k = 0; k < P; ++k) s = cfma(sQ[m2 * P + k], X1[n1 * P + k], s);
-      X2[w] = s;
+      for (int n = 0; n < P; ++n) z[n] = ((n & 1) == par) ? Z[g * P2 + n * P + n3] : 0.0;
+      for (int bb = 0; bb < H; ++bb) {
+        const double* q = sQ + bb * PP;
+        Z2[((g * 2 + par) * H + bb) * P + n3] = par ? dot_par<P, 1>(q, z) : dot_par<P, 0>(q, z);
+      }
     }
     __syncthreads();
-    double2* o3 = out + (size_t)m3 * N1 * N1;
-    for (int w = tid; w < N1 * N1; w += NT) {   // Phi[m3][m1][m2] = sum_n1 Q[m1][n1] X2[n1][m2]
-      int m1 = w / N1, m2 = w % N1;
-      double2 s = make_double2(0.0, 0.0);
+    // axis 3: Fs[ac][pi][b][c] = sum_{n3 = pi3} Qr[c][n3] Z2[ac][pi1 pi2][b][n3]
+    for (int w = tid; w < nac * 4 * H * 2; w += NT) {
+      const int par = w & 1, row = w >> 1, bb = row % H, g = row / H;   // g = ac*4 + pi12
+      double z[P];
 #pragma unroll
-      for (int k = 0; k < P; ++k) s = cfma(sQ[m1 * P + k], X2[k * N1 + m2], s);
-      o3[w] = s;
+      for (int n = 0; n < P; ++n) z[n] = ((n & 1) == par) ? Z2[row * P + n] : 0.0;
+      for (int c = 0; c < H; ++c) {
+        const double* q = sQ + c * PP;
+        Fs[((g * 2 + par) * H + bb) * H + c] = par ? dot_par<P, 1>(q, z) : dot_par<P, 0>(q, z);
+      }
+    }
+    __syncthreads();
+    double2* o = (double2*)(out + (size_t)a0 * G::SLAB);
+    const double2* f2 = (const double2*)Fs;
+    for (int i = tid; i < nac * G::SLAB / 2; i += NT) o[i] = f2[i];
+    // Z / Z2 / Fs are rewritten only after the next chunk's first barrier
+  }
+  (void)PH;
+}
+
+// Rotation-accumulate along one axis (bit ST of the parity index): acc += R(delta phi) g.
+template <int ST, int DELTA>
+__device__ __forceinline__ void rot_acc(double* acc, const double* g, double C, double S) {
+#pragma unroll
+  for (int p = 0; p < 8; ++p) {
+    if (p & ST) continue;
+    const double g0 = g[p], g1 = g[p + ST];
+    if (DELTA == 0) {
+      acc[p] += g0;
+      acc[p + ST] += g1;
+    } else if (DELTA > 0) {
+      acc[p] = fma(C, g0, fma(-S, g1, acc[p]));
+      acc[p + ST] = fma(S, g0, fma(C, g1, acc[p + ST]));
+    } else {
+      acc[p] = fma(C, g0, fma(S, g1, acc[p]));
+      acc[p + ST] = fma(-S, g0, fma(C, g1, acc[p + ST]));
     }
   }
 }
+__device__ __forceinline__ void rot_cs(int m, double& C, double& S) {
+  const int e = m % 3;   // angle 2 pi m / 3
+  C = e == 0 ? 1.0 : -0.5;
+  S = e == 0 ? 0.0 : (e == 1 ? 0.86602540378443864676 : -0.86602540378443864676);
+}
 
-// Incoming expansion + conversion to Chebyshev coefficients, fused per m3 slice.
-// ROOT: the root box with the window weights W0 (only colleague: itself).
-template <int P, int NF, bool ROOT>
-__global__ void __launch_bounds__(P* P) k_pwlocal(DevTree t, const int32_t* __restrict__ boxes,
-                                                  const double* __restrict__ Qg, const double* __restrict__ Wall,
-                                                  size_t wstride, const double* __restrict__ phi, size_t phi_base,
-                                                  size_t phi_stride, double* __restrict__ lam) {
-  constexpr int N1 = 2 * NF + 1, NH = NF + 1, P2 = P * P, NT = P2;
+// Incoming expansion + conversion to Chebyshev coefficients of one local-expansion box
+// (Eq. 3.39 fused with Eqs. 3.43-3.44): per chunk of AC slabs a, the 27-colleague
+// translation (separable rotations, three nested 3-point sums), the weights, then the
+// axis-3 and axis-2 back transforms in shared memory and a rank-AC update of the
+// register-resident Lambda (axis 1).  ROOT: the root box with the window weights (its
+// only colleague is itself, delta = 0).
+template <int P, int H, int AC>
+struct PwLocal {
+  using G = PwGeom<P, H>;
+  static constexpr int NT = ((P * P > AC * H * H ? P * P : AC * H * H) + 31) / 32 * 32;
+  static constexpr size_t smem = sizeof(double) * ((size_t)P * G::HH + (size_t)AC * G::SLAB +
+                                                   (size_t)AC * 4 * H * P + (size_t)AC * 2 * G::P2);
+};
+template <int P, int H, int AC, bool ROOT>
+__global__ void __launch_bounds__(PwLocal<P, H, AC>::NT)
+    k_pwlocal(DevTree t, const int32_t* __restrict__ boxes, const double* __restrict__ Gr,
+              const double* __restrict__ W, size_t wstride, const double* __restrict__ F, size_t base,
+              size_t stride, double* __restrict__ lam) {
+  using G = PwGeom<P, H>;
+  constexpr int NT = PwLocal<P, H, AC>::NT, P2 = G::P2, HH = G::HH, HSQ = G::HSQ, SLAB = G::SLAB;
   extern __shared__ double sm[];
-  double2* G = (double2*)sm;        // [P][N1]  G[n][m] = conj(Q[m][n])
-  double2* Ps = G + P * N1;         // [N1][N1]
-  double2* Y1 = Ps + N1 * N1;       // [P][N1]
-  __shared__ const double2* src[27];
-  __shared__ int dl[27][3];
-  __shared__ int nsrc;
+  double* sG = sm;                  // [P][HH]
+  double* T = sG + P * HH;          // [AC][8][H][H]  translated + weighted slab
+  double* U = T + AC * SLAB;        // [AC][4][H][P]  axis 3 done
+  double* V = U + AC * 4 * H * P;   // [AC][2][P2]    axes 3, 2 done
+  __shared__ const double* src[27];   // by delta slot (d1+1)*9 + (d2+1)*3 + (d3+1)
   const int b = boxes[blockIdx.x], tid = threadIdx.x;
-  if (!(t.flags[b] & F_IN)) return;   // leaf without incoming: Lambda = 0 before p2c
+  if (!(t.flags[b] & F_IN)) return;   // (never: every local box has F_in, tree.cu)
   const int l = t.level[b];
-  const double* W = Wall + (ROOT ? 0 : (size_t)l * wstride);
-  for (int i = tid; i < P * N1; i += NT) {
-    int n = i / N1, m = i % N1;
-    double2 qv = ((const double2*)Qg)[m * P + n];
-    G[i] = make_double2(qv.x, -qv.y);
-  }
-  if (tid == 0) {
-    int k2 = 0;
-    for (int k = 0; k < 27; ++k) {
-      int s = t.coll[27 * (int64_t)b + k];
-      if (s < 0 || !(t.flags[s] & F_OUT)) continue;
-      int r = t.fout_rank[s];
-      src[k2] = (const double2*)(phi + phi_base + (size_t)(r == 0 ? 0 : r - 1) * phi_stride);
-      // delta = coords(B) - coords(S) = -(dx, dy, dz) of the colleague slot
-      dl[k2][0] = -(k / 9 - 1);
-      dl[k2][1] = -((k / 3) % 3 - 1);
-      dl[k2][2] = -(k % 3 - 1);
-      ++k2;
+  const double* Wl = W + (ROOT ? 0 : (size_t)l * wstride);
+  for (int i = tid; i < P * HH; i += NT) sG[i] = Gr[i];
+  if (tid < 27) {
+    // colleague slot k = (dx+1)*9 + (dy+1)*3 + (dz+1) holds B + (dx,dy,dz); its
+    // delta = c_B - c_S = -(dx,dy,dz) has slot 26 - k
+    const double* p = nullptr;
+    if (ROOT) {
+      if (tid == 13) p = F;
+    } else {
+      const int s = t.coll[27 * (int64_t)b + tid];
+      if (s >= 0 && (t.flags[s] & F_OUT)) p = F + base + (size_t)(t.fout_rank[s] - 1) * stride;
     }
-    nsrc = k2;
+    src[26 - tid] = p;
   }
   __syncthreads();
-  const int ns = nsrc;
-  const int n1 = tid / P, n2 = tid % P;
   double acc[P];
 #pragma unroll
-  for (int k = 0; k < P; ++k) acc[k] = 0.0;
-  // omega^k, omega = exp(2 pi i / 3): the colleague shift exp(i h_l m.(c_B - c_S)), h_l r_l = 2 pi/3
-  const double2 om[3] = {make_double2(1.0, 0.0), make_double2(-0.5, 0.86602540378443864676),
-                         make_double2(-0.5, -0.86602540378443864676)};
-  for (int m3 = 0; m3 < NH; ++m3) {
-    for (int w = tid; w < N1 * N1; w += NT) {   // Psi slice
-      int m1 = w / N1 - NF, m2 = w % N1 - NF;
-      double2 s = make_double2(0.0, 0.0);
-      for (int k = 0; k < ns; ++k) {
-        double2 v = src[k][(size_t)m3 * N1 * N1 + w];
-        if (ROOT) {
-          s.x += v.x;
-          s.y += v.y;
-        } else {
-          int e = (m1 * dl[k][0] + m2 * dl[k][1] + m3 * dl[k][2]) % 3;
-          e = (e + 3) % 3;
-          s = cfma(v, om[e], s);
+  for (int n = 0; n < P; ++n) acc[n] = 0.0;
+  for (int a0 = 0; a0 < H; a0 += AC) {
+    const int nac = min(AC, H - a0);
+    // ---- translation (Eq. 3.39) and weights
+    for (int w = tid; w < nac * HSQ; w += NT) {
+      const int ac = w / HSQ, bc = w % HSQ, a = a0 + ac;
+      const size_t off = (size_t)a * SLAB + bc;
+      double o[8];
+      if (ROOT) {
+#pragma unroll
+        for (int p = 0; p < 8; ++p) o[p] = __ldg(src[13] + off + p * HSQ);
+      } else {
+        double Ca, Sa, Cb, Sb, Cc, Sc;
+        rot_cs(a, Ca, Sa);
+        rot_cs(bc / H, Cb, Sb);
+        rot_cs(bc % H, Cc, Sc);
+#pragma unroll
+        for (int p = 0; p < 8; ++p) o[p] = 0.0;
+#pragma unroll
+        for (int d1 = 0; d1 < 3; ++d1) {
+          double x[8];
+#pragma unroll
+          for (int p = 0; p < 8; ++p) x[p] = 0.0;
+#pragma unroll
+          for (int d2 = 0; d2 < 3; ++d2) {
+            double y[8];
+#pragma unroll
+            for (int p = 0; p < 8; ++p) y[p] = 0.0;
+#pragma unroll
+            for (int d3 = 0; d3 < 3; ++d3) {
+              const double* s = src[d1 * 9 + d2 * 3 + d3];
+              if (s == nullptr) continue;
+              double g[8];
+#pragma unroll
+              for (int p = 0; p < 8; ++p) g[p] = __ldg(s + off + p * HSQ);
+              if (d3 == 0) rot_acc<1, -1>(y, g, Cc, Sc);
+              else if (d3 == 1) rot_acc<1, 0>(y, g, Cc, Sc);
+              else rot_acc<1, 1>(y, g, Cc, Sc);
+            }
+            if (d2 == 0) rot_acc<2, -1>(x, y, Cb, Sb);
+            else if (d2 == 1) rot_acc<2, 0>(x, y, Cb, Sb);
+            else rot_acc<2, 1>(x, y, Cb, Sb);
+          }
+          if (d1 == 0) rot_acc<4, -1>(o, x, Ca, Sa);
+          else if (d1 == 1) rot_acc<4, 0>(o, x, Ca, Sa);
+          else rot_acc<4, 1>(o, x, Ca, Sa);
         }
       }
-      double wt = W[(size_t)m3 * N1 * N1 + w];
-      Ps[w] = make_double2(wt * s.x, wt * s.y);
-    }
-    __syncthreads();
-    for (int w = tid; w < P * N1; w += NT) {    // Y1[n1][m2] = sum_m1 G[n1][m1] Psi[m1][m2]
-      int a = w / N1, m2 = w % N1;
-      double2 s = make_double2(0.0, 0.0);
-#pragma unroll 5
-      for (int k = 0; k < N1; ++k) s = cfma(G[a * N1 + k], Ps[k * N1 + m2], s);
-      Y1[w] = s;
-    }
-    __syncthreads();
-    double2 y = make_double2(0.0, 0.0);          // Y2[n1][n2] = sum_m2 G[n2][m2] Y1[n1][m2]
-#pragma unroll 5
-    for (int k = 0; k < N1; ++k) y = cfma(G[n2 * N1 + k], Y1[n1 * N1 + k], y);
-    const double cw = (m3 == 0) ? 1.0 : 2.0;     // Hermitian half space
+      const double wt = __ldg(Wl + (size_t)a * HSQ + bc);
 #pragma unroll
-    for (int k = 0; k < P; ++k) {
-      double2 g = G[k * N1 + m3 + NF];
-      acc[k] = fma(cw, y.x * g.x - y.y * g.y, acc[k]);
+      for (int p = 0; p < 8; ++p) T[(ac * 8 + p) * HSQ + bc] = wt * o[p];
     }
     __syncthreads();
+    // ---- axis 3: U[ac][pi12][b][n3] = sum_c Gr[n3][c] T[ac][pi12*2 + n3%2][b][c]
+    for (int w = tid; w < nac * 4 * H * 2; w += NT) {
+      const int par = w & 1, row = w >> 1;   // row = (ac*4 + pi12)*H + b
+      const int bb = row % H, g = row / H;
+      double z[HH];
+#pragma unroll
+      for (int c = 0; c < HH; ++c) z[c] = c < H ? T[((g * 2 + par) * H + bb) * H + c] : 0.0;
+#pragma unroll
+      for (int n = par; n < P; n += 2) {
+        const double* gr = sG + n * HH;
+        double s = 0.0;
+#pragma unroll
+        for (int c = 0; c < HH; c += 2) {
+          const double2 q = *(const double2*)(gr + c);
+          s = fma(q.x, z[c], fma(q.y, z[c + 1], s));
+        }
+        U[row * P + n] = s;
+      }
+    }
+    __syncthreads();
+    // ---- axis 2: V[ac][pi1][n2][n3] = sum_b Gr[n2][b] U[ac][pi1*2 + n2%2][b][n3]
+    for (int w = tid; w < nac * 2 * P * 2; w += NT) {
+      const int par = w & 1, n3 = (w >> 1) % P, g = (w >> 1) / P;   // g = ac*2 + pi1
+      double z[HH];
+#pragma unroll
+      for (int bb = 0; bb < HH; ++bb) z[bb] = bb < H ? U[((g * 2 + par) * H + bb) * P + n3] : 0.0;
+#pragma unroll
+      for (int n = par; n < P; n += 2) {
+        const double* gr = sG + n * HH;
+        double s = 0.0;
+#pragma unroll
+        for (int bb = 0; bb < HH; bb += 2) {
+          const double2 q = *(const double2*)(gr + bb);
+          s = fma(q.x, z[bb], fma(q.y, z[bb + 1], s));
+        }
+        V[(g * P + n) * P + n3] = s;
+      }
+    }
+    __syncthreads();
+    // ---- axis 1: Lambda[n1][n2 n3] += sum_ac Gr[n1][a0+ac] V[ac][n1%2][n2 n3]
+    if (tid < P2) {
+      for (int ac = 0; ac < nac; ++ac) {
+        const double v0 = V[(ac * 2 + 0) * P2 + tid], v1 = V[(ac * 2 + 1) * P2 + tid];
+#pragma unroll
+        for (int n = 0; n < P; ++n) acc[n] = fma(sG[n * HH + a0 + ac], (n & 1) ? v1 : v0, acc[n]);
+      }
+    }
+    // next chunk: T's last readers (axis 3) finished before the barrier above; U and V
+    // are rewritten only after the next chunk's barriers
   }
-  double* dst = lam + (size_t)t.exp_rank[b] * P * P2 + (size_t)tid * P;
+  if (tid < P2) {
+    double* dst = lam + (size_t)t.exp_rank[b] * P * P2 + tid;
 #pragma unroll
-  for (int k = 0; k < P; ++k) dst[k] = acc[k];
+    for (int n = 0; n < P; ++n) dst[(size_t)n * P2] = acc[n];
+  }
 }
 
 // ---------------------------------------------------------------- evaluation
@@ -772,7 +911,8 @@ static DevTree dev_tree(const dmk_plan_s* P) {
 
 template <class Kern>
 static void set_smem(Kern k, size_t bytes) {
-  if (bytes > 48 * 1024) DMK_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  // always set: dynamic + static shared memory above 48 KB needs the opt-in
+  DMK_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
 }
 
 // Phase timing (DMK_PROFILE=1): CUDA events recorded on the plan stream around each
@@ -816,6 +956,19 @@ void resolve_timings(dmk_plan_s* P) {
   P->ev_marks.clear();
 }
 
+// slabs per chunk: prox2pw as many as fit ~100 KB of shared memory (<= 8); pwlocal 2
+// unless the translation items of two slabs exceed 1024 threads
+constexpr int px_ac(int P, int H) {
+  int best = 1;
+  for (int ac = 1; ac <= 8 && ac <= H; ++ac) {
+    size_t sm = sizeof(double) * ((size_t)H * ((P + 1) & ~1) + (size_t)ac * 2 * P * P + (size_t)ac * 4 * H * P +
+                                  (size_t)ac * 8 * H * H);
+    if (sm <= 100 * 1024) best = ac;
+  }
+  return best;
+}
+constexpr int pw_ac(int H) { return 2 * H * H <= 1024 ? 2 : 1; }
+
 template <int P, int NF, int NF0>
 static void run_eval(dmk_plan_s* PL) {
   using C = Cfg<P>;
@@ -853,34 +1006,36 @@ static void run_eval(dmk_plan_s* PL) {
     // ---- Step 3: downward pass
     tm.begin("prox2pw");
     {
-      constexpr size_t base_sm1 = sizeof(double2) * ((2 * NF + 1) * P + P * P + P * (2 * NF + 1));
-      constexpr bool MU1 = base_sm1 + sizeof(double) * P3 <= 200 * 1024;
-      size_t sm1 = base_sm1 + (MU1 ? sizeof(double) * P3 : 0);
-      constexpr size_t base_sm0 = sizeof(double2) * ((2 * NF0 + 1) * P + P * P + P * (2 * NF0 + 1));
-      constexpr bool MU0 = base_sm0 + sizeof(double) * P3 <= 200 * 1024;
-      size_t sm0 = base_sm0 + (MU0 ? sizeof(double) * P3 : 0);
-      set_smem(k_prox2pw<P, NF0, MU0>, sm0);
-      set_smem(k_prox2pw<P, NF, MU1>, sm1);
-      k_prox2pw<P, NF0, MU0><<<1, 256, sm0, s>>>(dt, PL->fout_list.p, T.dQ0, PL->mom.p, PL->phi.p, 0, 0);
+      constexpr int H = NF + 1, H0 = NF0 + 1, AC = px_ac(P, H), AC0 = px_ac(P, H0);
+      using K1 = Prox2pw<P, H, AC>;
+      using K0 = Prox2pw<P, H0, AC0>;
+      set_smem(k_prox2pw<P, H0, AC0>, K0::smem);
+      set_smem(k_prox2pw<P, H, AC>, K1::smem);
+      k_prox2pw<P, H0, AC0><<<1, K0::NT, K0::smem, s>>>(dt, PL->fout_list.p, T.dQr0, PL->mom.p, PL->phi.p, 0, 0);
       DMK_LAUNCH_CHECK();
-      if (PL->nfout > 1)
-        { k_prox2pw<P, NF, MU1><<<(int)(PL->nfout - 1), 256, sm1, s>>>(dt, PL->fout_list.p + 1, T.dQ1, PL->mom.p,
-                                                                    PL->phi.p, PL->phi_size0, PL->phi_size1); DMK_LAUNCH_CHECK(); }
+      if (PL->nfout > 1) {
+        k_prox2pw<P, H, AC><<<(int)(PL->nfout - 1), K1::NT, K1::smem, s>>>(dt, PL->fout_list.p + 1, T.dQr1, PL->mom.p,
+                                                                           PL->phi.p, PL->phi_size0, PL->phi_size1);
+        DMK_LAUNCH_CHECK();
+      }
     }
     tm.end();
     tm.begin("pwlocal");
     {
-      size_t sm0 = sizeof(double2) * (2 * P * (2 * NF0 + 1) + (2 * NF0 + 1) * (2 * NF0 + 1));
-      size_t sm1 = sizeof(double2) * (2 * P * (2 * NF + 1) + (2 * NF + 1) * (2 * NF + 1));
-      set_smem(k_pwlocal<P, NF0, true>, sm0);
-      set_smem(k_pwlocal<P, NF, false>, sm1);
+      constexpr int H = NF + 1, H0 = NF0 + 1, AC = pw_ac(H), AC0 = pw_ac(H0);
+      using K1 = PwLocal<P, H, AC>;
+      using K0 = PwLocal<P, H0, AC0>;
+      set_smem(k_pwlocal<P, H0, AC0, true>, K0::smem);
+      set_smem(k_pwlocal<P, H, AC, false>, K1::smem);
       // root: exp rank 0, F_out rank 0
-      k_pwlocal<P, NF0, true><<<1, P * P, sm0, s>>>(dt, PL->exp_list.p, T.dQ0, T.dW0, 0, PL->phi.p, 0, 0,
-                                                    PL->lam.p);
+      k_pwlocal<P, H0, AC0, true><<<1, K0::NT, K0::smem, s>>>(dt, PL->exp_list.p, T.dGr0, T.dW0, 0, PL->phi.p, 0, 0,
+                                                              PL->lam.p);
       DMK_LAUNCH_CHECK();
-      if (PL->nexp > 1)
-        { k_pwlocal<P, NF, false><<<(int)(PL->nexp - 1), P * P, sm1, s>>>(
-            dt, PL->exp_list.p + 1, T.dQ1, T.dW, T.wstride, PL->phi.p, PL->phi_size0, PL->phi_size1, PL->lam.p); DMK_LAUNCH_CHECK(); }
+      if (PL->nexp > 1) {
+        k_pwlocal<P, H, AC, false><<<(int)(PL->nexp - 1), K1::NT, K1::smem, s>>>(
+            dt, PL->exp_list.p + 1, T.dGr1, T.dW, T.wstride, PL->phi.p, PL->phi_size0, PL->phi_size1, PL->lam.p);
+        DMK_LAUNCH_CHECK();
+      }
     }
     tm.end();
     tm.begin("p2c");

@@ -11,7 +11,8 @@
 //   Root window weights (W_0 + D_0 = M_1 windowed by the truncated kernel, Sec. 4.7)
 //   Q = E V^{-T}: Chebyshev moments -> outgoing plane waves (T_prox2pw, Eq. 3.42)
 //     and conj(Q)^T = V^{-1} E: incoming plane waves -> Chebyshev coefficients
-//     (T_pw2poly, Eqs. 3.43-3.44)
+//     (T_pw2poly, Eqs. 3.43-3.44), kept in the real parity-split form Qr / Gr
+//     (kernels.cu explains the representation)
 //   A_s: Chebyshev re-expansion T_n(x/2 + s/2) = sum_k A_s[n][k] T_k(x) which gives
 //     both T_c2p in moment form (Lemma 2.2) and T_p2c = A_s^T (Lemma 2.3)
 //   Residual polynomial: r_L M_L(r) = m(r/r_L), m(t) = Phi(t)/t, fitted as a
@@ -183,12 +184,17 @@ void cheb_T(double x, int p, std::vector<double>& T) {
   for (int n = 2; n < p; ++n) T[n] = 2.0 * x * T[n - 1] - T[n - 2];
 }
 
-// Q[m'][n] = sum_i exp(-i a m x_i) V^{-1}[n][i],  m = m' - nf, a = h s / 2
-void make_Q(int p, int nf, double a, std::vector<double>& Q) {
-  int n1 = 2 * nf + 1;
-  Q.assign((size_t)n1 * p * 2, 0.0);
-  for (int mp = 0; mp < n1; ++mp) {
-    double m = mp - nf;
+// Q[m][n] = sum_i exp(-i a m x_i) V^{-1}[n][i],  a = h s / 2, m in [0, nf] only.
+// The Chebyshev nodes are symmetric (x_{p-1-i} = -x_i) and V^{-1}[n][.] has parity (-1)^n,
+// so Q[m][n] is real for even n and purely imaginary for odd n, and Q[-m][n] =
+// conj(Q[m][n]).  Qr keeps the one non-zero part: Qr[m][n] = Re Q (n even), Im Q (n odd),
+// row length pp (p rounded up to even, zero padded).  Gr[n][m] = c_m Qr[m][n] with c_0 = 1,
+// c_m = 2 (m > 0) is the matching back transform (T_pw2poly summed over +-m).
+void make_Qr(int p, int nf, double a, int pp, int hh, std::vector<double>& Qr, std::vector<double>& Gr) {
+  int nh = nf + 1;
+  Qr.assign((size_t)nh * pp, 0.0);
+  Gr.assign((size_t)p * hh, 0.0);
+  for (int m = 0; m < nh; ++m)
     for (int n = 0; n < p; ++n) {
       double re = 0, im = 0;
       for (int i = 0; i < p; ++i) {
@@ -196,22 +202,21 @@ void make_Q(int p, int nf, double a, std::vector<double>& Q) {
         re += std::cos(a * m * x) * v;
         im -= std::sin(a * m * x) * v;
       }
-      Q[(mp * p + n) * 2 + 0] = re;
-      Q[(mp * p + n) * 2 + 1] = im;
+      double q = (n % 2 == 0) ? re : im;
+      Qr[(size_t)m * pp + n] = q;
+      Gr[(size_t)n * hh + m] = (m == 0 ? 1.0 : 2.0) * q;
     }
-  }
 }
 
 template <class F>
-void make_weights(int nf, double h, F fhat, double* W) {   // layout [m3'][m1'][m2'], m3' >= 0
-  int n1 = 2 * nf + 1, nh = nf + 1;
+void make_weights(int nf, double h, F fhat, double* W) {   // layout [a][b][c], a, b, c in [0, nf]
+  int nh = nf + 1;
   double scale = std::pow(h / (2.0 * PI), 3);
-  for (int a3 = 0; a3 < nh; ++a3)
-    for (int a1 = 0; a1 < n1; ++a1)
-      for (int a2 = 0; a2 < n1; ++a2) {
-        double m1 = a1 - nf, m2 = a2 - nf, m3 = a3;
-        double k = h * std::sqrt(m1 * m1 + m2 * m2 + m3 * m3);
-        W[((size_t)a3 * n1 + a1) * n1 + a2] = scale * fhat(k);
+  for (int a = 0; a < nh; ++a)
+    for (int b = 0; b < nh; ++b)
+      for (int c = 0; c < nh; ++c) {
+        double k = h * std::sqrt((double)(a * a + b * b + c * c));
+        W[((size_t)a * nh + b) * nh + c] = scale * fhat(k);
       }
 }
 
@@ -239,8 +244,9 @@ Tables* build_tables(int kernel, double eps) {
   const double c = T->c;
 
   // plane-wave <-> Chebyshev matrices: h_l r_l = 2 pi / 3 for every l >= 1 (reading R2)
-  make_Q(p, nf, PI / 3.0, T->Q1);
-  make_Q(p, nf0, PI / T->P0, T->Q0);
+  T->pp = (p + 1) & ~1;
+  make_Qr(p, nf, PI / 3.0, T->pp, (nf + 2) & ~1, T->Qr1, T->Gr1);
+  make_Qr(p, nf0, PI / T->P0, T->pp, (nf0 + 2) & ~1, T->Qr0, T->Gr0);
 
   // Chebyshev re-expansion A_s
   T->A.assign(2 * p * p, 0.0);
@@ -255,8 +261,8 @@ Tables* build_tables(int kernel, double eps) {
   }
 
   // difference-kernel weights per level (Eq. 3.68)
-  int n1 = 2 * nf + 1, nh = nf + 1;
-  T->wstride = (size_t)nh * n1 * n1;
+  int nh = nf + 1;
+  T->wstride = (size_t)nh * nh * nh;
   T->W.assign((LMAX + 1) * T->wstride, 0.0);
   for (int l = 1; l <= LMAX; ++l) {
     double rl = std::ldexp(1.0, -l), rl1 = std::ldexp(1.0, -l - 1);
@@ -269,8 +275,8 @@ Tables* build_tables(int kernel, double eps) {
   }
   // root window: psi(k r_1/c)/psi(0) * 8 pi sin^2(k R_T/2)/k^2
   {
-    int n10 = 2 * nf0 + 1, nh0 = nf0 + 1;
-    T->W0.assign((size_t)nh0 * n10 * n10, 0.0);
+    int nh0 = nf0 + 1;
+    T->W0.assign((size_t)nh0 * nh0 * nh0, 0.0);
     double h0 = 2.0 * PI / T->P0, RT = T->RT;
     auto What = [&](double k) {
       double G = P.eval(k * 0.5 / c) / P.psi0;
@@ -323,8 +329,10 @@ Tables* build_tables(int kernel, double eps) {
     if (err <= 1e-2 * T->eps * T->m0) break;
   }
 
-  upload(T->Q1, &T->dQ1);
-  upload(T->Q0, &T->dQ0);
+  upload(T->Qr1, &T->dQr1);
+  upload(T->Qr0, &T->dQr0);
+  upload(T->Gr1, &T->dGr1);
+  upload(T->Gr0, &T->dGr0);
   upload(T->A, &T->dA);
   upload(T->W, &T->dW);
   upload(T->W0, &T->dW0);

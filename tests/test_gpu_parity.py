@@ -78,25 +78,39 @@ def test_moments_match_oracle_proxies(case):
         assert np.max(np.abs(got - ref)) <= 1e-11 * max(1.0, np.max(np.abs(ref)))
 
 
+def phi_from_parity_split(F, nf):
+    """Outgoing plane waves Phi(m1, m2, m3), m in [-nf, nf]^3, from the device's real
+    parity-split layout F[a][pi][b][c] (kernels.cu):
+    Phi(m) = sum_pi i^{|pi|} sgn(m1)^pi1 sgn(m2)^pi2 sgn(m3)^pi3 F_pi[|m1|][|m2|][|m3|]."""
+    h = nf + 1
+    Fp = F.reshape(h, 8, h, h).transpose(1, 0, 2, 3)
+    m = np.arange(-nf, nf + 1)
+    am, sg = np.abs(m), np.where(m < 0, -1.0, 1.0)
+    out = np.zeros((2 * nf + 1,) * 3, dtype=np.complex128)
+    for pi in range(8):
+        p1, p2, p3 = (pi >> 2) & 1, (pi >> 1) & 1, pi & 1
+        sign = (sg[:, None, None] ** p1) * (sg[None, :, None] ** p2) * (sg[None, None, :] ** p3)
+        out += (1j ** (p1 + p2 + p3)) * sign * Fp[pi][np.ix_(am, am, am)]
+    return out
+
+
 def test_outgoing_matches_oracle(case):
-    """Outgoing plane waves Phi_l(B) (Eq. 3.42), half space m3 >= 0."""
+    """Outgoing plane waves Phi_l(B) (Eq. 3.42) over the full mode cube, from the device's
+    real parity-split representation."""
     T, plan, st = case["T"], case["plan"], case["st"]
     inf = plan.info()
     nf, nf0 = inf.nf, inf.nf0
-    n10, n1 = 2 * nf0 + 1, 2 * nf + 1
-    s0, s1 = 2 * (nf0 + 1) * n10 * n10, 2 * (nf + 1) * n1 * n1
+    s0, s1 = 8 * (nf0 + 1) ** 3, 8 * (nf + 1) ** 3
     phi = plan.stage("outgoing")
+    assert phi.size == s0 + (inf.nfout - 1) * s1
     fout = plan.tree("fout")
     for i in np.nonzero(T.fout)[0]:
         r = fout[i]
         if r == 0:
-            a = phi[:s0].reshape(nf0 + 1, n10, n10, 2)
-            k = nf0
+            got = phi_from_parity_split(phi[:s0], nf0)
         else:
-            a = phi[s0 + (r - 1) * s1: s0 + r * s1].reshape(nf + 1, n1, n1, 2)
-            k = nf
-        got = a[..., 0] + 1j * a[..., 1]
-        ref = np.transpose(st["Phi"][i][:, :, k:], (2, 0, 1))
+            got = phi_from_parity_split(phi[s0 + (r - 1) * s1: s0 + r * s1], nf)
+        ref = st["Phi"][i]
         assert np.max(np.abs(got - ref)) <= 1e-11 * np.max(np.abs(ref))
 
 
