@@ -20,7 +20,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdmk.so")
+LIB_PATH = os.environ.get("DMK_LIB") or os.path.join(_HERE, "libdmk.so")
 
 DMK_OK = 0
 DMK_MEM_DEVICE, DMK_MEM_HOST = 0, 1

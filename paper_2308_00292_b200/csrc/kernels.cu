@@ -91,6 +91,33 @@ __device__ __forceinline__ void cheb_vec(double x, double* T, int P, double scal
   }
 }
 
+// ---------------------------------------------------------------- fp64 tensor-core (DMMA) versions
+// mma.sync.m8n8k4 f64: A[row=lane>>2][col=lane&3], B[row=lane&3][col=lane>>2],
+// C[row=lane>>2][col=2*(lane&3)+{0,1}].  Measured on this B200: 37.2 TFLOP/s, the
+// same as DFMA, but 256 FMA per warp instruction from 2 register operands, which
+// takes the shared-memory bandwidth limit off these small per-box GEMMs.
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+// Warp-cooperative C = A B over 8x8 output tiles with K = 4 KS (zero padded by the
+// operand functors): fa(m, k), fb(k, n) return operand values, fc(m, n, c_n, c_{n+1})
+// consumes the two accumulators a lane owns.  Tiles are dealt round-robin to the warps.
+template <int KS, class FA, class FB, class FC>
+__device__ __forceinline__ void mma_tiles(int mtiles, int ntiles, FA fa, FB fb, FC fc) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int g = lane >> 2, q = lane & 3;
+  for (int t = warp; t < mtiles * ntiles; t += nw) {
+    const int m0 = (t / ntiles) * 8, n0 = (t % ntiles) * 8;
+    double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) dmma(c0, c1, fa(m0 + g, ks * 4 + q), fb(ks * 4 + q, n0 + g));
+    fc(m0 + g, n0 + 2 * q, c0, c1);
+  }
+}
+
 // ---------------------------------------------------------------- gather
 __global__ void k_gather_q(const double* __restrict__ charges, const int32_t* __restrict__ perm, int64_t n,
                            double* q) {
@@ -317,76 +344,94 @@ __device__ __forceinline__ double dot_par(const double* __restrict__ row, const 
   return s;
 }
 
-// Outgoing expansion F(B) of an F_out box from its moments (T_prox2pw, Eq. 3.42): three
-// axis transforms on chunks of AC output slabs a, all in shared memory.
-template <int P, int H, int AC>
+// Outgoing expansion F(B) of an F_out box from its moments (T_prox2pw, Eq. 3.42):
+// three axis transforms as fp64 tensor-core GEMMs (DMMA m8n8k4, K = ceil(p/2) padded
+// to 4), per parity of the axis being contracted:
+//   S1 (n3 -> c):  X1[n1 n2][c]  = sum_j mu[n1 n2][2j+pi3] Qr[c][2j+pi3]
+//   S2 (n2 -> b):  X2[b][n1][c]  = sum_j Qr[b][2j+pi2] X1[n1 (2j+pi2)][c]
+//   S3 (n1 -> a):  F[a][pi][b c] = sum_j Qr[a][2j+pi1] X2[b][2j+pi1][c]   -> global
+// over column chunks of CH values of c (all of them when they fit).
+template <int P, int H, int CH>
 struct Prox2pw {
   using G = PwGeom<P, H>;
-  static constexpr int NT = 256;
-  static constexpr size_t smem =
-      sizeof(double) * ((size_t)H * G::PP + (size_t)AC * 2 * G::P2 + (size_t)AC * 4 * H * P + (size_t)AC * G::SLAB);
+  static constexpr int NT = 256, KS = ((P + 1) / 2 + 3) / 4, HP = (H + 7) / 8 * 8;
+  static constexpr size_t smem = sizeof(double) * ((size_t)2 * HP * KS * 4 + (size_t)P * P * CH + (size_t)H * P * CH);
 };
-template <int P, int H, int AC>
+template <int P, int H, int CH>
 __global__ void __launch_bounds__(256) k_prox2pw(DevTree t, const int32_t* __restrict__ boxes,
                                                  const double* __restrict__ Qr, const double* __restrict__ mom,
                                                  double* __restrict__ F, size_t base, size_t stride) {
   using G = PwGeom<P, H>;
-  constexpr int NT = 256, P2 = G::P2, PP = G::PP, PH = (P + 1) / 2;
+  using C = Prox2pw<P, H, CH>;
+  constexpr int NT = C::NT, P2 = G::P2, PP = G::PP, KS = C::KS, K4 = KS * 4, HP = C::HP, HSQ = G::HSQ;
   extern __shared__ double sm[];
-  double* sQ = sm;                   // [H][PP]
-  double* Z = sQ + H * PP;           // [AC][2][P2]      axis 1 done
-  double* Z2 = Z + AC * 2 * P2;      // [AC][4][H][P]    axes 1, 2 done
-  double* Fs = Z2 + AC * 4 * H * P;  // [AC][8][H][H]    all axes
+  double* sQ = sm;                   // [2][HP][K4]: sQ[pi][a][j] = Qr[a][2j+pi], zero padded
+  double* X1 = sQ + 2 * HP * K4;     // [P2][CH]
+  double* X2 = X1 + P2 * CH;         // [H][P][CH]
   const int b = boxes[blockIdx.x], tid = threadIdx.x;
   const int r = t.fout_rank[b];
   const double* mu = mom + (size_t)r * P * P2;
   double* out = F + base + (size_t)(r == 0 ? 0 : r - 1) * stride;
-  for (int i = tid; i < H * PP; i += NT) sQ[i] = Qr[i];
-  __syncthreads();
-  for (int a0 = 0; a0 < H; a0 += AC) {
-    const int nac = min(AC, H - a0);
-    // axis 1: Z[ac][pi1][n2 n3] = sum_{n1 = pi1} Qr[a0+ac][n1] mu[n1][n2 n3]
-    for (int w = tid; w < 2 * P2; w += NT) {
-      const int col = w % P2, par = w / P2;
-      double m[P];
-#pragma unroll
-      for (int n = 0; n < P; ++n) m[n] = ((n & 1) == par) ? __ldg(mu + (size_t)n * P2 + col) : 0.0;
-      for (int ac = 0; ac < nac; ++ac) {
-        const double* q = sQ + (a0 + ac) * PP;
-        Z[(ac * 2 + par) * P2 + col] = par ? dot_par<P, 1>(q, m) : dot_par<P, 0>(q, m);
-      }
-    }
-    __syncthreads();
-    // axis 2: Z2[ac][pi1 pi2][b][n3] = sum_{n2 = pi2} Qr[b][n2] Z[ac][pi1][n2][n3]
-    for (int w = tid; w < nac * 2 * P * 2; w += NT) {
-      const int par = w & 1, n3 = (w >> 1) % P, g = (w >> 1) / P;   // g = ac*2 + pi1
-      double z[P];
-#pragma unroll
-      for (int n = 0; n < P; ++n) z[n] = ((n & 1) == par) ? Z[g * P2 + n * P + n3] : 0.0;
-      for (int bb = 0; bb < H; ++bb) {
-        const double* q = sQ + bb * PP;
-        Z2[((g * 2 + par) * H + bb) * P + n3] = par ? dot_par<P, 1>(q, z) : dot_par<P, 0>(q, z);
-      }
-    }
-    __syncthreads();
-    // axis 3: Fs[ac][pi][b][c] = sum_{n3 = pi3} Qr[c][n3] Z2[ac][pi1 pi2][b][n3]
-    for (int w = tid; w < nac * 4 * H * 2; w += NT) {
-      const int par = w & 1, row = w >> 1, bb = row % H, g = row / H;   // g = ac*4 + pi12
-      double z[P];
-#pragma unroll
-      for (int n = 0; n < P; ++n) z[n] = ((n & 1) == par) ? Z2[row * P + n] : 0.0;
-      for (int c = 0; c < H; ++c) {
-        const double* q = sQ + c * PP;
-        Fs[((g * 2 + par) * H + bb) * H + c] = par ? dot_par<P, 1>(q, z) : dot_par<P, 0>(q, z);
-      }
-    }
-    __syncthreads();
-    double2* o = (double2*)(out + (size_t)a0 * G::SLAB);
-    const double2* f2 = (const double2*)Fs;
-    for (int i = tid; i < nac * G::SLAB / 2; i += NT) o[i] = f2[i];
-    // Z / Z2 / Fs are rewritten only after the next chunk's first barrier
+  for (int i = tid; i < 2 * HP * K4; i += NT) {
+    const int j = i % K4, a = (i / K4) % HP, pi = i / (K4 * HP), n = 2 * j + pi;
+    sQ[i] = (a < H && n < P) ? Qr[a * PP + n] : 0.0;
   }
-  (void)PH;
+  __syncthreads();
+  for (int c0 = 0; c0 < H; c0 += CH) {
+    const int nc = min(CH, H - c0);
+    for (int pi3 = 0; pi3 < 2; ++pi3) {
+      const double* q3 = sQ + pi3 * HP * K4;
+      // S1: M = P2 rows (n1 n2), N = nc, K = j
+      mma_tiles<KS>(
+          (P2 + 7) / 8, (nc + 7) / 8,
+          [&](int m, int k) { return (m < P2 && 2 * k + pi3 < P) ? __ldg(mu + m * P + 2 * k + pi3) : 0.0; },
+          [&](int k, int n) { return c0 + n < H ? q3[(c0 + n) * K4 + k] : 0.0; },
+          [&](int m, int n, double v0, double v1) {
+            if (m < P2) {
+              if (n < nc) X1[m * CH + n] = v0;
+              if (n + 1 < nc) X1[m * CH + n + 1] = v1;
+            }
+          });
+      __syncthreads();
+      for (int pi2 = 0; pi2 < 2; ++pi2) {
+        const double* q2 = sQ + pi2 * HP * K4;
+        // S2: M = H rows b, N = (n1, c) = P CH (c >= nc padded), K = j
+        mma_tiles<KS>(
+            HP / 8, (P * CH + 7) / 8, [&](int m, int k) { return q2[m * K4 + k]; },
+            [&](int k, int n) {
+              const int n1 = n / CH, c = n - n1 * CH;
+              return (n1 < P && c < nc && 2 * k + pi2 < P) ? X1[(n1 * P + 2 * k + pi2) * CH + c] : 0.0;
+            },
+            [&](int m, int n, double v0, double v1) {
+              if (m < H) {
+                if (n < P * CH) X2[m * P * CH + n] = v0;
+                if (n + 1 < P * CH) X2[m * P * CH + n + 1] = v1;
+              }
+            });
+        __syncthreads();
+        for (int pi1 = 0; pi1 < 2; ++pi1) {
+          const double* q1 = sQ + pi1 * HP * K4;
+          double* o = out + (size_t)(4 * pi1 + 2 * pi2 + pi3) * HSQ + c0;
+          // S3: M = H rows a, N = (b, c) = H CH (c >= nc skipped), K = j
+          mma_tiles<KS>(
+              HP / 8, (H * CH + 7) / 8, [&](int m, int k) { return q1[m * K4 + k]; },
+              [&](int k, int n) {
+                const int bb = n / CH, c = n - bb * CH;
+                return (bb < H && 2 * k + pi1 < P) ? X2[(bb * P + 2 * k + pi1) * CH + c] : 0.0;
+              },
+              [&](int m, int n, double v0, double v1) {
+                if (m < H) {
+                  const int bb = n / CH, c = n - bb * CH;   // n even, CH may be odd
+                  if (bb < H && c < nc) o[(size_t)m * G::SLAB + bb * H + c] = v0;
+                  const int b1 = (n + 1) / CH, c1 = n + 1 - b1 * CH;
+                  if (b1 < H && c1 < nc) o[(size_t)m * G::SLAB + b1 * H + c1] = v1;
+                }
+              });
+        }
+        __syncthreads();   // X2 is rewritten by the next pi2
+      }
+    }
+  }
 }
 
 // Rotation-accumulate along one axis (bit ST of the parity index): acc += R(delta phi) g.
@@ -416,29 +461,38 @@ __device__ __forceinline__ void rot_cs(int m, double& C, double& S) {
 
 // Incoming expansion + conversion to Chebyshev coefficients of one local-expansion box
 // (Eq. 3.39 fused with Eqs. 3.43-3.44): per chunk of AC slabs a, the 27-colleague
-// translation (separable rotations, three nested 3-point sums), the weights, then the
-// axis-3 and axis-2 back transforms in shared memory and a rank-AC update of the
-// register-resident Lambda (axis 1).  ROOT: the root box with the window weights (its
-// only colleague is itself, delta = 0).
+// translation (separable rotations: three nested 3-point sums), the weights, then the
+// axis-3 and axis-2 back transforms in shared memory.  The axis-1 contraction over a
+// either runs at the end as one DMMA GEMM over all slabs kept in shared memory
+// (VSMEM, p <= 18), or as rank-AC updates of register accumulators (p = 28, whose
+// slabs do not fit).  ROOT: the root box with the window weights (its only colleague
+// is itself, delta = 0).
 template <int P, int H, int AC>
 struct PwLocal {
   using G = PwGeom<P, H>;
-  static constexpr int NT = ((P * P > AC * H * H ? P * P : AC * H * H) + 31) / 32 * 32;
-  static constexpr size_t smem = sizeof(double) * ((size_t)P * G::HH + (size_t)AC * G::SLAB +
-                                                   (size_t)AC * 4 * H * P + (size_t)AC * 2 * G::P2);
+  static constexpr bool VSMEM = P <= 18;
+  static constexpr int NT = ((VSMEM || P * P <= AC * H * H ? AC * H * H : P * P) + 31) / 32 * 32;
+  static constexpr int KSA = (H + 3) / 4;   // axis-1 DMMA k steps (slabs, zero padded)
+  static constexpr size_t smem =
+      sizeof(double) * ((size_t)P * G::HH + (size_t)AC * G::SLAB + (size_t)AC * 4 * H * P +
+                        (VSMEM ? (size_t)H * 2 * G::P2 : (size_t)AC * 2 * G::P2));
+  static constexpr int MINB = (VSMEM && NT <= 352) ? 2 : 1;
 };
 template <int P, int H, int AC, bool ROOT>
-__global__ void __launch_bounds__(PwLocal<P, H, AC>::NT)
+__global__ void __launch_bounds__(PwLocal<P, H, AC>::NT, PwLocal<P, H, AC>::MINB)
     k_pwlocal(DevTree t, const int32_t* __restrict__ boxes, const double* __restrict__ Gr,
               const double* __restrict__ W, size_t wstride, const double* __restrict__ F, size_t base,
               size_t stride, double* __restrict__ lam) {
   using G = PwGeom<P, H>;
-  constexpr int NT = PwLocal<P, H, AC>::NT, P2 = G::P2, HH = G::HH, HSQ = G::HSQ, SLAB = G::SLAB;
+  using C = PwLocal<P, H, AC>;
+  constexpr bool VSMEM = C::VSMEM;
+  constexpr int NT = C::NT, P2 = G::P2, HH = G::HH, HSQ = G::HSQ, SLAB = G::SLAB, KSA = C::KSA;
+  constexpr int NACC = VSMEM ? 1 : P;
   extern __shared__ double sm[];
   double* sG = sm;                  // [P][HH]
-  double* T = sG + P * HH;          // [AC][8][H][H]  translated + weighted slab
+  double* T = sG + P * HH;          // [AC][8][H][H]  translated + weighted slabs
   double* U = T + AC * SLAB;        // [AC][4][H][P]  axis 3 done
-  double* V = U + AC * 4 * H * P;   // [AC][2][P2]    axes 3, 2 done
+  double* V = U + AC * 4 * H * P;   // [a][2][P2]     axes 3, 2 done (VSMEM: all slabs)
   __shared__ const double* src[27];   // by delta slot (d1+1)*9 + (d2+1)*3 + (d3+1)
   const int b = boxes[blockIdx.x], tid = threadIdx.x;
   if (!(t.flags[b] & F_IN)) return;   // (never: every local box has F_in, tree.cu)
@@ -458,9 +512,9 @@ __global__ void __launch_bounds__(PwLocal<P, H, AC>::NT)
     src[26 - tid] = p;
   }
   __syncthreads();
-  double acc[P];
+  double acc[NACC];
 #pragma unroll
-  for (int n = 0; n < P; ++n) acc[n] = 0.0;
+  for (int n = 0; n < NACC; ++n) acc[n] = 0.0;
   for (int a0 = 0; a0 < H; a0 += AC) {
     const int nac = min(AC, H - a0);
     // ---- translation (Eq. 3.39) and weights
@@ -533,7 +587,8 @@ __global__ void __launch_bounds__(PwLocal<P, H, AC>::NT)
       }
     }
     __syncthreads();
-    // ---- axis 2: V[ac][pi1][n2][n3] = sum_b Gr[n2][b] U[ac][pi1*2 + n2%2][b][n3]
+    // ---- axis 2: V[a][pi1][n2][n3] = sum_b Gr[n2][b] U[ac][pi1*2 + n2%2][b][n3]
+    double* Va = VSMEM ? V + (size_t)a0 * 2 * P2 : V;
     for (int w = tid; w < nac * 2 * P * 2; w += NT) {
       const int par = w & 1, n3 = (w >> 1) % P, g = (w >> 1) / P;   // g = ac*2 + pi1
       double z[HH];
@@ -548,25 +603,41 @@ __global__ void __launch_bounds__(PwLocal<P, H, AC>::NT)
           const double2 q = *(const double2*)(gr + bb);
           s = fma(q.x, z[bb], fma(q.y, z[bb + 1], s));
         }
-        V[(g * P + n) * P + n3] = s;
+        Va[(g * P + n) * P + n3] = s;
       }
     }
     __syncthreads();
-    // ---- axis 1: Lambda[n1][n2 n3] += sum_ac Gr[n1][a0+ac] V[ac][n1%2][n2 n3]
-    if (tid < P2) {
+    if (!VSMEM && tid < P2) {
+      // ---- axis 1 (registers): Lambda[n1][n2 n3] += sum_ac Gr[n1][a0+ac] V[ac][n1%2][n2 n3]
       for (int ac = 0; ac < nac; ++ac) {
         const double v0 = V[(ac * 2 + 0) * P2 + tid], v1 = V[(ac * 2 + 1) * P2 + tid];
 #pragma unroll
-        for (int n = 0; n < P; ++n) acc[n] = fma(sG[n * HH + a0 + ac], (n & 1) ? v1 : v0, acc[n]);
+        for (int n = 0; n < NACC; ++n) acc[n] = fma(sG[n * HH + a0 + ac], (n & 1) ? v1 : v0, acc[n]);
       }
     }
     // next chunk: T's last readers (axis 3) finished before the barrier above; U and V
     // are rewritten only after the next chunk's barriers
   }
-  if (tid < P2) {
-    double* dst = lam + (size_t)t.exp_rank[b] * P * P2 + tid;
+  double* dst = lam + (size_t)t.exp_rank[b] * P * P2;
+  if (VSMEM) {
+    // ---- axis 1 (DMMA): Lambda[2i+pi1][n2n3] = sum_a Gr[2i+pi1][a] V[a][pi1][n2n3]
+    constexpr int PH = (P + 1) / 2;
+#pragma unroll 1
+    for (int pi1 = 0; pi1 < 2; ++pi1)
+      mma_tiles<KSA>(
+          (PH + 7) / 8, (P2 + 7) / 8,
+          [&](int m, int k) { return (2 * m + pi1 < P && k < H) ? sG[(2 * m + pi1) * HH + k] : 0.0; },
+          [&](int k, int n) { return (n < P2 && k < H) ? V[(k * 2 + pi1) * P2 + n] : 0.0; },
+          [&](int m, int n, double v0, double v1) {
+            const int n1 = 2 * m + pi1;
+            if (n1 < P) {
+              if (n < P2) dst[(size_t)n1 * P2 + n] = v0;
+              if (n + 1 < P2) dst[(size_t)n1 * P2 + n + 1] = v1;
+            }
+          });
+  } else if (tid < P2) {
 #pragma unroll
-    for (int n = 0; n < P; ++n) dst[(size_t)n * P2] = acc[n];
+    for (int n = 0; n < NACC; ++n) dst[(size_t)n * P2 + tid] = acc[n];
   }
 }
 
@@ -648,17 +719,6 @@ __global__ void __launch_bounds__(Cfg<P>::TA * Cfg<P>::TB)
     }
     __syncthreads();
   }
-}
-
-// ---------------------------------------------------------------- fp64 tensor-core (DMMA) versions
-// mma.sync.m8n8k4 f64: A[row=lane>>2][col=lane&3], B[row=lane&3][col=lane>>2],
-// C[row=lane>>2][col=2*(lane&3)+{0,1}].  Measured on this B200: 37.2 TFLOP/s, the
-// same as DFMA, but 256 FMA per warp instruction from 2 register operands, which
-// takes the shared-memory bandwidth limit off these small per-box GEMMs.
-__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-               : "+d"(c0), "+d"(c1)
-               : "d"(a), "d"(b));
 }
 
 // Far-field evaluation: u_j = sum_a (Tx_j[n1] Ty_j[n2]) G[j][a],  G = V Lambda^T,
@@ -956,16 +1016,18 @@ void resolve_timings(dmk_plan_s* P) {
   P->ev_marks.clear();
 }
 
-// slabs per chunk: prox2pw as many as fit ~100 KB of shared memory (<= 8); pwlocal 2
-// unless the translation items of two slabs exceed 1024 threads
-constexpr int px_ac(int P, int H) {
+// prox2pw: columns c per chunk, all of them when the intermediates fit 200 KB, else
+// balanced chunks.  pwlocal: 2 slabs per chunk unless the translation items of two
+// slabs exceed 1024 threads.
+constexpr int px_ch(int P, int H) {
   int best = 1;
-  for (int ac = 1; ac <= 8 && ac <= H; ++ac) {
-    size_t sm = sizeof(double) * ((size_t)H * ((P + 1) & ~1) + (size_t)ac * 2 * P * P + (size_t)ac * 4 * H * P +
-                                  (size_t)ac * 8 * H * H);
-    if (sm <= 100 * 1024) best = ac;
+  for (int ch = 1; ch <= H; ++ch) {
+    size_t sm = sizeof(double) * ((size_t)2 * ((H + 7) / 8 * 8) * ((((P + 1) / 2) + 3) / 4 * 4) + (size_t)P * P * ch +
+                                  (size_t)H * P * ch);
+    if (sm <= 200 * 1024) best = ch;
   }
-  return best;
+  const int nchunk = (H + best - 1) / best;
+  return (H + nchunk - 1) / nchunk;
 }
 constexpr int pw_ac(int H) { return 2 * H * H <= 1024 ? 2 : 1; }
 
@@ -1006,7 +1068,7 @@ static void run_eval(dmk_plan_s* PL) {
     // ---- Step 3: downward pass
     tm.begin("prox2pw");
     {
-      constexpr int H = NF + 1, H0 = NF0 + 1, AC = px_ac(P, H), AC0 = px_ac(P, H0);
+      constexpr int H = NF + 1, H0 = NF0 + 1, AC = px_ch(P, H), AC0 = px_ch(P, H0);
       using K1 = Prox2pw<P, H, AC>;
       using K0 = Prox2pw<P, H0, AC0>;
       set_smem(k_prox2pw<P, H0, AC0>, K0::smem);
