@@ -25,6 +25,22 @@ def laplace3d(sources, charges, targets=None, chunk: int = 2048) -> np.ndarray:
     return out
 
 
+def yukawa3d(sources, charges, lam: float, targets=None, chunk: int = 2048) -> np.ndarray:
+    """sum_{j: y_j != x_i} rho_j exp(-lam |x_i - y_j|)/|x_i - y_j|  (Eq. 1.1 with the
+    Yukawa kernel of Sec. 4.6)."""
+    y = np.asarray(sources, dtype=np.float64)
+    q = np.asarray(charges, dtype=np.float64)
+    x = y if targets is None else np.asarray(targets, dtype=np.float64)
+    out = np.empty(x.shape[0])
+    for a in range(0, x.shape[0], chunk):
+        d = x[a:a + chunk, None, :] - y[None, :, :]
+        r = np.sqrt(np.einsum("ijk,ijk->ij", d, d))
+        with np.errstate(divide="ignore", invalid="ignore"):
+            k = np.where(r > 0.0, np.exp(-lam * r) / r, 0.0)
+        out[a:a + chunk] = k @ q
+    return out
+
+
 def rel_l2(a, b) -> float:
     """Relative l2 error ||a - b|| / ||b|| (the north-star accuracy metric)."""
     a = np.asarray(a, dtype=np.float64)

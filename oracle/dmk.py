@@ -1,4 +1,4 @@
-"""The discrete DMK algorithm for the 3D Laplace kernel  (oracle; test infrastructure).
+"""The discrete DMK algorithm for the 3D Laplace and Yukawa kernels  (oracle; test infrastructure).
 
 Follows "The full DMK algorithm for discrete sources", Sec. 3.5, PAPER.md:1414-1623,
 step by step and in the paper's order, with the PSWF kernel split of Sec. 3.6
@@ -15,6 +15,12 @@ step by step and in the paper's order, with the PSWF kernel split of Sec. 3.6
   Step 4  direct residual interactions over the lists
   Step 5  self-interaction corrections
 
+Kernels: 1/r with the PSWF split of Sec. 3.6 (LaplaceSplit), exp(-lam r)/r with the
+Fourier-space PSWF split of Sec. 4.6, Eq. 4.18 (YukawaSplit).  The points are mapped to
+the unit root cube (x -> (x - lo)/side); the kernel there is K_side(r') = K(side r') =
+exp(-(lam side) r')/(side r'), so the algorithm runs with lam' = lam * side and the
+result is divided by side (for 1/r: lam' = 0).
+
 Readings: R2 Fourier spacing, R4 root window M_1 = W_0 + D_0,
 R5-R8 tree conventions, R9 coincident pairs, R10 root-leaf case (N <= n_s: plain
 direct sum).  No blocking, fusion or reordering beyond the paper's; 1D factor
@@ -27,7 +33,7 @@ from __future__ import annotations
 import numpy as np
 
 from . import cheb
-from .kernels import LaplaceSplit, trapezoid_weights_3d, r_level
+from .kernels import LaplaceSplit, YukawaSplit, trapezoid_weights_3d, r_level
 from .params import for_eps
 from .tree import Tree
 
@@ -40,18 +46,35 @@ def _octant_sides(code: int):
 
 def dmk_laplace3d(points, charges, eps: float, ns: int, return_stages: bool = False):
     """u_i = sum_{j != i} rho_j / |x_i - x_j| by DMK.  points (N,3), charges (N,)."""
+    return dmk3d(points, charges, eps, ns, "laplace", 0.0, return_stages)
+
+
+def dmk_yukawa3d(points, charges, eps: float, ns: int, lam: float, return_stages: bool = False):
+    """u_i = sum_{j != i} rho_j exp(-lam |x_i - x_j|)/|x_i - x_j| by DMK."""
+    return dmk3d(points, charges, eps, ns, "yukawa", lam, return_stages)
+
+
+def dmk3d(points, charges, eps: float, ns: int, kernel: str = "laplace", lam: float = 0.0,
+          return_stages: bool = False):
     prm = for_eps(eps)
-    split = LaplaceSplit(prm.c)
     T = Tree(points, ns)                                   # Step 0
+    if kernel == "laplace":
+        split = LaplaceSplit(prm.c)
+        K = lambda r: 1.0 / r
+    elif kernel == "yukawa":
+        split = YukawaSplit(prm.c, lam * T.side)
+        K = split.K
+    else:
+        raise ValueError(kernel)
     rho = np.asarray(charges, dtype=np.float64)[T.perm]
     X = T.xs
     N = T.N
-    st = {"tree": T, "params": prm}
+    st = {"tree": T, "params": prm, "split": split}
     if T.box_leaf[0]:                                      # reading R10: root is a leaf
         d = X[:, None, :] - X[None, :, :]
         r = np.sqrt(np.einsum("ijk,ijk->ij", d, d))
         with np.errstate(divide="ignore"):
-            inv = np.where(r > 0.0, 1.0 / r, 0.0)
+            inv = np.where(r > 0.0, K(np.where(r > 0.0, r, 1.0)), 0.0)
         us = inv @ rho
         u = np.empty(N)
         u[T.perm] = us / T.side

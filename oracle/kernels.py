@@ -111,3 +111,97 @@ def fourier_sum_3d(w, h: float, nf: int, x):
     e = [np.exp(1j * h * np.outer(x[:, d], m)) for d in range(3)]   # (n, N1)
     out = np.einsum("abc,na,nb,nc->n", w, e[0], e[1], e[2], optimize=True)
     return out.real
+
+
+class YukawaSplit:
+    """PSWF kernel split of the 3D Yukawa kernel K(r) = exp(-lam r)/r, carried out in
+    Fourier space (Sec. 4.6, Eqs. 4.17-4.18):
+
+        Khat(k)    = 4 pi/(k^2 + lam^2)        (the paper's 1/(k^2+lam^2) for the
+                                                kernel normalised by 1/(4 pi), Eq. 4.16)
+        Ghat_l(k)  = psi(sqrt(k^2+lam^2) r_l/c)/psi(0)
+        Mhat_l     = Khat Ghat_l,   Dhat_l = Khat (Ghat_{l+1} - Ghat_l),
+        Rhat_L     = Khat (1 - Ghat_L)                                (Eq. 4.18)
+
+    In physical space M_l(r) is the radial inverse transform of Mhat_l (Eq. 3.12,
+    PAPER.md:641): M_l(r) = 1/(2 pi^2 r) int_0^inf Mhat_l(k) k sin(kr) dk, taken over
+    the support sqrt(k^2+lam^2) <= c/r_l of the truncated psi (reading R3) with
+    Gauss-Legendre quadrature; R_L = K - M_L (no truncation: the oracle never assumes
+    the compact support of R_L, it only computes it).
+    Root (reading R4): the window of Sec. 4.7 with the truncated
+    Yukawa kernel, That(k) = 4 pi int_0^{R_T} e^{-lam r} sin(kr)/k dr
+      = 4 pi/(k^2+lam^2) [1 - e^{-lam R_T}(cos k R_T + (lam/k) sin k R_T)].
+    lam is the Yukawa parameter in the units of the coordinates the split is used in
+    (oracle/dmk.py passes lam * side for the unit root cube)."""
+
+    NQ = 400
+
+    def __init__(self, c: float, lam: float):
+        if not lam > 0:
+            raise ValueError("YukawaSplit needs lam > 0 (lam = 0 is LaplaceSplit)")
+        self.psi = Pswf(c)
+        self.c = self.psi.c
+        self.lam = float(lam)
+        self._gl = np.polynomial.legendre.leggauss(self.NQ)
+
+    def K(self, r):
+        r = np.asarray(r, dtype=np.float64)
+        with np.errstate(divide="ignore"):
+            return np.exp(-self.lam * r) / r
+
+    def Khat(self, k):
+        k = np.asarray(k, dtype=np.float64)
+        return 4.0 * np.pi / (k ** 2 + self.lam ** 2)
+
+    def Ghat(self, l: int, k):
+        k = np.asarray(k, dtype=np.float64)
+        return self.psi(np.sqrt(k ** 2 + self.lam ** 2) * r_level(l) / self.c) / self.psi.psi0
+
+    def Dhat(self, l: int, k):
+        """Eq. 4.18, second line (times 4 pi)."""
+        return self.Khat(k) * (self.Ghat(l + 1, k) - self.Ghat(l, k))
+
+    def What_root(self, k, RT: float):
+        k = np.asarray(k, dtype=np.float64)
+        lam = self.lam
+        with np.errstate(divide="ignore", invalid="ignore"):
+            T = 4.0 * np.pi / (k ** 2 + lam ** 2) * (
+                1.0 - np.exp(-lam * RT) * (np.cos(k * RT) + lam / k * np.sin(k * RT)))
+        T0 = 4.0 * np.pi / lam ** 2 * (1.0 - np.exp(-lam * RT) * (1.0 + lam * RT))
+        return self.Ghat(1, k) * np.where(k == 0.0, T0, T)
+
+    def _kgrid(self, l: int):
+        kmax2 = (self.c / r_level(l)) ** 2 - self.lam ** 2
+        if kmax2 <= 0:
+            return None, None
+        x, w = self._gl
+        kmax = np.sqrt(kmax2)
+        return 0.5 * kmax * (x + 1.0), 0.5 * kmax * w
+
+    def M(self, l: int, r):
+        """Mollified kernel M_l(r) by the radial inverse Fourier transform."""
+        r = np.asarray(r, dtype=np.float64)
+        k, w = self._kgrid(l)
+        if k is None:
+            return np.zeros_like(r)
+        f = self.Khat(k) * self.Ghat(l, k) * w
+        flat = r.reshape(-1)
+        out = np.empty_like(flat)
+        for a in range(0, flat.size, 4096):
+            rr = flat[a:a + 4096]
+            kr = np.outer(rr, k)
+            with np.errstate(divide="ignore", invalid="ignore"):
+                s = np.where(kr > 0, np.sin(kr) / np.where(kr > 0, kr, 1.0), 1.0)
+            out[a:a + 4096] = (s * (f * k ** 2)[None, :]).sum(axis=1) / (2.0 * np.pi ** 2)
+        return out.reshape(r.shape)
+
+    def M0_at_zero(self, l: int) -> float:
+        return float(self.M(l, np.array([0.0]))[0])
+
+    def D(self, l: int, r):
+        return self.M(l + 1, r) - self.M(l, r)
+
+    def R(self, l: int, r):
+        """Residual kernel R_l = K - M_l (r > 0)."""
+        r = np.asarray(r, dtype=np.float64)
+        return self.K(r) - self.M(l, r)
