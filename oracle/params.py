@@ -49,9 +49,10 @@ class Params:
 
 def for_eps(eps: float) -> Params:
     row = None
-    for r in TABLE1:
-        if r[0] >= eps * (1 - 1e-9):
+    for r in TABLE1:                       # the loosest row at least as tight as eps
+        if r[0] <= eps * (1 + 1e-9):
             row = r
+            break
     if row is None:
         raise ValueError(f"eps={eps} tighter than Table 1 supports")
     e, c, N1, p = row

@@ -103,12 +103,12 @@ class Plan:
     """A dmk_plan_t: tree, lists and tables for one point set (sources = targets)."""
 
     def __init__(self, points, eps: float = 1e-6, leaf_capacity: int = 200, kernel: str = "laplace",
-                 stream=None):
+                 lam: float = 0.0, stream=None):
         ptr, mem, keep = _placement(points)
         n = keep.shape[0]
         if keep.ndim != 2 or keep.shape[1] != 3:
             raise DmkError("points must have shape (n, 3)")
-        opt = _Options(int(leaf_capacity), 0, 0.0, stream)
+        opt = _Options(int(leaf_capacity), 0, float(lam), stream)
         h = ctypes.c_void_p()
         _check(lib().dmk_plan(3, KERNELS[kernel], float(eps), int(n), ptr, mem, ctypes.byref(opt),
                               ctypes.byref(h)), "dmk_plan")
@@ -116,7 +116,7 @@ class Plan:
         self.n = int(n)
 
     def eval(self, charges, out=None):
-        """Potentials u_i = sum_{j: x_j != x_i} rho_j / |x_i - x_j| (caller order)."""
+        """Potentials u_i = sum_{j: x_j != x_i} K(|x_i - x_j|) rho_j (caller order)."""
         qptr, mem, qkeep = _placement(charges)
         if qkeep.shape != (self.n,):
             raise DmkError("charges must have shape (n,)")
@@ -176,8 +176,9 @@ class Plan:
         self.close()
 
 
-def dmk_plan(points, eps: float = 1e-6, leaf_capacity: int = 200, kernel: str = "laplace", stream=None) -> Plan:
-    return Plan(points, eps=eps, leaf_capacity=leaf_capacity, kernel=kernel, stream=stream)
+def dmk_plan(points, eps: float = 1e-6, leaf_capacity: int = 200, kernel: str = "laplace", lam: float = 0.0,
+             stream=None) -> Plan:
+    return Plan(points, eps=eps, leaf_capacity=leaf_capacity, kernel=kernel, lam=lam, stream=stream)
 
 
 def dmk_eval(plan: Plan, charges, out=None):

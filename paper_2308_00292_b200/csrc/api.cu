@@ -81,7 +81,11 @@ int dmk_plan(int dim, int kernel, double eps, int64_t n, const double* points, i
     if (mem != DMK_MEM_DEVICE && mem != DMK_MEM_HOST) fail(DMK_ERR_ARG, "bad mem");
     if (!(eps > 0)) fail(DMK_ERR_ARG, "eps must be > 0");
     if (dim != 3) fail(DMK_ERR_UNSUPPORTED, "only dim = 3 is implemented");
-    if (kernel != DMK_KERNEL_LAPLACE) fail(DMK_ERR_UNSUPPORTED, "only DMK_KERNEL_LAPLACE is implemented");
+    if (kernel != DMK_KERNEL_LAPLACE && kernel != DMK_KERNEL_YUKAWA)
+      fail(DMK_ERR_UNSUPPORTED, "kernel not implemented in 3D (DMK_KERNEL_LAPLACE, DMK_KERNEL_YUKAWA)");
+    if (kernel == DMK_KERNEL_YUKAWA && !(opt && opt->lambda > 0))
+      fail(DMK_ERR_ARG, "DMK_KERNEL_YUKAWA needs opt->lambda > 0");
+    if (snap_eps(eps) == 0) fail(DMK_ERR_UNSUPPORTED, "eps tighter than 1e-9 is not supported");
     require_device();
     dmk_plan_s* P = new dmk_plan_s();
     try {
@@ -93,12 +97,12 @@ int dmk_plan(int dim, int kernel, double eps, int64_t n, const double* points, i
         if (opt->leaf_capacity < 1) fail(DMK_ERR_ARG, "leaf_capacity must be >= 1");
         P->ns = opt->leaf_capacity;
         P->stream = (cudaStream_t)opt->stream;
+        P->lambda = opt->lambda;
       }
       const char* pe = std::getenv("DMK_PROFILE");
       P->profile = pe && pe[0] == '1';
       const char* pt = std::getenv("DMK_PROFILE_TREE");
       P->profile_tree = pt && pt[0] == '1';
-      P->tab = &get_tables(kernel, eps);
       const double* dpts = points;
       DevBuf<double> tmp;
       if (mem == DMK_MEM_HOST) {
@@ -107,6 +111,9 @@ int dmk_plan(int dim, int kernel, double eps, int64_t n, const double* points, i
         dpts = tmp.p;
       }
       build_tree(P, dpts);
+      // tables after the tree: the Yukawa split runs in unit-root-cube coordinates,
+      // lambda' = lambda * side (K(side r') = exp(-lambda' r')/(side r'))
+      P->tab = &get_tables(kernel, eps, kernel == DMK_KERNEL_YUKAWA ? P->lambda * P->side : 0.0);
       alloc_eval_buffers(P);
       DMK_CUDA(cudaStreamSynchronize(P->stream));
     } catch (...) {

@@ -64,6 +64,8 @@ struct DevBuf {
 // ---------------------------------------------------------------- tables (Step 1)
 // Per-precision tables, computed on the host once and kept on the device.
 struct Tables {
+  int kernel = 0;
+  double lam = 0;          // Yukawa parameter in unit-root-cube coordinates (0 for 1/r)
   double eps = 0, c = 0;
   int p = 0, nf = 0, nf0 = 0;
   double RT = 0, P0 = 0;   // root window truncation radius and Fourier period
@@ -75,13 +77,16 @@ struct Tables {
   std::vector<double> W;        // [LMAX+1][nh][nh][nh] difference-kernel weights (|m1|,|m2|,|m3|)
   std::vector<double> W0;       // [nh0][nh0][nh0] root window weights
   std::vector<double> respoly;  // residual: M_L(r) r_L ~= sum_k a_k s^k, s = 2 r^2/r_L^2 - 1
-  double m0 = 0;                // psi(0)/c0 = r_L M_L(0)
+  std::vector<double> respoly_lv;   // [LMAX+1][respoly_deg+1]: per-level coefficients
+  int respoly_deg = 0;
+  double m0 = 0;                // r_0 M_0(0) (1/r: psi(0)/c0 at every level)
   // device copies
   double *dQr1 = nullptr, *dQr0 = nullptr, *dGr1 = nullptr, *dGr0 = nullptr, *dA = nullptr, *dW = nullptr,
-         *dW0 = nullptr;
+         *dW0 = nullptr, *dRespoly = nullptr;
   size_t wstride = 0;
 };
-const Tables& get_tables(int kernel, double eps);  // cached; throws via fail()
+const Tables& get_tables(int kernel, double eps, double lam);  // cached; throws via fail()
+double snap_eps(double eps);
 
 // ---------------------------------------------------------------- plan
 struct TreeHost {
@@ -95,7 +100,7 @@ struct TreeHost {
 
 struct dmk_plan_s {
   int dim = 3, kernel = 0, ns = 200;
-  double eps = 0;
+  double eps = 0, lambda = 0;   // lambda: Yukawa parameter in the caller's units
   int64_t n = 0;
   cudaStream_t stream = 0;
   const dmk::Tables* tab = nullptr;

@@ -907,15 +907,19 @@ __global__ void __launch_bounds__(AntMma<P>::NW * 32)
 struct ResPoly {
   double a[25];   // monomial coefficients in s = 2 r^2/r_L^2 - 1
 };
+constexpr int KER_LAPLACE = 0, KER_YUKAWA = 1;
 
-// FULL: root is a leaf -> plain 1/r (no far field).  Otherwise R_L(r) =
-// 1/r - m(r/r_L)/r_L for r < r_L, and the r = 0 (self / coincident) term is
-// -m(0)/r_L = -M_L(0) (Step 5 folded in).
-template <int K, bool FULL>
+// FULL: root is a leaf -> the kernel itself (no far field).  Otherwise the residual of
+// the SOURCE level L, R_L(r) = K(r) - m_L(r/r_L)/r_L for r < r_L
+// with K = 1/r (Eq. 3.66) or exp(-lam r)/r (Eq. 4.18), and the r = 0 (self / coincident)
+// term is -m_L(0)/r_L = -M_L(0) (Step 5 folded in).  1/r uses one polynomial for all
+// levels (rp, by value); Yukawa reads the level's coefficients from lvpoly.
+template <int K, int KER, bool FULL>
 __global__ void __launch_bounds__(128) k_p2p(DevTree t, const int32_t* __restrict__ items, int64_t nitems,
                                              const int32_t* __restrict__ doff, const int32_t* __restrict__ dlist,
                                              const double* __restrict__ q, const double* __restrict__ ufar,
                                              const int32_t* __restrict__ perm, double inv_side, ResPoly rp,
+                                             const double* __restrict__ lvpoly, double lam,
                                              double* __restrict__ unear, double* __restrict__ out) {
   __shared__ double4 ssrc[4][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -930,6 +934,9 @@ __global__ void __launch_bounds__(128) k_p2p(DevTree t, const int32_t* __restric
     const int S = dlist[e];
     const int L = t.level[S];
     const double irl = ldexp(1.0, L), two_irl2 = ldexp(2.0, 2 * L), rl2 = ldexp(1.0, -2 * L);
+    double a[K + 1];
+#pragma unroll
+    for (int j = 0; j <= K; ++j) a[j] = (KER == KER_YUKAWA) ? __ldg(lvpoly + L * (K + 1) + j) : rp.a[j];
     for (int s0 = t.start[S]; s0 < t.end[S]; s0 += 32) {
       const int ns = min(32, t.end[S] - s0);
       if (lane < ns) {
@@ -942,14 +949,21 @@ __global__ void __launch_bounds__(128) k_p2p(DevTree t, const int32_t* __restric
         const double dx = xt - sp.x, dy = yt - sp.y, dz = zt - sp.z;
         const double r2 = fma(dx, dx, fma(dy, dy, dz * dz));
         if (FULL) {
-          acc += r2 > 0.0 ? sp.w * rsqrt(r2) : 0.0;
+          if (r2 > 0.0) {
+            const double rinv = rsqrt(r2);
+            acc += (KER == KER_YUKAWA) ? sp.w * exp(-lam * r2 * rinv) * rinv : sp.w * rinv;
+          }
         } else if (r2 < rl2) {
           const double s = fma(r2, two_irl2, -1.0);
-          double pv = rp.a[K];
+          double pv = a[K];
 #pragma unroll
-          for (int j = K - 1; j >= 0; --j) pv = fma(pv, s, rp.a[j]);
-          const double rinv = r2 > 0.0 ? rsqrt(r2) : 0.0;
-          acc = fma(sp.w, fma(-pv, irl, rinv), acc);
+          for (int j = K - 1; j >= 0; --j) pv = fma(pv, s, a[j]);
+          double kv = 0.0;
+          if (r2 > 0.0) {
+            const double rinv = rsqrt(r2);
+            kv = (KER == KER_YUKAWA) ? exp(-lam * r2 * rinv) * rinv : rinv;
+          }
+          acc = fma(sp.w, fma(-pv, irl, kv), acc);
         }
       }
       __syncwarp();
@@ -1125,17 +1139,18 @@ static void run_eval(dmk_plan_s* PL) {
   }
 }
 
-// P2P dispatch on the residual-polynomial degree
-template <bool FULL>
+// P2P dispatch on the kernel and the residual-polynomial degree
+template <int KER, bool FULL>
 static void run_p2p_deg(dmk_plan_s* PL, double* out, const ResPoly& rp, int K) {
   DevTree dt = dev_tree(PL);
   int nb = (int)((PL->np2p + 3) / 4);
   if (nb == 0) return;
-#define DMK_P2P_CASE(KK)                                                                                    \
-  case KK:                                                                                                  \
-    k_p2p<KK, FULL><<<nb, 128, 0, PL->stream>>>(dt, PL->p2p_items.p, PL->np2p, PL->dlist_off.p, PL->dlist.p, \
-                                                 PL->q.p, PL->ufar.p, PL->perm.p, 1.0 / PL->side, rp,       \
-                                                 PL->unear.p, out);                                         \
+  const Tables& T = *PL->tab;
+#define DMK_P2P_CASE(KK)                                                                                          \
+  case KK:                                                                                                        \
+    k_p2p<KK, KER, FULL><<<nb, 128, 0, PL->stream>>>(dt, PL->p2p_items.p, PL->np2p, PL->dlist_off.p, PL->dlist.p, \
+                                                      PL->q.p, PL->ufar.p, PL->perm.p, 1.0 / PL->side, rp,        \
+                                                      T.dRespoly, T.lam, PL->unear.p, out);                       \
     break;
   switch (K) {
     DMK_P2P_CASE(4) DMK_P2P_CASE(6) DMK_P2P_CASE(8) DMK_P2P_CASE(10) DMK_P2P_CASE(12) DMK_P2P_CASE(14)
@@ -1167,8 +1182,15 @@ void eval_plan(dmk_plan_s* PL, const double* dcharges, double* dout) {
   int K = (int)poly.size() - 1;
   for (int k = 0; k <= K && k < 25; ++k) rp.a[k] = poly[k];
   tm.begin("p2p");
-  if (PL->th.nlevels == 1) run_p2p_deg<true>(PL, dout, rp, K);
-  else run_p2p_deg<false>(PL, dout, rp, K);
+  const bool full = PL->th.nlevels == 1;
+  if (PL->tab->kernel == DMK_KERNEL_YUKAWA) {
+    K = PL->tab->respoly_deg;
+    if (full) run_p2p_deg<KER_YUKAWA, true>(PL, dout, rp, K);
+    else run_p2p_deg<KER_YUKAWA, false>(PL, dout, rp, K);
+  } else {
+    if (full) run_p2p_deg<KER_LAPLACE, true>(PL, dout, rp, K);
+    else run_p2p_deg<KER_LAPLACE, false>(PL, dout, rp, K);
+  }
   tm.end();
 }
 

@@ -19,6 +19,8 @@
 //     polynomial in s = 2 t^2 - 1 ("piecewise polynomial approximation ... Estrin",
 //     PAPER.md:2002-2008), so R_L(r) = 1/r - m(r/r_L)/r_L for r < r_L (Eq. 3.66).
 #include <cmath>
+#include <functional>
+#include <tuple>
 #include <map>
 #include <mutex>
 
@@ -225,13 +227,61 @@ void upload(const std::vector<double>& h, double** d) {
   DMK_CUDA(cudaMemcpy(*d, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice));
 }
 
-Tables* build_tables(int kernel, double eps) {
-  if (kernel != DMK_KERNEL_LAPLACE) fail(DMK_ERR_UNSUPPORTED, "only DMK_KERNEL_LAPLACE is implemented");
+// Fit g(u), u in [0, 1], by a degree-K polynomial in s = 2u - 1 (Chebyshev interpolation,
+// then monomial form); the smallest even K <= 24 whose max error on a grid is <= tol.
+static std::vector<double> fit_poly_s(const std::function<double(double)>& g, double tol, int ncheck) {
+  std::vector<double> best;
+  std::vector<double> gv(ncheck + 1);
+  for (int i = 0; i <= ncheck; ++i) gv[i] = g((double)i / ncheck);
+  for (int K = 4; K <= 24; K += 2) {
+    std::vector<double> cc(K + 1, 0.0);   // Chebyshev coefficients in s
+    std::vector<double> gn(K + 1);
+    for (int j = 0; j <= K; ++j) gn[j] = g((std::cos(PI * (j + 0.5) / (K + 1)) + 1.0) / 2.0);
+    for (int k = 0; k <= K; ++k) {
+      double sum = 0;
+      for (int j = 0; j <= K; ++j) sum += gn[j] * std::cos(k * PI * (j + 0.5) / (K + 1));
+      cc[k] = (k == 0 ? 1.0 : 2.0) / (K + 1) * sum;
+    }
+    std::vector<double> mono(K + 1, 0.0), t0(K + 1, 0.0), t1(K + 1, 0.0), t2(K + 1, 0.0);
+    t0[0] = 1.0;
+    t1[1] = 1.0;
+    for (int k = 0; k <= K; ++k) {
+      const std::vector<double>& tk = (k == 0) ? t0 : t1;
+      for (int j = 0; j <= K; ++j) mono[j] += cc[k] * tk[j];
+      if (k >= 1) {   // t2 = 2 s t1 - t0, then shift
+        std::fill(t2.begin(), t2.end(), 0.0);
+        for (int j = 0; j < K; ++j) t2[j + 1] += 2.0 * t1[j];
+        for (int j = 0; j <= K; ++j) t2[j] -= t0[j];
+        t0 = t1;
+        t1 = t2;
+      }
+    }
+    double err = 0;
+    for (int i = 0; i <= ncheck; ++i) {
+      double s = 2.0 * i / ncheck - 1.0, v = 0;
+      for (int j = K; j >= 0; --j) v = v * s + mono[j];
+      err = std::fmax(err, std::fabs(v - gv[i]));
+    }
+    best = mono;
+    if (err <= tol) break;
+  }
+  return best;
+}
+
+Tables* build_tables(int kernel, double eps, double lam) {
+  if (kernel != DMK_KERNEL_LAPLACE && kernel != DMK_KERNEL_YUKAWA)
+    fail(DMK_ERR_UNSUPPORTED, "kernel not implemented in 3D (DMK_KERNEL_LAPLACE, DMK_KERNEL_YUKAWA)");
+  const bool yuk = kernel == DMK_KERNEL_YUKAWA;
   const Row* row = nullptr;
-  for (const Row& r : TABLE1)
-    if (r.eps >= eps * (1 - 1e-9)) row = &r;
+  for (const Row& r : TABLE1)   // the loosest row at least as tight as eps (reading R1)
+    if (r.eps <= eps * (1 + 1e-9)) {
+      row = &r;
+      break;
+    }
   if (!row) fail(DMK_ERR_UNSUPPORTED, "eps tighter than 1e-9 is not supported");
   Tables* T = new Tables();
+  T->kernel = kernel;
+  T->lam = yuk ? lam : 0.0;
   T->eps = row->eps;
   T->c = row->c;
   T->p = row->p;
@@ -260,7 +310,14 @@ Tables* build_tables(int kernel, double eps) {
     }
   }
 
-  // difference-kernel weights per level (Eq. 3.68)
+  // Fourier-space split (Eq. 3.68; Yukawa: Eq. 4.18 times 4 pi): Khat Ghat_l with
+  // Ghat_l(k) = psi(sqrt(k^2 + lam^2) r_l/c)/psi(0)
+  const double lam2 = T->lam * T->lam;
+  auto Ghat = [&](double rl, double k) { return P.eval(std::sqrt(k * k + lam2) * rl / c) / P.psi0; };
+  if (yuk && 0.5 * T->lam >= c)
+    fail(DMK_ERR_UNSUPPORTED, "Yukawa lambda * (root side) must be < 2 c (level-1 mollifier vanishes)");
+
+  // difference-kernel weights per level
   int nh = nf + 1;
   T->wstride = (size_t)nh * nh * nh;
   T->W.assign((LMAX + 1) * T->wstride, 0.0);
@@ -268,18 +325,26 @@ Tables* build_tables(int kernel, double eps) {
     double rl = std::ldexp(1.0, -l), rl1 = std::ldexp(1.0, -l - 1);
     double h = 2.0 * PI / (3.0 * rl);
     auto Dhat = [&](double k) {
+      if (yuk) return 4.0 * PI / (k * k + lam2) * (Ghat(rl1, k) - Ghat(rl, k));
       if (k == 0.0) return 2.0 * PI * P.c2 / P.c0 * (rl * rl - rl1 * rl1);
       return 4.0 * PI / P.psi0 * (P.eval(k * rl1 / c) - P.eval(k * rl / c)) / (k * k);
     };
     make_weights(nf, h, Dhat, &T->W[l * T->wstride]);
   }
-  // root window: psi(k r_1/c)/psi(0) * 8 pi sin^2(k R_T/2)/k^2
+  // root window: Ghat_1(k) That(k), That the transform of K truncated at R_T (Sec. 4.7):
+  //   1/r:            8 pi sin^2(k R_T/2)/k^2
+  //   e^{-lam r}/r:   4 pi/(k^2+lam^2) [1 - e^{-lam R_T}(cos k R_T + (lam/k) sin k R_T)]
   {
     int nh0 = nf0 + 1;
     T->W0.assign((size_t)nh0 * nh0 * nh0, 0.0);
-    double h0 = 2.0 * PI / T->P0, RT = T->RT;
+    double h0 = 2.0 * PI / T->P0, RT = T->RT, lm = T->lam;
     auto What = [&](double k) {
-      double G = P.eval(k * 0.5 / c) / P.psi0;
+      double G = Ghat(0.5, k);
+      if (yuk) {
+        double E = std::exp(-lm * RT);
+        if (k == 0.0) return G * 4.0 * PI / lam2 * (1.0 - E * (1.0 + lm * RT));
+        return G * 4.0 * PI / (k * k + lam2) * (1.0 - E * (std::cos(k * RT) + lm / k * std::sin(k * RT)));
+      }
       if (k == 0.0) return 2.0 * PI * RT * RT;
       double sn = std::sin(k * RT / 2.0);
       return G * 8.0 * PI * sn * sn / (k * k);
@@ -287,46 +352,56 @@ Tables* build_tables(int kernel, double eps) {
     make_weights(nf0, h0, What, T->W0.data());
   }
 
-  // residual polynomial in s = 2u - 1, u = t^2:  g(u) = m(sqrt u), m(t) = Phi(t)/t
-  T->m0 = P.psi0 / P.c0;
-  auto g = [&](double u) {
-    if (u <= 0.0) return T->m0;
-    double t = std::sqrt(u);
-    return P.Phi(t) / t;
-  };
-  for (int K = 4; K <= 24; K += 2) {
-    std::vector<double> cc(K + 1, 0.0);   // Chebyshev coefficients in s
-    for (int k = 0; k <= K; ++k) {
-      double sum = 0;
-      for (int j = 0; j <= K; ++j) {
-        double th = PI * (j + 0.5) / (K + 1);
-        sum += g((std::cos(th) + 1.0) / 2.0) * std::cos(k * th);
+  // residual R_L(r) = K(r) - M_L(r), r < r_L (Eq. 3.66 / Eq. 4.18): the device evaluates
+  // K directly and r_L M_L(t r_L) = g_L(u), u = t^2, as a polynomial in s = 2u - 1
+  // ("piecewise polynomial approximation ... Estrin").
+  //   1/r: g(u) = Phi(t)/t, the same at every level (scale invariance).
+  //   Yukawa: g_L from the radial inverse transform of Khat Ghat_L (Gauss-Legendre over
+  //   the support sqrt(k^2+lam^2) <= c/r_L), one polynomial per level.
+  if (!yuk) {
+    T->m0 = P.psi0 / P.c0;
+    auto g = [&](double u) {
+      if (u <= 0.0) return T->m0;
+      double t = std::sqrt(u);
+      return P.Phi(t) / t;
+    };
+    T->respoly = fit_poly_s(g, 1e-2 * T->eps * T->m0, 4000);
+    T->respoly_deg = (int)T->respoly.size() - 1;
+    T->respoly_lv.assign((size_t)(LMAX + 1) * (T->respoly_deg + 1), 0.0);
+    for (int l = 0; l <= LMAX; ++l)
+      for (int j = 0; j <= T->respoly_deg; ++j) T->respoly_lv[l * (T->respoly_deg + 1) + j] = T->respoly[j];
+  } else {
+    std::vector<double> gx, gw;
+    const int NQ = 300;
+    gauss_legendre(NQ, gx, gw);
+    std::vector<std::vector<double>> polys(LMAX + 1);
+    int deg = 0;
+    for (int l = 0; l <= LMAX; ++l) {
+      const double rl = std::ldexp(1.0, -l), kmax2 = (c / rl) * (c / rl) - lam2;
+      std::vector<double> kq(NQ), fq(NQ);   // nodes and weights * Khat Ghat_l
+      const double kmax = kmax2 > 0 ? std::sqrt(kmax2) : 0.0;
+      for (int i = 0; i < NQ; ++i) {
+        kq[i] = 0.5 * kmax * (gx[i] + 1.0);
+        fq[i] = 0.5 * kmax * gw[i] * 4.0 * PI / (kq[i] * kq[i] + lam2) * Ghat(rl, kq[i]);
       }
-      cc[k] = (k == 0 ? 1.0 : 2.0) / (K + 1) * sum;
+      auto Mr = [&](double r) {   // M_l(r)
+        double sum = 0;
+        for (int i = 0; i < NQ; ++i)
+          sum += fq[i] * kq[i] * kq[i] * (r > 0 ? std::sin(kq[i] * r) / (kq[i] * r) : 1.0);
+        return sum / (2.0 * PI * PI);
+      };
+      const double m0l = rl * Mr(0.0);
+      auto g = [&](double u) { return rl * Mr(std::sqrt(u) * rl); };
+      polys[l] = fit_poly_s(g, 1e-2 * T->eps * std::fmax(m0l, 1e-300), 600);
+      deg = std::max(deg, (int)polys[l].size() - 1);
+      if (l == 0) T->m0 = m0l;
     }
-    // Chebyshev -> monomial in s
-    std::vector<double> mono(K + 1, 0.0), t0(K + 1, 0.0), t1(K + 1, 0.0), t2(K + 1, 0.0);
-    t0[0] = 1.0;
-    t1[1] = 1.0;
-    for (int k = 0; k <= K; ++k) {
-      const std::vector<double>& tk = (k == 0) ? t0 : t1;
-      for (int j = 0; j <= K; ++j) mono[j] += cc[k] * tk[j];
-      if (k >= 1) {   // t2 = 2 s t1 - t0, then shift
-        std::fill(t2.begin(), t2.end(), 0.0);
-        for (int j = 0; j < K; ++j) t2[j + 1] += 2.0 * t1[j];
-        for (int j = 0; j <= K; ++j) t2[j] -= t0[j];
-        t0 = t1;
-        t1 = t2;
-      }
-    }
-    double err = 0;
-    for (int i = 0; i <= 4000; ++i) {
-      double u = i / 4000.0, s = 2.0 * u - 1.0, v = 0;
-      for (int j = K; j >= 0; --j) v = v * s + mono[j];
-      err = std::fmax(err, std::fabs(v - g(u)));
-    }
-    T->respoly = mono;
-    if (err <= 1e-2 * T->eps * T->m0) break;
+    T->respoly_deg = deg;
+    T->respoly_lv.assign((size_t)(LMAX + 1) * (deg + 1), 0.0);
+    for (int l = 0; l <= LMAX; ++l)
+      for (size_t j = 0; j < polys[l].size(); ++j) T->respoly_lv[l * (deg + 1) + j] = polys[l][j];
+    T->respoly = polys[LMAX];
+    T->respoly.resize(deg + 1, 0.0);
   }
 
   upload(T->Qr1, &T->dQr1);
@@ -336,23 +411,27 @@ Tables* build_tables(int kernel, double eps) {
   upload(T->A, &T->dA);
   upload(T->W, &T->dW);
   upload(T->W0, &T->dW0);
+  upload(T->respoly_lv, &T->dRespoly);
   return T;
 }
 
 std::mutex g_mu;
-std::map<std::pair<int, double>, Tables*> g_cache;
+std::map<std::tuple<int, double, double>, Tables*> g_cache;
 
 }  // namespace
 
-const Tables& get_tables(int kernel, double eps) {
-  std::lock_guard<std::mutex> lk(g_mu);
-  double key_eps = 0;
+double snap_eps(double eps) {
   for (const Row& r : TABLE1)
-    if (r.eps >= eps * (1 - 1e-9)) key_eps = r.eps;
-  auto key = std::make_pair(kernel, key_eps);
+    if (r.eps <= eps * (1 + 1e-9)) return r.eps;
+  return 0;
+}
+
+const Tables& get_tables(int kernel, double eps, double lam) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto key = std::make_tuple(kernel, snap_eps(eps), kernel == DMK_KERNEL_YUKAWA ? lam : 0.0);
   auto it = g_cache.find(key);
   if (it != g_cache.end()) return *it->second;
-  Tables* T = build_tables(kernel, eps);
+  Tables* T = build_tables(kernel, eps, lam);
   g_cache[key] = T;
   return *T;
 }

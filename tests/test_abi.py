@@ -48,7 +48,12 @@ def test_bad_arguments_rejected(lib):
     assert lib.dmk_plan(3, 0, 1e-6, 4, None, 1, None, ctypes.byref(h)) == -1
     # unsupported dimension / kernel
     assert lib.dmk_plan(2, 0, 1e-6, 4, pts.ctypes.data, 1, None, ctypes.byref(h)) == -2
-    assert lib.dmk_plan(3, 1, 1e-6, 4, pts.ctypes.data, 1, None, ctypes.byref(h)) == -2
+    assert lib.dmk_plan(3, 2, 1e-6, 4, pts.ctypes.data, 1, None, ctypes.byref(h)) == -2   # log is 2D
+    # Yukawa needs lambda > 0
+    assert lib.dmk_plan(3, 1, 1e-6, 4, pts.ctypes.data, 1, None, ctypes.byref(h)) == -1
+    assert b"lambda" in lib.dmk_last_error()
+    # precision tighter than Table 1's 1e-9 row
+    assert lib.dmk_plan(3, 0, 1e-12, 4, pts.ctypes.data, 1, None, ctypes.byref(h)) == -2
     # eval on a null plan
     assert lib.dmk_eval(None, pts.ctypes.data, pts.ctypes.data, 1) == -1
     with pytest.raises(dmk.DmkError):

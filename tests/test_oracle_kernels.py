@@ -120,3 +120,11 @@ def test_compact_support_and_self_constant(eps):
         assert abs(S.R(l, rl * (1 - 1e-9))) < 1e-6 / rl
         # M_l(0) = psi(0)/(c0 r_l) is the r -> 0 limit (self-interaction constant)
         assert abs(S.M(l, 1e-9 * rl) - S.M0_at_zero(l)) < 1e-9 * S.M0_at_zero(l)
+
+
+def test_precision_snaps_to_next_tighter_row():
+    """Reading R1: a requested eps between Table 1 rows uses the next tighter row."""
+    assert params.for_eps(2e-6).eps == 1e-6 and params.for_eps(1e-3).eps == 1e-3
+    assert params.for_eps(0.5).eps == 1e-3 and params.for_eps(5e-8).eps == 1e-9
+    with pytest.raises(ValueError):
+        params.for_eps(1e-13)
