@@ -97,12 +97,12 @@ class Clocks:
                 "reasons": reasons, "samples": len(sm)}
 
 
-def stage_models(info, n, pairs, K):
-    """Algorithmic work per phase (DESIGN.md §6): (bound, amount, unit)."""
+def stage_models(info, n, pairs, K, inball):
+    """Algorithmic work per phase (DESIGN.md §8(d)): (bound, amount, unit)."""
     P, nf, nf0 = info.p, info.nf, info.nf0
-    n1, nh, n10, nh0 = 2 * nf + 1, nf + 1, 2 * nf0 + 1, nf0 + 1
     p3 = P ** 3
-    phi_bytes = 16 * (nh0 * n10 * n10 + (info.nfout - 1) * nh * n1 * n1)
+    # outgoing expansions, real parity-split form: 8 (nf+1)^3 doubles per box
+    phi_bytes = 8 * 8 * ((nf0 + 1) ** 3 + (info.nfout - 1) * (nf + 1) ** 3)
     return {
         "anterp": ("alu", 2.0 * p3 * n, "flop"),
         "c2p": ("alu", 2.0 * 3 * P ** 4 * (info.nfout - 1), "flop"),
@@ -110,7 +110,9 @@ def stage_models(info, n, pairs, K):
         "pwlocal": ("hbm", phi_bytes + 8.0 * p3 * info.nexp, "byte"),
         "p2c": ("alu", 2.0 * 3 * P ** 4 * (info.nexp - 1), "flop"),
         "eval": ("alu", 2.0 * p3 * n, "flop"),
-        "p2p": ("alu", float(pairs) * (2 * K + 16), "flop"),
+        # every list pair: distance test (9 flop); pairs inside the residual's ball
+        # r < r_L: polynomial (2K), rsqrt (~6), s and the accumulate (6)
+        "p2p": ("alu", 9.0 * pairs + (2.0 * K + 12.0) * inball, "flop"),
     }
 
 
@@ -122,6 +124,41 @@ def list_pairs(plan):
     per_box_src = np.add.reduceat(cnt[items], off[:-1]) if items.size else np.zeros(len(cnt))
     has = off[1:] > off[:-1]
     return int(np.sum(np.where(has, cnt * per_box_src, 0)))
+
+
+def inball_pairs(plan, x, dev):
+    """Number of (target, source) list pairs with |x_t - x_s| < r_L(source), counted on
+    the device with torch in padded box-pair batches (measurement only, not the
+    product path)."""
+    import numpy as np
+    import torch
+    inf = plan.info()
+    perm = plan.tree("perm")
+    xs = torch.as_tensor((x[perm] - np.asarray(inf.lo)) / inf.side, device=dev)
+    off, items = plan.tree("dlist_off"), plan.tree("dlist")
+    st, en, lev = plan.tree("box_start"), plan.tree("box_end"), plan.tree("box_level")
+    tb = np.repeat(np.arange(len(off) - 1), off[1:] - off[:-1])
+    sb = items
+    boxes = np.unique(np.concatenate([tb, sb]))
+    slot = np.full(len(st), -1, dtype=np.int64)
+    slot[boxes] = np.arange(len(boxes))
+    cnt = en[boxes] - st[boxes]
+    M = int(cnt.max())
+    idx = st[boxes][:, None] + np.arange(M)[None, :]
+    valid = np.arange(M)[None, :] < cnt[:, None]
+    idx = torch.as_tensor(np.where(valid, idx, 0), device=dev)
+    vt = torch.as_tensor(valid, device=dev)
+    pts = xs[idx]                                            # (nbox, M, 3)
+    tpts = torch.where(vt[..., None], pts, torch.full_like(pts, 1e10))
+    spts = torch.where(vt[..., None], pts, torch.full_like(pts, -1e10))
+    r2 = torch.as_tensor(4.0 ** (-lev[sb].astype(np.float64)), device=dev)
+    ts_, ss_ = torch.as_tensor(slot[tb], device=dev), torch.as_tensor(slot[sb], device=dev)
+    total = 0
+    chunk = max(1, 2 ** 26 // (M * M))
+    for a in range(0, len(sb), chunk):
+        d2 = torch.cdist(tpts[ts_[a:a + chunk]], spts[ss_[a:a + chunk]]) ** 2
+        total += int((d2 < r2[a:a + chunk, None, None]).sum())
+    return total
 
 
 def cpu_baseline(n_sample, eps, ns):
@@ -246,6 +283,7 @@ def main():
             info = plan.info()
             pairs = list_pairs(plan)
             u_last = u.cpu().numpy()
+            inball = inball_pairs(plan, x, dev) if rank == 0 else 0
         plan.close()
     launches = (L.dmk_kernel_launches(None) - launches0) // a.steps
     clocks = clk.stop()
@@ -292,7 +330,7 @@ def main():
 
     pk = peaks()
     fp64_peak = N_SM * FP64_FMA_PER_CLK_SM * 2 * pk.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
-    models = stage_models(info, a.n, pairs, info.respoly_degree)
+    models = stage_models(info, a.n, pairs, info.respoly_degree, inball)
     stages = {}
     for name, (bound, amount, unit) in models.items():
         ms = stage_ms.get(name)
@@ -329,7 +367,7 @@ def main():
         "stages_ms": {**{k: round(v, 4) for k, v in stage_ms.items()}, "tree_and_lists": round(tree_ms, 4)},
         "stages": stages,
         "tree": {"nbox": info.nbox, "nlevels": info.nlevels, "nfout": info.nfout, "nexp": info.nexp,
-                 "p2p_pairs": pairs},
+                 "p2p_pairs": pairs, "p2p_pairs_in_ball": inball},
     }
     if world == 1 and not a.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(a.cpu_sample, a.eps, a.ns)

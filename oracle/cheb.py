@@ -65,3 +65,12 @@ def apply3(mats, t):
     """Apply 1D matrices along the three axes of a (p,p,p)-like tensor:
     out[a,b,c] = sum_{ijk} M0[a,i] M1[b,j] M2[c,k] t[i,j,k]."""
     return np.einsum("ai,bj,ck,ijk->abc", mats[0], mats[1], mats[2], t, optimize=True)
+
+
+def applyd(mats, t):
+    """Apply 1D matrices along every axis of a d-dimensional tensor (d = len(mats))."""
+    d = len(mats)
+    ins = "ijk"[:d]
+    outs = "abc"[:d]
+    spec = ",".join(o + i for o, i in zip(outs, ins)) + "," + ins + "->" + outs
+    return np.einsum(spec, *mats, t, optimize=True)

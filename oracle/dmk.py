@@ -1,4 +1,5 @@
-"""The discrete DMK algorithm for the 3D Laplace and Yukawa kernels  (oracle; test infrastructure).
+"""The discrete DMK algorithm for the 3D Laplace and Yukawa kernels and the 2D log
+kernel  (oracle; test infrastructure).
 
 Follows "The full DMK algorithm for discrete sources", Sec. 3.5, PAPER.md:1414-1623,
 step by step and in the paper's order, with the PSWF kernel split of Sec. 3.6
@@ -16,10 +17,13 @@ step by step and in the paper's order, with the PSWF kernel split of Sec. 3.6
   Step 5  self-interaction corrections
 
 Kernels: 1/r with the PSWF split of Sec. 3.6 (LaplaceSplit), exp(-lam r)/r with the
-Fourier-space PSWF split of Sec. 4.6, Eq. 4.18 (YukawaSplit).  The points are mapped to
-the unit root cube (x -> (x - lo)/side); the kernel there is K_side(r') = K(side r') =
-exp(-(lam side) r')/(side r'), so the algorithm runs with lam' = lam * side and the
-result is divided by side (for 1/r: lam' = 0).
+Fourier-space PSWF split of Sec. 4.6, Eq. 4.18 (YukawaSplit), -log r in 2D with the same
+split at lam = 0 (LogSplit2D).  The points are mapped to the unit
+root box (x -> (x - lo)/side); the kernel there is K(side r'):
+  3D: exp(-(lam side) r')/(side r')  -> run with lam' = lam side, divide by side;
+  2D: -log r' - log side            -> subtract log(side) sum_{j: x_j != x_i} rho_j.
+The algorithm is written for general d (Sec. 3.5 states it so): 2^d children, 3^d
+colleagues, p^d Chebyshev tensors, (2 n_f + 1)^d plane waves.
 
 Readings: R2 Fourier spacing, R4 root window M_1 = W_0 + D_0,
 R5-R8 tree conventions, R9 coincident pairs, R10 root-leaf case (N <= n_s: plain
@@ -33,52 +37,75 @@ from __future__ import annotations
 import numpy as np
 
 from . import cheb
-from .kernels import LaplaceSplit, YukawaSplit, trapezoid_weights_3d, r_level
+from .kernels import LaplaceSplit, LogSplit2D, YukawaSplit, r_level, trapezoid_weights
 from .params import for_eps
 from .tree import Tree
 
 
-def _octant_sides(code: int):
-    """Child octant -> side (+-1) per axis; bit 2 = x, bit 1 = y, bit 0 = z."""
-    o = int(code) & 7
-    return [1 if (o >> (2 - d)) & 1 else -1 for d in range(3)]
+def _octant_sides(code: int, d: int = 3):
+    """Child orthant -> side (+-1) per axis; bit d-1-k of the child index is axis k."""
+    o = int(code) & (2 ** d - 1)
+    return [1 if (o >> (d - 1 - k)) & 1 else -1 for k in range(d)]
 
 
 def dmk_laplace3d(points, charges, eps: float, ns: int, return_stages: bool = False):
     """u_i = sum_{j != i} rho_j / |x_i - x_j| by DMK.  points (N,3), charges (N,)."""
-    return dmk3d(points, charges, eps, ns, "laplace", 0.0, return_stages)
+    return dmk(points, charges, eps, ns, "laplace", 0.0, return_stages)
 
 
 def dmk_yukawa3d(points, charges, eps: float, ns: int, lam: float, return_stages: bool = False):
     """u_i = sum_{j != i} rho_j exp(-lam |x_i - x_j|)/|x_i - x_j| by DMK."""
-    return dmk3d(points, charges, eps, ns, "yukawa", lam, return_stages)
+    return dmk(points, charges, eps, ns, "yukawa", lam, return_stages)
 
 
-def dmk3d(points, charges, eps: float, ns: int, kernel: str = "laplace", lam: float = 0.0,
-          return_stages: bool = False):
-    prm = for_eps(eps)
+def dmk_log2d(points, charges, eps: float, ns: int, return_stages: bool = False):
+    """u_i = -sum_{j: x_j != x_i} rho_j log|x_i - x_j| by DMK.  points (N,2)."""
+    return dmk(points, charges, eps, ns, "log", 0.0, return_stages)
+
+
+def dmk3d(points, charges, eps, ns, kernel="laplace", lam=0.0, return_stages=False):
+    return dmk(points, charges, eps, ns, kernel, lam, return_stages)
+
+
+def _finish(T, us, rho, kernel, coinc_sum):
+    """Back from the unit root box to the caller's units and order."""
+    u = np.empty(T.N)
+    if kernel == "log":
+        u[T.perm] = us - np.log(T.side) * (np.sum(rho) - coinc_sum)
+    else:
+        u[T.perm] = us / T.side
+    return u
+
+
+def dmk(points, charges, eps: float, ns: int, kernel: str = "laplace", lam: float = 0.0,
+        return_stages: bool = False):
     T = Tree(points, ns)                                   # Step 0
-    if kernel == "laplace":
+    D = T.d
+    prm = for_eps(eps, D)
+    if kernel == "laplace" and D == 3:
         split = LaplaceSplit(prm.c)
         K = lambda r: 1.0 / r
-    elif kernel == "yukawa":
+    elif kernel == "yukawa" and D == 3:
         split = YukawaSplit(prm.c, lam * T.side)
         K = split.K
+    elif kernel == "log" and D == 2:
+        split = LogSplit2D(prm.c)
+        K = split.K
     else:
-        raise ValueError(kernel)
+        raise ValueError(f"kernel {kernel} in {D}D")
     rho = np.asarray(charges, dtype=np.float64)[T.perm]
     X = T.xs
     N = T.N
     st = {"tree": T, "params": prm, "split": split}
     if T.box_leaf[0]:                                      # reading R10: root is a leaf
-        d = X[:, None, :] - X[None, :, :]
-        r = np.sqrt(np.einsum("ijk,ijk->ij", d, d))
+        dx = X[:, None, :] - X[None, :, :]
+        r = np.sqrt(np.einsum("ijk,ijk->ij", dx, dx))
         with np.errstate(divide="ignore"):
             inv = np.where(r > 0.0, K(np.where(r > 0.0, r, 1.0)), 0.0)
         us = inv @ rho
-        u = np.empty(N)
-        u[T.perm] = us / T.side
+        coinc_sum = (r == 0.0) @ rho
         st.update(u_far=np.zeros(N), u_near=us, u_self=np.zeros(N))
+        u = _finish(T, us, rho, kernel, coinc_sum)
         return (u, st) if return_stages else u
 
     p = prm.p
@@ -91,9 +118,9 @@ def dmk3d(points, charges, eps: float, ns: int, kernel: str = "laplace", lam: fl
     for l in range(T.nlevels):
         h, nf = prm.h(l), prm.nfl(l)
         if l == 0:
-            w = trapezoid_weights_3d(lambda k: split.What_root(k, prm.RT), h, nf)
+            w = trapezoid_weights(lambda k: split.What_root(k, prm.RT), h, nf, D)
         else:
-            w = trapezoid_weights_3d(lambda k, l=l: split.Dhat(l, k), h, nf)
+            w = trapezoid_weights(lambda k, l=l: split.Dhat(l, k), h, nf, D)
         m = np.arange(-nf, nf + 1, dtype=np.float64)
         s = r_level(l)
         E_out = np.exp(-1j * h * np.outer(m, xn * s / 2.0))     # T_prox2pw 1D factor (N1, p)
@@ -101,22 +128,29 @@ def dmk3d(points, charges, eps: float, ns: int, kernel: str = "laplace", lam: fl
         shift = {dd: np.exp(1j * h * m * dd * s) for dd in (-1, 0, 1)}   # T_pwshift factors
         lev[l] = dict(h=h, nf=nf, w=w, E_out=E_out, E_in=E_in, shift=shift)
 
+    def outer_shift(L, dd):
+        out = L["shift"][dd[0]]
+        for k in range(1, D):
+            out = np.multiply.outer(out, L["shift"][dd[k]])
+        return out
+
     # ---- Step 2: upward pass -----------------------------------------------
     proxy = {}
     for i in np.nonzero(T.box_leaf & (T.box_npts > 0))[0]:
         a, b = T.box_start[i], T.box_end[i]
         c, s = T.center(i), r_level(T.box_level[i])
-        U = [cheb.interp_matrix(2.0 * (X[a:b, d] - c[d]) / s, p) for d in range(3)]
-        proxy[i] = np.einsum("ja,jb,jc,j->abc", U[0], U[1], U[2], rho[a:b], optimize=True)
+        U = [cheb.interp_matrix(2.0 * (X[a:b, k] - c[k]) / s, p) for k in range(D)]
+        spec = ",".join("j" + "abc"[k] for k in range(D)) + ",j->" + "abc"[:D]
+        proxy[i] = np.einsum(spec, *U, rho[a:b], optimize=True)
     for l in range(T.nlevels - 2, -1, -1):
         for i in range(T.level_offset[l], T.level_offset[l + 1]):
             if T.box_leaf[i] or T.box_npts[i] == 0:
                 continue
-            acc = np.zeros((p, p, p))
+            acc = np.zeros((p,) * D)
             for ch in T.box_children[i]:
                 if ch >= 0 and ch in proxy:
-                    sd = _octant_sides(T.box_code[ch])
-                    acc += cheb.apply3([C2P[sd[0]], C2P[sd[1]], C2P[sd[2]]], proxy[ch])
+                    sd = _octant_sides(T.box_code[ch], D)
+                    acc += cheb.applyd([C2P[sd[k]] for k in range(D)], proxy[ch])
             proxy[i] = acc
     st["proxy"] = proxy
 
@@ -128,34 +162,33 @@ def dmk3d(points, charges, eps: float, ns: int, kernel: str = "laplace", lam: fl
         rng_ = range(T.level_offset[l], T.level_offset[l + 1])
         for i in rng_:                                    # outgoing expansions
             if T.fout[i]:
-                Phi[i] = cheb.apply3([L["E_out"]] * 3, proxy[i])
+                Phi[i] = cheb.applyd([L["E_out"]] * D, proxy[i])
         for i in rng_:                                    # incoming expansions
             if T.fin[i]:
                 acc = np.zeros_like(L["w"], dtype=np.complex128)
                 for sb in T.pwlist[i]:
                     dd = T.box_coords[i] - T.box_coords[sb]
-                    sh = (L["shift"][dd[0]][:, None, None] * L["shift"][dd[1]][None, :, None]
-                          * L["shift"][dd[2]][None, None, :])
-                    acc += L["w"] * sh * Phi[sb]
+                    acc += L["w"] * outer_shift(L, dd) * Phi[sb]
                 Psi[i] = acc
         for i in rng_:                                    # local expansions
             if T.box_npts[i] == 0:
                 continue
-            lam = np.zeros((p, p, p))
+            lam_ = np.zeros((p,) * D)
             if T.fin[i]:
-                vals = cheb.apply3([L["E_in"]] * 3, Psi[i]).real
-                lam += cheb.apply3([Vi, Vi, Vi], vals)
+                vals = cheb.applyd([L["E_in"]] * D, Psi[i]).real
+                lam_ += cheb.applyd([Vi] * D, vals)
             par = T.box_parent[i]                         # split from parent (Eq. 3.46)
             if par >= 0 and par in local:
-                sd = _octant_sides(T.box_code[i])
-                lam += cheb.apply3([P2C[sd[0]], P2C[sd[1]], P2C[sd[2]]], local[par])
-            local[i] = lam
+                sd = _octant_sides(T.box_code[i], D)
+                lam_ += cheb.applyd([P2C[sd[k]] for k in range(D)], local[par])
+            local[i] = lam_
         for i in rng_:                                    # evaluate at leaf targets
             if T.box_leaf[i] and T.box_npts[i] > 0:
                 a, b = T.box_start[i], T.box_end[i]
                 c, s = T.center(i), r_level(l)
-                E = [cheb.vander(2.0 * (X[a:b, d] - c[d]) / s, p) for d in range(3)]
-                u_far[a:b] = np.einsum("ja,jb,jc,abc->j", E[0], E[1], E[2], local[i], optimize=True)
+                E = [cheb.vander(2.0 * (X[a:b, k] - c[k]) / s, p) for k in range(D)]
+                spec = ",".join("j" + "abc"[k] for k in range(D)) + "," + "abc"[:D] + "->j"
+                u_far[a:b] = np.einsum(spec, *E, local[i], optimize=True)
     st.update(Phi=Phi, Psi=Psi, local=local)
 
     # ---- Step 4: direct interactions (residual kernel of the SOURCE level) ----
@@ -164,21 +197,22 @@ def dmk3d(points, charges, eps: float, ns: int, kernel: str = "laplace", lam: fl
         a, b = T.box_start[i], T.box_end[i]
         for sb in T.dlist[i]:
             sa, se = T.box_start[sb], T.box_end[sb]
-            d = X[a:b, None, :] - X[None, sa:se, :]
-            r = np.sqrt(np.einsum("ijk,ijk->ij", d, d))
+            dx = X[a:b, None, :] - X[None, sa:se, :]
+            r = np.sqrt(np.einsum("ijk,ijk->ij", dx, dx))
             R = np.where(r > 0.0, split.R(int(T.box_level[sb]), np.where(r > 0, r, 1.0)), 0.0)
             u_near[a:b] += R @ rho[sa:se]
 
     # ---- Step 5: self-interaction corrections --------------------------------
     u_self = np.zeros(N)
+    coinc_sum = np.zeros(N)
     for i in np.nonzero(T.box_leaf & (T.box_npts > 0))[0]:
         a, b = T.box_start[i], T.box_end[i]
-        d = X[a:b, None, :] - X[None, a:b, :]
-        coinc = np.all(d == 0.0, axis=2)
-        u_self[a:b] -= split.M0_at_zero(int(T.box_level[i])) * (coinc @ rho[a:b])
+        dx = X[a:b, None, :] - X[None, a:b, :]
+        coinc = np.all(dx == 0.0, axis=2)
+        coinc_sum[a:b] = coinc @ rho[a:b]
+        u_self[a:b] -= split.M0_at_zero(int(T.box_level[i])) * coinc_sum[a:b]
 
     us = u_far + u_near + u_self
-    u = np.empty(N)
-    u[T.perm] = us / T.side
     st.update(u_far=u_far, u_near=u_near, u_self=u_self)
+    u = _finish(T, us, rho, kernel, coinc_sum)
     return (u, st) if return_stages else u

@@ -205,3 +205,99 @@ class YukawaSplit:
         """Residual kernel R_l = K - M_l (r > 0)."""
         r = np.asarray(r, dtype=np.float64)
         return self.K(r) - self.M(l, r)
+
+
+def trapezoid_weights(fhat_radial, h: float, nf: int, d: int):
+    """Weights (h/2pi)^d fhat(h|m|) on m in [-nf, nf]^d (Eq. 3.37, reading R2)."""
+    if d == 3:
+        return trapezoid_weights_3d(fhat_radial, h, nf)
+    m = np.arange(-nf, nf + 1, dtype=np.float64)
+    kk = h * np.sqrt(m[:, None] ** 2 + m[None, :] ** 2)
+    return (h / (2.0 * np.pi)) ** 2 * fhat_radial(kk)
+
+
+def fourier_sum_2d(w, h: float, nf: int, x):
+    x = np.atleast_2d(np.asarray(x, dtype=np.float64))
+    m = np.arange(-nf, nf + 1, dtype=np.float64)
+    e = [np.exp(1j * h * np.outer(x[:, d], m)) for d in range(2)]
+    return np.einsum("ab,na,nb->n", w, e[0], e[1], optimize=True).real
+
+
+class LogSplit2D:
+    """PSWF kernel split of the 2D kernel K(r) = -log r in Fourier space (Sec. 4.6,
+    PAPER.md:2441-2447: Eq. 4.18 with lam = 0 "provides an efficient kernel splitting
+    for ... log(r)"):
+
+        Khat(k) = 2 pi/k^2 (-log r = 2 pi G_L, Ghat_L = 1/k^2, Eq. 4.16 in 2D)
+        Ghat_l(k) = psi(k r_l/c)/psi(0),  Dhat_l = Khat (Ghat_{l+1} - Ghat_l)
+        Dhat_l(0) = pi (c2/c0) (r_l^2 - r_{l+1}^2)
+
+    (the k -> 0 limit, with psi''(0)/psi(0) = -c^2 c2/c0 as in Eq. 3.68).  In physical
+    space (2D radial inverse transform f(r) = 1/(2 pi) int fhat(k) J_0(kr) k dk):
+        M_l(r) = M_l(0) + int_0^{c/r_l} Ghat_l(k) (J_0(kr) - 1)/k dk,
+        M_l(0) = -log r_l + log(c/2) + gamma + int_0^1 (psi(x)/psi(0) - 1)/x dx,
+    the constant being the one for which M_l(r) + log r -> 0 as r -> inf (the
+    distributional transform of -log r; uses int_0^X (1 - J_0(u))/u du = log(X/2) +
+    gamma + o(1)).  R_L = K - M_L.  Root window (reading R4, Sec. 4.7): the transform of
+    -log r truncated at R_T,
+        That(k) = 2 pi (1 - J_0(k R_T))/k^2 - 2 pi R_T log(R_T) J_1(k R_T)/k,
+        That(0) = pi R_T^2/2 - pi R_T^2 log R_T."""
+
+    NQ = 400
+
+    def __init__(self, c: float):
+        from scipy.special import j0, j1
+        self._j0, self._j1 = j0, j1
+        self.psi = Pswf(c)
+        self.c = self.psi.c
+        x, w = np.polynomial.legendre.leggauss(self.NQ)
+        self._gx, self._gw = 0.5 * (x + 1.0), 0.5 * w          # on [0, 1]
+        g = self.psi(self._gx) / self.psi.psi0
+        self.kappa = np.log(self.c / 2.0) + np.euler_gamma + np.sum(self._gw * (g - 1.0) / self._gx)
+
+    def K(self, r):
+        r = np.asarray(r, dtype=np.float64)
+        with np.errstate(divide="ignore"):
+            return -np.log(r)
+
+    def Ghat(self, l: int, k):
+        return self.psi(np.asarray(k, dtype=np.float64) * r_level(l) / self.c) / self.psi.psi0
+
+    def Dhat(self, l: int, k):
+        k = np.asarray(k, dtype=np.float64)
+        p = self.psi
+        rl, rl1 = r_level(l), r_level(l + 1)
+        with np.errstate(divide="ignore", invalid="ignore"):
+            v = 2.0 * np.pi * (self.Ghat(l + 1, k) - self.Ghat(l, k)) / k ** 2
+        v0 = np.pi * p.c2 / p.c0 * (rl ** 2 - rl1 ** 2)
+        return np.where(k == 0.0, v0, v)
+
+    def What_root(self, k, RT: float):
+        k = np.asarray(k, dtype=np.float64)
+        with np.errstate(divide="ignore", invalid="ignore"):
+            T = (2.0 * np.pi * (1.0 - self._j0(k * RT)) / k ** 2
+                 - 2.0 * np.pi * RT * np.log(RT) * self._j1(k * RT) / k)
+        T0 = np.pi * RT ** 2 / 2.0 - np.pi * RT ** 2 * np.log(RT)
+        return self.Ghat(1, k) * np.where(k == 0.0, T0, T)
+
+    def M0_at_zero(self, l: int) -> float:
+        return -np.log(r_level(l)) + self.kappa
+
+    def M(self, l: int, r):
+        r = np.asarray(r, dtype=np.float64)
+        kmax = self.c / r_level(l)
+        k, w = kmax * self._gx, kmax * self._gw
+        f = w * self.Ghat(l, k) / k
+        flat = r.reshape(-1)
+        out = np.empty_like(flat)
+        for a in range(0, flat.size, 4096):
+            kr = np.outer(flat[a:a + 4096], k)
+            out[a:a + 4096] = ((self._j0(kr) - 1.0) * f[None, :]).sum(axis=1)
+        return out.reshape(r.shape) + self.M0_at_zero(l)
+
+    def D(self, l: int, r):
+        return self.M(l + 1, r) - self.M(l, r)
+
+    def R(self, l: int, r):
+        r = np.asarray(r, dtype=np.float64)
+        return self.K(r) - self.M(l, r)

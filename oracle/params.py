@@ -9,7 +9,7 @@ table's h_0 = 1.33 pi (= 4 pi/3, Eq. 3.30) is off by the factor 2 of a
 half-width box convention.  With that spacing the table's N_1 and p reproduce
 eps (tests/test_oracle_kernels.py pins this).
 
-Root level (reading R4): windowed M_1, truncation radius R_T = (1 + sqrt 3) r_0
+Root level (reading R4): windowed M_1, truncation radius R_T = (1 + sqrt d) r_0
 (PAPER.md:2485), period P_0 = 1 + R_T + r_1, n_f0 = ceil(2 c P_0 / (2 pi)).
 Precisions not in the table snap to the next tighter tabulated one.
 """
@@ -47,7 +47,7 @@ class Params:
         return self.nf0 if l == 0 else self.nf
 
 
-def for_eps(eps: float) -> Params:
+def for_eps(eps: float, d: int = 3) -> Params:
     row = None
     for r in TABLE1:                       # the loosest row at least as tight as eps
         if r[0] <= eps * (1 + 1e-9):
@@ -56,7 +56,7 @@ def for_eps(eps: float) -> Params:
     if row is None:
         raise ValueError(f"eps={eps} tighter than Table 1 supports")
     e, c, N1, p = row
-    RT = 1.0 + math.sqrt(3.0)
+    RT = 1.0 + math.sqrt(d)            # (1 + sqrt d) r_0
     P0 = 1.0 + RT + 0.5
     nf0 = int(math.ceil(2.0 * c * P0 / (2.0 * math.pi)))
     return Params(eps=e, c=c, nf=(N1 - 1) // 2, p=p, RT=RT, P0=P0, nf0=nf0)

@@ -1,4 +1,5 @@
-"""Level-restricted adaptive octree and interaction lists  (oracle; test infrastructure).
+"""Level-restricted adaptive 2^d-tree (d = 3 octree, d = 2 quadtree) and interaction
+lists  (oracle; test infrastructure).
 
 Paper: Sec. 3.2 (adaptive refinement until a leaf holds at most
 n_s points, level restriction, colleagues C(B), coarse neighbours N(B)),
@@ -11,7 +12,9 @@ Conventions (readings R5-R8 in DESIGN.md):
   * Root cube: lo_d = min_i x_{i,d}; side = max_d (max_i x_{i,d} - lo_d) (1 if 0).
     Integer coordinates q_d = floor((x_d - lo_d) * (2^21 / side)) clipped to
     [0, 2^21 - 1]; Morton key interleaves bits with x most significant in each
-    triple.  Points are stably sorted by key.
+    d-tuple (63-bit keys in 3D, 42-bit in 2D).  Points are stably sorted by key.
+  * Everything below holds for d = 2 with 4 children / 9 colleagues in place of
+    8 / 27 (the paper's algorithm is stated for general d, Sec. 3.5).
   * A box is refined iff it holds more than n_s points (sources = targets) and its
     level is < LMAX.  "Share a boundary point" = closed boxes intersect.
   * 2:1 balance (level restriction): any level-l box that touches a non-leaf box
@@ -25,6 +28,8 @@ Conventions (readings R5-R8 in DESIGN.md):
     B's level-l ancestor, plus non-empty leaves at level L+1 touching B.
 """
 from __future__ import annotations
+
+import itertools
 
 import numpy as np
 
@@ -44,51 +49,65 @@ def normalize(points: np.ndarray):
     return lo, side, q
 
 
-def morton3(q: np.ndarray) -> np.ndarray:
-    """63-bit Morton key; bit 3b+2 = x bit b, 3b+1 = y bit b, 3b = z bit b."""
-    key = np.zeros(q.shape[0], dtype=np.int64)
+def morton(q: np.ndarray) -> np.ndarray:
+    """Morton key of integer coordinates q (n, d); bit d b + (d-1-k) = coordinate k bit b."""
+    n, d = q.shape
+    key = np.zeros(n, dtype=np.int64)
     for b in range(NBITS):
-        for d in range(3):
-            key |= ((q[:, d] >> b) & 1) << (3 * b + (2 - d))
+        for k in range(d):
+            key |= ((q[:, k] >> b) & 1) << (d * b + (d - 1 - k))
     return key
 
 
-def decode3(code: np.ndarray, level: int) -> np.ndarray:
-    """Box code at `level` -> integer box coordinates (n,3)."""
+def decode(code: np.ndarray, level: int, d: int = 3) -> np.ndarray:
+    """Box code at `level` -> integer box coordinates (n, d)."""
     code = np.asarray(code, dtype=np.int64)
-    out = np.zeros((code.shape[0], 3), dtype=np.int64)
+    out = np.zeros((code.shape[0], d), dtype=np.int64)
     for b in range(level):
-        for d in range(3):
-            out[:, d] |= ((code >> (3 * b + (2 - d))) & 1) << b
+        for k in range(d):
+            out[:, k] |= ((code >> (d * b + (d - 1 - k))) & 1) << b
     return out
 
 
-def encode3(c: np.ndarray, level: int) -> np.ndarray:
-    c = np.asarray(c, dtype=np.int64).reshape(-1, 3)
+def encode(c: np.ndarray, level: int, d: int = 3) -> np.ndarray:
+    c = np.asarray(c, dtype=np.int64).reshape(-1, d)
     code = np.zeros(c.shape[0], dtype=np.int64)
     for b in range(level):
-        for d in range(3):
-            code |= ((c[:, d] >> b) & 1) << (3 * b + (2 - d))
+        for k in range(d):
+            code |= ((c[:, k] >> b) & 1) << (d * b + (d - 1 - k))
     return code
 
 
+def morton3(q):
+    return morton(q)
+
+
+def decode3(code, level):
+    return decode(code, level, 3)
+
+
+def encode3(c, level):
+    return encode(c, level, 3)
+
+
 class Tree:
-    """Adaptive, level-restricted octree over one point set (sources = targets)."""
+    """Adaptive, level-restricted 2^d-tree over one point set (sources = targets)."""
 
     def __init__(self, points: np.ndarray, ns: int):
         pts = np.asarray(points, dtype=np.float64)
-        self.N = pts.shape[0]
+        self.N, self.d = pts.shape
+        self.nch, self.ncol = 2 ** self.d, 3 ** self.d
         self.ns = int(ns)
         self.lo, self.side, q = normalize(pts)
-        key = morton3(q)
+        key = morton(q)
         self.perm = np.argsort(key, kind="stable")          # sorted -> original
         self.keys = key[self.perm]
-        self.xs = (pts[self.perm] - self.lo) / self.side     # normalised coords in [0,1]^3
+        self.xs = (pts[self.perm] - self.lo) / self.side     # normalised coords in [0,1]^d
         self._build()
 
     # ------------------------------------------------------------------
     def _codes(self, l):
-        return self.keys >> (3 * (NBITS - l))
+        return self.keys >> (self.d * (NBITS - l))
 
     def _build(self):
         N, ns = self.N, self.ns
@@ -108,16 +127,14 @@ class Tree:
         if ltop >= 0:
             B[ltop] = U[ltop]
             for l in range(ltop - 1, -1, -1):
-                qc = decode3(B[l + 1], l + 1)
+                qc = decode(B[l + 1], l + 1, self.d)
                 lo_ = np.where(qc % 2 == 0, qc // 2 - 1, qc // 2)    # touching range per dim
                 cands = [U[l]]
                 n1 = 2 ** l
-                for ox in range(2):
-                    for oy in range(2):
-                        for oz in range(2):
-                            cc = lo_ + np.array([ox, oy, oz])
-                            ok = np.all((cc >= 0) & (cc < n1), axis=1)
-                            cands.append(encode3(cc[ok], l))
+                for o in itertools.product(range(2), repeat=self.d):
+                    cc = lo_ + np.array(o)
+                    ok = np.all((cc >= 0) & (cc < n1), axis=1)
+                    cands.append(encode(cc[ok], l, self.d))
                 B[l] = np.unique(np.concatenate(cands))
         self.nonleaf = B
         self.nlevels = ltop + 2 if ltop >= 0 else 1           # levels 0..nlevels-1 hold boxes
@@ -137,14 +154,14 @@ class Tree:
         self.box_level = np.concatenate(levels)
         self.box_code = np.concatenate(codes)
         nb = self.nbox = self.box_code.shape[0]
-        self.box_coords = np.zeros((nb, 3), dtype=np.int64)
+        self.box_coords = np.zeros((nb, self.d), dtype=np.int64)
         self.box_leaf = np.zeros(nb, dtype=bool)
         self.box_start = np.zeros(nb, dtype=np.int64)
         self.box_end = np.zeros(nb, dtype=np.int64)
         for l in range(self.nlevels):
             a, b = self.level_offset[l], self.level_offset[l + 1]
             cl = self.box_code[a:b]
-            self.box_coords[a:b] = decode3(cl, l)
+            self.box_coords[a:b] = decode(cl, l, self.d)
             self.box_leaf[a:b] = ~np.isin(cl, B[l]) if l <= ltop else True
             codes_l = self._codes(l)
             self.box_start[a:b] = np.searchsorted(codes_l, cl, side="left")
@@ -152,25 +169,22 @@ class Tree:
         self.box_npts = self.box_end - self.box_start
         # parent / children / colleagues
         self.box_parent = np.full(nb, -1, dtype=np.int64)
-        self.box_children = np.full((nb, 8), -1, dtype=np.int64)
-        self.box_colleagues = np.full((nb, 27), -1, dtype=np.int64)
+        self.box_children = np.full((nb, self.nch), -1, dtype=np.int64)
+        self.box_colleagues = np.full((nb, self.ncol), -1, dtype=np.int64)
         for i in range(nb):
             l = self.box_level[i]
             if l > 0:
-                p = self.find(l - 1, self.box_code[i] >> 3)
+                p = self.find(l - 1, self.box_code[i] >> self.d)
                 self.box_parent[i] = p
-                self.box_children[p, self.box_code[i] & 7] = i
+                self.box_children[p, self.box_code[i] & (self.nch - 1)] = i
         for i in range(nb):
             l = self.box_level[i]
             c = self.box_coords[i]
-            k = 0
-            for dx in (-1, 0, 1):
-                for dy in (-1, 0, 1):
-                    for dz in (-1, 0, 1):
-                        cc = c + np.array([dx, dy, dz])
-                        if np.all((cc >= 0) & (cc < 2 ** l)):
-                            self.box_colleagues[i, k] = self.find(l, encode3(cc, l)[0])
-                        k += 1
+            # colleague slot k enumerates offsets in {-1,0,1}^d, last axis fastest
+            for k, off in enumerate(itertools.product((-1, 0, 1), repeat=self.d)):
+                cc = c + np.array(off)
+                if np.all((cc >= 0) & (cc < 2 ** l)):
+                    self.box_colleagues[i, k] = self.find(l, encode(cc, l, self.d)[0])
         self.fout = (~self.box_leaf) & (self.box_npts > 0)
         # leaf of every (sorted) point
         self.point_leaf = np.full(self.N, -1, dtype=np.int64)
