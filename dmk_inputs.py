@@ -10,6 +10,8 @@ CUDA path consume these arrays; neither is imported here.
               standard-normal charges                             (config 2)
   sphere      uniform on the sphere of radius 0.45 centred at (0.5,0.5,0.5)
               (the paper's Sec. 5.1 surface distribution)
+  circle2d    2D: noisy circle, radius 0.4 + N(0, 1e-3), zero-mean U[-1,1] charges
+                                                                   (config 3)
 """
 from __future__ import annotations
 
@@ -46,7 +48,19 @@ def sphere(n: int, seed: int = 0, radius: float = 0.45):
     return x, q
 
 
-WORKLOADS = {"uniform": uniform, "clusters": clusters, "sphere": sphere}
+def circle2d(n: int, seed: int = 0, radius: float = 0.4, jitter: float = 1e-3):
+    """BASELINE config 3: N points on a noisy circle, radius 0.4 + N(0, jitter) about
+    (0.5, 0.5) in [0,1]^2; charges U[-1,1] shifted to zero mean."""
+    rng = np.random.default_rng(seed)
+    th = rng.uniform(0.0, 2.0 * np.pi, n)
+    r = radius + jitter * rng.standard_normal(n)
+    x = 0.5 + np.stack([r * np.cos(th), r * np.sin(th)], axis=1)
+    q = rng.uniform(-1.0, 1.0, size=n)
+    q -= q.mean()
+    return x, q
+
+
+WORKLOADS = {"uniform": uniform, "clusters": clusters, "sphere": sphere, "circle2d": circle2d}
 
 
 def make(kind: str, n: int, seed: int = 0):
