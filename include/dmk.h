@@ -112,7 +112,7 @@ typedef struct dmk_plan_info {
   double side;        /* root cube side */
   double c;           /* PSWF parameter (Table 1) */
   int32_t respoly_degree; /* degree of the residual-kernel polynomial */
-  int32_t reserved;
+  int32_t dim;            /* 2 or 3 */
 } dmk_plan_info;
 
 int dmk_plan_info_get(dmk_plan_t plan, dmk_plan_info* info);

@@ -46,7 +46,7 @@ class PlanInfo(ctypes.Structure):
                 ("p", ctypes.c_int32), ("nf", ctypes.c_int32), ("nf0", ctypes.c_int32),
                 ("nfout", ctypes.c_int64), ("nexp", ctypes.c_int64), ("ndlist", ctypes.c_int64),
                 ("lo", ctypes.c_double * 3), ("side", ctypes.c_double), ("c", ctypes.c_double),
-                ("respoly_degree", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+                ("respoly_degree", ctypes.c_int32), ("dim", ctypes.c_int32)]
 
 
 _lib = None
@@ -106,11 +106,12 @@ class Plan:
                  lam: float = 0.0, stream=None):
         ptr, mem, keep = _placement(points)
         n = keep.shape[0]
-        if keep.ndim != 2 or keep.shape[1] != 3:
-            raise DmkError("points must have shape (n, 3)")
+        if keep.ndim != 2 or keep.shape[1] not in (2, 3):
+            raise DmkError("points must have shape (n, 3) or (n, 2)")
+        dim = int(keep.shape[1])
         opt = _Options(int(leaf_capacity), 0, float(lam), stream)
         h = ctypes.c_void_p()
-        _check(lib().dmk_plan(3, KERNELS[kernel], float(eps), int(n), ptr, mem, ctypes.byref(opt),
+        _check(lib().dmk_plan(dim, KERNELS[kernel], float(eps), int(n), ptr, mem, ctypes.byref(opt),
                               ctypes.byref(h)), "dmk_plan")
         self._h = h
         self.n = int(n)
@@ -139,7 +140,7 @@ class Plan:
 
     def tree(self, which: str) -> np.ndarray:
         inf = self.info()
-        size = {"perm": inf.n, "colleagues": 27 * inf.nbox, "dlist_off": inf.nbox + 1,
+        size = {"perm": inf.n, "colleagues": (9 if inf.dim == 2 else 27) * inf.nbox, "dlist_off": inf.nbox + 1,
                 "dlist": inf.ndlist}.get(which, inf.nbox)
         out = np.empty(size, dtype=np.int64)
         _check(lib().dmk_tree_copy(self._h, TREE[which], out.ctypes.data), "dmk_tree_copy")

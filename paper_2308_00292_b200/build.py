@@ -7,7 +7,7 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
-SRC = ["api.cu", "tree.cu", "tables.cu", "kernels.cu"]
+SRC = ["api.cu", "tree.cu", "tables.cu", "kernels.cu", "kernels2d.cu"]
 LIB = os.path.join(HERE, "libdmk.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [

@@ -52,13 +52,17 @@ static void alloc_eval_buffers(dmk_plan_s* P) {
   P->q.alloc(P->n, s);
   P->ufar.alloc(P->n, s);
   P->unear.alloc(P->n, s);
-  // outgoing expansions in the real parity-split layout [a][pi][b][c] (kernels.cu)
-  P->phi_size0 = (int64_t)8 * (T.nf0 + 1) * (T.nf0 + 1) * (T.nf0 + 1);
-  P->phi_size1 = (int64_t)8 * (T.nf + 1) * (T.nf + 1) * (T.nf + 1);
+  // outgoing expansions in the real parity-split layout (2^d parity classes over the
+  // non-negative mode orthant, kernels.cu / kernels2d.cu)
+  const int64_t h0 = T.nf0 + 1, h1 = T.nf + 1;
+  const int64_t pd = P->dim == 2 ? (int64_t)T.p * T.p : p3;
+  P->phi_size0 = P->dim == 2 ? 4 * h0 * h0 : 8 * h0 * h0 * h0;
+  P->phi_size1 = P->dim == 2 ? 4 * h1 * h1 : 8 * h1 * h1 * h1;
+  P->scalar.alloc(1, s);
   if (P->th.nlevels > 1) {
-    P->mom.alloc(P->nfout * p3, s);
+    P->mom.alloc(P->nfout * pd, s);
     P->phi.alloc(P->phi_size0 + (P->nfout - 1) * P->phi_size1, s);
-    P->lam.alloc(P->nexp * p3, s);
+    P->lam.alloc(P->nexp * pd, s);
   }
 }
 
@@ -80,9 +84,11 @@ int dmk_plan(int dim, int kernel, double eps, int64_t n, const double* points, i
     if (n < 1 || n >= (int64_t)1 << 31) fail(DMK_ERR_ARG, "n must be in [1, 2^31)");
     if (mem != DMK_MEM_DEVICE && mem != DMK_MEM_HOST) fail(DMK_ERR_ARG, "bad mem");
     if (!(eps > 0)) fail(DMK_ERR_ARG, "eps must be > 0");
-    if (dim != 3) fail(DMK_ERR_UNSUPPORTED, "only dim = 3 is implemented");
-    if (kernel != DMK_KERNEL_LAPLACE && kernel != DMK_KERNEL_YUKAWA)
+    if (dim != 2 && dim != 3) fail(DMK_ERR_UNSUPPORTED, "dim must be 2 or 3");
+    if (dim == 3 && kernel != DMK_KERNEL_LAPLACE && kernel != DMK_KERNEL_YUKAWA)
       fail(DMK_ERR_UNSUPPORTED, "kernel not implemented in 3D (DMK_KERNEL_LAPLACE, DMK_KERNEL_YUKAWA)");
+    if (dim == 2 && kernel != DMK_KERNEL_LOG)
+      fail(DMK_ERR_UNSUPPORTED, "kernel not implemented in 2D (DMK_KERNEL_LOG)");
     if (kernel == DMK_KERNEL_YUKAWA && !(opt && opt->lambda > 0))
       fail(DMK_ERR_ARG, "DMK_KERNEL_YUKAWA needs opt->lambda > 0");
     if (snap_eps(eps) == 0) fail(DMK_ERR_UNSUPPORTED, "eps tighter than 1e-9 is not supported");
@@ -106,8 +112,8 @@ int dmk_plan(int dim, int kernel, double eps, int64_t n, const double* points, i
       const double* dpts = points;
       DevBuf<double> tmp;
       if (mem == DMK_MEM_HOST) {
-        tmp.alloc(3 * n, P->stream);
-        DMK_CUDA(cudaMemcpyAsync(tmp.p, points, 3 * n * sizeof(double), cudaMemcpyHostToDevice, P->stream));
+        tmp.alloc(dim * n, P->stream);
+        DMK_CUDA(cudaMemcpyAsync(tmp.p, points, dim * n * sizeof(double), cudaMemcpyHostToDevice, P->stream));
         dpts = tmp.p;
       }
       build_tree(P, dpts);
@@ -170,7 +176,8 @@ int dmk_plan_info_get(dmk_plan_t P, dmk_plan_info* info) {
     for (int d = 0; d < 3; ++d) info->lo[d] = P->lo[d];
     info->side = P->side;
     info->c = P->tab->c;
-    info->respoly_degree = (int32_t)P->tab->respoly.size() - 1;
+    info->respoly_degree = (int32_t)P->tab->respoly_deg;
+    info->dim = P->dim;
   });
 }
 
@@ -205,7 +212,7 @@ int dmk_tree_copy(dmk_plan_t P, int which, int64_t* out) {
         break;
       }
       case DMK_TREE_BOX_PARENT: copy_widen(s, P->box_parent.p, nb, out); break;
-      case DMK_TREE_COLLEAGUES: copy_widen(s, P->box_coll.p, 27 * nb, out); break;
+      case DMK_TREE_COLLEAGUES: copy_widen(s, P->box_coll.p, (P->dim == 2 ? 9 : 27) * nb, out); break;
       case DMK_TREE_DLIST_OFF: copy_widen(s, P->dlist_off.p, nb + 1, out); break;
       case DMK_TREE_DLIST: copy_widen(s, P->dlist.p, P->ndlist, out); break;
       case DMK_TREE_FOUT: copy_widen(s, P->fout_rank.p, nb, out); break;

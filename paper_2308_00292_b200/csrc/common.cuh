@@ -64,6 +64,7 @@ struct DevBuf {
 // ---------------------------------------------------------------- tables (Step 1)
 // Per-precision tables, computed on the host once and kept on the device.
 struct Tables {
+  int dim = 3;
   int kernel = 0;
   double lam = 0;          // Yukawa parameter in unit-root-cube coordinates (0 for 1/r)
   double eps = 0, c = 0;
@@ -140,6 +141,7 @@ struct dmk_plan_s {
 
   // eval buffers
   dmk::DevBuf<double> q, mom, phi, lam, ufar, unear;
+  dmk::DevBuf<double> scalar;             // device scratch scalar (2D: total charge)
   int64_t phi_size0 = 0, phi_size1 = 0;   // doubles per root / per other box
 
   // profiling
@@ -159,6 +161,7 @@ struct dmk_plan_s {
 
 namespace dmk {
 void resolve_timings(dmk_plan_s* P);
+void eval_plan_2d(dmk_plan_s* PL, double* dout);
 // cumulative number of libdmk kernel launches (this library's own kernels; the
 // CUB sort/scan/select kernels compiled into the library are counted separately)
 extern int64_t g_launches, g_cub_launches;

@@ -1,0 +1,156 @@
+// device.cuh -- device-side helpers shared by the 3D (kernels.cu) and 2D (kernels2d.cu)
+// DMK kernels: the tree view, Chebyshev vectors, the fp64 tensor-core (DMMA) tile
+// helper, point-range walks, launch helpers and phase timers.  Internal, not ABI.
+#pragma once
+#include <cstring>
+
+#include "common.cuh"
+
+namespace dmk {
+
+struct DevTree {
+  const uint64_t* code;
+  const int32_t* level;
+  const int32_t* start;
+  const int32_t* end;
+  const int32_t* parent;
+  const int32_t* child;
+  const int32_t* coll;
+  const uint8_t* flags;
+  const int32_t* fout_rank;
+  const int32_t* exp_rank;
+  const double* xs;
+  const double* ys;
+  const double* zs;
+};
+constexpr uint8_t F_LEAF = 1, F_OUT = 2, F_IN = 4, F_EXP = 8;
+
+__device__ __forceinline__ uint32_t compact3d(uint64_t x) {
+  x &= 0x1249249249249249ULL;
+  x = (x ^ (x >> 2)) & 0x10c30c30c30c30c3ULL;
+  x = (x ^ (x >> 4)) & 0x100f00f00f00f00fULL;
+  x = (x ^ (x >> 8)) & 0x1f0000ff0000ffULL;
+  x = (x ^ (x >> 16)) & 0x1f00000000ffffULL;
+  x = (x ^ (x >> 32)) & 0x1fffffULL;
+  return (uint32_t)x;
+}
+// centre of box (code, level) and the scale 2/side
+__device__ __forceinline__ void box_geom(uint64_t code, int l, double c[3], double& inv_half) {
+  double s = ldexp(1.0, -l);
+  c[0] = ((double)compact3d(code >> 2) + 0.5) * s;
+  c[1] = ((double)compact3d(code >> 1) + 0.5) * s;
+  c[2] = ((double)compact3d(code) + 0.5) * s;
+  inv_half = ldexp(1.0, l + 1);
+}
+
+__device__ __forceinline__ void cheb_vec(double x, double* T, int P, double scale0) {
+  // T[n] = scale0 * T_n(x)
+  double t0 = 1.0, t1 = x;
+  T[0] = scale0;
+  if (P > 1) T[1] = scale0 * x;
+  for (int n = 2; n < P; ++n) {
+    double t2 = 2.0 * x * t1 - t0;
+    T[n] = scale0 * t2;
+    t0 = t1;
+    t1 = t2;
+  }
+}
+
+// ---------------------------------------------------------------- fp64 tensor-core (DMMA) versions
+// mma.sync.m8n8k4 f64: A[row=lane>>2][col=lane&3], B[row=lane&3][col=lane>>2],
+// C[row=lane>>2][col=2*(lane&3)+{0,1}].  Measured on this B200: 37.2 TFLOP/s, the
+// same as DFMA, but 256 FMA per warp instruction from 2 register operands, which
+// takes the shared-memory bandwidth limit off these small per-box GEMMs.
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+// Warp-cooperative C = A B over 8x8 output tiles with K = 4 KS (zero padded by the
+// operand functors): fa(m, k), fb(k, n) return operand values, fc(m, n, c_n, c_{n+1})
+// consumes the two accumulators a lane owns.  Tiles are dealt round-robin to the warps.
+template <int KS, class FA, class FB, class FC>
+__device__ __forceinline__ void mma_tiles(int mtiles, int ntiles, FA fa, FB fb, FC fc) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int g = lane >> 2, q = lane & 3;
+  for (int t = warp; t < mtiles * ntiles; t += nw) {
+    const int m0 = (t / ntiles) * 8, n0 = (t % ntiles) * 8;
+    double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) dmma(c0, c1, fa(m0 + g, ks * 4 + q), fb(ks * 4 + q, n0 + g));
+    fc(m0 + g, n0 + 2 * q, c0, c1);
+  }
+}
+
+// collect the point ranges a box works on:
+//   ANTERP: leaf children with points (F_out box)
+//   EVAL:   own points if the box is a leaf, else leaf children without F_in
+template <bool EVAL, int NCH = 8>
+__device__ int box_ranges(const DevTree& t, int b, int2* rg) {
+  int nr = 0;
+  uint8_t f = t.flags[b];
+  if (EVAL && (f & F_LEAF)) {
+    rg[nr++] = make_int2(t.start[b], t.end[b]);
+    return nr;
+  }
+  for (int o = 0; o < NCH; ++o) {
+    int ch = t.child[NCH * (int64_t)b + o];
+    if (ch < 0) continue;
+    uint8_t fc = t.flags[ch];
+    if (!(fc & F_LEAF) || t.end[ch] <= t.start[ch]) continue;
+    if (EVAL && (fc & F_IN)) continue;
+    rg[nr++] = make_int2(t.start[ch], t.end[ch]);
+  }
+  return nr;
+}
+__device__ __forceinline__ int range_point(const int2* rg, int nr, int idx) {
+  for (int r = 0; r < nr; ++r) {
+    int len = rg[r].y - rg[r].x;
+    if (idx < len) return rg[r].x + idx;
+    idx -= len;
+  }
+  return -1;
+}
+
+// ---------------------------------------------------------------- host helpers
+static inline DevTree dev_tree(const dmk_plan_s* P) {
+  return DevTree{P->box_code.p, P->box_level.p, P->box_start.p, P->box_end.p, P->box_parent.p,
+                 P->box_child.p, P->box_coll.p, P->box_flags.p, P->fout_rank.p, P->exp_rank.p,
+                 P->xs.p,        P->ys.p,      P->zs.p};
+}
+
+template <class Kern>
+static inline void set_smem(Kern k, size_t bytes) {
+  // always set: dynamic + static shared memory above 48 KB needs the opt-in
+  DMK_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+}
+
+// Phase timing (DMK_PROFILE=1): CUDA events recorded on the plan stream around each
+// phase, no host synchronisation; resolved when dmk_eval_timings() is called.
+struct Timer {
+  dmk_plan_s* P;
+  Timer(dmk_plan_s* p) : P(p) {}
+  cudaEvent_t ev() {
+    if (P->ev_used == P->ev_pool.size()) {
+      cudaEvent_t e;
+      DMK_CUDA(cudaEventCreate(&e));
+      P->ev_pool.push_back(e);
+    }
+    return P->ev_pool[P->ev_used++];
+  }
+  void begin(const char* nm) {
+    if (!P->profile) return;
+    cudaEvent_t e = ev();
+    DMK_CUDA(cudaEventRecord(e, P->stream));
+    P->ev_marks.push_back({nm, e, nullptr});
+  }
+  void end() {
+    if (!P->profile) return;
+    cudaEvent_t e = ev();
+    DMK_CUDA(cudaEventRecord(e, P->stream));
+    P->ev_marks.back().e1 = e;
+  }
+};
+
+}  // namespace dmk

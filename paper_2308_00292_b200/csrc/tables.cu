@@ -18,6 +18,8 @@
 //   Residual polynomial: r_L M_L(r) = m(r/r_L), m(t) = Phi(t)/t, fitted as a
 //     polynomial in s = 2 t^2 - 1 ("piecewise polynomial approximation ... Estrin",
 //     PAPER.md:2002-2008), so R_L(r) = 1/r - m(r/r_L)/r_L for r < r_L (Eq. 3.66).
+#include <math.h>
+
 #include <cmath>
 #include <functional>
 #include <tuple>
@@ -268,7 +270,10 @@ static std::vector<double> fit_poly_s(const std::function<double(double)>& g, do
   return best;
 }
 
+Tables* build_log2d_tables(double eps);
+
 Tables* build_tables(int kernel, double eps, double lam) {
+  if (kernel == DMK_KERNEL_LOG) return build_log2d_tables(eps);
   if (kernel != DMK_KERNEL_LAPLACE && kernel != DMK_KERNEL_YUKAWA)
     fail(DMK_ERR_UNSUPPORTED, "kernel not implemented in 3D (DMK_KERNEL_LAPLACE, DMK_KERNEL_YUKAWA)");
   const bool yuk = kernel == DMK_KERNEL_YUKAWA;
@@ -404,6 +409,110 @@ Tables* build_tables(int kernel, double eps, double lam) {
     T->respoly.resize(deg + 1, 0.0);
   }
 
+  upload(T->Qr1, &T->dQr1);
+  upload(T->Qr0, &T->dQr0);
+  upload(T->Gr1, &T->dGr1);
+  upload(T->Gr0, &T->dGr0);
+  upload(T->A, &T->dA);
+  upload(T->W, &T->dW);
+  upload(T->W0, &T->dW0);
+  upload(T->respoly_lv, &T->dRespoly);
+  return T;
+}
+
+// 2D, K(r) = -log r: the Fourier-space split of Sec. 4.6 at lam = 0 in 2D
+// (PAPER.md:2441-2447): Khat = 2 pi/k^2, Dhat_l = Khat (Ghat_{l+1} - Ghat_l),
+// Dhat_l(0) = pi (c2/c0)(r_l^2 - r_{l+1}^2); root window Ghat_1 That with
+// That(k) = 2 pi (1 - J0(k R_T))/k^2 - 2 pi R_T log(R_T) J1(k R_T)/k, R_T = (1 + sqrt 2) r_0
+// (Sec. 4.7); weights (h/2pi)^2 Dhat(h |m|) on [0, nf]^2.  The residual
+// R_L(r) = -log(r/r_L) - g(t^2), t = r/r_L, with
+// g(u) = kappa + int_0^1 (psi(x)/psi(0)) (J0(c x sqrt u) - 1)/x dx,
+// kappa = log(c/2) + gamma + int_0^1 (psi(x)/psi(0) - 1)/x dx (the same at every level).
+Tables* build_log2d_tables(double eps) {
+  const Row* row = nullptr;
+  for (const Row& r : TABLE1)
+    if (r.eps <= eps * (1 + 1e-9)) {
+      row = &r;
+      break;
+    }
+  if (!row) fail(DMK_ERR_UNSUPPORTED, "eps tighter than 1e-9 is not supported");
+  Tables* T = new Tables();
+  T->dim = 2;
+  T->kernel = DMK_KERNEL_LOG;
+  T->eps = row->eps;
+  T->c = row->c;
+  T->p = row->p;
+  T->nf = (row->N1 - 1) / 2;
+  T->RT = 1.0 + std::sqrt(2.0);
+  T->P0 = 1.0 + T->RT + 0.5;
+  T->nf0 = (int)std::ceil(2.0 * T->c * T->P0 / (2.0 * PI));
+  const int p = T->p, nf = T->nf, nf0 = T->nf0;
+  Pswf P = make_pswf(T->c);
+  const double c = T->c;
+  T->pp = (p + 1) & ~1;
+  make_Qr(p, nf, PI / 3.0, T->pp, (nf + 2) & ~1, T->Qr1, T->Gr1);
+  make_Qr(p, nf0, PI / T->P0, T->pp, (nf0 + 2) & ~1, T->Qr0, T->Gr0);
+  T->A.assign(2 * p * p, 0.0);
+  std::vector<double> Tn;
+  for (int si = 0; si < 2; ++si) {
+    double s = si ? 1.0 : -1.0;
+    for (int i = 0; i < p; ++i) {
+      cheb_T(cheb_node(i, p) / 2.0 + s / 2.0, p, Tn);
+      for (int n = 0; n < p; ++n)
+        for (int k = 0; k < p; ++k) T->A[(si * p + n) * p + k] += vinv(k, i, p) * Tn[n];
+    }
+  }
+  auto weights2 = [](int nfw, double h, const std::function<double(double)>& fhat, double* W) {
+    int nh = nfw + 1;
+    double scale = (h / (2.0 * PI)) * (h / (2.0 * PI));
+    for (int a = 0; a < nh; ++a)
+      for (int b = 0; b < nh; ++b) W[(size_t)a * nh + b] = scale * fhat(h * std::sqrt((double)(a * a + b * b)));
+  };
+  const int nh = nf + 1;
+  T->wstride = (size_t)nh * nh;
+  T->W.assign((LMAX + 1) * T->wstride, 0.0);
+  for (int l = 1; l <= LMAX; ++l) {
+    double rl = std::ldexp(1.0, -l), rl1 = std::ldexp(1.0, -l - 1);
+    double h = 2.0 * PI / (3.0 * rl);
+    weights2(nf, h, [&](double k) {
+      if (k == 0.0) return PI * P.c2 / P.c0 * (rl * rl - rl1 * rl1);
+      return 2.0 * PI / P.psi0 * (P.eval(k * rl1 / c) - P.eval(k * rl / c)) / (k * k);
+    }, &T->W[l * T->wstride]);
+  }
+  {
+    const int nh0 = nf0 + 1;
+    T->W0.assign((size_t)nh0 * nh0, 0.0);
+    const double h0 = 2.0 * PI / T->P0, R = T->RT;
+    weights2(nf0, h0, [&](double k) {
+      double G = P.eval(k * 0.5 / c) / P.psi0;
+      if (k == 0.0) return PI * R * R / 2.0 - PI * R * R * std::log(R);
+      return G * (2.0 * PI * (1.0 - ::j0(k * R)) / (k * k) - 2.0 * PI * R * std::log(R) * ::j1(k * R) / k);
+    }, T->W0.data());
+  }
+  {
+    std::vector<double> gx, gw;
+    const int NQ = 240;
+    gauss_legendre(NQ, gx, gw);
+    std::vector<double> xq(NQ), wq(NQ), pq(NQ);
+    double kap = std::log(c / 2.0) + 0.57721566490153286061;
+    for (int i = 0; i < NQ; ++i) {
+      xq[i] = 0.5 * (gx[i] + 1.0);
+      wq[i] = 0.5 * gw[i];
+      pq[i] = P.eval(xq[i]) / P.psi0;
+      kap += wq[i] * (pq[i] - 1.0) / xq[i];
+    }
+    T->m0 = kap;
+    auto g = [&](double u) {
+      double t = std::sqrt(std::fmax(u, 0.0)), sum = 0;
+      for (int i = 0; i < NQ; ++i) sum += wq[i] * pq[i] * (::j0(c * xq[i] * t) - 1.0) / xq[i];
+      return kap + sum;
+    };
+    T->respoly = fit_poly_s(g, 1e-2 * T->eps, 1000);
+    T->respoly_deg = (int)T->respoly.size() - 1;
+    T->respoly_lv.assign((size_t)(LMAX + 1) * (T->respoly_deg + 1), 0.0);
+    for (int l = 0; l <= LMAX; ++l)
+      for (int j = 0; j <= T->respoly_deg; ++j) T->respoly_lv[l * (T->respoly_deg + 1) + j] = T->respoly[j];
+  }
   upload(T->Qr1, &T->dQr1);
   upload(T->Qr0, &T->dQr0);
   upload(T->Gr1, &T->dGr1);

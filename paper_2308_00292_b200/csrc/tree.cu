@@ -1,4 +1,5 @@
-// tree.cu -- device-resident adaptive octree and interaction lists
+// tree.cu -- device-resident adaptive 2^D-tree (octree D = 3, quadtree D = 2) and
+// interaction lists
 // (Sec. 3.5 Step 0; Sec. 3.2; lists of
 // Sec. 3.3 / Fig. 7).
 //
@@ -51,14 +52,46 @@ __device__ __forceinline__ uint32_t compact3(uint64_t x) {
   x = (x ^ (x >> 32)) & 0x1fffffULL;
   return (uint32_t)x;
 }
-__device__ __forceinline__ uint64_t encode(uint32_t x, uint32_t y, uint32_t z) {
-  return (spread3(x) << 2) | (spread3(y) << 1) | spread3(z);
+__device__ __forceinline__ uint64_t spread2(uint64_t x) {
+  x &= 0x1fffffULL;
+  x = (x | x << 16) & 0x0000ffff0000ffffULL;
+  x = (x | x << 8) & 0x00ff00ff00ff00ffULL;
+  x = (x | x << 4) & 0x0f0f0f0f0f0f0f0fULL;
+  x = (x | x << 2) & 0x3333333333333333ULL;
+  x = (x | x << 1) & 0x5555555555555555ULL;
+  return x;
 }
-__device__ __forceinline__ void decode(uint64_t c, int& x, int& y, int& z) {
-  x = (int)compact3(c >> 2);
-  y = (int)compact3(c >> 1);
-  z = (int)compact3(c);
+__device__ __forceinline__ uint32_t compact2(uint64_t x) {
+  x &= 0x5555555555555555ULL;
+  x = (x ^ (x >> 1)) & 0x3333333333333333ULL;
+  x = (x ^ (x >> 2)) & 0x0f0f0f0f0f0f0f0fULL;
+  x = (x ^ (x >> 4)) & 0x00ff00ff00ff00ffULL;
+  x = (x ^ (x >> 8)) & 0x0000ffff0000ffffULL;
+  x = (x ^ (x >> 16)) & 0x00000000ffffffffULL;
+  return (uint32_t)x & 0x1fffff;
 }
+// Morton code of integer box coordinates c[0..D-1]; coordinate 0 most significant in
+// each D-tuple of bits
+template <int D>
+__device__ __forceinline__ uint64_t encode(const int* c) {
+  if (D == 3) return (spread3(c[0]) << 2) | (spread3(c[1]) << 1) | spread3(c[2]);
+  return (spread2(c[0]) << 1) | spread2(c[1]);
+}
+template <int D>
+__device__ __forceinline__ void decode(uint64_t code, int* c) {
+  if (D == 3) {
+    c[0] = (int)compact3(code >> 2);
+    c[1] = (int)compact3(code >> 1);
+    c[2] = (int)compact3(code);
+  } else {
+    c[0] = (int)compact2(code >> 1);
+    c[1] = (int)compact2(code);
+  }
+}
+template <int D>
+struct Dim {
+  static constexpr int NCH = 1 << D, NCOL = D == 3 ? 27 : 9;
+};
 
 // binary search for `v` in sorted a[0..n); returns index or -1
 __device__ __forceinline__ int64_t bsearch_u64(const uint64_t* a, int64_t n, uint64_t v) {
@@ -79,11 +112,12 @@ __device__ __forceinline__ int64_t lower_bound_u64(const uint64_t* a, int64_t n,
 }
 
 // ---------------------------------------------------------------- kernels
+template <int D>
 __global__ void k_bbox_partial(const double* __restrict__ pts, int64_t n, double* out) {
   double mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    for (int d = 0; d < 3; ++d) {
-      double v = pts[3 * i + d];
+    for (int d = 0; d < D; ++d) {
+      double v = pts[D * i + d];
       mn[d] = fmin(mn[d], v);
       mx[d] = fmax(mx[d], v);
     }
@@ -104,38 +138,41 @@ __global__ void k_bbox_partial(const double* __restrict__ pts, int64_t n, double
   if (threadIdx.x < 6) out[blockIdx.x * 6 + threadIdx.x] = s[threadIdx.x][0];
 }
 
+template <int D>
 __global__ void k_keys(const double* __restrict__ pts, int64_t n, double lo0, double lo1, double lo2,
                        double scale, uint64_t* keys, int32_t* idx) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   const double lo[3] = {lo0, lo1, lo2};
-  uint32_t q[3];
-  for (int d = 0; d < 3; ++d) {
-    double t = floor(__dmul_rn(__dsub_rn(pts[3 * i + d], lo[d]), scale));
+  int q[3];
+  for (int d = 0; d < D; ++d) {
+    double t = floor(__dmul_rn(__dsub_rn(pts[D * i + d], lo[d]), scale));
     t = fmin(fmax(t, 0.0), (double)((1 << NBITS) - 1));
-    q[d] = (uint32_t)t;
+    q[d] = (int)t;
   }
-  keys[i] = encode(q[0], q[1], q[2]);
+  keys[i] = encode<D>(q);
   idx[i] = (int32_t)i;
 }
 
+template <int D>
 __global__ void k_gather_pts(const double* __restrict__ pts, const int32_t* __restrict__ perm, int64_t n,
                              double lo0, double lo1, double lo2, double side, double* xs, double* ys,
                              double* zs) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   int64_t j = perm[i];
-  xs[i] = __ddiv_rn(__dsub_rn(pts[3 * j + 0], lo0), side);
-  ys[i] = __ddiv_rn(__dsub_rn(pts[3 * j + 1], lo1), side);
-  zs[i] = __ddiv_rn(__dsub_rn(pts[3 * j + 2], lo2), side);
+  xs[i] = __ddiv_rn(__dsub_rn(pts[D * j + 0], lo0), side);
+  ys[i] = __ddiv_rn(__dsub_rn(pts[D * j + 1], lo1), side);
+  if (D == 3) zs[i] = __ddiv_rn(__dsub_rn(pts[D * j + 2], lo2), side);
 }
 
 // level-l box of point a is "big" (> ns points) and a is its first point
+template <int D>
 __global__ void k_big(const uint64_t* __restrict__ keys, int64_t n, int l, int ns, uint64_t* codes,
                       uint8_t* flags) {
   int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (a >= n) return;
-  int sh = 3 * (NBITS - l);
+  int sh = D * (NBITS - l);
   uint64_t c = (sh >= 64) ? 0 : (keys[a] >> sh);
   bool start = (a == 0) || (((sh >= 64) ? 0 : (keys[a - 1] >> sh)) != c);
   bool big = (a + ns < n) && ((((sh >= 64) ? 0 : (keys[a + ns] >> sh))) == c);
@@ -143,36 +180,38 @@ __global__ void k_big(const uint64_t* __restrict__ keys, int64_t n, int l, int n
   flags[a] = (start && big) ? 1 : 0;
 }
 
-// the level-l boxes touching each level-(l+1) box q (8 candidates, clipped)
+// the level-l boxes touching each level-(l+1) box q (2^D candidates, clipped)
+template <int D>
 __global__ void k_touch(const uint64_t* __restrict__ Bq, int64_t nq, int l, uint64_t* out, uint8_t* flags) {
+  constexpr int NCH = Dim<D>::NCH;
   int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (t >= nq * 8) return;
-  int64_t i = t >> 3;
-  int o = (int)(t & 7);
-  int qx, qy, qz;
-  decode(Bq[i], qx, qy, qz);
-  int q[3] = {qx, qy, qz}, c[3];
+  if (t >= nq * NCH) return;
+  int64_t i = t / NCH;
+  int o = (int)(t % NCH);
+  int q[3], c[3];
+  decode<D>(Bq[i], q);
   int n1 = 1 << l;
   bool ok = true;
-  for (int d = 0; d < 3; ++d) {
+  for (int d = 0; d < D; ++d) {
     int lo = (q[d] % 2 == 0) ? q[d] / 2 - 1 : q[d] / 2;
-    c[d] = lo + ((o >> (2 - d)) & 1);
+    c[d] = lo + ((o >> (D - 1 - d)) & 1);
     ok = ok && c[d] >= 0 && c[d] < n1;
   }
-  out[t] = ok ? encode(c[0], c[1], c[2]) : 0;
+  out[t] = ok ? encode<D>(c) : 0;
   flags[t] = ok ? 1 : 0;
 }
 
 // non-empty level-l boxes whose parent is non-leaf
+template <int D>
 __global__ void k_nonempty(const uint64_t* __restrict__ keys, int64_t n, int l, const uint64_t* __restrict__ Bp,
                            int64_t nBp, uint64_t* codes, uint8_t* flags) {
   int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (a >= n) return;
-  int sh = 3 * (NBITS - l);
+  int sh = D * (NBITS - l);
   uint64_t c = keys[a] >> sh;
   bool start = (a == 0) || ((keys[a - 1] >> sh) != c);
   codes[a] = c;
-  flags[a] = (start && bsearch_u64(Bp, nBp, c >> 3) >= 0) ? 1 : 0;
+  flags[a] = (start && bsearch_u64(Bp, nBp, c >> D) >= 0) ? 1 : 0;
 }
 
 __global__ void k_fill_level(int32_t* lev, int64_t a, int64_t b, int l) {
@@ -191,13 +230,15 @@ struct BoxCtx {
   int64_t n;
 };
 
+template <int D>
 __global__ void k_box_attrs(BoxCtx c, int64_t nbox, int32_t* start, int32_t* end, int32_t* parent,
                             int32_t* coll, uint8_t* flags) {
+  constexpr int NCOL = Dim<D>::NCOL;
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= nbox) return;
   int l = c.level[i];
   uint64_t code = c.code[i];
-  int sh = 3 * (NBITS - l);
+  int sh = D * (NBITS - l);
   uint64_t lo = (sh >= 64) ? 0 : (code << sh);
   uint64_t hiv = (sh >= 64) ? ~0ULL : ((code + 1) << sh);
   int64_t s = lower_bound_u64(c.keys, c.n, lo);
@@ -207,34 +248,41 @@ __global__ void k_box_attrs(BoxCtx c, int64_t nbox, int32_t* start, int32_t* end
   bool leaf = bsearch_u64(c.B + c.boff[l], c.boff[l + 1] - c.boff[l], code) < 0;
   flags[i] = leaf ? 1 : 0;
   if (l > 0) {
-    int64_t j = bsearch_u64(c.code + c.loff[l - 1], c.loff[l] - c.loff[l - 1], code >> 3);
+    int64_t j = bsearch_u64(c.code + c.loff[l - 1], c.loff[l] - c.loff[l - 1], code >> D);
     parent[i] = (int32_t)(j < 0 ? -1 : c.loff[l - 1] + j);
   } else {
     parent[i] = -1;
   }
-  int x, y, z;
-  decode(code, x, y, z);
-  int n1 = 1 << l, k = 0;
+  int x[3];
+  decode<D>(code, x);
+  int n1 = 1 << l;
   const uint64_t* lv = c.code + c.loff[l];
   int64_t nl = c.loff[l + 1] - c.loff[l];
-  for (int dx = -1; dx <= 1; ++dx)
-    for (int dy = -1; dy <= 1; ++dy)
-      for (int dz = -1; dz <= 1; ++dz, ++k) {
-        int xx = x + dx, yy = y + dy, zz = z + dz;
-        int32_t r = -1;
-        if (xx >= 0 && yy >= 0 && zz >= 0 && xx < n1 && yy < n1 && zz < n1) {
-          int64_t j = bsearch_u64(lv, nl, encode(xx, yy, zz));
-          if (j >= 0) r = (int32_t)(c.loff[l] + j);
-        }
-        coll[27 * i + k] = r;
-      }
+  // slot k enumerates offsets in {-1,0,1}^D, last axis fastest
+  for (int k = 0; k < NCOL; ++k) {
+    int cc[3], rem = k;
+    bool ok = true;
+    for (int d = D - 1; d >= 0; --d) {
+      cc[d] = x[d] + (rem % 3) - 1;
+      rem /= 3;
+      ok = ok && cc[d] >= 0 && cc[d] < n1;
+    }
+    int32_t r = -1;
+    if (ok) {
+      int64_t j = bsearch_u64(lv, nl, encode<D>(cc));
+      if (j >= 0) r = (int32_t)(c.loff[l] + j);
+    }
+    coll[NCOL * i + k] = r;
+  }
 }
 
+template <int D>
 __global__ void k_children(const uint64_t* code, const int32_t* parent, int64_t nbox, int32_t* child) {
+  constexpr int NCH = Dim<D>::NCH;
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= nbox) return;
   int32_t p = parent[i];
-  if (p >= 0) child[8 * (int64_t)p + (code[i] & 7)] = (int32_t)i;
+  if (p >= 0) child[NCH * (int64_t)p + (code[i] & (NCH - 1))] = (int32_t)i;
 }
 
 // flags: bit0 leaf, bit1 F_out, bit2 F_in, bit3 has local expansion
@@ -247,16 +295,18 @@ __global__ void k_flags_out(const int32_t* start, const int32_t* end, int64_t nb
   flags[i] = (uint8_t)((leaf ? 1 : 0) | (f ? 2 : 0));
   fout[i] = f ? 1 : 0;
 }
+template <int D>
 __global__ void k_flags_in(const int32_t* start, const int32_t* end, const int32_t* coll, int64_t nbox,
                            uint8_t* flags, uint8_t* exp) {
+  constexpr int NCOL = Dim<D>::NCOL;
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= nbox) return;
   uint8_t f = flags[i];
   bool nonempty = end[i] > start[i];
   bool fin = false;
   if (nonempty)
-    for (int k = 0; k < 27; ++k) {
-      int32_t s = coll[27 * i + k];
+    for (int k = 0; k < NCOL; ++k) {
+      int32_t s = coll[NCOL * i + k];
       if (s >= 0 && (flags[s] & 2)) fin = true;
     }
   bool e = nonempty && (!(f & 1) || fin);
@@ -272,10 +322,11 @@ __global__ void k_rank(const int32_t* scan, const uint8_t* sel, int64_t nbox, in
 }
 
 // direct lists: pass 0 counts, pass 1 fills
-template <bool FILL>
+template <int D, bool FILL>
 __global__ void k_dlist(const int32_t* start, const int32_t* end, const int32_t* parent, const int32_t* child,
                         const int32_t* coll, const uint8_t* flags, const uint64_t* code, const int32_t* level,
                         int64_t nbox, int32_t* cnt, const int32_t* off, int32_t* items) {
+  constexpr int NCH = Dim<D>::NCH, NCOL = Dim<D>::NCOL;
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= nbox) return;
   int n_ = 0;
@@ -284,8 +335,8 @@ __global__ void k_dlist(const int32_t* start, const int32_t* end, const int32_t*
   if (is_target) {
     int64_t a = i;
     while (a >= 0) {   // B and its ancestors: leaf colleagues at that level
-      for (int k = 0; k < 27; ++k) {
-        int32_t s = coll[27 * a + k];
+      for (int k = 0; k < NCOL; ++k) {
+        int32_t s = coll[NCOL * a + k];
         if (s >= 0 && (flags[s] & 1) && end[s] > start[s]) {
           if (FILL) items[base + n_] = s;
           ++n_;
@@ -293,18 +344,19 @@ __global__ void k_dlist(const int32_t* start, const int32_t* end, const int32_t*
       }
       a = parent[a];
     }
-    int bx, by, bz;
-    decode(code[i], bx, by, bz);
-    for (int k = 0; k < 27; ++k) {   // fine neighbours: leaves one level down touching B
-      int32_t s = coll[27 * i + k];
+    int bc[3];
+    decode<D>(code[i], bc);
+    for (int k = 0; k < NCOL; ++k) {   // fine neighbours: leaves one level down touching B
+      int32_t s = coll[NCOL * i + k];
       if (s < 0 || (flags[s] & 1)) continue;
-      for (int o = 0; o < 8; ++o) {
-        int32_t ch = child[8 * (int64_t)s + o];
+      for (int o = 0; o < NCH; ++o) {
+        int32_t ch = child[NCH * (int64_t)s + o];
         if (ch < 0 || !(flags[ch] & 1) || end[ch] <= start[ch]) continue;
-        int cx, cy, cz;
-        decode(code[ch], cx, cy, cz);
-        if (cx >= 2 * bx - 1 && cx <= 2 * bx + 2 && cy >= 2 * by - 1 && cy <= 2 * by + 2 &&
-            cz >= 2 * bz - 1 && cz <= 2 * bz + 2) {
+        int cc[3];
+        decode<D>(code[ch], cc);
+        bool touch = true;
+        for (int d = 0; d < D; ++d) touch = touch && cc[d] >= 2 * bc[d] - 1 && cc[d] <= 2 * bc[d] + 2;
+        if (touch) {
           if (FILL) items[base + n_] = ch;
           ++n_;
         }
@@ -394,8 +446,10 @@ T d2h_at(cudaStream_t s, const T* p) {
 
 }  // namespace
 
-// Build the tree of plan P from n points (device pointer, row-major n x 3).
-void build_tree(dmk_plan_s* P, const double* dpts) {
+// Build the tree of plan P from n points (device pointer, row-major n x D).
+template <int D>
+static void build_tree_d(dmk_plan_s* P, const double* dpts) {
+  constexpr int NCH = Dim<D>::NCH, NCOL = Dim<D>::NCOL;
   cudaStream_t s = P->stream;
   const int64_t n = P->n;
   const int ns = P->ns;
@@ -414,19 +468,19 @@ void build_tree(dmk_plan_s* P, const double* dpts) {
     int nb = std::min(nblk(n), 1024);
     DevBuf<double> part;
     part.alloc(6 * nb, s);
-    k_bbox_partial<<<nb, TPB, 0, s>>>(dpts, n, part.p);
+    k_bbox_partial<D><<<nb, TPB, 0, s>>>(dpts, n, part.p);
     DMK_LAUNCH_CHECK();
     std::vector<double> h(6 * nb);
     DMK_CUDA(cudaMemcpyAsync(h.data(), part.p, h.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
     DMK_CUDA(cudaStreamSynchronize(s));
     double mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
     for (int b = 0; b < nb; ++b)
-      for (int d = 0; d < 3; ++d) {
+      for (int d = 0; d < D; ++d) {
         mn[d] = std::fmin(mn[d], h[6 * b + d]);
         mx[d] = std::fmax(mx[d], h[6 * b + 3 + d]);
       }
     double ext = 0;
-    for (int d = 0; d < 3; ++d) {
+    for (int d = 0; d < D; ++d) {
       P->lo[d] = mn[d];
       ext = std::fmax(ext, mx[d] - mn[d]);
     }
@@ -442,17 +496,17 @@ void build_tree(dmk_plan_s* P, const double* dpts) {
     DevBuf<int32_t> i0;
     k0.alloc(n, s);
     i0.alloc(n, s);
-    k_keys<<<nblk(n), TPB, 0, s>>>(dpts, n, P->lo[0], P->lo[1], P->lo[2], scale, k0.p, i0.p);
+    k_keys<D><<<nblk(n), TPB, 0, s>>>(dpts, n, P->lo[0], P->lo[1], P->lo[2], scale, k0.p, i0.p);
     DMK_LAUNCH_CHECK();
     P->keys.alloc(n, s);
     P->perm.alloc(n, s);
     cub_run(s, [&](void* t, size_t& b) {
-      return cub::DeviceRadixSort::SortPairs(t, b, k0.p, P->keys.p, i0.p, P->perm.p, (int64_t)n, 0, 3 * NBITS, s);
+      return cub::DeviceRadixSort::SortPairs(t, b, k0.p, P->keys.p, i0.p, P->perm.p, (int64_t)n, 0, D * NBITS, s);
     });
     P->xs.alloc(n, s);
     P->ys.alloc(n, s);
-    P->zs.alloc(n, s);
-    k_gather_pts<<<nblk(n), TPB, 0, s>>>(dpts, P->perm.p, n, P->lo[0], P->lo[1], P->lo[2], P->side, P->xs.p,
+    if (D == 3) P->zs.alloc(n, s);
+    k_gather_pts<D><<<nblk(n), TPB, 0, s>>>(dpts, P->perm.p, n, P->lo[0], P->lo[1], P->lo[2], P->side, P->xs.p,
                                          P->ys.p, P->zs.p);
     DMK_LAUNCH_CHECK();
   }
@@ -468,7 +522,7 @@ void build_tree(dmk_plan_s* P, const double* dpts) {
     codes.alloc(n, s);
     flags.alloc(n, s);
     for (int l = 0; l < LMAX; ++l) {
-      k_big<<<nblk(n), TPB, 0, s>>>(P->keys.p, n, l, ns, codes.p, flags.p);
+      k_big<D><<<nblk(n), TPB, 0, s>>>(P->keys.p, n, l, ns, codes.p, flags.p);
       DMK_LAUNCH_CHECK();
       nU[l] = select_flagged(s, codes.p, flags.p, n, U[l]);
       if (nU[l] == 0) break;
@@ -485,7 +539,7 @@ void build_tree(dmk_plan_s* P, const double* dpts) {
     DMK_CUDA(cudaMemcpyAsync(B[ltop].p, U[ltop].p, nU[ltop] * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
     nB[ltop] = nU[ltop];
     for (int l = ltop - 1; l >= 0; --l) {
-      int64_t nc = nU[l] + 8 * nB[l + 1];
+      int64_t nc = nU[l] + NCH * nB[l + 1];
       DevBuf<uint64_t> cand;
       DevBuf<uint8_t> cf;
       cand.alloc(nc, s);
@@ -494,11 +548,11 @@ void build_tree(dmk_plan_s* P, const double* dpts) {
         DMK_CUDA(cudaMemcpyAsync(cand.p, U[l].p, nU[l] * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
         DMK_CUDA(cudaMemsetAsync(cf.p, 1, nU[l], s));
       }
-      k_touch<<<nblk(8 * nB[l + 1]), TPB, 0, s>>>(B[l + 1].p, nB[l + 1], l, cand.p + nU[l], cf.p + nU[l]);
+      k_touch<D><<<nblk(NCH * nB[l + 1]), TPB, 0, s>>>(B[l + 1].p, nB[l + 1], l, cand.p + nU[l], cf.p + nU[l]);
       DMK_LAUNCH_CHECK();
       DevBuf<uint64_t> valid;
       int64_t nv = select_flagged(s, cand.p, cf.p, nc, valid);
-      nB[l] = sort_unique(s, valid.p, nv, 3 * l, B[l]);
+      nB[l] = sort_unique(s, valid.p, nv, D * l, B[l]);
     }
   }
   const int nlevels = ltop + 2;
@@ -517,7 +571,7 @@ void build_tree(dmk_plan_s* P, const double* dpts) {
     codes.alloc(n, s);
     flags.alloc(n, s);
     for (int l = 1; l < nlevels; ++l) {
-      k_nonempty<<<nblk(n), TPB, 0, s>>>(P->keys.p, n, l, B[l - 1].p, nB[l - 1], codes.p, flags.p);
+      k_nonempty<D><<<nblk(n), TPB, 0, s>>>(P->keys.p, n, l, B[l - 1].p, nB[l - 1], codes.p, flags.p);
       DMK_LAUNCH_CHECK();
       DevBuf<uint64_t> ne;
       int64_t nne = select_flagged(s, codes.p, flags.p, n, ne);
@@ -526,7 +580,7 @@ void build_tree(dmk_plan_s* P, const double* dpts) {
       cat.alloc(nne + nb_l, s);
       if (nne) DMK_CUDA(cudaMemcpyAsync(cat.p, ne.p, nne * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
       if (nb_l) DMK_CUDA(cudaMemcpyAsync(cat.p + nne, B[l].p, nb_l * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
-      nE[l] = sort_unique(s, cat.p, nne + nb_l, 3 * l, E[l]);
+      nE[l] = sort_unique(s, cat.p, nne + nb_l, D * l, E[l]);
     }
   }
 
@@ -560,15 +614,15 @@ void build_tree(dmk_plan_s* P, const double* dpts) {
   P->box_start.alloc(nbox, s);
   P->box_end.alloc(nbox, s);
   P->box_parent.alloc(nbox, s);
-  P->box_coll.alloc(27 * nbox, s);
-  P->box_child.alloc(8 * nbox, s);
+  P->box_coll.alloc(NCOL * nbox, s);
+  P->box_child.alloc(NCH * nbox, s);
   P->box_flags.alloc(nbox, s);
   BoxCtx ctx{P->box_code.p, P->box_level.p, dloff.p, Bcat.p, dboff.p, nlevels, P->keys.p, n};
-  k_box_attrs<<<nblk(nbox), TPB, 0, s>>>(ctx, nbox, P->box_start.p, P->box_end.p, P->box_parent.p,
+  k_box_attrs<D><<<nblk(nbox), TPB, 0, s>>>(ctx, nbox, P->box_start.p, P->box_end.p, P->box_parent.p,
                                          P->box_coll.p, P->box_flags.p);
   DMK_LAUNCH_CHECK();
-  DMK_CUDA(cudaMemsetAsync(P->box_child.p, 0xff, 8 * nbox * sizeof(int32_t), s));
-  k_children<<<nblk(nbox), TPB, 0, s>>>(P->box_code.p, P->box_parent.p, nbox, P->box_child.p);
+  DMK_CUDA(cudaMemsetAsync(P->box_child.p, 0xff, NCH * nbox * sizeof(int32_t), s));
+  k_children<D><<<nblk(nbox), TPB, 0, s>>>(P->box_code.p, P->box_parent.p, nbox, P->box_child.p);
   DMK_LAUNCH_CHECK();
 
   mark("boxattrs");
@@ -578,7 +632,7 @@ void build_tree(dmk_plan_s* P, const double* dpts) {
   esel.alloc(nbox, s);
   k_flags_out<<<nblk(nbox), TPB, 0, s>>>(P->box_start.p, P->box_end.p, nbox, P->box_flags.p, fsel.p);
   DMK_LAUNCH_CHECK();
-  k_flags_in<<<nblk(nbox), TPB, 0, s>>>(P->box_start.p, P->box_end.p, P->box_coll.p, nbox, P->box_flags.p,
+  k_flags_in<D><<<nblk(nbox), TPB, 0, s>>>(P->box_start.p, P->box_end.p, P->box_coll.p, nbox, P->box_flags.p,
                                         esel.p);
   DMK_LAUNCH_CHECK();
   DevBuf<int32_t> fscan, escan;
@@ -626,7 +680,7 @@ void build_tree(dmk_plan_s* P, const double* dpts) {
     DevBuf<int32_t> cnt;
     cnt.alloc(nbox + 1, s);
     DMK_CUDA(cudaMemsetAsync(cnt.p, 0, (nbox + 1) * sizeof(int32_t), s));
-    k_dlist<false><<<nblk(nbox), TPB, 0, s>>>(P->box_start.p, P->box_end.p, P->box_parent.p, P->box_child.p,
+    k_dlist<D, false><<<nblk(nbox), TPB, 0, s>>>(P->box_start.p, P->box_end.p, P->box_parent.p, P->box_child.p,
                                               P->box_coll.p, P->box_flags.p, P->box_code.p, P->box_level.p, nbox,
                                               cnt.p, nullptr, nullptr);
     DMK_LAUNCH_CHECK();
@@ -634,7 +688,7 @@ void build_tree(dmk_plan_s* P, const double* dpts) {
     exclusive_scan(s, cnt.p, P->dlist_off.p, nbox + 1);
     P->ndlist = d2h_at(s, P->dlist_off.p + nbox);
     P->dlist.alloc(P->ndlist ? P->ndlist : 1, s);
-    k_dlist<true><<<nblk(nbox), TPB, 0, s>>>(P->box_start.p, P->box_end.p, P->box_parent.p, P->box_child.p,
+    k_dlist<D, true><<<nblk(nbox), TPB, 0, s>>>(P->box_start.p, P->box_end.p, P->box_parent.p, P->box_child.p,
                                              P->box_coll.p, P->box_flags.p, P->box_code.p, P->box_level.p, nbox,
                                              nullptr, P->dlist_off.p, P->dlist.p);
     DMK_LAUNCH_CHECK();
@@ -656,6 +710,12 @@ void build_tree(dmk_plan_s* P, const double* dpts) {
   }
   DMK_CUDA(cudaStreamSynchronize(s));
   mark("p2pitems");
+}
+
+
+void build_tree(dmk_plan_s* P, const double* dpts) {
+  if (P->dim == 2) build_tree_d<2>(P, dpts);
+  else build_tree_d<3>(P, dpts);
 }
 
 }  // namespace dmk
