@@ -59,9 +59,14 @@ typedef struct dmk_plan_s* dmk_plan_t;
 typedef struct dmk_options {
   int32_t leaf_capacity;   /* n_s: a box holding more than n_s points is refined
                               (PAPER.md:804-806); default 200 */
-  int32_t reserved0;
-  double lambda;           /* Yukawa parameter (reserved) */
+  int32_t min_level;       /* 0 (default), or L >= 1: every box of levels < L exists and is
+                              refined (empty or not) -- the shared coarse tree of a
+                              distributed evaluation (see dmk_level_moments) */
+  double lambda;           /* Yukawa parameter lambda > 0 (DMK_KERNEL_YUKAWA only) */
   void* stream;            /* cudaStream_t for all device work; NULL = default stream */
+  const double* root;      /* NULL (default: root box from the points, reading R5), or a
+                              HOST array {lo_0, .., lo_{dim-1}, side}: the root box
+                              [lo, lo + side]^dim to use (all points must lie inside) */
 } dmk_options;
 
 /* dmk_plan: build the plan for N points in `dim` dimensions.
@@ -84,6 +89,26 @@ int dmk_plan(int dim, int kernel, double eps, int64_t n, const double* points, i
  *   charges     n fp64 (caller's point order), in `mem`.
  *   potentials  n fp64 output (caller's point order), in `mem`; may not alias charges. */
 int dmk_eval(dmk_plan_t plan, const double* charges, double* potentials, int mem);
+
+/* dmk_eval in two halves, for a distributed evaluation (paper_2308_00292_b200/parallel.py):
+ *   dmk_upward    Step 2: charges (caller order, n fp64 in `mem`) ->
+ *                 Chebyshev moments of every F_out box, kept in the plan.
+ *   dmk_downward  Steps 3-5 from the plan's moments -> potentials
+ *                 (caller order, n fp64 in `mem`).  DMK_ERR_STATE before dmk_upward.
+ * dmk_upward + dmk_downward == dmk_eval.  2D plans: dmk_upward only gathers; the whole
+ * evaluation runs in dmk_downward. */
+int dmk_upward(dmk_plan_t plan, const double* charges, int mem);
+int dmk_downward(dmk_plan_t plan, double* potentials, int mem);
+
+/* dmk_level_moments: read (set = 0) or overwrite (set = 1) the Chebyshev moments of
+ * every box of `level` (< the plan's min_level, 3D only) as a dense array
+ * [8^level][p][p][p] indexed by the box's Morton code at that level (fp64 in `mem`,
+ * count = 8^level p^3; absent boxes read as 0).  set = 1 also rebuilds the levels above
+ * from it by T_c2p (Lemma 2.2) -- the coarse-level exchange of a distributed
+ * evaluation: each rank reads the moments its own charges give, the ranks sum them
+ * (all-reduce), and each rank sets the sum before dmk_downward.  Call after
+ * dmk_upward. */
+int dmk_level_moments(dmk_plan_t plan, int level, double* dense, int64_t count, int mem, int set);
 
 /* dmk_destroy: free the plan (NULL is a no-op). */
 int dmk_destroy(dmk_plan_t plan);

@@ -78,8 +78,13 @@ def _finish(T, us, rho, kernel, coinc_sum):
 
 
 def dmk(points, charges, eps: float, ns: int, kernel: str = "laplace", lam: float = 0.0,
-        return_stages: bool = False):
-    T = Tree(points, ns)                                   # Step 0
+        return_stages: bool = False, root=None, min_level: int = 0, level_get=None, level_set=None):
+    """level_get = C: stop after Step 2 and return the proxy charges of every box of level
+    C as a dense array [2^{dC}][p]*d indexed by Morton code (0 for absent boxes).
+    level_set = (C, dense): after Step 2 replace the proxy charges of level C by `dense`
+    and rebuild the coarser levels by T_c2p.  Both need C < min_level; together with
+    root/min_level they are the hooks of a distributed evaluation."""
+    T = Tree(points, ns, root=root, min_level=min_level)   # Step 0
     D = T.d
     prm = for_eps(eps, D)
     if kernel == "laplace" and D == 3:
@@ -142,16 +147,32 @@ def dmk(points, charges, eps: float, ns: int, kernel: str = "laplace", lam: floa
         U = [cheb.interp_matrix(2.0 * (X[a:b, k] - c[k]) / s, p) for k in range(D)]
         spec = ",".join("j" + "abc"[k] for k in range(D)) + ",j->" + "abc"[:D]
         proxy[i] = np.einsum(spec, *U, rho[a:b], optimize=True)
-    for l in range(T.nlevels - 2, -1, -1):
-        for i in range(T.level_offset[l], T.level_offset[l + 1]):
-            if T.box_leaf[i] or T.box_npts[i] == 0:
-                continue
-            acc = np.zeros((p,) * D)
-            for ch in T.box_children[i]:
-                if ch >= 0 and ch in proxy:
-                    sd = _octant_sides(T.box_code[ch], D)
-                    acc += cheb.applyd([C2P[sd[k]] for k in range(D)], proxy[ch])
-            proxy[i] = acc
+    def c2p_levels(top):
+        for l in range(top, -1, -1):
+            for i in range(T.level_offset[l], T.level_offset[l + 1]):
+                if not T.fout[i]:
+                    continue
+                acc = np.zeros((p,) * D)
+                for ch in T.box_children[i]:
+                    if ch >= 0 and ch in proxy:
+                        sd = _octant_sides(T.box_code[ch], D)
+                        acc += cheb.applyd([C2P[sd[k]] for k in range(D)], proxy[ch])
+                proxy[i] = acc
+
+    c2p_levels(T.nlevels - 2)
+    if level_get is not None:
+        C = int(level_get)
+        dense = np.zeros((2 ** (D * C),) + (p,) * D)
+        for i in range(T.level_offset[C], T.level_offset[C + 1]):
+            if i in proxy:
+                dense[T.box_code[i]] = proxy[i]
+        return dense
+    if level_set is not None:
+        C, dense = int(level_set[0]), level_set[1]
+        for i in range(T.level_offset[C], T.level_offset[C + 1]):
+            if T.fout[i]:
+                proxy[i] = np.array(dense[T.box_code[i]])
+        c2p_levels(C - 1)
     st["proxy"] = proxy
 
     # ---- Step 3: downward pass ---------------------------------------------

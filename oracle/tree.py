@@ -37,12 +37,17 @@ NBITS = 21          # bits per coordinate in the 63-bit Morton key
 LMAX = 20           # deepest level a box may be refined into
 
 
-def normalize(points: np.ndarray):
-    """Root cube and integer coordinates (reading R5).  Returns (lo, side, q)."""
+def normalize(points: np.ndarray, root=None):
+    """Root cube and integer coordinates (reading R5).  Returns (lo, side, q).
+    root = (lo_0, .., lo_{d-1}, side) fixes the cube (a distributed evaluation)."""
     x = np.asarray(points, dtype=np.float64)
-    lo = x.min(axis=0)
-    ext = (x.max(axis=0) - lo).max()
-    side = float(ext) if ext > 0 else 1.0
+    if root is not None:
+        d = x.shape[1]
+        lo, side = np.asarray(root[:d], dtype=np.float64), float(root[d])
+    else:
+        lo = x.min(axis=0)
+        ext = (x.max(axis=0) - lo).max()
+        side = float(ext) if ext > 0 else 1.0
     scale = float(2 ** NBITS) / side
     q = np.floor((x - lo) * scale)
     q = np.clip(q, 0, 2 ** NBITS - 1).astype(np.int64)
@@ -93,12 +98,16 @@ def encode3(c, level):
 class Tree:
     """Adaptive, level-restricted 2^d-tree over one point set (sources = targets)."""
 
-    def __init__(self, points: np.ndarray, ns: int):
+    def __init__(self, points: np.ndarray, ns: int, root=None, min_level: int = 0):
+        """root: fixed root cube (lo..., side); min_level: every box of levels < min_level
+        exists and is refined, empty or not (the shared coarse tree of a distributed
+        evaluation, paper_2308_00292_b200/parallel.py)."""
         pts = np.asarray(points, dtype=np.float64)
         self.N, self.d = pts.shape
         self.nch, self.ncol = 2 ** self.d, 3 ** self.d
         self.ns = int(ns)
-        self.lo, self.side, q = normalize(pts)
+        self.min_level = int(min_level)
+        self.lo, self.side, q = normalize(pts, root)
         key = morton(q)
         self.perm = np.argsort(key, kind="stable")          # sorted -> original
         self.keys = key[self.perm]
@@ -114,6 +123,9 @@ class Tree:
         # unbalanced refinement: U[l] = level-l boxes holding > ns points
         U = []
         for l in range(0, LMAX):
+            if l < self.min_level:
+                U.append(np.arange(2 ** (self.d * l), dtype=np.int64))
+                continue
             if N == 0:
                 break
             uq, cnt = np.unique(self._codes(l), return_counts=True)
@@ -185,7 +197,8 @@ class Tree:
                 cc = c + np.array(off)
                 if np.all((cc >= 0) & (cc < 2 ** l)):
                     self.box_colleagues[i, k] = self.find(l, encode(cc, l, self.d)[0])
-        self.fout = (~self.box_leaf) & (self.box_npts > 0)
+        # F_out: non-leaf and non-empty (reading R6), or forced (level < min_level)
+        self.fout = (~self.box_leaf) & ((self.box_npts > 0) | (self.box_level < self.min_level))
         # leaf of every (sorted) point
         self.point_leaf = np.full(self.N, -1, dtype=np.int64)
         for i in np.nonzero(self.box_leaf)[0]:

@@ -37,8 +37,9 @@ class DmkError(RuntimeError):
 
 
 class _Options(ctypes.Structure):
-    _fields_ = [("leaf_capacity", ctypes.c_int32), ("reserved0", ctypes.c_int32),
-                ("lam", ctypes.c_double), ("stream", ctypes.c_void_p)]
+    _fields_ = [("leaf_capacity", ctypes.c_int32), ("min_level", ctypes.c_int32),
+                ("lam", ctypes.c_double), ("stream", ctypes.c_void_p),
+                ("root", ctypes.POINTER(ctypes.c_double))]
 
 
 class PlanInfo(ctypes.Structure):
@@ -63,6 +64,9 @@ def lib() -> ctypes.CDLL:
         vp, i64, dbl, ci = ctypes.c_void_p, ctypes.c_int64, ctypes.c_double, ctypes.c_int
         L.dmk_plan.argtypes = [ci, ci, dbl, i64, vp, ci, ctypes.POINTER(_Options), ctypes.POINTER(vp)]
         L.dmk_eval.argtypes = [vp, vp, vp, ci]
+        L.dmk_upward.argtypes = [vp, vp, ci]
+        L.dmk_downward.argtypes = [vp, vp, ci]
+        L.dmk_level_moments.argtypes = [vp, ci, vp, i64, ci, ci]
         L.dmk_destroy.argtypes = [vp]
         L.dmk_last_error.restype = ctypes.c_char_p
         L.dmk_version.restype = ctypes.c_char_p
@@ -72,7 +76,8 @@ def lib() -> ctypes.CDLL:
         L.dmk_stage_size.argtypes = [vp, ci]
         L.dmk_stage_size.restype = i64
         L.dmk_eval_timings.argtypes = [vp, ctypes.POINTER(dbl), ctypes.POINTER(ctypes.c_char_p), ci]
-        for f in ("dmk_plan", "dmk_eval", "dmk_destroy", "dmk_plan_info_get", "dmk_tree_copy",
+        for f in ("dmk_plan", "dmk_eval", "dmk_upward", "dmk_downward", "dmk_level_moments",
+                  "dmk_destroy", "dmk_plan_info_get", "dmk_tree_copy",
                   "dmk_stage_copy", "dmk_eval_timings"):
             getattr(L, f).restype = ci
         _lib = L
@@ -103,13 +108,18 @@ class Plan:
     """A dmk_plan_t: tree, lists and tables for one point set (sources = targets)."""
 
     def __init__(self, points, eps: float = 1e-6, leaf_capacity: int = 200, kernel: str = "laplace",
-                 lam: float = 0.0, stream=None):
+                 lam: float = 0.0, stream=None, root=None, min_level: int = 0):
         ptr, mem, keep = _placement(points)
         n = keep.shape[0]
         if keep.ndim != 2 or keep.shape[1] not in (2, 3):
             raise DmkError("points must have shape (n, 3) or (n, 2)")
         dim = int(keep.shape[1])
-        opt = _Options(int(leaf_capacity), 0, float(lam), stream)
+        self._root = None
+        rootp = None
+        if root is not None:
+            self._root = (ctypes.c_double * (dim + 1))(*[float(v) for v in root])
+            rootp = ctypes.cast(self._root, ctypes.POINTER(ctypes.c_double))
+        opt = _Options(int(leaf_capacity), int(min_level), float(lam), stream, rootp)
         h = ctypes.c_void_p()
         _check(lib().dmk_plan(dim, KERNELS[kernel], float(eps), int(n), ptr, mem, ctypes.byref(opt),
                               ctypes.byref(h)), "dmk_plan")
@@ -132,6 +142,37 @@ class Plan:
             raise DmkError("charges and output must live in the same memory")
         _check(lib().dmk_eval(self._h, qptr, optr, mem), "dmk_eval")
         return okeep
+
+    def upward(self, charges):
+        """Step 2 only: moments of the charges (caller order), kept in the plan."""
+        qptr, mem, qkeep = _placement(charges)
+        if qkeep.shape != (self.n,):
+            raise DmkError("charges must have shape (n,)")
+        _check(lib().dmk_upward(self._h, qptr, mem), "dmk_upward")
+
+    def downward(self, out=None, device=None):
+        """Steps 3-5 from the plan's moments; returns the potentials (caller order)."""
+        if out is None:
+            if device is not None:
+                import torch
+                out = torch.empty(self.n, dtype=torch.float64, device=device)
+            else:
+                out = np.empty(self.n, dtype=np.float64)
+        optr, mem, okeep = _placement(out)
+        _check(lib().dmk_downward(self._h, optr, mem), "dmk_downward")
+        return okeep
+
+    def level_moments(self, level: int, dense=None, set: bool = False):
+        """Dense [8^level, p, p, p] moments of the boxes at `level` (read, or write with
+        set=True and rebuild the coarser levels)."""
+        p = self.info().p
+        if dense is None:
+            dense = np.empty((8 ** level, p, p, p), dtype=np.float64)
+        ptr, mem, keep = _placement(dense)
+        _check(lib().dmk_level_moments(self._h, int(level), ptr, int(keep.numel() if hasattr(keep, "numel")
+                                                                       else keep.size), mem, int(bool(set))),
+               "dmk_level_moments")
+        return keep
 
     def info(self) -> PlanInfo:
         inf = PlanInfo()
@@ -178,8 +219,9 @@ class Plan:
 
 
 def dmk_plan(points, eps: float = 1e-6, leaf_capacity: int = 200, kernel: str = "laplace", lam: float = 0.0,
-             stream=None) -> Plan:
-    return Plan(points, eps=eps, leaf_capacity=leaf_capacity, kernel=kernel, lam=lam, stream=stream)
+             stream=None, root=None, min_level: int = 0) -> Plan:
+    return Plan(points, eps=eps, leaf_capacity=leaf_capacity, kernel=kernel, lam=lam, stream=stream, root=root,
+                min_level=min_level)
 
 
 def dmk_eval(plan: Plan, charges, out=None):

@@ -104,6 +104,13 @@ int dmk_plan(int dim, int kernel, double eps, int64_t n, const double* points, i
         P->ns = opt->leaf_capacity;
         P->stream = (cudaStream_t)opt->stream;
         P->lambda = opt->lambda;
+        if (opt->min_level < 0 || opt->min_level > 6) fail(DMK_ERR_ARG, "min_level must be in [0, 6]");
+        P->min_level = opt->min_level;
+        if (opt->root) {
+          P->root_fixed = true;
+          for (int d = 0; d < dim; ++d) P->lo[d] = opt->root[d];
+          P->side = opt->root[dim];
+        }
       }
       const char* pe = std::getenv("DMK_PROFILE");
       P->profile = pe && pe[0] == '1';
@@ -148,6 +155,67 @@ int dmk_eval(dmk_plan_t P, const double* charges, double* potentials, int mem) {
       eval_plan(P, charges, potentials);
     }
     P->evaluated = true;
+    P->upward_done = true;
+  });
+}
+
+int dmk_upward(dmk_plan_t P, const double* charges, int mem) {
+  return guard([&] {
+    if (!P || !charges) fail(DMK_ERR_ARG, "null argument");
+    if (mem != DMK_MEM_DEVICE && mem != DMK_MEM_HOST) fail(DMK_ERR_ARG, "bad mem");
+    cudaStream_t s = P->stream;
+    if (mem == DMK_MEM_HOST) {
+      DevBuf<double> dq;
+      dq.alloc(P->n, s);
+      DMK_CUDA(cudaMemcpyAsync(dq.p, charges, P->n * sizeof(double), cudaMemcpyHostToDevice, s));
+      eval_upward(P, dq.p);
+      DMK_CUDA(cudaStreamSynchronize(s));
+    } else {
+      eval_upward(P, charges);
+    }
+    P->upward_done = true;
+  });
+}
+
+int dmk_downward(dmk_plan_t P, double* potentials, int mem) {
+  return guard([&] {
+    if (!P || !potentials) fail(DMK_ERR_ARG, "null argument");
+    if (mem != DMK_MEM_DEVICE && mem != DMK_MEM_HOST) fail(DMK_ERR_ARG, "bad mem");
+    if (!P->upward_done) fail(DMK_ERR_STATE, "dmk_downward before dmk_upward");
+    cudaStream_t s = P->stream;
+    if (mem == DMK_MEM_HOST) {
+      DevBuf<double> du;
+      du.alloc(P->n, s);
+      eval_downward(P, du.p);
+      DMK_CUDA(cudaMemcpyAsync(potentials, du.p, P->n * sizeof(double), cudaMemcpyDeviceToHost, s));
+      DMK_CUDA(cudaStreamSynchronize(s));
+    } else {
+      eval_downward(P, potentials);
+    }
+    P->evaluated = true;
+  });
+}
+
+int dmk_level_moments(dmk_plan_t P, int level, double* dense, int64_t count, int mem, int set) {
+  return guard([&] {
+    if (!P || !dense) fail(DMK_ERR_ARG, "null argument");
+    if (mem != DMK_MEM_DEVICE && mem != DMK_MEM_HOST) fail(DMK_ERR_ARG, "bad mem");
+    if (!P->upward_done) fail(DMK_ERR_STATE, "dmk_level_moments before dmk_upward");
+    if (level < 0 || level > 6) fail(DMK_ERR_ARG, "level out of range");
+    const int64_t p3 = (int64_t)P->tab->p * P->tab->p * P->tab->p;
+    const int64_t need = ((int64_t)1 << (3 * level)) * p3;
+    if (count != need) fail(DMK_ERR_ARG, "count must be 8^level * p^3 = " + std::to_string(need));
+    cudaStream_t s = P->stream;
+    if (mem == DMK_MEM_HOST) {
+      DevBuf<double> d;
+      d.alloc(need, s);
+      if (set) DMK_CUDA(cudaMemcpyAsync(d.p, dense, need * sizeof(double), cudaMemcpyHostToDevice, s));
+      level_moments(P, level, d.p, set != 0);
+      if (!set) DMK_CUDA(cudaMemcpyAsync(dense, d.p, need * sizeof(double), cudaMemcpyDeviceToHost, s));
+      DMK_CUDA(cudaStreamSynchronize(s));
+    } else {
+      level_moments(P, level, dense, set != 0);
+    }
   });
 }
 

@@ -108,10 +108,13 @@ struct dmk_plan_s {
   bool profile = false;        // DMK_PROFILE=1: per-phase CUDA events in dmk_eval (no host syncs)
   bool profile_tree = false;   // DMK_PROFILE_TREE=1: synchronising phase marks in dmk_plan
   bool evaluated = false;
+  bool upward_done = false;
 
   // root cube
   double lo[3] = {0, 0, 0};
   double side = 1;
+  bool root_fixed = false;   // lo/side given by the caller (dmk_options.root)
+  int min_level = 0;         // levels < min_level fully refined (dmk_options.min_level)
 
   // sorted points (normalised coordinates in [0,1]^3) and permutation
   dmk::DevBuf<uint64_t> keys;
@@ -162,6 +165,9 @@ struct dmk_plan_s {
 namespace dmk {
 void resolve_timings(dmk_plan_s* P);
 void eval_plan_2d(dmk_plan_s* PL, double* dout);
+void eval_upward(dmk_plan_s* PL, const double* dcharges);
+void eval_downward(dmk_plan_s* PL, double* dout);
+void level_moments(dmk_plan_s* PL, int level, double* ddense, bool set);
 // cumulative number of libdmk kernel launches (this library's own kernels; the
 // CUB sort/scan/select kernels compiled into the library are counted separately)
 extern int64_t g_launches, g_cub_launches;

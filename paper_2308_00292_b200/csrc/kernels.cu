@@ -22,6 +22,7 @@
 //   k_p2p<K>       residual kernel R_{L_S} over the direct lists (warp per 32
 //                  targets), self terms, final combine and scatter to caller order
 #include <cstring>
+#include <type_traits>
 
 #include "device.cuh"
 
@@ -901,8 +902,12 @@ constexpr int px_ch(int P, int H) {
 }
 constexpr int pw_ac(int H) { return 2 * H * H <= 1024 ? 2 : 1; }
 
+// Phases of run_eval: UP = anterpolation + c2p (Step 2), DOWN = Step 3; C2P_ONLY =
+// c2p for the levels above `top` only (after dmk_level_moments injected level `top`).
+constexpr int PH_UP = 1, PH_DOWN = 2, PH_C2P_ONLY = 4;
+
 template <int P, int NF, int NF0>
-static void run_eval(dmk_plan_s* PL) {
+static void run_eval(dmk_plan_s* PL, int phase = PH_UP | PH_DOWN, int top = 0) {
   using C = Cfg<P>;
   cudaStream_t s = PL->stream;
   const Tables& T = *PL->tab;
@@ -912,7 +917,19 @@ static void run_eval(dmk_plan_s* PL) {
   constexpr int P3 = P * P * P;
   Timer tm(PL);
   const int64_t n = PL->n;
-  if (nl > 1) {
+  if (nl > 1 && (phase & PH_C2P_ONLY)) {
+    size_t sm = sizeof(double) * (P3 + 2 * P * P);
+    set_smem(k_c2p<P>, sm);
+    for (int l = top - 1; l >= 0; --l) {
+      int64_t a = th.fout_off[l], b = th.fout_off[l + 1];
+      if (b > a) {
+        k_c2p<P><<<(int)(b - a), P * P, sm, s>>>(dt, PL->fout_list.p + a, T.dA, PL->mom.p);
+        DMK_LAUNCH_CHECK();
+      }
+    }
+    return;
+  }
+  if (nl > 1 && (phase & PH_UP)) {
     // ---- Step 2: upward pass
     tm.begin("anterp");
     DMK_CUDA(cudaMemsetAsync(PL->mom.p, 0, PL->mom.bytes(), s));
@@ -935,6 +952,8 @@ static void run_eval(dmk_plan_s* PL) {
       }
     }
     tm.end();
+  }
+  if (nl > 1 && (phase & PH_DOWN)) {
     // ---- Step 3: downward pass
     tm.begin("prox2pw");
     {
@@ -990,7 +1009,7 @@ static void run_eval(dmk_plan_s* PL) {
       }
     }
     tm.end();
-  } else {
+  } else if (nl == 1 && (phase & PH_DOWN)) {
     DMK_CUDA(cudaMemsetAsync(PL->ufar.p, 0, n * sizeof(double), s));
   }
 }
@@ -1017,7 +1036,19 @@ static void run_p2p_deg(dmk_plan_s* PL, double* out, const ResPoly& rp, int K) {
   DMK_LAUNCH_CHECK();
 }
 
-void eval_plan(dmk_plan_s* PL, const double* dcharges, double* dout) {
+template <class F>
+static void dispatch_p(dmk_plan_s* PL, F f) {
+  switch (PL->tab->p) {
+    case 9: f(std::integral_constant<int, 9>(), std::integral_constant<int, 6>(), std::integral_constant<int, 10>()); break;
+    case 18: f(std::integral_constant<int, 18>(), std::integral_constant<int, 12>(), std::integral_constant<int, 19>()); break;
+    case 28: f(std::integral_constant<int, 28>(), std::integral_constant<int, 19>(), std::integral_constant<int, 28>()); break;
+    default: fail(DMK_ERR_UNSUPPORTED, "unsupported Chebyshev order");
+  }
+}
+
+// Step 2 (charges -> moments), 3D: gather the charges into Morton order, anterpolate,
+// c2p.  The moments stay in the plan for eval_downward().
+void eval_upward(dmk_plan_s* PL, const double* dcharges) {
   cudaStream_t s = PL->stream;
   PL->timings.clear();
   PL->ev_marks.clear();
@@ -1027,16 +1058,18 @@ void eval_plan(dmk_plan_s* PL, const double* dcharges, double* dout) {
   k_gather_q<<<(int)((PL->n + 255) / 256), 256, 0, s>>>(dcharges, PL->perm.p, PL->n, PL->q.p);
   DMK_LAUNCH_CHECK();
   tm.end();
+  if (PL->dim == 2) return;   // the 2D path runs as one piece (eval_plan_2d)
+  dispatch_p(PL, [&](auto P_, auto NF_, auto NF0_) { run_eval<P_(), NF_(), NF0_()>(PL, PH_UP); });
+}
+
+// Steps 3-5, 3D: plane waves, local expansions, evaluation, P2P, scatter to dout.
+void eval_downward(dmk_plan_s* PL, double* dout) {
   if (PL->dim == 2) {
     eval_plan_2d(PL, dout);
     return;
   }
-  switch (PL->tab->p) {
-    case 9: run_eval<9, 6, 10>(PL); break;
-    case 18: run_eval<18, 12, 19>(PL); break;
-    case 28: run_eval<28, 19, 28>(PL); break;
-    default: fail(DMK_ERR_UNSUPPORTED, "unsupported Chebyshev order");
-  }
+  dispatch_p(PL, [&](auto P_, auto NF_, auto NF0_) { run_eval<P_(), NF_(), NF0_()>(PL, PH_DOWN); });
+  Timer tm(PL);
   ResPoly rp{};
   const auto& poly = PL->tab->respoly;
   int K = (int)poly.size() - 1;
@@ -1052,6 +1085,53 @@ void eval_plan(dmk_plan_s* PL, const double* dcharges, double* dout) {
     else run_p2p_deg<KER_LAPLACE, false>(PL, dout, rp, K);
   }
   tm.end();
+}
+
+void eval_plan(dmk_plan_s* PL, const double* dcharges, double* dout) {
+  eval_upward(PL, dcharges);
+  eval_downward(PL, dout);
+}
+
+// ---- level moments (distributed evaluation): dense [2^{3l}][p^3] by Morton code
+__global__ void k_level_get(const uint64_t* __restrict__ code, const int32_t* __restrict__ fout_rank, int64_t b0,
+                            int p3, const double* __restrict__ mom, double* __restrict__ dense) {
+  const int64_t i = b0 + blockIdx.x;
+  const int r = fout_rank[i];
+  if (r < 0) return;
+  const double* src = mom + (size_t)r * p3;
+  double* dst = dense + (size_t)code[i] * p3;
+  for (int k = threadIdx.x; k < p3; k += blockDim.x) dst[k] = src[k];
+}
+__global__ void k_level_set(const uint64_t* __restrict__ code, const int32_t* __restrict__ fout_rank, int64_t b0,
+                            int p3, const double* __restrict__ dense, double* __restrict__ mom) {
+  const int64_t i = b0 + blockIdx.x;
+  const int r = fout_rank[i];
+  if (r < 0) return;
+  const double* src = dense + (size_t)code[i] * p3;
+  double* dst = mom + (size_t)r * p3;
+  for (int k = threadIdx.x; k < p3; k += blockDim.x) dst[k] = src[k];
+}
+
+void level_moments(dmk_plan_s* PL, int level, double* ddense, bool set) {
+  if (PL->dim != 3) fail(DMK_ERR_UNSUPPORTED, "level moments are implemented for dim = 3");
+  if (level < 0 || level >= PL->min_level) fail(DMK_ERR_ARG, "level must be in [0, min_level)");
+  if (level >= PL->th.nlevels - 1) fail(DMK_ERR_STATE, "the tree has no non-leaf boxes at that level");
+  cudaStream_t s = PL->stream;
+  const int p3 = PL->tab->p * PL->tab->p * PL->tab->p;
+  const int64_t a = PL->th.level_off[level], b = PL->th.level_off[level + 1];
+  if (!set) {
+    DMK_CUDA(cudaMemsetAsync(ddense, 0, ((size_t)1 << (3 * level)) * p3 * sizeof(double), s));
+    k_level_get<<<(int)(b - a), 256, 0, s>>>(PL->box_code.p, PL->fout_rank.p, a, p3, PL->mom.p, ddense);
+    DMK_LAUNCH_CHECK();
+    return;
+  }
+  // levels above `level` are pure c2p sums (all their children are forced non-leaf), so
+  // zero them, inject `level`, and rebuild them
+  const int64_t r0 = PL->th.fout_off[0], r1 = PL->th.fout_off[level];
+  if (r1 > r0) DMK_CUDA(cudaMemsetAsync(PL->mom.p + (size_t)r0 * p3, 0, (size_t)(r1 - r0) * p3 * sizeof(double), s));
+  k_level_set<<<(int)(b - a), 256, 0, s>>>(PL->box_code.p, PL->fout_rank.p, a, p3, ddense, PL->mom.p);
+  DMK_LAUNCH_CHECK();
+  dispatch_p(PL, [&](auto P_, auto NF_, auto NF0_) { run_eval<P_(), NF_(), NF0_()>(PL, PH_C2P_ONLY, level); });
 }
 
 }  // namespace dmk

@@ -214,6 +214,11 @@ __global__ void k_nonempty(const uint64_t* __restrict__ keys, int64_t n, int l, 
   flags[a] = (start && bsearch_u64(Bp, nBp, c >> D) >= 0) ? 1 : 0;
 }
 
+__global__ void k_iota_u64(uint64_t* out, int64_t n) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) out[i] = (uint64_t)i;
+}
+
 __global__ void k_fill_level(int32_t* lev, int64_t a, int64_t b, int l) {
   int64_t i = a + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < b) lev[i] = l;
@@ -286,12 +291,14 @@ __global__ void k_children(const uint64_t* code, const int32_t* parent, int64_t 
 }
 
 // flags: bit0 leaf, bit1 F_out, bit2 F_in, bit3 has local expansion
-__global__ void k_flags_out(const int32_t* start, const int32_t* end, int64_t nbox, uint8_t* flags,
-                            uint8_t* fout) {
+__global__ void k_flags_out(const int32_t* start, const int32_t* end, const int32_t* level, int min_level,
+                            int64_t nbox, uint8_t* flags, uint8_t* fout) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= nbox) return;
   bool leaf = flags[i] & 1;
-  bool f = !leaf && end[i] > start[i];
+  // forced coarse boxes (level < min_level) carry outgoing expansions even when locally
+  // empty: their moments are injected from the other ranks (dmk_level_moments)
+  bool f = !leaf && (end[i] > start[i] || level[i] < min_level);
   flags[i] = (uint8_t)((leaf ? 1 : 0) | (f ? 2 : 0));
   fout[i] = f ? 1 : 0;
 }
@@ -463,8 +470,10 @@ static void build_tree_d(dmk_plan_s* P, const double* dpts) {
     t_last = now;
   };
 
-  // ---- root cube (reading R5)
-  {
+  // ---- root cube (reading R5), or the caller's (distributed plans share one root)
+  if (P->root_fixed) {
+    if (!(P->side > 0) || !std::isfinite(P->side)) fail(DMK_ERR_ARG, "fixed root side must be > 0");
+  } else {
     int nb = std::min(nblk(n), 1024);
     DevBuf<double> part;
     part.alloc(6 * nb, s);
@@ -522,6 +531,16 @@ static void build_tree_d(dmk_plan_s* P, const double* dpts) {
     codes.alloc(n, s);
     flags.alloc(n, s);
     for (int l = 0; l < LMAX; ++l) {
+      if (l < P->min_level) {
+        // forced refinement (distributed plans): every box of the levels above min_level
+        // exists and is refined, empty or not, so that all ranks share the coarse tree
+        nU[l] = (int64_t)1 << (D * l);
+        U[l].alloc(nU[l], s);
+        k_iota_u64<<<nblk(nU[l]), TPB, 0, s>>>(U[l].p, nU[l]);
+        DMK_LAUNCH_CHECK();
+        ltop = l;
+        continue;
+      }
       k_big<D><<<nblk(n), TPB, 0, s>>>(P->keys.p, n, l, ns, codes.p, flags.p);
       DMK_LAUNCH_CHECK();
       nU[l] = select_flagged(s, codes.p, flags.p, n, U[l]);
@@ -630,7 +649,8 @@ static void build_tree_d(dmk_plan_s* P, const double* dpts) {
   DevBuf<uint8_t> fsel, esel;
   fsel.alloc(nbox, s);
   esel.alloc(nbox, s);
-  k_flags_out<<<nblk(nbox), TPB, 0, s>>>(P->box_start.p, P->box_end.p, nbox, P->box_flags.p, fsel.p);
+  k_flags_out<<<nblk(nbox), TPB, 0, s>>>(P->box_start.p, P->box_end.p, P->box_level.p, P->min_level, nbox,
+                                         P->box_flags.p, fsel.p);
   DMK_LAUNCH_CHECK();
   k_flags_in<D><<<nblk(nbox), TPB, 0, s>>>(P->box_start.p, P->box_end.p, P->box_coll.p, nbox, P->box_flags.p,
                                         esel.p);
