@@ -11,8 +11,9 @@ max over ranks.  Prints ONE JSON line (rank 0).
 
 --impl reference times the CPU oracle (oracle/dmk.py, fp64 numpy, as it stands) on a
 bounded sample of the same workload on the host cores; under torchrun only rank 0
-runs it.  N > 1 runs independent replicas (one problem per GPU, weak scaling): the
-partitioned multi-GPU DMK is not built yet (DESIGN.md §8 row "multi-GPU").
+runs it.  N > 1 (torchrun, one rank per GPU, NCCL) runs the partitioned DMK of
+paper_2308_00292_b200/parallel.py on one global problem of N x (--n) uniform points (weak
+scaling: --n points per GPU): Morton partition, particle halo, coarse-moment all-reduce.
 """
 from __future__ import annotations
 
@@ -215,10 +216,120 @@ def run_reference(a):
     print(json.dumps(line), flush=True)
 
 
+def run_distributed(a):
+    """N > 1: one global uniform problem of world * a.n points, a.n generated per rank,
+    evaluated by the partitioned DMK (weak scaling).  Device-event timing on each rank
+    between barriers, max over ranks."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import dmk_inputs
+    import paper_2308_00292_b200 as dmk
+    from paper_2308_00292_b200 import parallel as par
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29517")
+    os.environ.setdefault("WORLD_SIZE", str(world))
+    os.environ.setdefault("RANK", str(rank))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    comm = par.TorchComm()
+    backend = par.GpuBackend(dev)
+    x, q = dmk_inputs.uniform(a.n, seed=1 + rank)
+    X, Q = torch.as_tensor(x, device=dev), torch.as_tensor(q, device=dev)
+    flush = torch.empty(256 * 2 ** 20 // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    st = {}
+
+    def step(Xs, Qs):
+        return par.dmk_eval_distributed(Xs, Qs, comm, backend, eps=a.eps, ns=a.ns, stats=st)
+
+    for _ in range(a.warmup):
+        step(X, Q)
+    torch.cuda.synchronize(dev)
+    L = dmk.lib()
+    import ctypes
+    L.dmk_kernel_launches.restype = ctypes.c_int64
+    L.dmk_kernel_launches.argtypes = [ctypes.c_void_p]
+    launches0 = L.dmk_kernel_launches(None)
+    clk = Clocks(local)
+    clk.start()
+    times = []
+    for _ in range(a.steps):
+        flush.zero_()
+        torch.cuda.synchronize(dev)
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        u = step(X, Q)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        dist.barrier()
+        times.append(e0.elapsed_time(e1))
+    clocks = clk.stop()
+    launches = (L.dmk_kernel_launches(None) - launches0) // a.steps
+    t = torch.tensor([float(np.mean(times))], device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t_step = float(t.item())
+    # end to end: host points/charges copied in and potentials copied out every step
+    Xh, Qh = torch.as_tensor(x).pin_memory(), torch.as_tensor(q).pin_memory()
+    e2e = []
+    for k in range(a.warmup + a.steps):
+        torch.cuda.synchronize(dev)
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        uh = step(Xh.to(dev, non_blocking=True), Qh.to(dev, non_blocking=True)).cpu()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        if k >= a.warmup:
+            e2e.append(e0.elapsed_time(e1))
+    te = torch.tensor([float(np.mean(e2e))], device=dev)
+    dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    # accuracy: direct sum over all ranks' points at 100 of rank 0's targets
+    xa = [torch.zeros_like(X) for _ in range(world)]
+    qa = [torch.zeros_like(Q) for _ in range(world)]
+    dist.all_gather(xa, X)
+    dist.all_gather(qa, Q)
+    if rank == 0:
+        xs, qs = torch.cat(xa).cpu().numpy(), torch.cat(qa).cpu().numpy()
+        idx = np.random.default_rng(7).choice(a.n, 100, replace=False)
+        ref = np.array([np.sum(np.delete(qs, i) / np.linalg.norm(np.delete(xs, i, axis=0) - xs[i], axis=1))
+                        for i in idx])
+        rel = float(np.linalg.norm(u.cpu().numpy()[idx] - ref) / np.linalg.norm(ref))
+        line = {
+            "metric": METRIC, "value": a.n * world / (t_step * 1e-3), "unit": "points/s", "n_gpus": world,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": t_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"uniform iid in [0,1]^3, {a.n} points per GPU, one global problem of "
+                                   f"{a.n * world} points, 3D Laplace, eps={a.eps}, leaf capacity {a.ns}",
+                       "N_per_gpu": a.n, "eps": a.eps, "leaf_capacity": a.ns,
+                       "step": "partitioned DMK: root all-reduce, Morton partition, all-to-all, halo, "
+                               "coarse-moment all-reduce, plan + upward x2 + downward, return all-to-all",
+                       "l2": "flushed by a 256 MiB write between timed steps",
+                       "parallelism": f"Morton partition over {world} ranks (NCCL)",
+                       "partition_level": st.get("level"), "halo_points_rank0": st.get("n_halo"),
+                       "own_points_rank0": st.get("n_own")},
+            "rel_l2_err_sampled": rel, "clocks": clocks,
+            "e2e": {"value": a.n * world / (float(te.item()) * 1e-3), "unit": "points/s",
+                    "h2d_bytes_per_step": a.n * 4 * 8, "d2h_bytes_per_step": a.n * 8,
+                    "api": "paper_2308_00292_b200.parallel.dmk_eval_distributed(host tensors copied in/out)"},
+            "gpu_launches": int(launches),
+        }
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+
+
 def main():
     a = parse()
     if a.impl == "reference":
         return run_reference(a)
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1 or os.environ.get("DMK_BENCH_DISTRIBUTED") == "1":
+        return run_distributed(a)
     os.environ.setdefault("DMK_PROFILE", "1")
     import numpy as np
     import torch
