@@ -358,8 +358,10 @@ def main():
     sptr = stream.cuda_stream
     flush = torch.empty(256 * 2 ** 20 // 4, dtype=torch.float32, device=dev)
 
-    def step():
+    def step(mid=None):
         plan = dmk.dmk_plan(X, eps=a.eps, leaf_capacity=a.ns, stream=sptr)
+        if mid is not None:
+            mid.record(stream)
         u = plan.eval(Q)
         return plan, u
 
@@ -374,7 +376,7 @@ def main():
     L.dmk_kernel_launches.argtypes = [ctypes.c_void_p]
     clk = Clocks(local)
     clk.start()
-    times, stage_ms = [], {}
+    times, stage_ms, plan_ms = [], {}, []
     launches0 = L.dmk_kernel_launches(None)
     info = pairs = None
     for k in range(a.steps):
@@ -382,12 +384,14 @@ def main():
         torch.cuda.synchronize(dev)
         barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        em = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        plan, u = step()
+        plan, u = step(em)
         e1.record(stream)
         torch.cuda.synchronize(dev)
         barrier()
         times.append(e0.elapsed_time(e1))
+        plan_ms.append(e0.elapsed_time(em))
         for name, ms in plan.timings().items():
             stage_ms[name] = stage_ms.get(name, 0.0) + ms / a.steps
         if k == a.steps - 1:
@@ -453,7 +457,7 @@ def main():
             ach, peak, u_ = amount / (ms * 1e-3) / 1e12, fp64_peak, "TFLOP/s"
         stages[name] = {"ms": round(ms, 4), "bound": bound, "achieved": round(ach, 3), "peak": round(peak, 1),
                         "unit": u_, "frac": round(ach / peak, 4)}
-    tree_ms = t_step - sum(stage_ms.get(s, 0.0) for s in ["gather", *models.keys()])
+    tree_ms = float(np.mean(plan_ms))          # dmk_plan: tree, lists, tables (cached)
     dom = max(stages, key=lambda s: stages[s]["ms"])
     roof = dict(stages[dom])
     roof.pop("ms")
@@ -475,7 +479,8 @@ def main():
                 "api": "paper_2308_00292_b200.dmk_plan(host points) + Plan.eval(host charges -> host potentials)"},
         "gpu_launches": int(launches),
         "roofline": roof,
-        "stages_ms": {**{k: round(v, 4) for k, v in stage_ms.items()}, "tree_and_lists": round(tree_ms, 4)},
+        "stages_ms": {**{k: round(v, 4) for k, v in stage_ms.items()}, "tree_and_lists": round(tree_ms, 4),
+                      "note": "p2p runs on a side stream concurrently with anterp..eval; stages overlap"},
         "stages": stages,
         "tree": {"nbox": info.nbox, "nlevels": info.nlevels, "nfout": info.nfout, "nexp": info.nexp,
                  "p2p_pairs": pairs, "p2p_pairs_in_ball": inball},

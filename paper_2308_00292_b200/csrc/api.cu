@@ -112,6 +112,12 @@ int dmk_plan(int dim, int kernel, double eps, int64_t n, const double* points, i
           P->side = opt->root[dim];
         }
       }
+      int prio_lo = 0, prio_hi = 0;
+      DMK_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+      DMK_CUDA(cudaStreamCreateWithPriority(&P->side_stream, cudaStreamNonBlocking, prio_lo));
+      DMK_CUDA(cudaStreamCreateWithPriority(&P->hi_stream, cudaStreamNonBlocking, prio_hi));
+      DMK_CUDA(cudaEventCreateWithFlags(&P->ev_fork, cudaEventDisableTiming));
+      DMK_CUDA(cudaEventCreateWithFlags(&P->ev_join, cudaEventDisableTiming));
       const char* pe = std::getenv("DMK_PROFILE");
       P->profile = pe && pe[0] == '1';
       const char* pt = std::getenv("DMK_PROFILE_TREE");
@@ -223,6 +229,9 @@ int dmk_destroy(dmk_plan_t P) {
   return guard([&] {
     if (!P) return;
     cudaStream_t s = P->stream;
+    if (P->p2p_pending) cudaStreamWaitEvent(s, P->ev_join, 0);   // near-field branch still running
+    if (P->side_stream) cudaStreamSynchronize(P->side_stream);
+    if (P->hi_stream) cudaStreamSynchronize(P->hi_stream);
     delete P;   // DevBuf destructors enqueue cudaFreeAsync on the plan stream
     cudaStreamSynchronize(s);
   });

@@ -157,8 +157,17 @@ struct dmk_plan_s {
   std::vector<Mark> ev_marks;
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
+  // near-field branch: side stream + fork/join events (created with the plan)
+  cudaStream_t side_stream = nullptr;   // near field, lowest priority
+  cudaStream_t hi_stream = nullptr;     // far field, highest priority
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  bool p2p_pending = false;   // a near-field branch was forked and not yet joined
   ~dmk_plan_s() {
     for (auto e : ev_pool) cudaEventDestroy(e);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+    if (side_stream) cudaStreamDestroy(side_stream);
+    if (hi_stream) cudaStreamDestroy(hi_stream);
   }
 };
 

@@ -139,16 +139,16 @@ struct Timer {
     }
     return P->ev_pool[P->ev_used++];
   }
-  void begin(const char* nm) {
+  void begin(const char* nm, cudaStream_t st = nullptr) {
     if (!P->profile) return;
     cudaEvent_t e = ev();
-    DMK_CUDA(cudaEventRecord(e, P->stream));
+    DMK_CUDA(cudaEventRecord(e, st ? st : P->stream));
     P->ev_marks.push_back({nm, e, nullptr});
   }
-  void end() {
+  void end(cudaStream_t st = nullptr) {
     if (!P->profile) return;
     cudaEvent_t e = ev();
-    DMK_CUDA(cudaEventRecord(e, P->stream));
+    DMK_CUDA(cudaEventRecord(e, st ? st : P->stream));
     P->ev_marks.back().e1 = e;
   }
 };

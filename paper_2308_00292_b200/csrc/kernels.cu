@@ -865,11 +865,14 @@ __global__ void __launch_bounds__(128) k_p2p(DevTree t, const int32_t* __restric
       __syncwarp();
     }
   }
-  if (lane < nt) {
-    const int i = t0 + lane;
-    unear[i] = acc;
-    out[perm[i]] = (ufar[i] + acc) * inv_side;
-  }
+  if (lane < nt) unear[t0 + lane] = acc;
+}
+
+// u = (u_far + u_near)/side, scattered to the caller's order (after both branches)
+__global__ void k_combine(const double* __restrict__ ufar, const double* __restrict__ unear,
+                          const int32_t* __restrict__ perm, int64_t n, double inv_side, double* __restrict__ out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) out[perm[i]] = (ufar[i] + unear[i]) * inv_side;
 }
 
 // ---------------------------------------------------------------- host launchers
@@ -904,7 +907,7 @@ constexpr int pw_ac(int H) { return 2 * H * H <= 1024 ? 2 : 1; }
 
 // Phases of run_eval: UP = anterpolation + c2p (Step 2), DOWN = Step 3; C2P_ONLY =
 // c2p for the levels above `top` only (after dmk_level_moments injected level `top`).
-constexpr int PH_UP = 1, PH_DOWN = 2, PH_C2P_ONLY = 4;
+constexpr int PH_ANTERP = 1, PH_DOWN = 2, PH_C2P_ONLY = 4, PH_C2P = 8, PH_UP = PH_ANTERP | PH_C2P;
 
 template <int P, int NF, int NF0>
 static void run_eval(dmk_plan_s* PL, int phase = PH_UP | PH_DOWN, int top = 0) {
@@ -929,7 +932,7 @@ static void run_eval(dmk_plan_s* PL, int phase = PH_UP | PH_DOWN, int top = 0) {
     }
     return;
   }
-  if (nl > 1 && (phase & PH_UP)) {
+  if (nl > 1 && (phase & PH_ANTERP)) {
     // ---- Step 2: upward pass
     tm.begin("anterp");
     DMK_CUDA(cudaMemsetAsync(PL->mom.p, 0, PL->mom.bytes(), s));
@@ -942,6 +945,8 @@ static void run_eval(dmk_plan_s* PL, int phase = PH_UP | PH_DOWN, int top = 0) {
       }
     }
     tm.end();
+  }
+  if (nl > 1 && (phase & PH_C2P)) {
     tm.begin("c2p");
     {
       size_t sm = sizeof(double) * (P3 + 2 * P * P);
@@ -1016,14 +1021,14 @@ static void run_eval(dmk_plan_s* PL, int phase = PH_UP | PH_DOWN, int top = 0) {
 
 // P2P dispatch on the kernel and the residual-polynomial degree
 template <int KER, bool FULL>
-static void run_p2p_deg(dmk_plan_s* PL, double* out, const ResPoly& rp, int K) {
+static void run_p2p_deg(dmk_plan_s* PL, double* out, const ResPoly& rp, int K, cudaStream_t st) {
   DevTree dt = dev_tree(PL);
   int nb = (int)((PL->np2p + 3) / 4);
   if (nb == 0) return;
   const Tables& T = *PL->tab;
 #define DMK_P2P_CASE(KK)                                                                                          \
   case KK:                                                                                                        \
-    k_p2p<KK, KER, FULL><<<nb, 128, 0, PL->stream>>>(dt, PL->p2p_items.p, PL->np2p, PL->dlist_off.p, PL->dlist.p, \
+    k_p2p<KK, KER, FULL><<<nb, 128, 0, st>>>(dt, PL->p2p_items.p, PL->np2p, PL->dlist_off.p, PL->dlist.p,         \
                                                       PL->q.p, PL->ufar.p, PL->perm.p, 1.0 / PL->side, rp,        \
                                                       T.dRespoly, T.lam, PL->unear.p, out);                       \
     break;
@@ -1048,43 +1053,81 @@ static void dispatch_p(dmk_plan_s* PL, F f) {
 
 // Step 2 (charges -> moments), 3D: gather the charges into Morton order, anterpolate,
 // c2p.  The moments stay in the plan for eval_downward().
+// Stream structure of one evaluation (3D).  The near field (Steps 4-5, P2P) needs only
+// the gathered charges; it runs on a LOW-priority side stream while the far field
+// (Steps 2-3) runs on a HIGH-priority stream, so the far field's level-by-level
+// launches keep their SMs and the P2P blocks fill whatever they leave idle.  Both
+// branches fork from and join back into the caller's plan stream.
+struct StreamSwap {   // run_eval launches on PL->stream: point it at a branch stream
+  dmk_plan_s* P;
+  cudaStream_t keep;
+  StreamSwap(dmk_plan_s* p, cudaStream_t st) : P(p), keep(p->stream) { p->stream = st; }
+  ~StreamSwap() { P->stream = keep; }
+};
+static void fork_to(dmk_plan_s* PL, cudaStream_t from, cudaStream_t to) {
+  DMK_CUDA(cudaEventRecord(PL->ev_fork, from));
+  DMK_CUDA(cudaStreamWaitEvent(to, PL->ev_fork, 0));
+}
+
 void eval_upward(dmk_plan_s* PL, const double* dcharges) {
-  cudaStream_t s = PL->stream;
+  cudaStream_t s = PL->stream, slo = PL->side_stream, shi = PL->hi_stream;
   PL->timings.clear();
   PL->ev_marks.clear();
   PL->ev_used = 0;
   Timer tm(PL);
+  // a near-field branch of an earlier call may still read q: join it first
+  if (PL->p2p_pending) DMK_CUDA(cudaStreamWaitEvent(s, PL->ev_join, 0));
   tm.begin("gather");
   k_gather_q<<<(int)((PL->n + 255) / 256), 256, 0, s>>>(dcharges, PL->perm.p, PL->n, PL->q.p);
   DMK_LAUNCH_CHECK();
   tm.end();
   if (PL->dim == 2) return;   // the 2D path runs as one piece (eval_plan_2d)
-  dispatch_p(PL, [&](auto P_, auto NF_, auto NF0_) { run_eval<P_(), NF_(), NF0_()>(PL, PH_UP); });
+  fork_to(PL, s, slo);
+  ResPoly rp{};
+  const auto& poly = PL->tab->respoly;
+  int K = (int)poly.size() - 1;
+  for (int k = 0; k <= K && k < 25; ++k) rp.a[k] = poly[k];
+  tm.begin("p2p", slo);
+  const bool full = PL->th.nlevels == 1;
+  if (PL->tab->kernel == DMK_KERNEL_YUKAWA) {
+    K = PL->tab->respoly_deg;
+    if (full) run_p2p_deg<KER_YUKAWA, true>(PL, nullptr, rp, K, slo);
+    else run_p2p_deg<KER_YUKAWA, false>(PL, nullptr, rp, K, slo);
+  } else {
+    if (full) run_p2p_deg<KER_LAPLACE, true>(PL, nullptr, rp, K, slo);
+    else run_p2p_deg<KER_LAPLACE, false>(PL, nullptr, rp, K, slo);
+  }
+  tm.end(slo);
+  DMK_CUDA(cudaEventRecord(PL->ev_join, slo));
+  PL->p2p_pending = true;
+  // far field, upward part, on the high-priority stream; joined back into s
+  fork_to(PL, s, shi);
+  {
+    StreamSwap sw(PL, shi);
+    dispatch_p(PL, [&](auto P_, auto NF_, auto NF0_) { run_eval<P_(), NF_(), NF0_()>(PL, PH_UP); });
+  }
+  fork_to(PL, shi, s);
 }
 
-// Steps 3-5, 3D: plane waves, local expansions, evaluation, P2P, scatter to dout.
+// Step 3 on the high-priority stream, then the join with the near-field branch and the
+// combine on the plan stream.
 void eval_downward(dmk_plan_s* PL, double* dout) {
   if (PL->dim == 2) {
     eval_plan_2d(PL, dout);
     return;
   }
-  dispatch_p(PL, [&](auto P_, auto NF_, auto NF0_) { run_eval<P_(), NF_(), NF0_()>(PL, PH_DOWN); });
-  Timer tm(PL);
-  ResPoly rp{};
-  const auto& poly = PL->tab->respoly;
-  int K = (int)poly.size() - 1;
-  for (int k = 0; k <= K && k < 25; ++k) rp.a[k] = poly[k];
-  tm.begin("p2p");
-  const bool full = PL->th.nlevels == 1;
-  if (PL->tab->kernel == DMK_KERNEL_YUKAWA) {
-    K = PL->tab->respoly_deg;
-    if (full) run_p2p_deg<KER_YUKAWA, true>(PL, dout, rp, K);
-    else run_p2p_deg<KER_YUKAWA, false>(PL, dout, rp, K);
-  } else {
-    if (full) run_p2p_deg<KER_LAPLACE, true>(PL, dout, rp, K);
-    else run_p2p_deg<KER_LAPLACE, false>(PL, dout, rp, K);
+  cudaStream_t s = PL->stream, shi = PL->hi_stream;
+  fork_to(PL, s, shi);
+  {
+    StreamSwap sw(PL, shi);
+    dispatch_p(PL, [&](auto P_, auto NF_, auto NF0_) { run_eval<P_(), NF_(), NF0_()>(PL, PH_DOWN); });
   }
-  tm.end();
+  fork_to(PL, shi, s);
+  DMK_CUDA(cudaStreamWaitEvent(s, PL->ev_join, 0));
+  PL->p2p_pending = false;
+  k_combine<<<(int)((PL->n + 255) / 256), 256, 0, s>>>(PL->ufar.p, PL->unear.p, PL->perm.p, PL->n, 1.0 / PL->side,
+                                                       dout);
+  DMK_LAUNCH_CHECK();
 }
 
 void eval_plan(dmk_plan_s* PL, const double* dcharges, double* dout) {
