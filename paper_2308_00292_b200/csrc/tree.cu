@@ -180,9 +180,31 @@ __global__ void k_big(const uint64_t* __restrict__ keys, int64_t n, int l, int n
   flags[a] = (start && big) ? 1 : 0;
 }
 
+// number of "big" level-l boxes (> ns points) for every level, one pass over the keys
+template <int D>
+__global__ void k_count_big(const uint64_t* __restrict__ keys, int64_t n, int ns, int l0, unsigned long long* cnt) {
+  __shared__ unsigned int c[LMAX];
+  for (int l = threadIdx.x; l < LMAX; l += blockDim.x) c[l] = 0;
+  __syncthreads();
+  for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < n; a += (int64_t)gridDim.x * blockDim.x) {
+    for (int l = l0; l < LMAX; ++l) {
+      const int sh = D * (NBITS - l);
+      const uint64_t cd = (sh >= 64) ? 0 : (keys[a] >> sh);
+      const bool big = (a + ns < n) && (((sh >= 64) ? 0 : (keys[a + ns] >> sh)) == cd);
+      if (!big) break;   // the level-l box of a holds <= ns points from a on: so do its children
+      const bool start = (a == 0) || (((sh >= 64) ? 0 : (keys[a - 1] >> sh)) != cd);
+      if (start) atomicAdd(&c[l], 1u);
+    }
+  }
+  __syncthreads();
+  for (int l = threadIdx.x; l < LMAX; l += blockDim.x)
+    if (c[l]) atomicAdd(&cnt[l], (unsigned long long)c[l]);
+}
+
 // the level-l boxes touching each level-(l+1) box q (2^D candidates, clipped)
 template <int D>
-__global__ void k_touch(const uint64_t* __restrict__ Bq, int64_t nq, int l, uint64_t* out, uint8_t* flags) {
+__global__ void k_touch(const uint64_t* __restrict__ Bq, int64_t nq, int l, uint64_t* out, uint8_t* flags,
+                        uint64_t sentinel = 0) {
   constexpr int NCH = Dim<D>::NCH;
   int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t >= nq * NCH) return;
@@ -197,8 +219,8 @@ __global__ void k_touch(const uint64_t* __restrict__ Bq, int64_t nq, int l, uint
     c[d] = lo + ((o >> (D - 1 - d)) & 1);
     ok = ok && c[d] >= 0 && c[d] < n1;
   }
-  out[t] = ok ? encode<D>(c) : 0;
-  flags[t] = ok ? 1 : 0;
+  out[t] = ok ? encode<D>(c) : sentinel;
+  if (flags) flags[t] = ok ? 1 : 0;
 }
 
 // non-empty level-l boxes whose parent is non-leaf
@@ -212,6 +234,34 @@ __global__ void k_nonempty(const uint64_t* __restrict__ keys, int64_t n, int l, 
   bool start = (a == 0) || ((keys[a - 1] >> sh) != c);
   codes[a] = c;
   flags[a] = (start && bsearch_u64(Bp, nBp, c >> D) >= 0) ? 1 : 0;
+}
+
+// box set of level l: children of the level-(l-1) non-leaf boxes that hold points or are
+// themselves non-leaf (candidates enumerated in Morton order, so the selection is sorted)
+template <int D>
+__global__ void k_child_cand(const uint64_t* __restrict__ Bp, int64_t nBp, const uint64_t* __restrict__ Bl,
+                             int64_t nBl, const uint64_t* __restrict__ keys, int64_t n, int l, uint64_t* codes,
+                             uint8_t* flags) {
+  constexpr int NCH = 1 << D;
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= nBp * NCH) return;
+  const uint64_t c = (Bp[t / NCH] << D) | (uint64_t)(t % NCH);
+  const int sh = D * (NBITS - l);
+  const int64_t lb = lower_bound_u64(keys, n, c << sh);
+  const bool nonempty = lb < n && (keys[lb] >> sh) == c;
+  const bool nonleaf = nBl > 0 && bsearch_u64(Bl, nBl, c) >= 0;
+  codes[t] = c;
+  flags[t] = (nonempty || nonleaf) ? 1 : 0;
+}
+
+// out[i] = a[idx[i]], out[m + i] = b[idx[i]]: many scalar reads, one round trip
+__global__ void k_read_at(const int32_t* __restrict__ a, const int32_t* __restrict__ b,
+                          const int64_t* __restrict__ idx, int m, int64_t* out) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < m) {
+    out[i] = a[idx[i]];
+    out[m + i] = b[idx[i]];
+  }
 }
 
 __global__ void k_iota_u64(uint64_t* out, int64_t n) {
@@ -435,6 +485,38 @@ int64_t sort_unique(cudaStream_t s, const uint64_t* in, int64_t n, int bits, Dev
   return h;
 }
 
+__global__ void k_is_sentinel(const uint64_t* a, const int64_t* cnt, uint64_t sentinel, int64_t* out) {
+  const int64_t c = *cnt;
+  out[0] = c;
+  out[1] = (c > 0 && a[c - 1] == sentinel) ? 1 : 0;
+}
+
+// sort + unique of n codes < 2^bits plus possibly the sentinel 2^bits (dropped): one
+// round trip for the count
+int64_t sort_unique_drop(cudaStream_t s, const uint64_t* in, int64_t n, int bits, DevBuf<uint64_t>& out) {
+  const uint64_t sentinel = (uint64_t)1 << bits;
+  DevBuf<uint64_t> sorted, tmp;
+  sorted.alloc(n, s);
+  tmp.alloc(n, s);
+  cub_run(s, [&](void* t, size_t& b) {
+    return cub::DeviceRadixSort::SortKeys(t, b, in, sorted.p, (int64_t)n, 0, bits + 1, s);
+  });
+  DevBuf<int64_t> cnt, res;
+  cnt.alloc(1, s);
+  res.alloc(2, s);
+  cub_run(s, [&](void* t, size_t& b) {
+    return cub::DeviceSelect::Unique(t, b, sorted.p, tmp.p, cnt.p, (int64_t)n, s);
+  });
+  k_is_sentinel<<<1, 1, 0, s>>>(tmp.p, cnt.p, sentinel, res.p);
+  int64_t h[2];
+  DMK_CUDA(cudaMemcpyAsync(h, res.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+  DMK_CUDA(cudaStreamSynchronize(s));
+  const int64_t m = h[0] - h[1];
+  out.alloc(m ? m : 1, s);
+  if (m) DMK_CUDA(cudaMemcpyAsync(out.p, tmp.p, m * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
+  return m;
+}
+
 void exclusive_scan(cudaStream_t s, const int32_t* in, int32_t* out, int64_t n) {
   cub_run(s, [&](void* t, size_t& b) { return cub::DeviceScan::ExclusiveSum(t, b, in, out, n, s); });
 }
@@ -526,10 +608,21 @@ static void build_tree_d(dmk_plan_s* P, const double* dpts) {
   std::vector<int64_t> nU(LMAX, 0);
   int ltop = -1;
   {
+    // the counts of every level in one pass and one round trip, then the selections
+    DevBuf<unsigned long long> dcnt;
+    dcnt.alloc(LMAX, s);
+    DMK_CUDA(cudaMemsetAsync(dcnt.p, 0, LMAX * sizeof(unsigned long long), s));
+    k_count_big<D><<<std::min(nblk(n), 4 * 148), TPB, 0, s>>>(P->keys.p, n, ns, P->min_level, dcnt.p);
+    DMK_LAUNCH_CHECK();
+    unsigned long long hc[LMAX];
+    DMK_CUDA(cudaMemcpyAsync(hc, dcnt.p, sizeof(hc), cudaMemcpyDeviceToHost, s));
+    DMK_CUDA(cudaStreamSynchronize(s));
     DevBuf<uint64_t> codes;
     DevBuf<uint8_t> flags;
+    DevBuf<int64_t> nsel;
     codes.alloc(n, s);
     flags.alloc(n, s);
+    nsel.alloc(1, s);
     for (int l = 0; l < LMAX; ++l) {
       if (l < P->min_level) {
         // forced refinement (distributed plans): every box of the levels above min_level
@@ -541,10 +634,14 @@ static void build_tree_d(dmk_plan_s* P, const double* dpts) {
         ltop = l;
         continue;
       }
+      nU[l] = (int64_t)hc[l];
+      if (nU[l] == 0) break;
       k_big<D><<<nblk(n), TPB, 0, s>>>(P->keys.p, n, l, ns, codes.p, flags.p);
       DMK_LAUNCH_CHECK();
-      nU[l] = select_flagged(s, codes.p, flags.p, n, U[l]);
-      if (nU[l] == 0) break;
+      U[l].alloc(nU[l], s);
+      cub_run(s, [&](void* t, size_t& b) {
+        return cub::DeviceSelect::Flagged(t, b, codes.p, flags.p, U[l].p, nsel.p, n, s);
+      });
       ltop = l;
     }
   }
@@ -560,18 +657,13 @@ static void build_tree_d(dmk_plan_s* P, const double* dpts) {
     for (int l = ltop - 1; l >= 0; --l) {
       int64_t nc = nU[l] + NCH * nB[l + 1];
       DevBuf<uint64_t> cand;
-      DevBuf<uint8_t> cf;
       cand.alloc(nc, s);
-      cf.alloc(nc, s);
-      if (nU[l]) {
-        DMK_CUDA(cudaMemcpyAsync(cand.p, U[l].p, nU[l] * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
-        DMK_CUDA(cudaMemsetAsync(cf.p, 1, nU[l], s));
-      }
-      k_touch<D><<<nblk(NCH * nB[l + 1]), TPB, 0, s>>>(B[l + 1].p, nB[l + 1], l, cand.p + nU[l], cf.p + nU[l]);
+      if (nU[l]) DMK_CUDA(cudaMemcpyAsync(cand.p, U[l].p, nU[l] * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
+      // out-of-domain touches become the sentinel 2^{D l}, dropped after the sort
+      k_touch<D><<<nblk(NCH * nB[l + 1]), TPB, 0, s>>>(B[l + 1].p, nB[l + 1], l, cand.p + nU[l], nullptr,
+                                                       (uint64_t)1 << (D * l));
       DMK_LAUNCH_CHECK();
-      DevBuf<uint64_t> valid;
-      int64_t nv = select_flagged(s, cand.p, cf.p, nc, valid);
-      nB[l] = sort_unique(s, valid.p, nv, D * l, B[l]);
+      nB[l] = sort_unique_drop(s, cand.p, nc, D * l, B[l]);
     }
   }
   const int nlevels = ltop + 2;
@@ -584,23 +676,17 @@ static void build_tree_d(dmk_plan_s* P, const double* dpts) {
   E[0].alloc(1, s);
   DMK_CUDA(cudaMemsetAsync(E[0].p, 0, sizeof(uint64_t), s));
   nE[0] = 1;
-  {
+  for (int l = 1; l < nlevels; ++l) {
+    const int64_t nc = (int64_t)NCH * nB[l - 1];
+    const int64_t nb_l = (l <= ltop) ? nB[l] : 0;
     DevBuf<uint64_t> codes;
     DevBuf<uint8_t> flags;
-    codes.alloc(n, s);
-    flags.alloc(n, s);
-    for (int l = 1; l < nlevels; ++l) {
-      k_nonempty<D><<<nblk(n), TPB, 0, s>>>(P->keys.p, n, l, B[l - 1].p, nB[l - 1], codes.p, flags.p);
-      DMK_LAUNCH_CHECK();
-      DevBuf<uint64_t> ne;
-      int64_t nne = select_flagged(s, codes.p, flags.p, n, ne);
-      int64_t nb_l = (l <= ltop) ? nB[l] : 0;
-      DevBuf<uint64_t> cat;
-      cat.alloc(nne + nb_l, s);
-      if (nne) DMK_CUDA(cudaMemcpyAsync(cat.p, ne.p, nne * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
-      if (nb_l) DMK_CUDA(cudaMemcpyAsync(cat.p + nne, B[l].p, nb_l * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
-      nE[l] = sort_unique(s, cat.p, nne + nb_l, D * l, E[l]);
-    }
+    codes.alloc(nc, s);
+    flags.alloc(nc, s);
+    k_child_cand<D><<<nblk(nc), TPB, 0, s>>>(B[l - 1].p, nB[l - 1], nb_l ? B[l].p : nullptr, nb_l, P->keys.p, n, l,
+                                             codes.p, flags.p);
+    DMK_LAUNCH_CHECK();
+    nE[l] = select_flagged(s, codes.p, flags.p, nc, E[l]);
   }
 
   mark("boxsets");
@@ -647,8 +733,10 @@ static void build_tree_d(dmk_plan_s* P, const double* dpts) {
   mark("boxattrs");
   // ---- flags, ranks, compact lists
   DevBuf<uint8_t> fsel, esel;
-  fsel.alloc(nbox, s);
-  esel.alloc(nbox, s);
+  fsel.alloc(nbox + 1, s);
+  esel.alloc(nbox + 1, s);
+  DMK_CUDA(cudaMemsetAsync(fsel.p + nbox, 0, 1, s));
+  DMK_CUDA(cudaMemsetAsync(esel.p + nbox, 0, 1, s));
   k_flags_out<<<nblk(nbox), TPB, 0, s>>>(P->box_start.p, P->box_end.p, P->box_level.p, P->min_level, nbox,
                                          P->box_flags.p, fsel.p);
   DMK_LAUNCH_CHECK();
@@ -658,27 +746,36 @@ static void build_tree_d(dmk_plan_s* P, const double* dpts) {
   DevBuf<int32_t> fscan, escan;
   fscan.alloc(nbox + 1, s);
   escan.alloc(nbox + 1, s);
-  exclusive_scan_u8(s, fsel.p, fscan.p, nbox);
-  exclusive_scan_u8(s, esel.p, escan.p, nbox);
+  exclusive_scan_u8(s, fsel.p, fscan.p, nbox + 1);
+  exclusive_scan_u8(s, esel.p, escan.p, nbox + 1);
   P->fout_rank.alloc(nbox, s);
   P->exp_rank.alloc(nbox, s);
   k_rank<<<nblk(nbox), TPB, 0, s>>>(fscan.p, fsel.p, nbox, P->fout_rank.p);
   k_rank<<<nblk(nbox), TPB, 0, s>>>(escan.p, esel.p, nbox, P->exp_rank.p);
   DMK_LAUNCH_CHECK();
   {
-    std::vector<int32_t> fs(nlevels + 1), es(nlevels + 1);
-    int32_t lastf = d2h_at(s, fscan.p + nbox - 1), laste = d2h_at(s, escan.p + nbox - 1);
-    uint8_t lf = d2h_at(s, fsel.p + nbox - 1), le = d2h_at(s, esel.p + nbox - 1);
-    P->nfout = lastf + lf;
-    P->nexp = laste + le;
+    // totals and per-level rank offsets in one round trip
+    std::vector<int64_t> idx(nlevels + 1);
+    for (int l = 0; l < nlevels; ++l) idx[l] = th.level_off[l];
+    idx[nlevels] = nbox;
+    const int m = nlevels + 1;
+    DevBuf<int64_t> didx, dout;
+    didx.alloc(m, s);
+    dout.alloc(2 * m, s);
+    DMK_CUDA(cudaMemcpyAsync(didx.p, idx.data(), m * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    k_read_at<<<1, 64, 0, s>>>(fscan.p, escan.p, didx.p, m, dout.p);
+    DMK_LAUNCH_CHECK();
+    std::vector<int64_t> h(2 * m);
+    DMK_CUDA(cudaMemcpyAsync(h.data(), dout.p, 2 * m * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    DMK_CUDA(cudaStreamSynchronize(s));
+    P->nfout = h[nlevels];
+    P->nexp = h[m + nlevels];
     th.fout_off.assign(nlevels + 1, 0);
     th.exp_off.assign(nlevels + 1, 0);
-    for (int l = 1; l < nlevels; ++l) {
-      th.fout_off[l] = d2h_at(s, fscan.p + th.level_off[l]);
-      th.exp_off[l] = d2h_at(s, escan.p + th.level_off[l]);
+    for (int l = 0; l <= nlevels; ++l) {
+      th.fout_off[l] = h[l];
+      th.exp_off[l] = h[m + l];
     }
-    th.fout_off[nlevels] = P->nfout;
-    th.exp_off[nlevels] = P->nexp;
   }
   {
     cub::CountingInputIterator<int32_t> cnt_it(0);
@@ -695,37 +792,44 @@ static void build_tree_d(dmk_plan_s* P, const double* dpts) {
   }
 
   mark("flags");
-  // ---- direct lists (CSR over boxes)
+  // ---- direct lists (CSR over boxes) and P2P work items: counts, scans, one round trip
+  // for both totals, fills
   {
-    DevBuf<int32_t> cnt;
+    DevBuf<int32_t> cnt, pcnt, poff;
     cnt.alloc(nbox + 1, s);
+    pcnt.alloc(nbox + 1, s);
+    poff.alloc(nbox + 1, s);
     DMK_CUDA(cudaMemsetAsync(cnt.p, 0, (nbox + 1) * sizeof(int32_t), s));
+    DMK_CUDA(cudaMemsetAsync(pcnt.p, 0, (nbox + 1) * sizeof(int32_t), s));
     k_dlist<D, false><<<nblk(nbox), TPB, 0, s>>>(P->box_start.p, P->box_end.p, P->box_parent.p, P->box_child.p,
                                               P->box_coll.p, P->box_flags.p, P->box_code.p, P->box_level.p, nbox,
                                               cnt.p, nullptr, nullptr);
     DMK_LAUNCH_CHECK();
+    k_p2p_count<<<nblk(nbox), TPB, 0, s>>>(P->box_start.p, P->box_end.p, P->box_flags.p, nbox, pcnt.p);
+    DMK_LAUNCH_CHECK();
     P->dlist_off.alloc(nbox + 1, s);
     exclusive_scan(s, cnt.p, P->dlist_off.p, nbox + 1);
-    P->ndlist = d2h_at(s, P->dlist_off.p + nbox);
+    exclusive_scan(s, pcnt.p, poff.p, nbox + 1);
+    DevBuf<int64_t> didx, dout;
+    didx.alloc(1, s);
+    dout.alloc(2, s);
+    const int64_t last = nbox;
+    DMK_CUDA(cudaMemcpyAsync(didx.p, &last, sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    k_read_at<<<1, 32, 0, s>>>(P->dlist_off.p, poff.p, didx.p, 1, dout.p);
+    DMK_LAUNCH_CHECK();
+    int64_t h[2];
+    DMK_CUDA(cudaMemcpyAsync(h, dout.p, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    DMK_CUDA(cudaStreamSynchronize(s));
+    P->ndlist = h[0];
+    P->np2p = h[1];
     P->dlist.alloc(P->ndlist ? P->ndlist : 1, s);
     k_dlist<D, true><<<nblk(nbox), TPB, 0, s>>>(P->box_start.p, P->box_end.p, P->box_parent.p, P->box_child.p,
                                              P->box_coll.p, P->box_flags.p, P->box_code.p, P->box_level.p, nbox,
                                              nullptr, P->dlist_off.p, P->dlist.p);
     DMK_LAUNCH_CHECK();
-  }
-  mark("dlists");
-  // ---- P2P work items
-  {
-    DevBuf<int32_t> cnt, off;
-    cnt.alloc(nbox + 1, s);
-    off.alloc(nbox + 1, s);
-    DMK_CUDA(cudaMemsetAsync(cnt.p, 0, (nbox + 1) * sizeof(int32_t), s));
-    k_p2p_count<<<nblk(nbox), TPB, 0, s>>>(P->box_start.p, P->box_end.p, P->box_flags.p, nbox, cnt.p);
-    DMK_LAUNCH_CHECK();
-    exclusive_scan(s, cnt.p, off.p, nbox + 1);
-    P->np2p = d2h_at(s, off.p + nbox);
+    mark("dlists");
     P->p2p_items.alloc(2 * (P->np2p ? P->np2p : 1), s);
-    k_p2p_fill<<<nblk(nbox), TPB, 0, s>>>(P->box_start.p, cnt.p, off.p, nbox, P->p2p_items.p);
+    k_p2p_fill<<<nblk(nbox), TPB, 0, s>>>(P->box_start.p, pcnt.p, poff.p, nbox, P->p2p_items.p);
     DMK_LAUNCH_CHECK();
   }
   DMK_CUDA(cudaStreamSynchronize(s));
