@@ -177,6 +177,54 @@ __global__ void __launch_bounds__(P* P) k_c2p(DevTree t, const int32_t* __restri
   }
 }
 
+// c2p split over the children for parallelism (the per-parent kernel above runs its 8
+// children one after the other, which leaves the coarse levels latency-bound):
+// k_c2p_child transforms one F_out child's moments into a scratch slot, k_c2p_sum adds
+// the slots of each parent's children in octant order (deterministic).
+template <int P>
+__global__ void __launch_bounds__(P* P) k_c2p_child(DevTree t, const int32_t* __restrict__ boxes, int64_t r0,
+                                                    const double* __restrict__ A, const double* __restrict__ mom,
+                                                    double* __restrict__ scratch) {
+  constexpr int P2 = P * P, P3 = P2 * P, NT = P2;
+  extern __shared__ double sm[];
+  double* cube = sm;
+  double* sA = cube + P3;
+  const int b = boxes[blockIdx.x], tid = threadIdx.x;
+  const int o = (int)(t.code[b] & 7);
+  for (int i = tid; i < 2 * P2; i += NT) sA[i] = A[i];
+  const double* src = mom + (size_t)t.fout_rank[b] * P3;
+  for (int i = tid; i < P3; i += NT) cube[i] = src[i];
+  __syncthreads();
+  line_apply<P, false>(cube, sA + ((o >> 0) & 1) * P2, 2, tid, NT);
+  __syncthreads();
+  line_apply<P, false>(cube, sA + ((o >> 1) & 1) * P2, 1, tid, NT);
+  __syncthreads();
+  line_apply<P, false>(cube, sA + ((o >> 2) & 1) * P2, 0, tid, NT);
+  __syncthreads();
+  double* dst = scratch + (size_t)(t.fout_rank[b] - r0) * P3;
+  for (int i = tid; i < P3; i += NT) dst[i] = cube[i];
+}
+template <int P>
+__global__ void __launch_bounds__(256) k_c2p_sum(DevTree t, const int32_t* __restrict__ boxes, int64_t r0,
+                                                 const double* __restrict__ scratch, double* __restrict__ mom) {
+  constexpr int P3 = P * P * P;
+  const int b = boxes[blockIdx.x];
+  __shared__ int slot[8];
+  if (threadIdx.x < 8) {
+    const int ch = t.child[8 * (int64_t)b + threadIdx.x];
+    slot[threadIdx.x] = (ch >= 0 && (t.flags[ch] & F_OUT)) ? (int)(t.fout_rank[ch] - r0) : -1;
+  }
+  __syncthreads();
+  double* dst = mom + (size_t)t.fout_rank[b] * P3;
+  for (int i = threadIdx.x; i < P3; i += 256) {
+    double v = dst[i];
+#pragma unroll
+    for (int o = 0; o < 8; ++o)
+      if (slot[o] >= 0) v += scratch[(size_t)slot[o] * P3 + i];
+    dst[i] = v;
+  }
+}
+
 // p2c: Lambda(B) += (A_sx^T (x) A_sy^T (x) A_sz^T) Lambda(parent)
 template <int P>
 __global__ void __launch_bounds__(P* P) k_p2c(DevTree t, const int32_t* __restrict__ boxes, const double* __restrict__ A,
@@ -909,6 +957,25 @@ constexpr int pw_ac(int H) { return 2 * H * H <= 1024 ? 2 : 1; }
 // c2p for the levels above `top` only (after dmk_level_moments injected level `top`).
 constexpr int PH_ANTERP = 1, PH_DOWN = 2, PH_C2P_ONLY = 4, PH_C2P = 8, PH_UP = PH_ANTERP | PH_C2P;
 
+// c2p into the level-l parents: transform every F_out child (level l+1) in parallel
+// into scratch (the plane-wave buffer, unused until prox2pw), then add per parent.
+template <int P>
+static void run_c2p_level(dmk_plan_s* PL, const DevTree& dt, int l) {
+  constexpr int P3 = P * P * P;
+  cudaStream_t s = PL->stream;
+  const auto& th = PL->th;
+  const int64_t a = th.fout_off[l], b = th.fout_off[l + 1];
+  const int64_t ca = th.fout_off[l + 1], cb = th.fout_off[l + 2];
+  if (b <= a || cb <= ca) return;
+  if ((size_t)(cb - ca) * P3 > PL->phi.n) fail(DMK_ERR_STATE, "c2p scratch too small");
+  const size_t sm = sizeof(double) * (P3 + 2 * P * P);
+  set_smem(k_c2p_child<P>, sm);
+  k_c2p_child<P><<<(int)(cb - ca), P * P, sm, s>>>(dt, PL->fout_list.p + ca, ca, PL->tab->dA, PL->mom.p, PL->phi.p);
+  DMK_LAUNCH_CHECK();
+  k_c2p_sum<P><<<(int)(b - a), 256, 0, s>>>(dt, PL->fout_list.p + a, ca, PL->phi.p, PL->mom.p);
+  DMK_LAUNCH_CHECK();
+}
+
 template <int P, int NF, int NF0>
 static void run_eval(dmk_plan_s* PL, int phase = PH_UP | PH_DOWN, int top = 0) {
   using C = Cfg<P>;
@@ -921,15 +988,7 @@ static void run_eval(dmk_plan_s* PL, int phase = PH_UP | PH_DOWN, int top = 0) {
   Timer tm(PL);
   const int64_t n = PL->n;
   if (nl > 1 && (phase & PH_C2P_ONLY)) {
-    size_t sm = sizeof(double) * (P3 + 2 * P * P);
-    set_smem(k_c2p<P>, sm);
-    for (int l = top - 1; l >= 0; --l) {
-      int64_t a = th.fout_off[l], b = th.fout_off[l + 1];
-      if (b > a) {
-        k_c2p<P><<<(int)(b - a), P * P, sm, s>>>(dt, PL->fout_list.p + a, T.dA, PL->mom.p);
-        DMK_LAUNCH_CHECK();
-      }
-    }
+    for (int l = top - 1; l >= 0; --l) run_c2p_level<P>(PL, dt, l);
     return;
   }
   if (nl > 1 && (phase & PH_ANTERP)) {
@@ -948,14 +1007,7 @@ static void run_eval(dmk_plan_s* PL, int phase = PH_UP | PH_DOWN, int top = 0) {
   }
   if (nl > 1 && (phase & PH_C2P)) {
     tm.begin("c2p");
-    {
-      size_t sm = sizeof(double) * (P3 + 2 * P * P);
-      set_smem(k_c2p<P>, sm);
-      for (int l = nl - 2; l >= 0; --l) {
-        int64_t a = th.fout_off[l], b = th.fout_off[l + 1];
-        if (b > a) { k_c2p<P><<<(int)(b - a), P * P, sm, s>>>(dt, PL->fout_list.p + a, T.dA, PL->mom.p); DMK_LAUNCH_CHECK(); }
-      }
-    }
+    for (int l = nl - 2; l >= 0; --l) run_c2p_level<P>(PL, dt, l);
     tm.end();
   }
   if (nl > 1 && (phase & PH_DOWN)) {
