@@ -752,6 +752,98 @@ __global__ void __launch_bounds__(256) k_eval_mma(DevTree t, const int32_t* __re
   }
 }
 
+// Far-field evaluation, padded-tile form (P <= 18): the DMMA n dimension runs over
+// (n1, n2) with n2 padded to NB blocks of 8, so every output tile has a single n1 and
+// the epilogue u_j += Tx_j[n1] (c0 Ty_j[n2] + c1 Ty_j[n2+1]) needs no index division
+// (the unpadded version spends most of its issue slots there).
+template <int P>
+struct EvalPad {
+  static constexpr int KS = (P + 3) / 4, NB = (P + 7) / 8, NTL = P * NB, NW = 8;
+  static constexpr size_t smem = sizeof(double) * ((size_t)NTL * KS * 32 + (size_t)NW * 8 * 3 * P);
+};
+template <int P>
+__global__ void __launch_bounds__(256) k_eval_pad(DevTree t, const int32_t* __restrict__ boxes,
+                                                  const double* __restrict__ lam, double* __restrict__ ufar) {
+  using E = EvalPad<P>;
+  constexpr int P2 = P * P, KS = E::KS, NB = E::NB, NTL = E::NTL, NW = E::NW;
+  extern __shared__ double sm[];
+  double* lamF = sm;                        // [NTL][KS][32] B fragments, tile nt = n1*NB + blk
+  double* Tv = lamF + NTL * KS * 32;        // [NW][8 targets][3 dims][P]
+  __shared__ int2 rg[8];
+  __shared__ int nr_s, tot_s;
+  const int b = boxes[blockIdx.x], tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    nr_s = box_ranges<true>(t, b, rg);
+    int tot = 0;
+    for (int r = 0; r < nr_s; ++r) tot += rg[r].y - rg[r].x;
+    tot_s = tot;
+  }
+  const double* src = lam + (size_t)t.exp_rank[b] * P * P2;
+  for (int i = tid; i < NTL * KS * 32; i += NW * 32) {
+    const int ln = i & 31, ks = (i >> 5) % KS, nt = (i >> 5) / KS;
+    const int n1 = nt / NB, n2 = (nt % NB) * 8 + (ln >> 2), n3 = ks * 4 + (ln & 3);
+    lamF[i] = (n2 < P && n3 < P) ? src[(n1 * P + n2) * P + n3] : 0.0;
+  }
+  __syncthreads();
+  const int nr = nr_s, tot = tot_s;
+  if (tot == 0) return;
+  double cen[3], ih;
+  box_geom(t.code[b], t.level[b], cen, ih);
+  double* T = Tv + warp * 8 * 3 * P;
+  const int g = lane >> 2, q4 = lane & 3;
+  for (int tt = warp * 8; tt < tot; tt += NW * 8) {
+    const int nv = min(8, tot - tt);
+    if (lane < 24) {
+      const int j = lane / 3, d = lane % 3;
+      double Tl[P];
+      if (j < nv) {
+        const int pi = range_point(rg, nr, tt + j);
+        const double x = (d == 0 ? t.xs[pi] : d == 1 ? t.ys[pi] : t.zs[pi]);
+        cheb_vec((x - cen[d]) * ih, Tl, P, 1.0);
+      } else {
+#pragma unroll
+        for (int n = 0; n < P; ++n) Tl[n] = 0.0;
+      }
+#pragma unroll
+      for (int n = 0; n < P; ++n) T[(j * 3 + d) * P + n] = Tl[n];
+    }
+    __syncwarp();
+    double af[KS], ty[NB][2];
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      const int n3 = ks * 4 + q4;
+      af[ks] = n3 < P ? T[(g * 3 + 2) * P + n3] : 0.0;
+    }
+#pragma unroll
+    for (int bl = 0; bl < NB; ++bl)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int n2 = bl * 8 + 2 * q4 + e;
+        ty[bl][e] = n2 < P ? T[(g * 3 + 1) * P + n2] : 0.0;
+      }
+    const double* Tx = T + (g * 3 + 0) * P;
+    double part = 0.0;
+#pragma unroll 1
+    for (int n1 = 0; n1 < P; ++n1) {
+      double c[NB][2];
+#pragma unroll
+      for (int bl = 0; bl < NB; ++bl) c[bl][0] = c[bl][1] = 0.0;
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+        for (int bl = 0; bl < NB; ++bl) dmma(c[bl][0], c[bl][1], af[ks], lamF[((n1 * NB + bl) * KS + ks) * 32 + lane]);
+      double v = 0.0;
+#pragma unroll
+      for (int bl = 0; bl < NB; ++bl) v = fma(c[bl][0], ty[bl][0], fma(c[bl][1], ty[bl][1], v));
+      part = fma(Tx[n1], v, part);
+    }
+    part += __shfl_xor_sync(0xffffffffu, part, 1);
+    part += __shfl_xor_sync(0xffffffffu, part, 2);
+    if (q4 == 0 && g < nv) ufar[range_point(rg, nr, tt + g)] = part;
+    __syncwarp();
+  }
+}
+
 // Anterpolation: mu[a][b] = sum_j (rho_j Tx_j[n1] Ty_j[n2]) Tz_j[b] as C = U^T V with
 // the points as the DMMA k dimension; each warp keeps its m-tiles x all n-tiles of mu
 // in registers.  One CTA per F_out box.
@@ -1058,10 +1150,16 @@ static void run_eval(dmk_plan_s* PL, int phase = PH_UP | PH_DOWN, int top = 0) {
     tm.end();
     tm.begin("eval");
     {
-      size_t sm = EvalMma<P>::smem;
-      set_smem(k_eval_mma<P>, sm);
       if (PL->nexp) {
-        k_eval_mma<P><<<(int)PL->nexp, 256, sm, s>>>(dt, PL->exp_list.p, PL->lam.p, PL->ufar.p);
+        if constexpr (P <= 18) {
+          size_t sm = EvalPad<P>::smem;
+          set_smem(k_eval_pad<P>, sm);
+          k_eval_pad<P><<<(int)PL->nexp, 256, sm, s>>>(dt, PL->exp_list.p, PL->lam.p, PL->ufar.p);
+        } else {
+          size_t sm = EvalMma<P>::smem;
+          set_smem(k_eval_mma<P>, sm);
+          k_eval_mma<P><<<(int)PL->nexp, 256, sm, s>>>(dt, PL->exp_list.p, PL->lam.p, PL->ufar.p);
+        }
         DMK_LAUNCH_CHECK();
       }
     }
