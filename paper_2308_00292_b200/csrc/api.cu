@@ -118,6 +118,8 @@ int dmk_plan(int dim, int kernel, double eps, int64_t n, const double* points, i
       DMK_CUDA(cudaStreamCreateWithPriority(&P->hi_stream, cudaStreamNonBlocking, prio_hi));
       DMK_CUDA(cudaEventCreateWithFlags(&P->ev_fork, cudaEventDisableTiming));
       DMK_CUDA(cudaEventCreateWithFlags(&P->ev_join, cudaEventDisableTiming));
+      const char* ps = std::getenv("DMK_SERIAL");
+      P->serial = ps && ps[0] == '1';
       const char* pe = std::getenv("DMK_PROFILE");
       P->profile = pe && pe[0] == '1';
       const char* pt = std::getenv("DMK_PROFILE_TREE");

@@ -162,6 +162,7 @@ struct dmk_plan_s {
   cudaStream_t hi_stream = nullptr;     // far field, highest priority
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   bool p2p_pending = false;   // a near-field branch was forked and not yet joined
+  bool serial = false;        // DMK_SERIAL=1: near field on the plan stream (no overlap)
   ~dmk_plan_s() {
     for (auto e : ev_pool) cudaEventDestroy(e);
     if (ev_fork) cudaEventDestroy(ev_fork);

@@ -849,7 +849,7 @@ __global__ void __launch_bounds__(256) k_eval_pad(DevTree t, const int32_t* __re
 // in registers.  One CTA per F_out box.
 template <int P>
 struct AntMma {
-  static constexpr int P2 = P * P, MT = (P2 + 7) / 8, NTB = (P + 7) / 8, NW = (P >= 28) ? 16 : 8;
+  static constexpr int P2 = P * P, MT = (P2 + 7) / 8, NTB = (P + 7) / 8, NW = (P >= 18) ? 16 : 8;
   static constexpr int MPW = (MT + NW - 1) / NW, CH = 64;
   static constexpr size_t smem = sizeof(double) * 3 * CH * P;
 };
@@ -1232,6 +1232,7 @@ void eval_upward(dmk_plan_s* PL, const double* dcharges) {
   DMK_LAUNCH_CHECK();
   tm.end();
   if (PL->dim == 2) return;   // the 2D path runs as one piece (eval_plan_2d)
+  if (PL->serial) slo = s;    // DMK_SERIAL=1: no overlap (per-stage timing / profiling)
   fork_to(PL, s, slo);
   ResPoly rp{};
   const auto& poly = PL->tab->respoly;
