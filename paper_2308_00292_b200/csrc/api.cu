@@ -308,7 +308,17 @@ int dmk_stage_copy(dmk_plan_t P, int which, double* out, int64_t count) {
     const DevBuf<double>* b = nullptr;
     switch (which) {
       case DMK_STAGE_MOMENTS: b = &P->mom; break;
-      case DMK_STAGE_OUTGOING: b = &P->phi; break;
+      case DMK_STAGE_OUTGOING:
+        if (P->dim == 3 && P->tab->p <= 18) {   // stored in fp32 (reading R16): widen
+          if (count != (int64_t)P->phi.n) fail(DMK_ERR_ARG, "count must equal the stage size");
+          std::vector<float> h(count);
+          DMK_CUDA(cudaMemcpyAsync(h.data(), P->phi.p, count * sizeof(float), cudaMemcpyDeviceToHost, P->stream));
+          DMK_CUDA(cudaStreamSynchronize(P->stream));
+          for (int64_t i = 0; i < count; ++i) out[i] = h[i];
+          return;
+        }
+        b = &P->phi;
+        break;
       case DMK_STAGE_LOCAL: b = &P->lam; break;
       case DMK_STAGE_UFAR: b = &P->ufar; break;
       case DMK_STAGE_UNEAR: b = &P->unear; break;

@@ -267,6 +267,13 @@ __global__ void __launch_bounds__(P* P) k_p2c(DevTree t, const int32_t* __restri
 // with Gr[n][a] = c_a Qr[a][n], c_0 = 1, c_a = 2.  Everything is real and each 1D factor
 // has half of p columns: 4x fewer flops than the complex form.
 // Per-box layout F[a][pi][b][c], pi = 4 pi1 + 2 pi2 + pi3: one slab a is contiguous.
+// Storage precision of the outgoing plane waves F (precision tier, DESIGN.md reading
+// R16): fp32 for eps >= 1e-6 (p <= 18) -- F is re-read 27 times per level from L2 and
+// its rounding adds < 2% of the 1e-6 error budget -- fp64 for eps = 1e-9.  All
+// arithmetic is fp64; only the stored values are rounded.
+template <int P>
+using FStore = typename std::conditional<(P <= 18), float, double>::type;
+
 template <int P, int H>
 struct PwGeom {
   static constexpr int PP = (P + 1) & ~1, HH = (H + 1) & ~1, P2 = P * P, HSQ = H * H;
@@ -304,9 +311,10 @@ struct Prox2pw {
 template <int P, int H, int CH>
 __global__ void __launch_bounds__(256) k_prox2pw(DevTree t, const int32_t* __restrict__ boxes,
                                                  const double* __restrict__ Qr, const double* __restrict__ mom,
-                                                 double* __restrict__ F, size_t base, size_t stride) {
+                                                 FStore<P>* __restrict__ F, size_t base, size_t stride) {
   using G = PwGeom<P, H>;
   using C = Prox2pw<P, H, CH>;
+  using TF = FStore<P>;
   constexpr int NT = C::NT, P2 = G::P2, PP = G::PP, KS = C::KS, K4 = KS * 4, HP = C::HP, HSQ = G::HSQ;
   extern __shared__ double sm[];
   double* sQ = sm;                   // [2][HP][K4]: sQ[pi][a][j] = Qr[a][2j+pi], zero padded
@@ -315,7 +323,7 @@ __global__ void __launch_bounds__(256) k_prox2pw(DevTree t, const int32_t* __res
   const int b = boxes[blockIdx.x], tid = threadIdx.x;
   const int r = t.fout_rank[b];
   const double* mu = mom + (size_t)r * P * P2;
-  double* out = F + base + (size_t)(r == 0 ? 0 : r - 1) * stride;
+  TF* out = F + base + (size_t)(r == 0 ? 0 : r - 1) * stride;
   for (int i = tid; i < 2 * HP * K4; i += NT) {
     const int j = i % K4, a = (i / K4) % HP, pi = i / (K4 * HP), n = 2 * j + pi;
     sQ[i] = (a < H && n < P) ? Qr[a * PP + n] : 0.0;
@@ -355,7 +363,7 @@ __global__ void __launch_bounds__(256) k_prox2pw(DevTree t, const int32_t* __res
         __syncthreads();
         for (int pi1 = 0; pi1 < 2; ++pi1) {
           const double* q1 = sQ + pi1 * HP * K4;
-          double* o = out + (size_t)(4 * pi1 + 2 * pi2 + pi3) * HSQ + c0;
+          TF* o = out + (size_t)(4 * pi1 + 2 * pi2 + pi3) * HSQ + c0;
           // S3: M = H rows a, N = (b, c) = H CH (c >= nc skipped), K = j
           mma_tiles<KS>(
               HP / 8, (H * CH + 7) / 8, [&](int m, int k) { return q1[m * K4 + k]; },
@@ -366,9 +374,9 @@ __global__ void __launch_bounds__(256) k_prox2pw(DevTree t, const int32_t* __res
               [&](int m, int n, double v0, double v1) {
                 if (m < H) {
                   const int bb = n / CH, c = n - bb * CH;   // n even, CH may be odd
-                  if (bb < H && c < nc) o[(size_t)m * G::SLAB + bb * H + c] = v0;
+                  if (bb < H && c < nc) o[(size_t)m * G::SLAB + bb * H + c] = (TF)v0;
                   const int b1 = (n + 1) / CH, c1 = n + 1 - b1 * CH;
-                  if (b1 < H && c1 < nc) o[(size_t)m * G::SLAB + b1 * H + c1] = v1;
+                  if (b1 < H && c1 < nc) o[(size_t)m * G::SLAB + b1 * H + c1] = (TF)v1;
                 }
               });
         }
@@ -425,10 +433,11 @@ struct PwLocal {
 template <int P, int H, int AC, bool ROOT>
 __global__ void __launch_bounds__(PwLocal<P, H, AC>::NT, PwLocal<P, H, AC>::MINB)
     k_pwlocal(DevTree t, const int32_t* __restrict__ boxes, const double* __restrict__ Gr,
-              const double* __restrict__ W, size_t wstride, const double* __restrict__ F, size_t base,
+              const double* __restrict__ W, size_t wstride, const FStore<P>* __restrict__ F, size_t base,
               size_t stride, double* __restrict__ lam) {
   using G = PwGeom<P, H>;
   using C = PwLocal<P, H, AC>;
+  using TF = FStore<P>;
   constexpr bool VSMEM = C::VSMEM;
   constexpr int NT = C::NT, P2 = G::P2, HH = G::HH, HSQ = G::HSQ, SLAB = G::SLAB, KSA = C::KSA;
   constexpr int NACC = VSMEM ? 1 : P;
@@ -437,7 +446,7 @@ __global__ void __launch_bounds__(PwLocal<P, H, AC>::NT, PwLocal<P, H, AC>::MINB
   double* T = sG + P * HH;          // [AC][8][H][H]  translated + weighted slabs
   double* U = T + AC * SLAB;        // [AC][4][H][P]  axis 3 done
   double* V = U + AC * 4 * H * P;   // [a][2][P2]     axes 3, 2 done (VSMEM: all slabs)
-  __shared__ const double* src[27];   // by delta slot (d1+1)*9 + (d2+1)*3 + (d3+1)
+  __shared__ const TF* src[27];   // by delta slot (d1+1)*9 + (d2+1)*3 + (d3+1)
   const int b = boxes[blockIdx.x], tid = threadIdx.x;
   if (!(t.flags[b] & F_IN)) return;   // (never: every local box has F_in, tree.cu)
   const int l = t.level[b];
@@ -446,7 +455,7 @@ __global__ void __launch_bounds__(PwLocal<P, H, AC>::NT, PwLocal<P, H, AC>::MINB
   if (tid < 27) {
     // colleague slot k = (dx+1)*9 + (dy+1)*3 + (dz+1) holds B + (dx,dy,dz); its
     // delta = c_B - c_S = -(dx,dy,dz) has slot 26 - k
-    const double* p = nullptr;
+    const TF* p = nullptr;
     if (ROOT) {
       if (tid == 13) p = F;
     } else {
@@ -468,7 +477,7 @@ __global__ void __launch_bounds__(PwLocal<P, H, AC>::NT, PwLocal<P, H, AC>::MINB
       double o[8];
       if (ROOT) {
 #pragma unroll
-        for (int p = 0; p < 8; ++p) o[p] = __ldg(src[13] + off + p * HSQ);
+        for (int p = 0; p < 8; ++p) o[p] = (double)__ldg(src[13] + off + p * HSQ);
       } else {
         double Ca, Sa, Cb, Sb, Cc, Sc;
         rot_cs(a, Ca, Sa);
@@ -488,11 +497,11 @@ __global__ void __launch_bounds__(PwLocal<P, H, AC>::NT, PwLocal<P, H, AC>::MINB
             for (int p = 0; p < 8; ++p) y[p] = 0.0;
 #pragma unroll
             for (int d3 = 0; d3 < 3; ++d3) {
-              const double* s = src[d1 * 9 + d2 * 3 + d3];
+              const TF* s = src[d1 * 9 + d2 * 3 + d3];
               if (s == nullptr) continue;
               double g[8];
 #pragma unroll
-              for (int p = 0; p < 8; ++p) g[p] = __ldg(s + off + p * HSQ);
+              for (int p = 0; p < 8; ++p) g[p] = (double)__ldg(s + off + p * HSQ);
               if (d3 == 0) rot_acc<1, -1>(y, g, Cc, Sc);
               else if (d3 == 1) rot_acc<1, 0>(y, g, Cc, Sc);
               else rot_acc<1, 1>(y, g, Cc, Sc);
@@ -1111,11 +1120,12 @@ static void run_eval(dmk_plan_s* PL, int phase = PH_UP | PH_DOWN, int top = 0) {
       using K0 = Prox2pw<P, H0, AC0>;
       set_smem(k_prox2pw<P, H0, AC0>, K0::smem);
       set_smem(k_prox2pw<P, H, AC>, K1::smem);
-      k_prox2pw<P, H0, AC0><<<1, K0::NT, K0::smem, s>>>(dt, PL->fout_list.p, T.dQr0, PL->mom.p, PL->phi.p, 0, 0);
+      FStore<P>* Fp = reinterpret_cast<FStore<P>*>(PL->phi.p);
+      k_prox2pw<P, H0, AC0><<<1, K0::NT, K0::smem, s>>>(dt, PL->fout_list.p, T.dQr0, PL->mom.p, Fp, 0, 0);
       DMK_LAUNCH_CHECK();
       if (PL->nfout > 1) {
         k_prox2pw<P, H, AC><<<(int)(PL->nfout - 1), K1::NT, K1::smem, s>>>(dt, PL->fout_list.p + 1, T.dQr1, PL->mom.p,
-                                                                           PL->phi.p, PL->phi_size0, PL->phi_size1);
+                                                                           Fp, PL->phi_size0, PL->phi_size1);
         DMK_LAUNCH_CHECK();
       }
     }
@@ -1128,12 +1138,13 @@ static void run_eval(dmk_plan_s* PL, int phase = PH_UP | PH_DOWN, int top = 0) {
       set_smem(k_pwlocal<P, H0, AC0, true>, K0::smem);
       set_smem(k_pwlocal<P, H, AC, false>, K1::smem);
       // root: exp rank 0, F_out rank 0
-      k_pwlocal<P, H0, AC0, true><<<1, K0::NT, K0::smem, s>>>(dt, PL->exp_list.p, T.dGr0, T.dW0, 0, PL->phi.p, 0, 0,
+      const FStore<P>* Fp = reinterpret_cast<const FStore<P>*>(PL->phi.p);
+      k_pwlocal<P, H0, AC0, true><<<1, K0::NT, K0::smem, s>>>(dt, PL->exp_list.p, T.dGr0, T.dW0, 0, Fp, 0, 0,
                                                               PL->lam.p);
       DMK_LAUNCH_CHECK();
       if (PL->nexp > 1) {
         k_pwlocal<P, H, AC, false><<<(int)(PL->nexp - 1), K1::NT, K1::smem, s>>>(
-            dt, PL->exp_list.p + 1, T.dGr1, T.dW, T.wstride, PL->phi.p, PL->phi_size0, PL->phi_size1, PL->lam.p);
+            dt, PL->exp_list.p + 1, T.dGr1, T.dW, T.wstride, Fp, PL->phi_size0, PL->phi_size1, PL->lam.p);
         DMK_LAUNCH_CHECK();
       }
     }

@@ -18,6 +18,13 @@ torch = pytest.importorskip("torch")
 dmk = pytest.importorskip("paper_2308_00292_b200")
 
 
+def fp_tol(p):
+    """Stage tolerance: fp64 everywhere for p = 28 (eps 1e-9); for p <= 18 the outgoing
+    plane waves are stored in fp32 (reading R16), which bounds every stage
+    downstream of them at ~1e-7 relative."""
+    return 1e-11 if p >= 28 else 1e-6
+
+
 def cuda(a):
     return torch.as_tensor(np.ascontiguousarray(a), dtype=torch.float64, device="cuda")
 
@@ -111,7 +118,7 @@ def test_outgoing_matches_oracle(case):
         else:
             got = phi_from_parity_split(phi[s0 + (r - 1) * s1: s0 + r * s1], nf)
         ref = st["Phi"][i]
-        assert np.max(np.abs(got - ref)) <= 1e-11 * np.max(np.abs(ref))
+        assert np.max(np.abs(got - ref)) <= (1e-11 if inf.p >= 28 else 2e-7) * np.max(np.abs(ref))
 
 
 def test_local_expansions_match_oracle(case):
@@ -121,13 +128,14 @@ def test_local_expansions_match_oracle(case):
     exp = plan.tree("exp")
     scale = max(np.max(np.abs(st["local"][i])) for i in st["local"])
     for i in np.nonzero(exp >= 0)[0]:
-        assert np.max(np.abs(lam[exp[i]] - st["local"][i])) <= 1e-11 * scale
+        assert np.max(np.abs(lam[exp[i]] - st["local"][i])) <= fp_tol(p) * scale
 
 
 def test_far_and_near_fields_match_oracle(case):
     st, plan = case["st"], case["plan"]
     ufar, unear = plan.stage("ufar"), plan.stage("unear")
-    assert np.max(np.abs(ufar - st["u_far"])) <= 1e-11 * np.max(np.abs(st["u_far"]))
+    tol = fp_tol(plan.info().p)
+    assert np.max(np.abs(ufar - st["u_far"])) <= tol * np.max(np.abs(st["u_far"]))
     # the device evaluates r_L M_L(r) through a polynomial fitted to 1e-2 eps m0
     # (tables.cu); the oracle uses the exact Legendre series
     ref_near = st["u_near"] + st["u_self"]
@@ -136,7 +144,7 @@ def test_far_and_near_fields_match_oracle(case):
 
 def test_potential_matches_oracle_dmk_and_direct(case):
     u, ref_u = case["u"], case["ref_u"]
-    assert np.max(np.abs(u - ref_u)) <= 1e-8 * np.max(np.abs(ref_u))
+    assert np.max(np.abs(u - ref_u)) <= max(1e-8, fp_tol(case["plan"].info().p)) * np.max(np.abs(ref_u))
     ref = direct.laplace3d(case["x"], case["q"])
     assert direct.rel_l2(u, ref) <= 2e-6
 
@@ -229,4 +237,5 @@ def test_linearity():
     plan = dmk.dmk_plan(cuda(x), eps=1e-6, leaf_capacity=100)
     a, b, c = (plan.eval(cuda(v)).cpu().numpy() for v in (q1, q2, q1 + q2))
     plan.close()
-    assert np.max(np.abs(a + b - c)) <= 1e-12 * np.max(np.abs(c))
+    # linear up to the rounding of the fp32-stored plane waves (reading R16, p = 18)
+    assert np.max(np.abs(a + b - c)) <= 1e-7 * np.max(np.abs(c))

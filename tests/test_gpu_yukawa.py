@@ -47,10 +47,11 @@ def test_yukawa_local_expansions_and_fields(staged):
     lam = plan.stage("local").reshape(-1, p, p, p)
     exp = plan.tree("exp")
     scale = max(np.max(np.abs(st["local"][i])) for i in st["local"])
+    # p = 18: plane waves stored in fp32 (reading R16)
     for i in np.nonzero(exp >= 0)[0]:
-        assert np.max(np.abs(lam[exp[i]] - st["local"][i])) <= 1e-11 * scale
+        assert np.max(np.abs(lam[exp[i]] - st["local"][i])) <= 1e-6 * scale
     ufar, unear = plan.stage("ufar"), plan.stage("unear")
-    assert np.max(np.abs(ufar - st["u_far"])) <= 1e-11 * np.max(np.abs(st["u_far"]))
+    assert np.max(np.abs(ufar - st["u_far"])) <= 1e-6 * np.max(np.abs(st["u_far"]))
     ref_near = st["u_near"] + st["u_self"]
     # The device culls list pairs with r >= r_L, where R_L = K - M_L is below eps M_L(0)
     # but (unlike 1/r) not exactly 0 (reading R13); the
