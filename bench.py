@@ -392,8 +392,6 @@ def main():
         barrier()
         times.append(e0.elapsed_time(e1))
         plan_ms.append(e0.elapsed_time(em))
-        for name, ms in plan.timings().items():
-            stage_ms[name] = stage_ms.get(name, 0.0) + ms / a.steps
         if k == a.steps - 1:
             info = plan.info()
             pairs = list_pairs(plan)
@@ -403,6 +401,20 @@ def main():
     launches = (L.dmk_kernel_launches(None) - launches0) // a.steps
     clocks = clk.stop()
     t_step = float(np.mean(times))
+    # per-stage kernel times for the roofline, measured in isolation: the timed steps run
+    # the near field concurrently with the far field, which makes stage times overlap;
+    # DMK_SERIAL=1 plans run the stages back to back (same kernels, same launches)
+    os.environ["DMK_SERIAL"] = "1"
+    stage_ms = {}
+    for k in range(3):
+        flush.zero_()
+        torch.cuda.synchronize(dev)
+        plan, _ = step()
+        torch.cuda.synchronize(dev)
+        for name, ms in plan.timings().items():
+            stage_ms[name] = stage_ms.get(name, 0.0) + ms / 3
+        plan.close()
+    os.environ.pop("DMK_SERIAL")
     if dist is not None:
         t = torch.tensor([t_step], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -480,7 +492,8 @@ def main():
         "gpu_launches": int(launches),
         "roofline": roof,
         "stages_ms": {**{k: round(v, 4) for k, v in stage_ms.items()}, "tree_and_lists": round(tree_ms, 4),
-                      "note": "p2p runs on a side stream concurrently with anterp..eval; stages overlap"},
+                      "note": "stage kernels timed back to back (DMK_SERIAL=1); the timed steps overlap "
+                              "p2p (low-priority stream) with c2p..eval (high-priority stream)"},
         "stages": stages,
         "tree": {"nbox": info.nbox, "nlevels": info.nlevels, "nfout": info.nfout, "nexp": info.nexp,
                  "p2p_pairs": pairs, "p2p_pairs_in_ball": inball},
