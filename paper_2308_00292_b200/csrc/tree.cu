@@ -378,49 +378,56 @@ __global__ void k_rank(const int32_t* scan, const uint8_t* sel, int64_t nbox, in
   rank[i] = sel[i] ? scan[i] : -1;
 }
 
-// direct lists: pass 0 counts, pass 1 fills
+// direct lists: pass 0 counts, pass 1 fills; one warp per box, lanes over the colleague
+// slots (and over the 3^D x 2^D fine-neighbour candidates), ballots for the positions
 template <int D, bool FILL>
 __global__ void k_dlist(const int32_t* start, const int32_t* end, const int32_t* parent, const int32_t* child,
                         const int32_t* coll, const uint8_t* flags, const uint64_t* code, const int32_t* level,
                         int64_t nbox, int32_t* cnt, const int32_t* off, int32_t* items) {
   constexpr int NCH = Dim<D>::NCH, NCOL = Dim<D>::NCOL;
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
   if (i >= nbox) return;
-  int n_ = 0;
-  int64_t base = FILL ? off[i] : 0;
-  bool is_target = (flags[i] & 1) && end[i] > start[i];
-  if (is_target) {
-    int64_t a = i;
-    while (a >= 0) {   // B and its ancestors: leaf colleagues at that level
-      for (int k = 0; k < NCOL; ++k) {
-        int32_t s = coll[NCOL * a + k];
-        if (s >= 0 && (flags[s] & 1) && end[s] > start[s]) {
-          if (FILL) items[base + n_] = s;
-          ++n_;
-        }
-      }
-      a = parent[a];
-    }
-    int bc[3];
-    decode<D>(code[i], bc);
-    for (int k = 0; k < NCOL; ++k) {   // fine neighbours: leaves one level down touching B
-      int32_t s = coll[NCOL * i + k];
-      if (s < 0 || (flags[s] & 1)) continue;
-      for (int o = 0; o < NCH; ++o) {
-        int32_t ch = child[NCH * (int64_t)s + o];
-        if (ch < 0 || !(flags[ch] & 1) || end[ch] <= start[ch]) continue;
-        int cc[3];
-        decode<D>(code[ch], cc);
-        bool touch = true;
-        for (int d = 0; d < D; ++d) touch = touch && cc[d] >= 2 * bc[d] - 1 && cc[d] <= 2 * bc[d] + 2;
-        if (touch) {
-          if (FILL) items[base + n_] = ch;
-          ++n_;
-        }
-      }
-    }
+  const bool is_target = (flags[i] & 1) && end[i] > start[i];
+  if (!is_target) {
+    if (!FILL && lane == 0) cnt[i] = 0;
+    return;
   }
-  if (!FILL) cnt[i] = n_;
+  const unsigned below = (1u << lane) - 1;
+  int n_ = 0;
+  const int64_t base = FILL ? off[i] : 0;
+  int64_t a = i;
+  while (a >= 0) {   // B and its ancestors: leaf colleagues at that level
+    int32_t s = lane < NCOL ? coll[NCOL * a + lane] : -1;
+    const bool ok = s >= 0 && (flags[s] & 1) && end[s] > start[s];
+    const unsigned m = __ballot_sync(0xffffffffu, ok);
+    if (FILL && ok) items[base + n_ + __popc(m & below)] = s;
+    n_ += __popc(m);
+    a = parent[a];
+  }
+  int bc[3];
+  decode<D>(code[i], bc);
+  for (int c0 = 0; c0 < NCOL * NCH; c0 += 32) {   // fine neighbours: leaves one level down touching B
+    const int c = c0 + lane;
+    bool ok = false;
+    int32_t ch = -1;
+    if (c < NCOL * NCH) {
+      const int32_t s = coll[NCOL * i + c / NCH];
+      if (s >= 0 && !(flags[s] & 1)) {
+        ch = child[NCH * (int64_t)s + c % NCH];
+        if (ch >= 0 && (flags[ch] & 1) && end[ch] > start[ch]) {
+          int cc[3];
+          decode<D>(code[ch], cc);
+          ok = true;
+          for (int d = 0; d < D; ++d) ok = ok && cc[d] >= 2 * bc[d] - 1 && cc[d] <= 2 * bc[d] + 2;
+        }
+      }
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, ok);
+    if (FILL && ok) items[base + n_ + __popc(m & below)] = ch;
+    n_ += __popc(m);
+  }
+  if (!FILL && lane == 0) cnt[i] = n_;
 }
 
 // P2P work items: (leaf, first target) for every chunk of 32 targets
@@ -801,7 +808,7 @@ static void build_tree_d(dmk_plan_s* P, const double* dpts) {
     poff.alloc(nbox + 1, s);
     DMK_CUDA(cudaMemsetAsync(cnt.p, 0, (nbox + 1) * sizeof(int32_t), s));
     DMK_CUDA(cudaMemsetAsync(pcnt.p, 0, (nbox + 1) * sizeof(int32_t), s));
-    k_dlist<D, false><<<nblk(nbox), TPB, 0, s>>>(P->box_start.p, P->box_end.p, P->box_parent.p, P->box_child.p,
+    k_dlist<D, false><<<nblk(32 * nbox), TPB, 0, s>>>(P->box_start.p, P->box_end.p, P->box_parent.p, P->box_child.p,
                                               P->box_coll.p, P->box_flags.p, P->box_code.p, P->box_level.p, nbox,
                                               cnt.p, nullptr, nullptr);
     DMK_LAUNCH_CHECK();
@@ -823,7 +830,7 @@ static void build_tree_d(dmk_plan_s* P, const double* dpts) {
     P->ndlist = h[0];
     P->np2p = h[1];
     P->dlist.alloc(P->ndlist ? P->ndlist : 1, s);
-    k_dlist<D, true><<<nblk(nbox), TPB, 0, s>>>(P->box_start.p, P->box_end.p, P->box_parent.p, P->box_child.p,
+    k_dlist<D, true><<<nblk(32 * nbox), TPB, 0, s>>>(P->box_start.p, P->box_end.p, P->box_parent.p, P->box_child.p,
                                              P->box_coll.p, P->box_flags.p, P->box_code.p, P->box_level.p, nbox,
                                              nullptr, P->dlist_off.p, P->dlist.p);
     DMK_LAUNCH_CHECK();
