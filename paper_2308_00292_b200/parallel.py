@@ -8,8 +8,9 @@ through a Comm -- NCCL/gloo via torch.distributed, or in-process threads):
                 cube of reading R5 (lo = min, side = max extent), shared by all ranks.
   2. partition  every point's box at level Lc (its Morton code, computed exactly as the
                 library does: q = floor((x - lo) * 2^21/side)); all-reduce SUM of the
-                level-Lc histogram; contiguous Morton ranges of Lc-boxes with balanced
-                point counts -> owner(box).
+                level-Lc histogram; contiguous Morton ranges of level-(Lc-1) boxes with
+                balanced point counts -> owner(box) (an Lc-box belongs to its parent's
+                owner, so every level-(Lc-1) box lies on one rank).
   3. exchange   all-to-all: each point goes to the owner of its Lc-box.
   4. halo       all-to-all: each owned point also goes to every rank owning a colleague
                 of its Lc-box (the neighbour-halo particles).  Every colleague, at any
@@ -18,12 +19,13 @@ through a Comm -- NCCL/gloo via torch.distributed, or in-process threads):
                 < Lc (the difference kernels D_l, l >= Lc, vanish beyond r_l).
   5. local plan dmk_plan over own + halo points with the shared root and min_level = Lc
                 (levels < Lc forced dense, so every rank has the same coarse boxes).
-  6. coarse     dmk_upward with the halo charges zeroed -> moments of level Lc-1 from the
-                rank's OWN charges (dmk_level_moments get); all-reduce SUM -> the global
-                coarse moments (the replicated coarse levels of the north star).
-  7. local      dmk_upward with all local charges, dmk_level_moments set (level Lc-1 and
-                the c2p rebuild of the levels above), dmk_downward -> potentials of own
-                + halo points; the own ones are kept.
+  6. coarse     dmk_upward with all local charges; the moments of the OWNED level-(Lc-1)
+                boxes are exact (all their points are own points), the others are zeroed
+                (dmk_level_moments get); all-reduce SUM -> the global coarse moments (the
+                replicated coarse levels of the north star).
+  7. local      dmk_level_moments set (level Lc-1 and the c2p rebuild of the levels
+                above), dmk_downward -> potentials of own + halo points; the own ones are
+                kept.
   8. return     all-to-all of the potentials back to the ranks/indices the points came from.
 
 The halo is one Lc-box thick; the ghost work it costs is the price of this first
@@ -35,6 +37,7 @@ tests plug an oracle-backed backend in through the same four calls.
 """
 from __future__ import annotations
 
+import functools
 import math
 import threading
 from typing import List, Sequence
@@ -193,6 +196,7 @@ def level_codes(x: torch.Tensor, lo: Sequence[float], side: float, level: int) -
     return code
 
 
+@functools.lru_cache(maxsize=8)
 def colleague_table(level: int) -> np.ndarray:
     """[8^level, 27] Morton codes of the colleagues of every box at `level` (-1 outside)."""
     n1 = 2 ** level
@@ -254,11 +258,20 @@ def dmk_eval_distributed(points: torch.Tensor, charges: torch.Tensor, comm: Comm
     side = ext if ext > 0 else 1.0
     n_total = int(comm.allreduce(torch.tensor([float(n_local)], dtype=torch.float64, device=dev), "sum").item())
     Lc = level if level is not None else choose_level(n_total, ns, R)
-    # 2. partition
+    if R == 1:   # one rank: the plain single-device evaluation
+        plan = backend.plan(x.contiguous(), eps, ns, kernel, lam, None, 0)
+        backend.upward(plan, q.contiguous())
+        u = torch.as_tensor(backend.downward(plan), device=dev)
+        backend.close(plan)
+        if stats is not None:
+            stats.update(level=0, n_own=n_local, n_halo=0, n_total=n_total)
+        return u
+    # 2. partition: owners of level-(Lc-1) boxes, inherited by their Lc-children
     code = level_codes(x, lo, side, Lc)
     hist = torch.bincount(code, minlength=8 ** Lc).to(torch.float64)
     hist = comm.allreduce(hist, "sum").cpu().numpy()
-    owner = owners_from_histogram(hist, R)
+    owner_c = owners_from_histogram(hist.reshape(-1, 8).sum(1), R)
+    owner = np.repeat(owner_c, 8)
     owner_t = torch.as_tensor(owner, device=dev)
     # 3. exchange to owners: rows [x, y, z, q, src_rank, src_index]
     rows = torch.cat([x, q[:, None], torch.full((n_local, 1), float(me), dtype=torch.float64, device=dev),
@@ -286,10 +299,11 @@ def dmk_eval_distributed(points: torch.Tensor, charges: torch.Tensor, comm: Comm
     if n_own:
         X = torch.cat([own[:, :3], halo[:, :3]], 0).contiguous()
         Q = torch.cat([own[:, 3], halo[:, 3]], 0).contiguous()
-        Qown = torch.cat([own[:, 3], torch.zeros(n_halo, dtype=torch.float64, device=dev)], 0)
         plan = backend.plan(X, eps, ns, kernel, lam, lo + [side], Lc)
-        backend.upward(plan, Qown)
-        p_dense = backend.get_level(plan, C)
+        backend.upward(plan, Q)
+        p_dense = torch.as_tensor(backend.get_level(plan, C), device=dev)
+        mine = torch.as_tensor(owner_c == me, device=dev)
+        p_dense = p_dense * mine.reshape((-1,) + (1,) * (p_dense.dim() - 1)).to(p_dense.dtype)
     # ranks without points still take part in the reduction (zeros of the agreed shape)
     shape = torch.tensor(list(p_dense.shape) if p_dense is not None else [0, 0, 0, 0], dtype=torch.float64,
                          device=dev)
@@ -299,7 +313,6 @@ def dmk_eval_distributed(points: torch.Tensor, charges: torch.Tensor, comm: Comm
     g_dense = comm.allreduce(torch.as_tensor(p_dense, device=dev), "sum")
     u_own = torch.zeros(0, dtype=torch.float64, device=dev)
     if n_own:
-        backend.upward(plan, Q)
         backend.set_level(plan, C, g_dense)
         u = torch.as_tensor(backend.downward(plan), device=dev)
         u_own = u[:n_own]

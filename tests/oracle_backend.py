@@ -11,7 +11,7 @@ from oracle.dmk import dmk
 
 class OracleBackend:
     def plan(self, points, eps, ns, kernel, lam, root, min_level):
-        return {"x": points.cpu().numpy(), "eps": eps, "ns": ns, "kernel": kernel, "lam": lam, "root": list(root),
+        return {"x": points.cpu().numpy(), "eps": eps, "ns": ns, "kernel": kernel, "lam": lam, "root": list(root) if root is not None else None,
                 "min_level": min_level}
 
     def upward(self, plan, charges):
