@@ -859,7 +859,7 @@ __global__ void __launch_bounds__(256) k_eval_pad(DevTree t, const int32_t* __re
 template <int P>
 struct AntMma {
   static constexpr int P2 = P * P, MT = (P2 + 7) / 8, NTB = (P + 7) / 8, NW = (P >= 18) ? 16 : 8;
-  static constexpr int MPW = (MT + NW - 1) / NW, CH = 64;
+  static constexpr int MPW = (MT + NW - 1) / NW, CH = 128;
   static constexpr size_t smem = sizeof(double) * 3 * CH * P;
 };
 template <int P>
