@@ -473,7 +473,12 @@ def main():
     dom = max(stages, key=lambda s: stages[s]["ms"])
     roof = dict(stages[dom])
     roof.pop("ms")
-    roof.update({"kernel": dom, "traffic": None,
+    try:
+        traffic = json.load(open(os.path.join(ROOT, "profiles", "r01_traffic.json")))["bytes"].get(dom)
+    except Exception:
+        traffic = None
+    roof.update({"kernel": dom, "traffic": traffic,
+                 "traffic_source": "profiles/r01_traffic.json (ncu --set full, dram bytes per launch)",
                  "peak_source": ("MEASURED_PEAKS.json hbm_gbs" if roof["bound"] == "hbm" else
                                  "derived: 148 SM x 64 fp64 FMA/clk x 2 x sm_max_mhz (DESIGN.md §6)")})
     line = {
