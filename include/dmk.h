@@ -67,6 +67,10 @@ typedef struct dmk_options {
   const double* root;      /* NULL (default: root box from the points, reading R5), or a
                               HOST array {lo_0, .., lo_{dim-1}, side}: the root box
                               [lo, lo + side]^dim to use (all points must lie inside) */
+  int64_t n_targets;       /* 0 (default: every point is a target), or t in [1, n]: only
+                              the first t points (caller order) are targets; the others
+                              are sources only and get no meaningful potential (the halo
+                              of a distributed evaluation) */
 } dmk_options;
 
 /* dmk_plan: build the plan for N points in `dim` dimensions.

@@ -39,7 +39,7 @@ class DmkError(RuntimeError):
 class _Options(ctypes.Structure):
     _fields_ = [("leaf_capacity", ctypes.c_int32), ("min_level", ctypes.c_int32),
                 ("lam", ctypes.c_double), ("stream", ctypes.c_void_p),
-                ("root", ctypes.POINTER(ctypes.c_double))]
+                ("root", ctypes.POINTER(ctypes.c_double)), ("n_targets", ctypes.c_int64)]
 
 
 class PlanInfo(ctypes.Structure):
@@ -108,7 +108,7 @@ class Plan:
     """A dmk_plan_t: tree, lists and tables for one point set (sources = targets)."""
 
     def __init__(self, points, eps: float = 1e-6, leaf_capacity: int = 200, kernel: str = "laplace",
-                 lam: float = 0.0, stream=None, root=None, min_level: int = 0):
+                 lam: float = 0.0, stream=None, root=None, min_level: int = 0, n_targets: int = 0):
         ptr, mem, keep = _placement(points)
         n = keep.shape[0]
         if keep.ndim != 2 or keep.shape[1] not in (2, 3):
@@ -119,7 +119,7 @@ class Plan:
         if root is not None:
             self._root = (ctypes.c_double * (dim + 1))(*[float(v) for v in root])
             rootp = ctypes.cast(self._root, ctypes.POINTER(ctypes.c_double))
-        opt = _Options(int(leaf_capacity), int(min_level), float(lam), stream, rootp)
+        opt = _Options(int(leaf_capacity), int(min_level), float(lam), stream, rootp, int(n_targets))
         h = ctypes.c_void_p()
         _check(lib().dmk_plan(dim, KERNELS[kernel], float(eps), int(n), ptr, mem, ctypes.byref(opt),
                               ctypes.byref(h)), "dmk_plan")
@@ -219,9 +219,9 @@ class Plan:
 
 
 def dmk_plan(points, eps: float = 1e-6, leaf_capacity: int = 200, kernel: str = "laplace", lam: float = 0.0,
-             stream=None, root=None, min_level: int = 0) -> Plan:
+             stream=None, root=None, min_level: int = 0, n_targets: int = 0) -> Plan:
     return Plan(points, eps=eps, leaf_capacity=leaf_capacity, kernel=kernel, lam=lam, stream=stream, root=root,
-                min_level=min_level)
+                min_level=min_level, n_targets=n_targets)
 
 
 def dmk_eval(plan: Plan, charges, out=None):

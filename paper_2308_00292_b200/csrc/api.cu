@@ -97,6 +97,7 @@ int dmk_plan(int dim, int kernel, double eps, int64_t n, const double* points, i
     try {
       P->dim = dim;
       P->kernel = kernel;
+      P->n_targets = n;
       P->eps = eps;
       P->n = n;
       if (opt) {
@@ -106,6 +107,8 @@ int dmk_plan(int dim, int kernel, double eps, int64_t n, const double* points, i
         P->lambda = opt->lambda;
         if (opt->min_level < 0 || opt->min_level > 6) fail(DMK_ERR_ARG, "min_level must be in [0, 6]");
         P->min_level = opt->min_level;
+        if (opt->n_targets < 0 || opt->n_targets > n) fail(DMK_ERR_ARG, "n_targets must be in [0, n]");
+        if (opt->n_targets > 0) P->n_targets = opt->n_targets;
         if (opt->root) {
           P->root_fixed = true;
           for (int d = 0; d < dim; ++d) P->lo[d] = opt->root[d];

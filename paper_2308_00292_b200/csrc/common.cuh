@@ -115,6 +115,7 @@ struct dmk_plan_s {
   double side = 1;
   bool root_fixed = false;   // lo/side given by the caller (dmk_options.root)
   int min_level = 0;         // levels < min_level fully refined (dmk_options.min_level)
+  int64_t n_targets = 0;     // the first n_targets caller points are targets (= n by default)
 
   // sorted points (normalised coordinates in [0,1]^3) and permutation
   dmk::DevBuf<uint64_t> keys;

@@ -23,7 +23,7 @@ struct DevTree {
   const double* ys;
   const double* zs;
 };
-constexpr uint8_t F_LEAF = 1, F_OUT = 2, F_IN = 4, F_EXP = 8;
+constexpr uint8_t F_LEAF = 1, F_OUT = 2, F_IN = 4, F_EXP = 8, F_TGT = 16;
 
 __device__ __forceinline__ uint32_t compact3d(uint64_t x) {
   x &= 0x1249249249249249ULL;
@@ -99,7 +99,7 @@ __device__ int box_ranges(const DevTree& t, int b, int2* rg) {
     if (ch < 0) continue;
     uint8_t fc = t.flags[ch];
     if (!(fc & F_LEAF) || t.end[ch] <= t.start[ch]) continue;
-    if (EVAL && (fc & F_IN)) continue;
+    if (EVAL && ((fc & F_IN) || !(fc & F_TGT))) continue;
     rg[nr++] = make_int2(t.start[ch], t.end[ch]);
   }
   return nr;

@@ -366,10 +366,25 @@ __global__ void k_flags_in(const int32_t* start, const int32_t* end, const int32
       int32_t s = coll[NCOL * i + k];
       if (s >= 0 && (flags[s] & 2)) fin = true;
     }
-  bool e = nonempty && (!(f & 1) || fin);
+  // a local expansion only where there are targets (bit 4, k_flag_targets)
+  bool e = nonempty && (f & 16) && (!(f & 1) || fin);
   // other threads only read bit 1 (F_out), which this write leaves unchanged
   flags[i] = (uint8_t)(f | (fin ? 4 : 0) | (e ? 8 : 0));
   exp[i] = e ? 1 : 0;
+}
+
+// bit 4 (F_TGT): the box holds at least one target point (all points, unless the plan
+// was given n_targets < n: then the first n_targets caller points)
+__global__ void k_target_flag_pts(const int32_t* __restrict__ perm, int64_t n, int64_t n_targets, int32_t* tf) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) tf[i] = perm[i] < n_targets ? 1 : 0;
+}
+__global__ void k_flag_targets(const int32_t* start, const int32_t* end, const int32_t* tscan, int64_t nbox,
+                               uint8_t* flags) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= nbox) return;
+  const bool tgt = tscan ? tscan[end[i]] > tscan[start[i]] : end[i] > start[i];
+  if (tgt) flags[i] |= 16;
 }
 
 __global__ void k_rank(const int32_t* scan, const uint8_t* sel, int64_t nbox, int32_t* rank) {
@@ -436,7 +451,7 @@ __global__ void k_p2p_count(const int32_t* start, const int32_t* end, const uint
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= nbox) return;
   int n_ = end[i] - start[i];
-  cnt[i] = ((flags[i] & 1) && n_ > 0) ? (n_ + 31) / 32 : 0;
+  cnt[i] = ((flags[i] & 1) && (flags[i] & 16) && n_ > 0) ? (n_ + 31) / 32 : 0;
 }
 __global__ void k_p2p_fill(const int32_t* start, const int32_t* cnt, const int32_t* off, int64_t nbox,
                            int32_t* items) {
@@ -747,6 +762,20 @@ static void build_tree_d(dmk_plan_s* P, const double* dpts) {
   k_flags_out<<<nblk(nbox), TPB, 0, s>>>(P->box_start.p, P->box_end.p, P->box_level.p, P->min_level, nbox,
                                          P->box_flags.p, fsel.p);
   DMK_LAUNCH_CHECK();
+  {
+    DevBuf<int32_t> tf, tscan;
+    if (P->n_targets < n) {
+      tf.alloc(n + 1, s);
+      tscan.alloc(n + 1, s);
+      DMK_CUDA(cudaMemsetAsync(tf.p + n, 0, sizeof(int32_t), s));
+      k_target_flag_pts<<<nblk(n), TPB, 0, s>>>(P->perm.p, n, P->n_targets, tf.p);
+      DMK_LAUNCH_CHECK();
+      exclusive_scan(s, tf.p, tscan.p, n + 1);
+    }
+    k_flag_targets<<<nblk(nbox), TPB, 0, s>>>(P->box_start.p, P->box_end.p, P->n_targets < n ? tscan.p : nullptr,
+                                              nbox, P->box_flags.p);
+    DMK_LAUNCH_CHECK();
+  }
   k_flags_in<D><<<nblk(nbox), TPB, 0, s>>>(P->box_start.p, P->box_end.p, P->box_coll.p, nbox, P->box_flags.p,
                                         esel.p);
   DMK_LAUNCH_CHECK();

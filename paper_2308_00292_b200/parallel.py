@@ -159,10 +159,10 @@ class GpuBackend:
     def __init__(self, device):
         self.device = torch.device(device)
 
-    def plan(self, points, eps, ns, kernel, lam, root, min_level):
+    def plan(self, points, eps, ns, kernel, lam, root, min_level, n_targets=0):
         import paper_2308_00292_b200 as dmk
         return dmk.dmk_plan(points.to(self.device), eps=eps, leaf_capacity=ns, kernel=kernel, lam=lam, root=root,
-                            min_level=min_level)
+                            min_level=min_level, n_targets=n_targets)
 
     def upward(self, plan, charges):
         plan.upward(charges.to(self.device))
@@ -299,7 +299,8 @@ def dmk_eval_distributed(points: torch.Tensor, charges: torch.Tensor, comm: Comm
     if n_own:
         X = torch.cat([own[:, :3], halo[:, :3]], 0).contiguous()
         Q = torch.cat([own[:, 3], halo[:, 3]], 0).contiguous()
-        plan = backend.plan(X, eps, ns, kernel, lam, lo + [side], Lc)
+        # the halo points are sources only: no local expansions / P2P for their boxes
+        plan = backend.plan(X, eps, ns, kernel, lam, lo + [side], Lc, n_own)
         backend.upward(plan, Q)
         p_dense = torch.as_tensor(backend.get_level(plan, C), device=dev)
         mine = torch.as_tensor(owner_c == me, device=dev)

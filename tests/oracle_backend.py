@@ -10,7 +10,7 @@ from oracle.dmk import dmk
 
 
 class OracleBackend:
-    def plan(self, points, eps, ns, kernel, lam, root, min_level):
+    def plan(self, points, eps, ns, kernel, lam, root, min_level, n_targets=0):
         return {"x": points.cpu().numpy(), "eps": eps, "ns": ns, "kernel": kernel, "lam": lam, "root": list(root) if root is not None else None,
                 "min_level": min_level}
 

@@ -54,3 +54,23 @@ def test_thread_ranks_on_one_gpu(world, kernel):
     assert sum(r[1]["n_own"] for r in res) == len(x)
     ref = direct.laplace3d(x, q) if kernel == "laplace" else direct.yukawa3d(x, q, lam)
     assert direct.rel_l2(u, ref) <= 2e-6
+
+
+def test_n_targets_restricts_work_not_results():
+    """dmk_options.n_targets: only the first t caller points are targets (a distributed
+    rank's own points ahead of its halo).  Their potentials are bit-identical to those of
+    a plan in which every point is a target; fewer local expansions and P2P items run."""
+    x, q = dmk_inputs.uniform(60000, seed=12)
+    order = np.argsort(x[:, 0], kind="stable")     # targets: the half with x < median, first
+    x, q = x[order], q[order]
+    t = 30000
+    full = dmk.dmk_plan(cuda(x), eps=1e-6, leaf_capacity=80)
+    a = full.eval(cuda(q)).cpu().numpy()
+    nexp_full = full.info().nexp
+    full.close()
+    part = dmk.dmk_plan(cuda(x), eps=1e-6, leaf_capacity=80, n_targets=t)
+    b = part.eval(cuda(q)).cpu().numpy()
+    nexp_part = part.info().nexp
+    part.close()
+    assert np.array_equal(a[:t], b[:t])
+    assert nexp_part < nexp_full
