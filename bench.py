@@ -33,6 +33,7 @@ METRIC = "points/sec, 3D Laplace DMK, eps=1e-6, 1/2/4/8 B200; rel ℓ2 err vs di
 WORKLOAD = ("config1: 3D Laplace K=1/r, N=1e6 uniform iid in [0,1]^3, charges U[-1,1], "
             "eps=1e-6, leaf capacity 200, single B200 per rank")
 FP64_FMA_PER_CLK_SM = 64
+FP32_FMA_PER_CLK_SM = 128
 N_SM = 148
 
 
@@ -208,7 +209,7 @@ def run_reference(a):
         cores = os.cpu_count()
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "points/s", "n_gpus": a.gpus,
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64+f32" if info.p <= 18 else "f64", "data": "synthetic",
             "config": {"workload": WORKLOAD, "sample_points": n_s, "eps": a.eps, "leaf_capacity": a.ns},
             "cpu_baseline": {"value": value, "unit": "points/s", "cores": cores, "kind": "oracle",
                              "sample": f"each step: oracle DMK on {n_s} points of the config-1 distribution"},
@@ -304,7 +305,7 @@ def run_distributed(a):
         line = {
             "metric": METRIC, "value": a.n * world / (t_step * 1e-3), "unit": "points/s", "n_gpus": world,
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": t_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64+f32" if info.p <= 18 else "f64", "data": "synthetic",
             "config": {"workload": f"uniform iid in [0,1]^3, {a.n} points per GPU, one global problem of "
                                    f"{a.n * world} points, 3D Laplace, eps={a.eps}, leaf capacity {a.ns}",
                        "N_per_gpu": a.n, "eps": a.eps, "leaf_capacity": a.ns,
@@ -457,6 +458,9 @@ def main():
 
     pk = peaks()
     fp64_peak = N_SM * FP64_FMA_PER_CLK_SM * 2 * pk.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+    # fp32 tier (reading R16, p <= 18): the P2P pairs run in single precision
+    fp32_peak = N_SM * FP32_FMA_PER_CLK_SM * 2 * pk.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+    p2p32 = info.p <= 18
     models = stage_models(info, a.n, pairs, info.respoly_degree, inball)
     stages = {}
     for name, (bound, amount, unit) in models.items():
@@ -466,7 +470,8 @@ def main():
         if bound == "hbm":
             ach, peak, u_ = amount / (ms * 1e-3) / 1e9, pk["hbm_gbs"], "GB/s"
         else:
-            ach, peak, u_ = amount / (ms * 1e-3) / 1e12, fp64_peak, "TFLOP/s"
+            pk_ = fp32_peak if (name == "p2p" and p2p32) else fp64_peak
+            ach, peak, u_ = amount / (ms * 1e-3) / 1e12, pk_, "TFLOP/s"
         stages[name] = {"ms": round(ms, 4), "bound": bound, "achieved": round(ach, 3), "peak": round(peak, 1),
                         "unit": u_, "frac": round(ach / peak, 4)}
     tree_ms = float(np.mean(plan_ms))          # dmk_plan: tree, lists, tables (cached)
@@ -480,11 +485,13 @@ def main():
     roof.update({"kernel": dom, "traffic": traffic,
                  "traffic_source": "profiles/r01_traffic.json (ncu --set full, dram bytes per launch)",
                  "peak_source": ("MEASURED_PEAKS.json hbm_gbs" if roof["bound"] == "hbm" else
-                                 "derived: 148 SM x 64 fp64 FMA/clk x 2 x sm_max_mhz (DESIGN.md §6)")})
+                                 "derived: 148 SM x 128 fp32 FMA/clk x 2 x sm_max_mhz (DESIGN.md 8(d))"
+                                 if (dom == "p2p" and p2p32) else
+                                 "derived: 148 SM x 64 fp64 FMA/clk x 2 x sm_max_mhz (DESIGN.md 8(d))")})
     line = {
         "metric": METRIC, "value": value, "unit": "points/s", "n_gpus": world, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": t_step, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "vs_baseline": None, "dtype": "f64+f32" if info.p <= 18 else "f64", "data": "synthetic",
         "config": {"workload": WORKLOAD, "N_per_gpu": a.n, "eps": a.eps, "leaf_capacity": a.ns,
                    "step": "dmk_plan (tree+lists) + dmk_eval, device-resident inputs",
                    "l2": "flushed by a 256 MiB write between timed steps",

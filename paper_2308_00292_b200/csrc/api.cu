@@ -63,6 +63,8 @@ static void alloc_eval_buffers(dmk_plan_s* P) {
     P->mom.alloc(P->nfout * pd, s);
     P->phi.alloc(P->phi_size0 + (P->nfout - 1) * P->phi_size1, s);
     P->lam.alloc(P->nexp * pd, s);
+    // fp32 tier (p <= 18, 3D): weighted incoming plane waves of every local box (k_pwshift)
+    if (P->dim == 3 && T.p <= 18) P->pwt.alloc(P->nexp * P->phi_size1, s);
   }
 }
 

@@ -138,6 +138,9 @@ struct dmk_plan_s {
   // work list for the P2P kernel: (leaf box, first target) items of <= 32 targets
   dmk::DevBuf<int32_t> p2p_items;
   int64_t np2p = 0;
+  // fp32 P2P tier (p <= 18): leaf-local double-single source records, Morton order:
+  // (x, y, z, rho) high parts and (x, y, z, 0) low parts
+  dmk::DevBuf<float4> xl4, xl4lo;
   // anterpolation / evaluation work: box ids
   dmk::DevBuf<int32_t> anterp_list, eval_list;
   int64_t nanterp = 0, neval = 0;
@@ -145,6 +148,7 @@ struct dmk_plan_s {
 
   // eval buffers
   dmk::DevBuf<double> q, mom, phi, lam, ufar, unear;
+  dmk::DevBuf<float> pwt;                 // fp32 tier: translated + weighted plane waves per local box
   dmk::DevBuf<double> scalar;             // device scratch scalar (2D: total charge)
   int64_t phi_size0 = 0, phi_size1 = 0;   // doubles per root / per other box
 

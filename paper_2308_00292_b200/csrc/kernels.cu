@@ -45,10 +45,15 @@ struct Cfg<28> {
 };
 
 // ---------------------------------------------------------------- gather
+// q[i] = charges[perm[i]] (Morton order, fp64); with the fp32 P2P tier also the charge
+// slot of the leaf-local source record.
 __global__ void k_gather_q(const double* __restrict__ charges, const int32_t* __restrict__ perm, int64_t n,
-                           double* q) {
+                           double* q, float4* __restrict__ xl4) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i < n) q[i] = charges[perm[i]];
+  if (i >= n) return;
+  const double v = charges[perm[i]];
+  q[i] = v;
+  if (xl4) xl4[i].w = (float)v;
 }
 
 // ---------------------------------------------------------------- anterpolation
@@ -411,6 +416,146 @@ __device__ __forceinline__ void rot_cs(int m, double& C, double& S) {
   S = e == 0 ? 0.0 : (e == 1 ? 0.86602540378443864676 : -0.86602540378443864676);
 }
 
+// ---- fp32 tier (reading R16, p <= 18): translation by parent groups.
+// The 8 children of a parent B have their 27 colleagues inside the 4x4x4 window of
+// level-l boxes around them (the children of B's colleagues), so one pass over the
+// window's 64 outgoing expansions serves all 8 (64 instead of 8 x 27 = 216 reads of F,
+// which is re-read from L2 and bounds the per-box form).  For one mode (a, b, c) a
+// thread keeps the window sums in registers as three separable passes (Eq. 3.39 with
+// e^{i h m . delta r_l} = product of per-axis rotations by 2 pi m_d delta_d / 3 of the
+// parity pairs): Z over w3, Y over w2, X over w1, for child offsets o in {0,1}^3 with
+// delta = o + 1 - w.  Sums in fp32 (the F values are fp32-rounded already); the level's
+// difference-kernel weights are applied and the weighted incoming expansion of each
+// local-expansion child is written to T[exp_rank] for k_pwlocal<..., FROMT>.
+template <int ST, int DELTA>
+__device__ __forceinline__ void rot_accf(float* acc, const float* g, float C, float S) {
+#pragma unroll
+  for (int p = 0; p < 8; ++p) {
+    if (p & ST) continue;
+    const float g0 = g[p], g1 = g[p + ST];
+    if (DELTA == 0) {
+      acc[p] += g0;
+      acc[p + ST] += g1;
+    } else if (DELTA > 0) {
+      acc[p] = fmaf(C, g0, fmaf(-S, g1, acc[p]));
+      acc[p + ST] = fmaf(S, g0, fmaf(C, g1, acc[p + ST]));
+    } else {
+      acc[p] = fmaf(C, g0, fmaf(S, g1, acc[p]));
+      acc[p + ST] = fmaf(-S, g0, fmaf(C, g1, acc[p + ST]));
+    }
+  }
+}
+template <int ST>
+__device__ __forceinline__ void rot_accf_d(int delta, float* acc, const float* g, float C, float S) {
+  if (delta > 0) rot_accf<ST, 1>(acc, g, C, S);
+  else if (delta < 0) rot_accf<ST, -1>(acc, g, C, S);
+  else rot_accf<ST, 0>(acc, g, C, S);
+}
+__device__ __forceinline__ void rot_csf(int m, float& C, float& S) {
+  const int e = m % 3;   // angle 2 pi m / 3
+  C = e == 0 ? 1.0f : -0.5f;
+  S = e == 0 ? 0.0f : (e == 1 ? 0.866025403784438647f : -0.866025403784438647f);
+}
+constexpr int PWS_NT = 128, PWS_GY = 2;
+template <int H>
+__global__ void __launch_bounds__(PWS_NT, 3)
+    k_pwshift(DevTree t, const int32_t* __restrict__ parents, const float* __restrict__ F, size_t base,
+              size_t stride, const double* __restrict__ W, size_t wstride, float* __restrict__ Tout) {
+  constexpr int HSQ = H * H, NM = H * HSQ, SLAB = 8 * HSQ;
+  __shared__ const float* win[64];   // window box (w1 w2 w3), null: absent or not F_out
+  __shared__ int rank[8];            // exp rank of child o = (o1 o2 o3), -1: none
+  __shared__ int lvl;
+  const int pb = parents[blockIdx.x], tid = threadIdx.x;
+  if (tid < 64) {
+    const int w1 = tid >> 4, w2 = (tid >> 2) & 3, w3 = tid & 3;
+    // window index w = 2 D + c + 1 for the child c of the parent colleague B + D
+    const int D1 = w1 == 0 ? -1 : (w1 == 3 ? 1 : 0), D2 = w2 == 0 ? -1 : (w2 == 3 ? 1 : 0),
+              D3 = w3 == 0 ? -1 : (w3 == 3 ? 1 : 0);
+    const int c1 = w1 - 2 * D1 - 1, c2 = w2 - 2 * D2 - 1, c3 = w3 - 2 * D3 - 1;
+    const int S = t.coll[27 * (int64_t)pb + (D1 + 1) * 9 + (D2 + 1) * 3 + (D3 + 1)];
+    const float* ptr = nullptr;
+    if (S >= 0) {
+      const int ch = t.child[8 * (int64_t)S + (c1 << 2) + (c2 << 1) + c3];
+      if (ch >= 0 && (t.flags[ch] & F_OUT)) ptr = F + base + (size_t)(t.fout_rank[ch] - 1) * stride;
+    }
+    win[tid] = ptr;
+  } else if (tid < 72) {
+    const int ch = t.child[8 * (int64_t)pb + (tid - 64)];
+    rank[tid - 64] = (ch >= 0 && (t.flags[ch] & F_EXP)) ? t.exp_rank[ch] : -1;
+    if (tid == 64) lvl = t.level[pb] + 1;
+  }
+  __syncthreads();
+  bool any = false;
+#pragma unroll
+  for (int o = 0; o < 8; ++o) any |= rank[o] >= 0;
+  if (!any) return;
+  const double* Wl = W + (size_t)lvl * wstride;
+  for (int m = blockIdx.y * PWS_NT + tid; m < NM; m += gridDim.y * PWS_NT) {
+    const int a = m / HSQ, bc = m - a * HSQ;
+    float Ca, Sa, Cb, Sb, Cc, Sc;
+    rot_csf(a, Ca, Sa);
+    rot_csf(bc / H, Cb, Sb);
+    rot_csf(bc % H, Cc, Sc);
+    const size_t off = (size_t)a * SLAB + bc;
+    float X[8][8];
+#pragma unroll
+    for (int o = 0; o < 8; ++o)
+#pragma unroll
+      for (int p = 0; p < 8; ++p) X[o][p] = 0.0f;
+#pragma unroll
+    for (int w1 = 0; w1 < 4; ++w1) {
+      float Y[2][2][8];
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+          for (int p = 0; p < 8; ++p) Y[i][j][p] = 0.0f;
+#pragma unroll
+      for (int w2 = 0; w2 < 4; ++w2) {
+        float g[4][8];
+#pragma unroll
+        for (int w3 = 0; w3 < 4; ++w3) {
+          const float* sp = win[w1 * 16 + w2 * 4 + w3];
+#pragma unroll
+          for (int p = 0; p < 8; ++p) g[w3][p] = sp ? __ldg(sp + off + p * HSQ) : 0.0f;
+        }
+        float Z[2][8];
+#pragma unroll
+        for (int o3 = 0; o3 < 2; ++o3) {
+#pragma unroll
+          for (int p = 0; p < 8; ++p) Z[o3][p] = 0.0f;
+#pragma unroll
+          for (int w3 = o3; w3 < o3 + 3; ++w3) rot_accf_d<1>(o3 + 1 - w3, Z[o3], g[w3], Cc, Sc);
+        }
+#pragma unroll
+        for (int o2 = 0; o2 < 2; ++o2) {
+          if (w2 < o2 || w2 > o2 + 2) continue;
+#pragma unroll
+          for (int o3 = 0; o3 < 2; ++o3) rot_accf_d<2>(o2 + 1 - w2, Y[o2][o3], Z[o3], Cb, Sb);
+        }
+      }
+#pragma unroll
+      for (int o1 = 0; o1 < 2; ++o1) {
+        if (w1 < o1 || w1 > o1 + 2) continue;
+#pragma unroll
+        for (int o2 = 0; o2 < 2; ++o2)
+#pragma unroll
+          for (int o3 = 0; o3 < 2; ++o3) rot_accf_d<4>(o1 + 1 - w1, X[o1 * 4 + o2 * 2 + o3], Y[o2][o3], Ca, Sa);
+      }
+    }
+    const float wt = (float)__ldg(Wl + m);
+#pragma unroll
+    for (int o = 0; o < 8; ++o) {
+      const int r = rank[o];
+      if (r < 0) continue;
+      float* dst = Tout + (size_t)r * H * SLAB + off;
+#pragma unroll
+      for (int p = 0; p < 8; ++p) dst[p * HSQ] = wt * X[o][p];
+    }
+  }
+}
+
 // Incoming expansion + conversion to Chebyshev coefficients of one local-expansion box
 // (Eq. 3.39 fused with Eqs. 3.43-3.44): per chunk of AC slabs a, the 27-colleague
 // translation (separable rotations: three nested 3-point sums), the weights, then the
@@ -430,11 +575,11 @@ struct PwLocal {
                         (VSMEM ? (size_t)H * 2 * G::P2 : (size_t)AC * 2 * G::P2));
   static constexpr int MINB = (VSMEM && NT <= 352) ? 2 : 1;
 };
-template <int P, int H, int AC, bool ROOT>
+template <int P, int H, int AC, bool ROOT, bool FROMT = false>
 __global__ void __launch_bounds__(PwLocal<P, H, AC>::NT, PwLocal<P, H, AC>::MINB)
     k_pwlocal(DevTree t, const int32_t* __restrict__ boxes, const double* __restrict__ Gr,
               const double* __restrict__ W, size_t wstride, const FStore<P>* __restrict__ F, size_t base,
-              size_t stride, double* __restrict__ lam) {
+              size_t stride, double* __restrict__ lam, const float* __restrict__ Tin = nullptr) {
   using G = PwGeom<P, H>;
   using C = PwLocal<P, H, AC>;
   using TF = FStore<P>;
@@ -452,7 +597,7 @@ __global__ void __launch_bounds__(PwLocal<P, H, AC>::NT, PwLocal<P, H, AC>::MINB
   const int l = t.level[b];
   const double* Wl = W + (ROOT ? 0 : (size_t)l * wstride);
   for (int i = tid; i < P * HH; i += NT) sG[i] = Gr[i];
-  if (tid < 27) {
+  if (!FROMT && tid < 27) {
     // colleague slot k = (dx+1)*9 + (dy+1)*3 + (dz+1) holds B + (dx,dy,dz); its
     // delta = c_B - c_S = -(dx,dy,dz) has slot 26 - k
     const TF* p = nullptr;
@@ -475,7 +620,11 @@ __global__ void __launch_bounds__(PwLocal<P, H, AC>::NT, PwLocal<P, H, AC>::MINB
       const int ac = w / HSQ, bc = w % HSQ, a = a0 + ac;
       const size_t off = (size_t)a * SLAB + bc;
       double o[8];
-      if (ROOT) {
+      if (FROMT) {   // translated and weighted by k_pwshift
+        const float* tb = Tin + (size_t)t.exp_rank[b] * H * SLAB + off;
+#pragma unroll
+        for (int p = 0; p < 8; ++p) o[p] = (double)__ldg(tb + p * HSQ);
+      } else if (ROOT) {
 #pragma unroll
         for (int p = 0; p < 8; ++p) o[p] = (double)__ldg(src[13] + off + p * HSQ);
       } else {
@@ -515,7 +664,7 @@ __global__ void __launch_bounds__(PwLocal<P, H, AC>::NT, PwLocal<P, H, AC>::MINB
           else rot_acc<4, 1>(o, x, Ca, Sa);
         }
       }
-      const double wt = __ldg(Wl + (size_t)a * HSQ + bc);
+      const double wt = FROMT ? 1.0 : __ldg(Wl + (size_t)a * HSQ + bc);
 #pragma unroll
       for (int p = 0; p < 8; ++p) T[(ac * 8 + p) * HSQ + bc] = wt * o[p];
     }
@@ -1017,6 +1166,99 @@ __global__ void __launch_bounds__(128) k_p2p(DevTree t, const int32_t* __restric
   if (lane < nt) unear[t0 + lane] = acc;
 }
 
+// fp32 tier (reading R16, p <= 18, eps >= 1e-6).  The same sum as k_p2p, every pair
+// evaluated in single precision on leaf-local double-single coordinates: a source
+// record holds x - c_S split as hi + lo (k_leaf_local4), the target's record is shifted
+// once per list entry by c_T - c_S (exact in fp32: dyadic centres, level <= 20) with an
+// error-free TwoSum, and a pair difference is (x_hi - y_hi) + (x_lo - y_lo), so |dx|
+// carries a relative error of ~2^-23 whatever its size against r_L (plain fp32
+// coordinates would carry 2^-25 r_L absolute: 4x the eps = 1e-6 error budget on
+// surface distributions).  The terms of one list entry are summed in fp32 and added to
+// an fp64 accumulator.  R_L(r) = K(r) - m_L(s)/r_L as in k_p2p (Horner in fp32: the
+// monomial coefficients of m are O(1), |s| <= 1).
+__device__ __forceinline__ float rsqrt_approx(float x) {   // MUFU.RSQ, flush-to-zero
+  float y;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ void two_sum(float a, float b, float& s, float& e) {
+  s = __fadd_rn(a, b);
+  const float bb = __fsub_rn(s, a);
+  e = __fadd_rn(__fsub_rn(a, __fsub_rn(s, bb)), __fsub_rn(b, bb));
+}
+template <int K, int KER>
+__global__ void __launch_bounds__(128) k_p2p32(DevTree t, const int32_t* __restrict__ items, int64_t nitems,
+                                               const int32_t* __restrict__ doff, const int32_t* __restrict__ dlist,
+                                               const float4* __restrict__ src, const float4* __restrict__ srclo,
+                                               ResPoly rp, const double* __restrict__ lvpoly, float lam,
+                                               double* __restrict__ unear) {
+  __shared__ float4 ssrc[4][32], slo[4][32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t it = (int64_t)blockIdx.x * 4 + warp;
+  if (it >= nitems) return;
+  const int B = items[2 * it], t0 = items[2 * it + 1];
+  const int nt = min(32, t.end[B] - t0);
+  const float4 tp = src[t0 + min(lane, nt - 1)], tl = srclo[t0 + min(lane, nt - 1)];
+  const uint64_t cB = t.code[B];
+  const int LB = t.level[B];
+  const float bx = (float)compact3d(cB >> 2) + 0.5f, by = (float)compact3d(cB >> 1) + 0.5f,
+              bz = (float)compact3d(cB) + 0.5f;
+  float a[K + 1];
+  if (KER == KER_LAPLACE) {
+#pragma unroll
+    for (int j = 0; j <= K; ++j) a[j] = (float)rp.a[j];
+  }
+  double acc = 0.0;
+  for (int e = doff[B]; e < doff[B + 1]; ++e) {
+    const int S = dlist[e];
+    const int L = t.level[S];
+    const uint64_t cS = t.code[S];
+    // c_T - c_S, exact: both are dyadic with <= 22 significant bits
+    const float sT = ldexpf(1.0f, -LB), sS = ldexpf(1.0f, -L);
+    float xt, yt, zt, xe, ye, ze;
+    two_sum(tp.x, bx * sT - ((float)compact3d(cS >> 2) + 0.5f) * sS, xt, xe);
+    two_sum(tp.y, by * sT - ((float)compact3d(cS >> 1) + 0.5f) * sS, yt, ye);
+    two_sum(tp.z, bz * sT - ((float)compact3d(cS) + 0.5f) * sS, zt, ze);
+    xe += tl.x;
+    ye += tl.y;
+    ze += tl.z;
+    const float irl = ldexpf(1.0f, L), two_irl2 = ldexpf(2.0f, 2 * L), rl2 = ldexpf(1.0f, -2 * L);
+    if (KER == KER_YUKAWA) {
+#pragma unroll
+      for (int j = 0; j <= K; ++j) a[j] = (float)__ldg(lvpoly + L * (K + 1) + j);
+    }
+    float part = 0.0f;
+    for (int s0 = t.start[S]; s0 < t.end[S]; s0 += 32) {
+      const int ns = min(32, t.end[S] - s0);
+      if (lane < ns) {
+        ssrc[warp][lane] = src[s0 + lane];
+        slo[warp][lane] = srclo[s0 + lane];
+      }
+      __syncwarp();
+#pragma unroll 2
+      for (int k = 0; k < ns; ++k) {
+        const float4 sp = ssrc[warp][k], sl = slo[warp][k];
+        const float dx = (xt - sp.x) + (xe - sl.x), dy = (yt - sp.y) + (ye - sl.y), dz = (zt - sp.z) + (ze - sl.z);
+        const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+        if (r2 < rl2) {
+          const float s = fmaf(r2, two_irl2, -1.0f);
+          float pv = a[K];
+#pragma unroll
+          for (int j = K - 1; j >= 0; --j) pv = fmaf(pv, s, a[j]);
+          // r^2 below FLT_MIN (|x_t - x_s| < 1e-19 r_L) counts as coincident
+          const float rinv = rsqrt_approx(r2);
+          float kv = (KER == KER_YUKAWA) ? expf(-lam * r2 * rinv) * rinv : rinv;
+          kv = r2 >= 1.17549435e-38f ? kv : 0.0f;
+          part = fmaf(sp.w, fmaf(-pv, irl, kv), part);
+        }
+      }
+      __syncwarp();
+    }
+    acc += (double)part;
+  }
+  if (lane < nt) unear[t0 + lane] = acc;
+}
+
 // u = (u_far + u_near)/side, scattered to the caller's order (after both branches)
 __global__ void k_combine(const double* __restrict__ ufar, const double* __restrict__ unear,
                           const int32_t* __restrict__ perm, int64_t n, double inv_side, double* __restrict__ out) {
@@ -1143,8 +1385,22 @@ static void run_eval(dmk_plan_s* PL, int phase = PH_UP | PH_DOWN, int top = 0) {
                                                               PL->lam.p);
       DMK_LAUNCH_CHECK();
       if (PL->nexp > 1) {
-        k_pwlocal<P, H, AC, false><<<(int)(PL->nexp - 1), K1::NT, K1::smem, s>>>(
-            dt, PL->exp_list.p + 1, T.dGr1, T.dW, T.wstride, Fp, PL->phi_size0, PL->phi_size1, PL->lam.p);
+        if constexpr (P <= 18) {
+          // parent-group translation (k_pwshift) into T, then the back transforms
+          if (PL->nfout > 0) {
+            dim3 grid((unsigned)PL->nfout, PWS_GY);
+            k_pwshift<H><<<grid, PWS_NT, 0, s>>>(dt, PL->fout_list.p, reinterpret_cast<const float*>(Fp),
+                                                  PL->phi_size0, PL->phi_size1, T.dW, T.wstride, PL->pwt.p);
+            DMK_LAUNCH_CHECK();
+          }
+          set_smem(k_pwlocal<P, H, AC, false, true>, K1::smem);
+          k_pwlocal<P, H, AC, false, true><<<(int)(PL->nexp - 1), K1::NT, K1::smem, s>>>(
+              dt, PL->exp_list.p + 1, T.dGr1, T.dW, T.wstride, Fp, PL->phi_size0, PL->phi_size1, PL->lam.p,
+              PL->pwt.p);
+        } else {
+          k_pwlocal<P, H, AC, false><<<(int)(PL->nexp - 1), K1::NT, K1::smem, s>>>(
+              dt, PL->exp_list.p + 1, T.dGr1, T.dW, T.wstride, Fp, PL->phi_size0, PL->phi_size1, PL->lam.p);
+        }
         DMK_LAUNCH_CHECK();
       }
     }
@@ -1202,6 +1458,26 @@ static void run_p2p_deg(dmk_plan_s* PL, double* out, const ResPoly& rp, int K, c
   DMK_LAUNCH_CHECK();
 }
 
+template <int KER>
+static void run_p2p32_deg(dmk_plan_s* PL, const ResPoly& rp, int K, cudaStream_t st) {
+  DevTree dt = dev_tree(PL);
+  int nb = (int)((PL->np2p + 3) / 4);
+  if (nb == 0) return;
+  const Tables& T = *PL->tab;
+#define DMK_P2P_CASE(KK)                                                                                   \
+  case KK:                                                                                                 \
+    k_p2p32<KK, KER><<<nb, 128, 0, st>>>(dt, PL->p2p_items.p, PL->np2p, PL->dlist_off.p, PL->dlist.p,      \
+                                         PL->xl4.p, PL->xl4lo.p, rp, T.dRespoly, (float)T.lam, PL->unear.p);            \
+    break;
+  switch (K) {
+    DMK_P2P_CASE(4) DMK_P2P_CASE(6) DMK_P2P_CASE(8) DMK_P2P_CASE(10) DMK_P2P_CASE(12) DMK_P2P_CASE(14)
+    DMK_P2P_CASE(16) DMK_P2P_CASE(18) DMK_P2P_CASE(20) DMK_P2P_CASE(22) DMK_P2P_CASE(24)
+    default: fail(DMK_ERR_UNSUPPORTED, "residual polynomial degree out of range");
+  }
+#undef DMK_P2P_CASE
+  DMK_LAUNCH_CHECK();
+}
+
 template <class F>
 static void dispatch_p(dmk_plan_s* PL, F f) {
   switch (PL->tab->p) {
@@ -1239,7 +1515,9 @@ void eval_upward(dmk_plan_s* PL, const double* dcharges) {
   // a near-field branch of an earlier call may still read q: join it first
   if (PL->p2p_pending) DMK_CUDA(cudaStreamWaitEvent(s, PL->ev_join, 0));
   tm.begin("gather");
-  k_gather_q<<<(int)((PL->n + 255) / 256), 256, 0, s>>>(dcharges, PL->perm.p, PL->n, PL->q.p);
+  const bool p2p32 = PL->dim == 3 && PL->tab->p <= 18 && PL->th.nlevels > 1;   // reading R16
+  k_gather_q<<<(int)((PL->n + 255) / 256), 256, 0, s>>>(dcharges, PL->perm.p, PL->n, PL->q.p,
+                                                        p2p32 ? PL->xl4.p : nullptr);
   DMK_LAUNCH_CHECK();
   tm.end();
   if (PL->dim == 2) return;   // the 2D path runs as one piece (eval_plan_2d)
@@ -1253,10 +1531,12 @@ void eval_upward(dmk_plan_s* PL, const double* dcharges) {
   const bool full = PL->th.nlevels == 1;
   if (PL->tab->kernel == DMK_KERNEL_YUKAWA) {
     K = PL->tab->respoly_deg;
-    if (full) run_p2p_deg<KER_YUKAWA, true>(PL, nullptr, rp, K, slo);
+    if (p2p32) run_p2p32_deg<KER_YUKAWA>(PL, rp, K, slo);
+    else if (full) run_p2p_deg<KER_YUKAWA, true>(PL, nullptr, rp, K, slo);
     else run_p2p_deg<KER_YUKAWA, false>(PL, nullptr, rp, K, slo);
   } else {
-    if (full) run_p2p_deg<KER_LAPLACE, true>(PL, nullptr, rp, K, slo);
+    if (p2p32) run_p2p32_deg<KER_LAPLACE>(PL, rp, K, slo);
+    else if (full) run_p2p_deg<KER_LAPLACE, true>(PL, nullptr, rp, K, slo);
     else run_p2p_deg<KER_LAPLACE, false>(PL, nullptr, rp, K, slo);
   }
   tm.end(slo);

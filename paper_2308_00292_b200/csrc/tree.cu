@@ -17,6 +17,7 @@
 #include <cub/cub.cuh>
 
 #include "common.cuh"
+#include "device.cuh"
 
 namespace dmk {
 namespace {
@@ -463,6 +464,26 @@ __global__ void k_p2p_fill(const int32_t* start, const int32_t* cnt, const int32
   }
 }
 
+// Leaf-local double-single source records for the fp32 P2P tier (reading R16): for the
+// leaf B holding point i, d = x_i - c_B (fp64, exact), hi = fl32(d), lo = fl32(d - hi);
+// xl4[i] = (hi_x, hi_y, hi_z, rho_i) (the charge slot is filled per evaluation) and
+// xl4lo[i] = (lo_x, lo_y, lo_z, 0).
+__global__ void k_leaf_local4(const uint64_t* code, const int32_t* level, const int32_t* start, const int32_t* end,
+                              const uint8_t* flags, int64_t nbox, const double* xs, const double* ys,
+                              const double* zs, float4* xl4, float4* xl4lo) {
+  const int64_t b = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (b >= nbox || !(flags[b] & 1)) return;
+  double c[3], ih;
+  box_geom(code[b], level[b], c, ih);
+  for (int i = start[b] + lane; i < end[b]; i += 32) {
+    const double dx = xs[i] - c[0], dy = ys[i] - c[1], dz = zs[i] - c[2];
+    const float hx = (float)dx, hy = (float)dy, hz = (float)dz;
+    xl4[i] = make_float4(hx, hy, hz, 0.0f);
+    xl4lo[i] = make_float4((float)(dx - hx), (float)(dy - hy), (float)(dz - hz), 0.0f);
+  }
+}
+
 // ---------------------------------------------------------------- host helpers
 int64_t select_flagged(cudaStream_t s, const uint64_t* in, const uint8_t* flags, int64_t n,
                        DevBuf<uint64_t>& out) {
@@ -866,6 +887,14 @@ static void build_tree_d(dmk_plan_s* P, const double* dpts) {
     mark("dlists");
     P->p2p_items.alloc(2 * (P->np2p ? P->np2p : 1), s);
     k_p2p_fill<<<nblk(nbox), TPB, 0, s>>>(P->box_start.p, pcnt.p, poff.p, nbox, P->p2p_items.p);
+    DMK_LAUNCH_CHECK();
+  }
+  if (D == 3) {
+    P->xl4.alloc(n ? n : 1, s);
+    P->xl4lo.alloc(n ? n : 1, s);
+    k_leaf_local4<<<nblk(32 * nbox), TPB, 0, s>>>(P->box_code.p, P->box_level.p, P->box_start.p, P->box_end.p,
+                                                   P->box_flags.p, nbox, P->xs.p, P->ys.p, P->zs.p, P->xl4.p,
+                                                   P->xl4lo.p);
     DMK_LAUNCH_CHECK();
   }
   DMK_CUDA(cudaStreamSynchronize(s));

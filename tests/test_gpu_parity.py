@@ -138,8 +138,12 @@ def test_far_and_near_fields_match_oracle(case):
     assert np.max(np.abs(ufar - st["u_far"])) <= tol * np.max(np.abs(st["u_far"]))
     # the device evaluates r_L M_L(r) through a polynomial fitted to 1e-2 eps m0
     # (tables.cu); the oracle uses the exact Legendre series
+    # p <= 18: pairs in fp32 on double-single leaf-local coordinates (reading R16): ~1e-7
+    # relative per term (2^-23 on |x - y|, rsqrt.approx, fp32 Horner on O(1) coefficients)
     ref_near = st["u_near"] + st["u_self"]
-    assert np.max(np.abs(unear - ref_near)) <= 1e-7 * np.max(np.abs(ref_near))
+    near_tol = 1e-7 if plan.info().p >= 28 else 1e-6
+    assert np.max(np.abs(unear - ref_near)) <= near_tol * np.max(np.abs(ref_near))
+    assert np.linalg.norm(unear - ref_near) <= near_tol * np.linalg.norm(ref_near)
 
 
 def test_potential_matches_oracle_dmk_and_direct(case):
