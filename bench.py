@@ -416,6 +416,11 @@ def main():
             stage_ms[name] = stage_ms.get(name, 0.0) + ms / 3
         plan.close()
     os.environ.pop("DMK_SERIAL")
+    # p <= 18: the plane-wave stage runs as k_pwshift (parent-group translation) and the
+    # back transforms (pw2poly); the roofline takes them together as "pwlocal"
+    pw_parts = {k: round(stage_ms.pop(k), 4) for k in ("pwshift", "pw2poly") if k in stage_ms}
+    if pw_parts:
+        stage_ms["pwlocal"] = stage_ms.get("pwlocal", 0.0) + sum(pw_parts.values())
     if dist is not None:
         t = torch.tensor([t_step], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -507,6 +512,7 @@ def main():
                       "note": "stage kernels timed back to back (DMK_SERIAL=1); the timed steps overlap "
                               "p2p (low-priority stream) with c2p..eval (high-priority stream)"},
         "stages": stages,
+        "pwlocal_parts_ms": pw_parts,
         "tree": {"nbox": info.nbox, "nlevels": info.nlevels, "nfout": info.nfout, "nexp": info.nexp,
                  "p2p_pairs": pairs, "p2p_pairs_in_ball": inball},
     }

@@ -62,7 +62,7 @@ __device__ __forceinline__ void cheb_vec(double x, double* T, int P, double scal
 // same as DFMA, but 256 FMA per warp instruction from 2 register operands, which
 // takes the shared-memory bandwidth limit off these small per-box GEMMs.
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(c0), "+d"(c1)
                : "d"(a), "d"(b));
 }
@@ -76,9 +76,16 @@ __device__ __forceinline__ void mma_tiles(int mtiles, int ntiles, FA fa, FB fb, 
   const int g = lane >> 2, q = lane & 3;
   for (int t = warp; t < mtiles * ntiles; t += nw) {
     const int m0 = (t / ntiles) * 8, n0 = (t % ntiles) * 8;
+    // all operands of the tile first (independent loads in flight), then the DMMA chain
+    double av[KS], bv[KS];
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      av[ks] = fa(m0 + g, ks * 4 + q);
+      bv[ks] = fb(ks * 4 + q, n0 + g);
+    }
     double c0 = 0.0, c1 = 0.0;
 #pragma unroll
-    for (int ks = 0; ks < KS; ++ks) dmma(c0, c1, fa(m0 + g, ks * 4 + q), fb(ks * 4 + q, n0 + g));
+    for (int ks = 0; ks < KS; ++ks) dmma(c0, c1, av[ks], bv[ks]);
     fc(m0 + g, n0 + 2 * q, c0, c1);
   }
 }

@@ -10,17 +10,21 @@
 // only (Hermitian symmetry of real sources).
 //
 // Kernels (one CTA per box unless noted):
-//   k_gather_q     charges into Morton order
-//   k_anterp<P>    moments of each F_out box from the points of its leaf children
-//                  (register-tiled rank-CH updates: a small fp64 GEMM per box)
-//   k_c2p<P>       child -> parent moments, one tree level per launch
-//   k_prox2pw<P,NF>   Phi_l(B) = (Q (x) Q (x) Q) mu(B), m3-sliced (T_prox2pw)
-//   k_pwlocal<P,NF>   Psi_l(B) = w_l sum_S shift(B,S) Phi_l(S) (Eq. 3.39) fused with
-//                  Lambda_own(B) = (G (x) G (x) G) Psi_l(B), G = conj(Q)^T (T_pw2poly)
-//   k_p2c<P>       Lambda(B) += (A^T)^{(x)3} Lambda(parent), one level per launch
-//   k_eval<P>      far field at targets from Lambda (Chebyshev sums)
-//   k_p2p<K>       residual kernel R_{L_S} over the direct lists (warp per 32
-//                  targets), self terms, final combine and scatter to caller order
+//   k_gather_q     charges into Morton order (+ the charge slot of the fp32 P2P records)
+//   k_anterp_mma<P>   moments of each F_out box from the points of its leaf children
+//                  (fp64 tensor-core GEMMs, DMMA)
+//   k_c2p_grp<P>   child -> parent moments by parent groups (8 children, 3 DMMA
+//                  contractions over K = 2p), one tree level per launch
+//   k_prox2pw<P,H>    outgoing plane waves F(B) from mu(B) (T_prox2pw, DMMA)
+//   k_pwshift<H>   fp32 tier: colleague translation (Eq. 3.39) + weights for the 8
+//                  children of a parent from the 4x4x4 window of outgoing expansions
+//   k_pwlocal<P,H>    translation (p = 28) or its k_pwshift result, then T_pw2poly
+//                  Lambda_own(B) = (Gr (x) Gr (x) Gr) Psi_l(B)
+//   k_p2c_grp<P>   Lambda(children) += (A^T)^{(x)3} Lambda(parent) by parent groups
+//   k_eval_pad<P> / k_eval_mma<P>   far field at targets from Lambda (DMMA)
+//   k_p2p<K> / k_p2p32<K>   residual kernel R_{L_S} over the direct lists (warp per
+//                  item of <= 32 targets, fp64 or the fp32 tier), self terms
+//   k_combine      (u_far + u_near)/side, scattered to the caller's order
 #include <cstring>
 #include <type_traits>
 
@@ -129,131 +133,195 @@ __global__ void __launch_bounds__(Cfg<P>::TA * Cfg<P>::TB)
     for (int k = 0; k < C::RB; ++k) out[(ta + i * C::TA) * P + tb + k * C::TB] = acc[i][k];
 }
 
-// ---------------------------------------------------------------- line transforms
-// In-place 1D transform of a P^3 smem cube along axis `ax` (0: n1, 1: n2, 2: n3):
-//   out[n] = sum_k M[n][k] in[k]   (TRANS: out[n] = sum_k M[k][n] in[k])
-template <int P, bool TRANS>
-__device__ __forceinline__ void line_apply(double* cube, const double* M, int ax, int tid, int nt) {
-  for (int line = tid; line < P * P; line += nt) {
-    int u = line / P, v = line % P;
-    size_t base, stride;
-    if (ax == 2) { base = ((size_t)u * P + v) * P; stride = 1; }
-    else if (ax == 1) { base = (size_t)u * P * P + v; stride = P; }
-    else { base = (size_t)u * P + v; stride = (size_t)P * P; }
-    double in[P];
-#pragma unroll
-    for (int k = 0; k < P; ++k) in[k] = cube[base + k * stride];
-#pragma unroll 1
-    for (int nn = 0; nn < P; ++nn) {
-      double s = 0.0;
-#pragma unroll
-      for (int k = 0; k < P; ++k) s = fma(TRANS ? M[k * P + nn] : M[nn * P + k], in[k], s);
-      cube[base + nn * stride] = s;
-    }
-  }
-}
-
-// c2p: mu(P) += sum over non-leaf children C of (A_sx (x) A_sy (x) A_sz) mu(C)
-template <int P>
-__global__ void __launch_bounds__(P* P) k_c2p(DevTree t, const int32_t* __restrict__ boxes, const double* __restrict__ A,
-                                              double* __restrict__ mom) {
-  constexpr int P2 = P * P, P3 = P2 * P, NT = P2;
+// ---------------------------------------------------------------- c2p / p2c
+// ---- c2p / p2c by parent groups on fp64 tensor cores (Lemmas 2.2-2.3).
+// The 8 children of a parent share the axis factors: with octant o = (o1 o2 o3),
+//   c2p: mu_P = sum_o (A_o1 (x) A_o2 (x) A_o3) mu_o
+//           = sum_o3 [sum_o2 [sum_o1 A_o1 mu_(o1 o2 o3)]_axis1 ...]
+// so the axis-1 contraction runs over K = 2p (both o1) for each (o2, o3), the axis-2
+// one over K = 2p for each o3, and the axis-3 one over K = 2p once: 14 p^4 instead of
+// 48 p^4 flops per parent.  p2c is the transpose (axis 1 first, expanding 1 -> 2 -> 4
+// -> 8).  A CTA owns a tile of MT rows of the first-contracted axis (c2p: output rows
+// m1 of the parent; p2c: output rows k1 of the children), intermediates in shared
+// memory, each contraction a DMMA GEMM (mma_tiles).
+template <int P, int MT>
+struct GrpCfg {
+  static constexpr int P2 = P * P, NTILE = (P + MT - 1) / MT;
+  static constexpr int KS2 = (2 * P + 3) / 4, KS1 = (P + 3) / 4;
+  static constexpr size_t smem_c2p = sizeof(double) * ((size_t)2 * P2 + 6 * (size_t)MT * P2);
+  static constexpr size_t smem_p2c = sizeof(double) * ((size_t)2 * P2 + 6 * (size_t)MT * P2);
+};
+template <int P, int MT>
+__global__ void __launch_bounds__(256) k_c2p_grp(DevTree t, const int32_t* __restrict__ parents,
+                                                 const double* __restrict__ A, double* __restrict__ mom) {
+  using C = GrpCfg<P, MT>;
+  constexpr int P2 = C::P2, P3 = P2 * P, KS2 = C::KS2;
   extern __shared__ double sm[];
-  double* cube = sm;          // P3
-  double* sA = cube + P3;     // [2][P][P]
-  const int b = boxes[blockIdx.x], tid = threadIdx.x;
-  for (int i = tid; i < 2 * P2; i += NT) sA[i] = A[i];
-  double* dst = mom + (size_t)t.fout_rank[b] * P3 + (size_t)tid * P;
-  for (int o = 0; o < 8; ++o) {
-    int ch = t.child[8 * (int64_t)b + o];
-    if (ch < 0 || !(t.flags[ch] & F_OUT)) continue;
-    const double* src = mom + (size_t)t.fout_rank[ch] * P3;
-    __syncthreads();
-    for (int i = tid; i < P3; i += NT) cube[i] = src[i];
-    __syncthreads();
-    // child octant bits: bit2 = x (axis n1), bit1 = y (n2), bit0 = z (n3); side +1 if set
-    line_apply<P, false>(cube, sA + ((o >> 0) & 1) * P2, 2, tid, NT);
-    __syncthreads();
-    line_apply<P, false>(cube, sA + ((o >> 1) & 1) * P2, 1, tid, NT);
-    __syncthreads();
-    line_apply<P, false>(cube, sA + ((o >> 2) & 1) * P2, 0, tid, NT);
-    __syncthreads();
-    for (int k = 0; k < P; ++k) dst[k] += cube[(size_t)tid * P + k];   // this CTA owns mu(P)
+  double* sA = sm;                  // [2][P][P]: A_s[n][k]
+  double* xi = sA + 2 * P2;         // [(o2 o3)][MT][P2]
+  double* eta = xi + 4 * MT * P2;   // [o3][MT][P2]
+  __shared__ const double* ch[8];
+  const int b = parents[blockIdx.x], tid = threadIdx.x, m0 = blockIdx.y * MT;
+  if (tid < 8) {
+    const int c = t.child[8 * (int64_t)b + tid];
+    ch[tid] = (c >= 0 && (t.flags[c] & F_OUT)) ? mom + (size_t)t.fout_rank[c] * P3 : nullptr;
   }
-}
-
-// c2p split over the children for parallelism (the per-parent kernel above runs its 8
-// children one after the other, which leaves the coarse levels latency-bound):
-// k_c2p_child transforms one F_out child's moments into a scratch slot, k_c2p_sum adds
-// the slots of each parent's children in octant order (deterministic).
-template <int P>
-__global__ void __launch_bounds__(P* P) k_c2p_child(DevTree t, const int32_t* __restrict__ boxes, int64_t r0,
-                                                    const double* __restrict__ A, const double* __restrict__ mom,
-                                                    double* __restrict__ scratch) {
-  constexpr int P2 = P * P, P3 = P2 * P, NT = P2;
-  extern __shared__ double sm[];
-  double* cube = sm;
-  double* sA = cube + P3;
-  const int b = boxes[blockIdx.x], tid = threadIdx.x;
-  const int o = (int)(t.code[b] & 7);
-  for (int i = tid; i < 2 * P2; i += NT) sA[i] = A[i];
-  const double* src = mom + (size_t)t.fout_rank[b] * P3;
-  for (int i = tid; i < P3; i += NT) cube[i] = src[i];
+  for (int i = tid; i < 2 * P2; i += 256) sA[i] = A[i];
   __syncthreads();
-  line_apply<P, false>(cube, sA + ((o >> 0) & 1) * P2, 2, tid, NT);
-  __syncthreads();
-  line_apply<P, false>(cube, sA + ((o >> 1) & 1) * P2, 1, tid, NT);
-  __syncthreads();
-  line_apply<P, false>(cube, sA + ((o >> 2) & 1) * P2, 0, tid, NT);
-  __syncthreads();
-  double* dst = scratch + (size_t)(t.fout_rank[b] - r0) * P3;
-  for (int i = tid; i < P3; i += NT) dst[i] = cube[i];
-}
-template <int P>
-__global__ void __launch_bounds__(256) k_c2p_sum(DevTree t, const int32_t* __restrict__ boxes, int64_t r0,
-                                                 const double* __restrict__ scratch, double* __restrict__ mom) {
-  constexpr int P3 = P * P * P;
-  const int b = boxes[blockIdx.x];
-  __shared__ int slot[8];
-  if (threadIdx.x < 8) {
-    const int ch = t.child[8 * (int64_t)b + threadIdx.x];
-    slot[threadIdx.x] = (ch >= 0 && (t.flags[ch] & F_OUT)) ? (int)(t.fout_rank[ch] - r0) : -1;
+  bool any = false;
+#pragma unroll
+  for (int o = 0; o < 8; ++o) any |= ch[o] != nullptr;
+  if (!any) return;
+  // axis 1: xi[g][i][n2n3] = sum_{o1,k1} A_o1[m0+i][k1] mu_(o1 g)[k1][n2n3]
+  for (int g = 0; g < 4; ++g) {
+    const double* c0 = ch[g];
+    const double* c1 = ch[4 + g];
+    mma_tiles<KS2>(
+        (MT + 7) / 8, (P2 + 7) / 8,
+        [&](int m, int k) {
+          const int o1 = k >= P, k1 = k - o1 * P;
+          return (m < MT && m0 + m < P && k < 2 * P) ? sA[(o1 * P + m0 + m) * P + k1] : 0.0;
+        },
+        [&](int k, int n) {
+          const int o1 = k >= P, k1 = k - o1 * P;
+          const double* c = o1 ? c1 : c0;
+          return (c && k < 2 * P && n < P2) ? __ldg(c + (size_t)k1 * P2 + n) : 0.0;
+        },
+        [&](int m, int n, double v0, double v1) {
+          if (m < MT) {
+            if (n < P2) xi[(g * MT + m) * P2 + n] = v0;
+            if (n + 1 < P2) xi[(g * MT + m) * P2 + n + 1] = v1;
+          }
+        });
   }
   __syncthreads();
+  // axis 2: eta[o3][i][m2 n3] = sum_{o2,k2} A_o2[m2][k2] xi[(o2 o3)][i][k2 n3]
+  for (int o3 = 0; o3 < 2; ++o3) {
+    mma_tiles<KS2>(
+        (P + 7) / 8, (MT * P + 7) / 8,
+        [&](int m, int k) {
+          const int o2 = k >= P, k2 = k - o2 * P;
+          return (m < P && k < 2 * P) ? sA[(o2 * P + m) * P + k2] : 0.0;
+        },
+        [&](int k, int n) {
+          const int o2 = k >= P, k2 = k - o2 * P, i = n / P, n3 = n - i * P;
+          return (k < 2 * P && i < MT) ? xi[((o2 * 2 + o3) * MT + i) * P2 + k2 * P + n3] : 0.0;
+        },
+        [&](int m, int n, double v0, double v1) {
+          if (m >= P) return;
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int nn = n + e, i = nn / P, n3 = nn - i * P;
+            if (i < MT) eta[(o3 * MT + i) * P2 + m * P + n3] = e ? v1 : v0;
+          }
+        });
+  }
+  __syncthreads();
+  // axis 3: mu_P[m0+i][m2][m3] += sum_{o3,k3} eta[o3][i][m2][k3] A_o3[m3][k3]
   double* dst = mom + (size_t)t.fout_rank[b] * P3;
-  for (int i = threadIdx.x; i < P3; i += 256) {
-    double v = dst[i];
-#pragma unroll
-    for (int o = 0; o < 8; ++o)
-      if (slot[o] >= 0) v += scratch[(size_t)slot[o] * P3 + i];
-    dst[i] = v;
-  }
+  mma_tiles<KS2>(
+      (MT * P + 7) / 8, (P + 7) / 8,
+      [&](int m, int k) {
+        const int o3 = k >= P, k3 = k - o3 * P, i = m / P, m2 = m - i * P;
+        return (i < MT && k < 2 * P) ? eta[(o3 * MT + i) * P2 + m2 * P + k3] : 0.0;
+      },
+      [&](int k, int n) {
+        const int o3 = k >= P, k3 = k - o3 * P;
+        return (n < P && k < 2 * P) ? sA[(o3 * P + n) * P + k3] : 0.0;
+      },
+      [&](int m, int n, double v0, double v1) {
+        const int i = m / P, m2 = m - i * P;
+        if (i >= MT || m0 + i >= P) return;
+        // one writer per element: fire-and-forget reductions (RED), no read latency
+        double* row = dst + (size_t)(m0 + i) * P2 + m2 * P;
+        if (n < P) atomicAdd(row + n, v0);
+        if (n + 1 < P) atomicAdd(row + n + 1, v1);
+      });
 }
 
-// p2c: Lambda(B) += (A_sx^T (x) A_sy^T (x) A_sz^T) Lambda(parent)
-template <int P>
-__global__ void __launch_bounds__(P* P) k_p2c(DevTree t, const int32_t* __restrict__ boxes, const double* __restrict__ A,
-                                              double* __restrict__ lam) {
-  constexpr int P2 = P * P, P3 = P2 * P, NT = P2;
+template <int P, int MT>
+__global__ void __launch_bounds__(256) k_p2c_grp(DevTree t, const int32_t* __restrict__ parents,
+                                                 const double* __restrict__ A, double* __restrict__ lam) {
+  using C = GrpCfg<P, MT>;
+  constexpr int P2 = C::P2, P3 = P2 * P, KS1 = C::KS1, KS2 = C::KS2;
   extern __shared__ double sm[];
-  double* cube = sm;
-  double* sA = cube + P3;
-  const int b = boxes[blockIdx.x], tid = threadIdx.x;
-  const int par = t.parent[b];
-  const int o = (int)(t.code[b] & 7);
-  for (int i = tid; i < 2 * P2; i += NT) sA[i] = A[i];
-  const double* src = lam + (size_t)t.exp_rank[par] * P3;
-  for (int i = tid; i < P3; i += NT) cube[i] = src[i];
+  double* sA = sm;                   // [2][P][P]: A_s[n][k]
+  double* zeta = sA + 2 * P2;        // [o1][MT][P2]        (k1 m2 m3)
+  double* zeta2 = zeta + 2 * MT * P2;   // [o1][o2][MT][P2]  (k1 k2 m3)
+  __shared__ double* ch[8];
+  const int b = parents[blockIdx.x], tid = threadIdx.x, k0 = blockIdx.y * MT;
+  if (tid < 8) {
+    const int c = t.child[8 * (int64_t)b + tid];
+    ch[tid] = (c >= 0 && (t.flags[c] & F_EXP)) ? lam + (size_t)t.exp_rank[c] * P3 : nullptr;
+  }
+  for (int i = tid; i < 2 * P2; i += 256) sA[i] = A[i];
   __syncthreads();
-  line_apply<P, true>(cube, sA + ((o >> 0) & 1) * P2, 2, tid, NT);
-  __syncthreads();
-  line_apply<P, true>(cube, sA + ((o >> 1) & 1) * P2, 1, tid, NT);
-  __syncthreads();
-  line_apply<P, true>(cube, sA + ((o >> 2) & 1) * P2, 0, tid, NT);
-  __syncthreads();
-  double* dst = lam + (size_t)t.exp_rank[b] * P3 + (size_t)tid * P;
+  bool any = false;
 #pragma unroll
-  for (int k = 0; k < P; ++k) dst[k] += cube[(size_t)tid * P + k];
+  for (int o = 0; o < 8; ++o) any |= ch[o] != nullptr;
+  if (!any) return;
+  const double* src = lam + (size_t)t.exp_rank[b] * P3;
+  // axis 1: zeta[o1][i][m2m3] = sum_m1 A_o1[m1][k0+i] Lambda_P[m1][m2m3]
+  mma_tiles<KS1>(
+      (2 * MT + 7) / 8, (P2 + 7) / 8,
+      [&](int m, int k) {
+        const int o1 = m >= MT, i = m - o1 * MT;
+        return (m < 2 * MT && k0 + i < P && k < P) ? sA[(o1 * P + k) * P + k0 + i] : 0.0;
+      },
+      [&](int k, int n) { return (k < P && n < P2) ? __ldg(src + (size_t)k * P2 + n) : 0.0; },
+      [&](int m, int n, double v0, double v1) {
+        if (m < 2 * MT) {
+          if (n < P2) zeta[m * P2 + n] = v0;
+          if (n + 1 < P2) zeta[m * P2 + n + 1] = v1;
+        }
+      });
+  __syncthreads();
+  // axis 2: zeta2[o1][o2][i][k2 m3] = sum_m2 A_o2[m2][k2] zeta[o1][i][m2 m3]
+  mma_tiles<KS1>(
+      (2 * P + 7) / 8, (2 * MT * P + 7) / 8,
+      [&](int m, int k) {
+        const int o2 = m >= P, k2 = m - o2 * P;
+        return (m < 2 * P && k < P) ? sA[(o2 * P + k) * P + k2] : 0.0;
+      },
+      [&](int k, int n) {
+        const int r = n / P, m3 = n - r * P;   // r = o1 * MT + i
+        return (k < P && r < 2 * MT) ? zeta[r * P2 + k * P + m3] : 0.0;
+      },
+      [&](int m, int n, double v0, double v1) {
+        if (m >= 2 * P) return;
+        const int o2 = m >= P, k2 = m - o2 * P;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int nn = n + e, r = nn / P, m3 = nn - r * P;
+          if (r < 2 * MT) {
+            const int o1 = r >= MT, i = r - o1 * MT;
+            zeta2[((o1 * 2 + o2) * MT + i) * P2 + k2 * P + m3] = e ? v1 : v0;
+          }
+        }
+      });
+  __syncthreads();
+  // axis 3: Lambda_(o1 o2 o3)[k0+i][k2][k3] += sum_m3 zeta2[o1][o2][i][k2][m3] A_o3[m3][k3]
+  mma_tiles<KS1>(
+      (4 * MT * P + 7) / 8, (2 * P + 7) / 8,
+      [&](int m, int k) { return (m < 4 * MT * P && k < P) ? zeta2[(size_t)(m / P) * P2 + (m % P) * P + k] : 0.0; },
+      [&](int k, int n) {
+        const int o3 = n >= P, k3 = n - o3 * P;
+        return (k < P && n < 2 * P) ? sA[(o3 * P + k) * P + k3] : 0.0;
+      },
+      [&](int m, int n, double v0, double v1) {
+        const int r = m / P, k2 = m - r * P;   // r = (o1 o2) * MT + i
+        if (r >= 4 * MT) return;
+        const int g = r / MT, i = r - g * MT;
+        if (k0 + i >= P) return;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int nn = n + e;
+          if (nn >= 2 * P) continue;
+          const int o3 = nn >= P, k3 = nn - o3 * P;
+          double* c = ch[g * 2 + o3];
+          if (c) atomicAdd(c + (size_t)(k0 + i) * P2 + k2 * P + k3, e ? v1 : v0);   // one writer: RED
+        }
+      });
 }
 
 // ---------------------------------------------------------------- plane waves
@@ -1193,12 +1261,16 @@ __global__ void __launch_bounds__(128) k_p2p32(DevTree t, const int32_t* __restr
                                                ResPoly rp, const double* __restrict__ lvpoly, float lam,
                                                double* __restrict__ unear) {
   __shared__ float4 ssrc[4][32], slo[4][32];
+  __shared__ double red[4][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t it = (int64_t)blockIdx.x * 4 + warp;
   if (it >= nitems) return;
   const int B = items[2 * it], t0 = items[2 * it + 1];
   const int nt = min(32, t.end[B] - t0);
-  const float4 tp = src[t0 + min(lane, nt - 1)], tl = srclo[t0 + min(lane, nt - 1)];
+  // an item of nt < 16 targets (the tail of a leaf) splits each source tile over
+  // f = 32/nt lane groups: lane = target + nt * phase, phase strides the sources
+  const int f = 32 / nt, tj = lane % nt, ph = lane / nt;
+  const float4 tp = src[t0 + tj], tl = srclo[t0 + tj];
   const uint64_t cB = t.code[B];
   const int LB = t.level[B];
   const float bx = (float)compact3d(cB >> 2) + 0.5f, by = (float)compact3d(cB >> 1) + 0.5f,
@@ -1236,7 +1308,7 @@ __global__ void __launch_bounds__(128) k_p2p32(DevTree t, const int32_t* __restr
       }
       __syncwarp();
 #pragma unroll 2
-      for (int k = 0; k < ns; ++k) {
+      for (int k = ph; k < ns; k += f) {
         const float4 sp = ssrc[warp][k], sl = slo[warp][k];
         const float dx = (xt - sp.x) + (xe - sl.x), dy = (yt - sp.y) + (ye - sl.y), dz = (zt - sp.z) + (ze - sl.z);
         const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
@@ -1256,7 +1328,13 @@ __global__ void __launch_bounds__(128) k_p2p32(DevTree t, const int32_t* __restr
     }
     acc += (double)part;
   }
-  if (lane < nt) unear[t0 + lane] = acc;
+  red[warp][lane] = ph < f ? acc : 0.0;
+  __syncwarp();
+  if (lane < nt) {
+    double u = 0.0;
+    for (int k = 0; k < f; ++k) u += red[warp][lane + k * nt];
+    unear[t0 + lane] = u;
+  }
 }
 
 // u = (u_far + u_near)/side, scattered to the caller's order (after both branches)
@@ -1300,22 +1378,21 @@ constexpr int pw_ac(int H) { return 2 * H * H <= 1024 ? 2 : 1; }
 // c2p for the levels above `top` only (after dmk_level_moments injected level `top`).
 constexpr int PH_ANTERP = 1, PH_DOWN = 2, PH_C2P_ONLY = 4, PH_C2P = 8, PH_UP = PH_ANTERP | PH_C2P;
 
-// c2p into the level-l parents: transform every F_out child (level l+1) in parallel
-// into scratch (the plane-wave buffer, unused until prox2pw), then add per parent.
+// c2p into the level-l parents (k_c2p_grp: parent groups, MT parent rows per CTA)
+template <int P>
+constexpr int grp_mt() { return P <= 9 ? 9 : (P <= 18 ? 6 : 4); }
 template <int P>
 static void run_c2p_level(dmk_plan_s* PL, const DevTree& dt, int l) {
-  constexpr int P3 = P * P * P;
+  constexpr int MT = grp_mt<P>();
+  using G = GrpCfg<P, MT>;
   cudaStream_t s = PL->stream;
   const auto& th = PL->th;
   const int64_t a = th.fout_off[l], b = th.fout_off[l + 1];
   const int64_t ca = th.fout_off[l + 1], cb = th.fout_off[l + 2];
   if (b <= a || cb <= ca) return;
-  if ((size_t)(cb - ca) * P3 > PL->phi.n) fail(DMK_ERR_STATE, "c2p scratch too small");
-  const size_t sm = sizeof(double) * (P3 + 2 * P * P);
-  set_smem(k_c2p_child<P>, sm);
-  k_c2p_child<P><<<(int)(cb - ca), P * P, sm, s>>>(dt, PL->fout_list.p + ca, ca, PL->tab->dA, PL->mom.p, PL->phi.p);
-  DMK_LAUNCH_CHECK();
-  k_c2p_sum<P><<<(int)(b - a), 256, 0, s>>>(dt, PL->fout_list.p + a, ca, PL->phi.p, PL->mom.p);
+  set_smem(k_c2p_grp<P, MT>, G::smem_c2p);
+  dim3 grid((unsigned)(b - a), G::NTILE);
+  k_c2p_grp<P, MT><<<grid, 256, G::smem_c2p, s>>>(dt, PL->fout_list.p + a, PL->tab->dA, PL->mom.p);
   DMK_LAUNCH_CHECK();
 }
 
@@ -1387,12 +1464,16 @@ static void run_eval(dmk_plan_s* PL, int phase = PH_UP | PH_DOWN, int top = 0) {
       if (PL->nexp > 1) {
         if constexpr (P <= 18) {
           // parent-group translation (k_pwshift) into T, then the back transforms
+          tm.end();
+          tm.begin("pwshift");
           if (PL->nfout > 0) {
             dim3 grid((unsigned)PL->nfout, PWS_GY);
             k_pwshift<H><<<grid, PWS_NT, 0, s>>>(dt, PL->fout_list.p, reinterpret_cast<const float*>(Fp),
                                                   PL->phi_size0, PL->phi_size1, T.dW, T.wstride, PL->pwt.p);
             DMK_LAUNCH_CHECK();
           }
+          tm.end();
+          tm.begin("pw2poly");
           set_smem(k_pwlocal<P, H, AC, false, true>, K1::smem);
           k_pwlocal<P, H, AC, false, true><<<(int)(PL->nexp - 1), K1::NT, K1::smem, s>>>(
               dt, PL->exp_list.p + 1, T.dGr1, T.dW, T.wstride, Fp, PL->phi_size0, PL->phi_size1, PL->lam.p,
@@ -1407,11 +1488,16 @@ static void run_eval(dmk_plan_s* PL, int phase = PH_UP | PH_DOWN, int top = 0) {
     tm.end();
     tm.begin("p2c");
     {
-      size_t sm = sizeof(double) * (P3 + 2 * P * P);
-      set_smem(k_p2c<P>, sm);
+      // parents at level l-1 push their local expansions into their level-l children
+      constexpr int MT = grp_mt<P>();
+      using G = GrpCfg<P, MT>;
+      set_smem(k_p2c_grp<P, MT>, G::smem_p2c);
       for (int l = 1; l < nl; ++l) {
-        int64_t a = th.exp_off[l], b = th.exp_off[l + 1];
-        if (b > a) { k_p2c<P><<<(int)(b - a), P * P, sm, s>>>(dt, PL->exp_list.p + a, T.dA, PL->lam.p); DMK_LAUNCH_CHECK(); }
+        const int64_t a = th.exp_off[l - 1], b = th.exp_off[l];
+        if (b <= a || th.exp_off[l + 1] <= th.exp_off[l]) continue;
+        dim3 grid((unsigned)(b - a), G::NTILE);
+        k_p2c_grp<P, MT><<<grid, 256, G::smem_p2c, s>>>(dt, PL->exp_list.p + a, T.dA, PL->lam.p);
+        DMK_LAUNCH_CHECK();
       }
     }
     tm.end();
