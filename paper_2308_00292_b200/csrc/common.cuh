@@ -141,6 +141,7 @@ struct dmk_plan_s {
   // fp32 P2P tier (p <= 18): leaf-local double-single source records, Morton order:
   // (x, y, z, rho) high parts and (x, y, z, 0) low parts
   dmk::DevBuf<float4> xl4, xl4lo;
+  dmk::DevBuf<float4> box_c4;       // 3D: box centre and side in fp32 (exact, dyadic)
   // anterpolation / evaluation work: box ids
   dmk::DevBuf<int32_t> anterp_list, eval_list;
   int64_t nanterp = 0, neval = 0;

@@ -1257,8 +1257,9 @@ __device__ __forceinline__ void two_sum(float a, float b, float& s, float& e) {
 template <int K, int KER>
 __global__ void __launch_bounds__(128) k_p2p32(DevTree t, const int32_t* __restrict__ items, int64_t nitems,
                                                const int32_t* __restrict__ doff, const int32_t* __restrict__ dlist,
-                                               const float4* __restrict__ src, const float4* __restrict__ srclo,
-                                               ResPoly rp, const double* __restrict__ lvpoly, float lam,
+                                               const float4* __restrict__ boxc, const float4* __restrict__ src,
+                                               const float4* __restrict__ srclo, ResPoly rp,
+                                               const double* __restrict__ lvpoly, float lam,
                                                double* __restrict__ unear) {
   __shared__ float4 ssrc[4][32], slo[4][32];
   __shared__ double red[4][32];
@@ -1271,10 +1272,7 @@ __global__ void __launch_bounds__(128) k_p2p32(DevTree t, const int32_t* __restr
   // f = 32/nt lane groups: lane = target + nt * phase, phase strides the sources
   const int f = 32 / nt, tj = lane % nt, ph = lane / nt;
   const float4 tp = src[t0 + tj], tl = srclo[t0 + tj];
-  const uint64_t cB = t.code[B];
-  const int LB = t.level[B];
-  const float bx = (float)compact3d(cB >> 2) + 0.5f, by = (float)compact3d(cB >> 1) + 0.5f,
-              bz = (float)compact3d(cB) + 0.5f;
+  const float4 cB = boxc[B];
   float a[K + 1];
   if (KER == KER_LAPLACE) {
 #pragma unroll
@@ -1283,19 +1281,19 @@ __global__ void __launch_bounds__(128) k_p2p32(DevTree t, const int32_t* __restr
   double acc = 0.0;
   for (int e = doff[B]; e < doff[B + 1]; ++e) {
     const int S = dlist[e];
-    const int L = t.level[S];
-    const uint64_t cS = t.code[S];
+    const float4 cS = boxc[S];   // centre and side 2^-L (fp32, exact)
     // c_T - c_S, exact: both are dyadic with <= 22 significant bits
-    const float sT = ldexpf(1.0f, -LB), sS = ldexpf(1.0f, -L);
     float xt, yt, zt, xe, ye, ze;
-    two_sum(tp.x, bx * sT - ((float)compact3d(cS >> 2) + 0.5f) * sS, xt, xe);
-    two_sum(tp.y, by * sT - ((float)compact3d(cS >> 1) + 0.5f) * sS, yt, ye);
-    two_sum(tp.z, bz * sT - ((float)compact3d(cS) + 0.5f) * sS, zt, ze);
+    two_sum(tp.x, cB.x - cS.x, xt, xe);
+    two_sum(tp.y, cB.y - cS.y, yt, ye);
+    two_sum(tp.z, cB.z - cS.z, zt, ze);
     xe += tl.x;
     ye += tl.y;
     ze += tl.z;
-    const float irl = ldexpf(1.0f, L), two_irl2 = ldexpf(2.0f, 2 * L), rl2 = ldexpf(1.0f, -2 * L);
+    const float irl = __int_as_float(0x7F000000 - __float_as_int(cS.w));   // 2^L
+    const float two_irl2 = 2.0f * irl * irl, rl2 = cS.w * cS.w;
     if (KER == KER_YUKAWA) {
+      const int L = t.level[S];
 #pragma unroll
       for (int j = 0; j <= K; ++j) a[j] = (float)__ldg(lvpoly + L * (K + 1) + j);
     }
@@ -1553,7 +1551,7 @@ static void run_p2p32_deg(dmk_plan_s* PL, const ResPoly& rp, int K, cudaStream_t
 #define DMK_P2P_CASE(KK)                                                                                   \
   case KK:                                                                                                 \
     k_p2p32<KK, KER><<<nb, 128, 0, st>>>(dt, PL->p2p_items.p, PL->np2p, PL->dlist_off.p, PL->dlist.p,      \
-                                         PL->xl4.p, PL->xl4lo.p, rp, T.dRespoly, (float)T.lam, PL->unear.p);            \
+                                         PL->box_c4.p, PL->xl4.p, PL->xl4lo.p, rp, T.dRespoly, (float)T.lam, PL->unear.p);            \
     break;
   switch (K) {
     DMK_P2P_CASE(4) DMK_P2P_CASE(6) DMK_P2P_CASE(8) DMK_P2P_CASE(10) DMK_P2P_CASE(12) DMK_P2P_CASE(14)

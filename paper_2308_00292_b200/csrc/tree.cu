@@ -255,6 +255,103 @@ __global__ void k_child_cand(const uint64_t* __restrict__ Bp, int64_t nBp, const
   flags[t] = (nonempty || nonleaf) ? 1 : 0;
 }
 
+// ---- coarse levels as dense bitmaps (levels 0..LBC: 2^{D l} bits each), so that the
+// balance and the box sets of these levels need no sort and no host round trip.
+template <int D>
+struct Coarse {
+  static constexpr int LBC = D == 3 ? 7 : 10;   // 2^21 bits at the finest coarse level
+  int64_t woff[LBC + 2];                        // word offset of each level
+};
+__device__ __forceinline__ void bm_set(uint32_t* bm, uint64_t bit) { atomicOr(bm + (bit >> 5), 1u << (bit & 31)); }
+__device__ __forceinline__ bool bm_get(const uint32_t* bm, uint64_t bit) { return (bm[bit >> 5] >> (bit & 31)) & 1u; }
+
+// per point: non-empty boxes (NE) and big boxes (U, > ns points, level >= l0) of every
+// coarse level whose first point it is
+template <int D>
+__global__ void k_mark_coarse(const uint64_t* __restrict__ keys, int64_t n, int ns, int l0, Coarse<D> cs,
+                              uint32_t* bmU, uint32_t* bmNE) {
+  const int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (a >= n) return;
+  const uint64_t k = keys[a], kp = a > 0 ? keys[a - 1] : 0, kb = a + ns < n ? keys[a + ns] : 0;
+  for (int l = 0; l <= Coarse<D>::LBC; ++l) {
+    const int sh = D * (NBITS - l);
+    const uint64_t c = k >> sh;
+    if (a > 0 && (kp >> sh) == c) continue;   // not the first point of its level-l box
+    bm_set(bmNE + cs.woff[l], c);
+    if (l >= l0 && l < LMAX && a + ns < n && (kb >> sh) == c) bm_set(bmU + cs.woff[l], c);
+  }
+}
+// every bit of a level (forced refinement of the levels above min_level)
+__global__ void k_bm_all(uint32_t* bm, int64_t nbits) {
+  const int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (w * 32 >= nbits) return;
+  const int64_t r = nbits - w * 32;
+  bm[w] = r >= 32 ? 0xffffffffu : ((1u << r) - 1u);
+}
+// balance: the level-l boxes touching each level-(l+1) box of B_{l+1} (list or bitmap),
+// set in the level-l bitmap (R7, closed contact; see k_touch)
+template <int D>
+__device__ __forceinline__ void touch_set(uint64_t q, int l, uint32_t* out) {
+  constexpr int NCH = Dim<D>::NCH;
+  int x[3], c[3];
+  decode<D>(q, x);
+  const int n1 = 1 << l;
+  for (int o = 0; o < NCH; ++o) {
+    bool ok = true;
+    for (int d = 0; d < D; ++d) {
+      const int lo = (x[d] % 2 == 0) ? x[d] / 2 - 1 : x[d] / 2;
+      c[d] = lo + ((o >> (D - 1 - d)) & 1);
+      ok = ok && c[d] >= 0 && c[d] < n1;
+    }
+    if (ok) bm_set(out, encode<D>(c));
+  }
+}
+template <int D>
+__global__ void k_touch_list_bm(const uint64_t* __restrict__ Bq, int64_t nq, int l, uint32_t* out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < nq) touch_set<D>(Bq[i], l, out);
+}
+template <int D>
+__global__ void k_touch_bm(const uint32_t* __restrict__ in, int64_t nbits_in, int l, uint32_t* out) {
+  const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (b < nbits_in && bm_get(in, b)) touch_set<D>((uint64_t)b, l, out);
+}
+// E_l = B_l + non-empty children of B_{l-1}, word by word
+template <int D>
+__global__ void k_E_bm(const uint32_t* __restrict__ Bl, const uint32_t* __restrict__ NEl,
+                       const uint32_t* __restrict__ Bp, int64_t nbits, uint32_t* El) {
+  const int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (w * 32 >= nbits) return;
+  uint32_t e = Bl[w], ne = NEl[w], m = 0;
+  for (int i = 0; i < 32 && w * 32 + i < nbits; ++i)
+    if (bm_get(Bp, (uint64_t)(w * 32 + i) >> D)) m |= 1u << i;
+  El[w] = e | (ne & m);
+}
+__global__ void k_popc(const uint32_t* __restrict__ bm, int64_t nw, int32_t* cnt) {
+  const int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (w < nw) cnt[w] = __popc(bm[w]);
+}
+// codes of the set bits of one level (sorted), at exclusive-scan positions
+__global__ void k_bm_fill(const uint32_t* __restrict__ bm, const int32_t* __restrict__ pos, int64_t nw,
+                          uint64_t* out) {
+  const int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (w >= nw) return;
+  uint32_t x = bm[w];
+  int32_t p = pos[w] - pos[0];
+  while (x) {
+    const int b = __ffs(x) - 1;
+    out[p++] = (uint64_t)(w * 32 + b);
+    x &= x - 1;
+  }
+}
+// per-level totals of a scanned bitmap: tot[l] = pos[woff[l+1]] - pos[woff[l]] (pos has
+// one extra trailing entry)
+template <int D>
+__global__ void k_bm_totals(const int32_t* __restrict__ pos, Coarse<D> cs, int64_t base, int64_t* tot) {
+  const int l = threadIdx.x;
+  if (l <= Coarse<D>::LBC) tot[l] = pos[base + cs.woff[l + 1]] - pos[base + cs.woff[l]];
+}
+
 // out[i] = a[idx[i]], out[m + i] = b[idx[i]]: many scalar reads, one round trip
 __global__ void k_read_at(const int32_t* __restrict__ a, const int32_t* __restrict__ b,
                           const int64_t* __restrict__ idx, int m, int64_t* out) {
@@ -484,6 +581,16 @@ __global__ void k_leaf_local4(const uint64_t* code, const int32_t* level, const 
   }
 }
 
+// box centres and sizes in fp32 (exact: dyadic, level <= 20): (c_x, c_y, c_z, 2^-l)
+__global__ void k_box_c4(const uint64_t* code, const int32_t* level, int64_t nbox, float4* c4) {
+  const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (b >= nbox) return;
+  const uint64_t c = code[b];
+  const float s = ldexpf(1.0f, -level[b]);
+  c4[b] = make_float4(((float)compact3d(c >> 2) + 0.5f) * s, ((float)compact3d(c >> 1) + 0.5f) * s,
+                      ((float)compact3d(c) + 0.5f) * s, s);
+}
+
 // ---------------------------------------------------------------- host helpers
 int64_t select_flagged(cudaStream_t s, const uint64_t* in, const uint8_t* flags, int64_t n,
                        DevBuf<uint64_t>& out) {
@@ -646,7 +753,20 @@ static void build_tree_d(dmk_plan_s* P, const double* dpts) {
   }
 
   mark("sort");
-  // ---- unbalanced refinement: U[l] = level-l boxes with > ns points
+  // ---- unbalanced refinement: U[l] = level-l boxes with > ns points.  Coarse levels
+  // (<= LBC) are dense bitmaps filled in one pass over the keys; finer levels are
+  // selected as sorted lists.
+  using CS = Coarse<D>;
+  constexpr int LBC = CS::LBC;
+  CS cs;
+  cs.woff[0] = 0;
+  for (int l = 0; l <= LBC; ++l) cs.woff[l + 1] = cs.woff[l] + std::max<int64_t>(1, ((int64_t)1 << (D * l)) / 32);
+  const int64_t W = cs.woff[LBC + 1];
+  auto nbits = [](int l) { return (int64_t)1 << (D * l); };
+  DevBuf<uint32_t> bmbuf;   // [U | NE | B | E], W words each
+  bmbuf.alloc(4 * W, s);
+  uint32_t *bmU = bmbuf.p, *bmNE = bmU + W, *bmB = bmNE + W, *bmE = bmB + W;
+  DMK_CUDA(cudaMemsetAsync(bmbuf.p, 0, 4 * W * sizeof(uint32_t), s));
   std::vector<DevBuf<uint64_t>> U(LMAX);
   std::vector<int64_t> nU(LMAX, 0);
   int ltop = -1;
@@ -657,35 +777,42 @@ static void build_tree_d(dmk_plan_s* P, const double* dpts) {
     DMK_CUDA(cudaMemsetAsync(dcnt.p, 0, LMAX * sizeof(unsigned long long), s));
     k_count_big<D><<<std::min(nblk(n), 4 * 148), TPB, 0, s>>>(P->keys.p, n, ns, P->min_level, dcnt.p);
     DMK_LAUNCH_CHECK();
+    k_mark_coarse<D><<<nblk(n), TPB, 0, s>>>(P->keys.p, n, ns, P->min_level, cs, bmU, bmNE);
+    DMK_LAUNCH_CHECK();
+    for (int l = 0; l < P->min_level && l <= LBC; ++l) {
+      k_bm_all<<<nblk(nbits(l) / 32 + 1), TPB, 0, s>>>(bmU + cs.woff[l], nbits(l));
+      DMK_LAUNCH_CHECK();
+    }
     unsigned long long hc[LMAX];
     DMK_CUDA(cudaMemcpyAsync(hc, dcnt.p, sizeof(hc), cudaMemcpyDeviceToHost, s));
     DMK_CUDA(cudaStreamSynchronize(s));
     DevBuf<uint64_t> codes;
     DevBuf<uint8_t> flags;
     DevBuf<int64_t> nsel;
-    codes.alloc(n, s);
-    flags.alloc(n, s);
-    nsel.alloc(1, s);
     for (int l = 0; l < LMAX; ++l) {
       if (l < P->min_level) {
         // forced refinement (distributed plans): every box of the levels above min_level
         // exists and is refined, empty or not, so that all ranks share the coarse tree
         nU[l] = (int64_t)1 << (D * l);
-        U[l].alloc(nU[l], s);
-        k_iota_u64<<<nblk(nU[l]), TPB, 0, s>>>(U[l].p, nU[l]);
-        DMK_LAUNCH_CHECK();
+        if (l > LBC) fail(DMK_ERR_ARG, "min_level beyond the coarse levels");
         ltop = l;
         continue;
       }
       nU[l] = (int64_t)hc[l];
       if (nU[l] == 0) break;
+      ltop = l;
+      if (l <= LBC) continue;   // bitmap
+      if (!codes.p) {
+        codes.alloc(n, s);
+        flags.alloc(n, s);
+        nsel.alloc(1, s);
+      }
       k_big<D><<<nblk(n), TPB, 0, s>>>(P->keys.p, n, l, ns, codes.p, flags.p);
       DMK_LAUNCH_CHECK();
       U[l].alloc(nU[l], s);
       cub_run(s, [&](void* t, size_t& b) {
         return cub::DeviceSelect::Flagged(t, b, codes.p, flags.p, U[l].p, nsel.p, n, s);
       });
-      ltop = l;
     }
   }
 
@@ -693,11 +820,14 @@ static void build_tree_d(dmk_plan_s* P, const double* dpts) {
   // ---- 2:1 balance, bottom-up: B[l] = U[l] + level-l boxes touching B[l+1]
   std::vector<DevBuf<uint64_t>> B(ltop + 1);
   std::vector<int64_t> nB(ltop + 1, 0);
-  if (ltop >= 0) {
+  DMK_CUDA(cudaMemcpyAsync(bmB, bmU, W * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));   // B >= U
+  if (ltop > LBC) {
     B[ltop].alloc(nU[ltop], s);
     DMK_CUDA(cudaMemcpyAsync(B[ltop].p, U[ltop].p, nU[ltop] * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
     nB[ltop] = nU[ltop];
-    for (int l = ltop - 1; l >= 0; --l) {
+  }
+  for (int l = ltop - 1; l >= 0; --l) {
+    if (l > LBC) {
       int64_t nc = nU[l] + NCH * nB[l + 1];
       DevBuf<uint64_t> cand;
       cand.alloc(nc, s);
@@ -707,6 +837,14 @@ static void build_tree_d(dmk_plan_s* P, const double* dpts) {
                                                        (uint64_t)1 << (D * l));
       DMK_LAUNCH_CHECK();
       nB[l] = sort_unique_drop(s, cand.p, nc, D * l, B[l]);
+    } else if (l + 1 > LBC) {
+      if (nB[l + 1]) {
+        k_touch_list_bm<D><<<nblk(nB[l + 1]), TPB, 0, s>>>(B[l + 1].p, nB[l + 1], l, bmB + cs.woff[l]);
+        DMK_LAUNCH_CHECK();
+      }
+    } else {
+      k_touch_bm<D><<<nblk(nbits(l + 1)), TPB, 0, s>>>(bmB + cs.woff[l + 1], nbits(l + 1), l, bmB + cs.woff[l]);
+      DMK_LAUNCH_CHECK();
     }
   }
   const int nlevels = ltop + 2;
@@ -716,10 +854,48 @@ static void build_tree_d(dmk_plan_s* P, const double* dpts) {
   // ---- box sets per level: E_l = B_l + non-empty children of B_{l-1}
   std::vector<DevBuf<uint64_t>> E(nlevels);
   std::vector<int64_t> nE(nlevels, 0);
-  E[0].alloc(1, s);
-  DMK_CUDA(cudaMemsetAsync(E[0].p, 0, sizeof(uint64_t), s));
-  nE[0] = 1;
-  for (int l = 1; l < nlevels; ++l) {
+  {
+    // coarse levels: E bitmaps, then all coarse B and E lists from one scan and one
+    // round trip for their sizes
+    const uint32_t one = 1u;
+    DMK_CUDA(cudaMemcpyAsync(bmE, &one, sizeof(uint32_t), cudaMemcpyHostToDevice, s));   // E_0 = {root}
+    const int lc = std::min(LBC, nlevels - 1);
+    for (int l = 1; l <= lc; ++l) {
+      k_E_bm<D><<<nblk(nbits(l) / 32 + 1), TPB, 0, s>>>(bmB + cs.woff[l], bmNE + cs.woff[l], bmB + cs.woff[l - 1],
+                                                       nbits(l), bmE + cs.woff[l]);
+      DMK_LAUNCH_CHECK();
+    }
+    DevBuf<int32_t> cnt, pos;
+    DevBuf<int64_t> tot;
+    cnt.alloc(2 * W + 1, s);
+    pos.alloc(2 * W + 1, s);
+    tot.alloc(2 * (LBC + 1), s);
+    DMK_CUDA(cudaMemsetAsync(cnt.p + 2 * W, 0, sizeof(int32_t), s));
+    k_popc<<<nblk(2 * W), TPB, 0, s>>>(bmB, 2 * W, cnt.p);   // B and E are adjacent
+    DMK_LAUNCH_CHECK();
+    exclusive_scan(s, cnt.p, pos.p, 2 * W + 1);
+    k_bm_totals<D><<<1, 32, 0, s>>>(pos.p, cs, 0, tot.p);
+    k_bm_totals<D><<<1, 32, 0, s>>>(pos.p, cs, W, tot.p + LBC + 1);
+    DMK_LAUNCH_CHECK();
+    int64_t ht[2 * (LBC + 1)];
+    DMK_CUDA(cudaMemcpyAsync(ht, tot.p, sizeof(ht), cudaMemcpyDeviceToHost, s));
+    DMK_CUDA(cudaStreamSynchronize(s));
+    for (int l = 0; l <= std::min(LBC, ltop); ++l) {
+      nB[l] = ht[l];
+      B[l].alloc(nB[l] ? nB[l] : 1, s);
+      const int64_t nw = cs.woff[l + 1] - cs.woff[l];
+      k_bm_fill<<<nblk(nw), TPB, 0, s>>>(bmB + cs.woff[l], pos.p + cs.woff[l], nw, B[l].p);
+      DMK_LAUNCH_CHECK();
+    }
+    for (int l = 0; l <= lc; ++l) {
+      nE[l] = ht[LBC + 1 + l];
+      E[l].alloc(nE[l] ? nE[l] : 1, s);
+      const int64_t nw = cs.woff[l + 1] - cs.woff[l];
+      k_bm_fill<<<nblk(nw), TPB, 0, s>>>(bmE + cs.woff[l], pos.p + W + cs.woff[l], nw, E[l].p);
+      DMK_LAUNCH_CHECK();
+    }
+  }
+  for (int l = LBC + 1; l < nlevels; ++l) {
     const int64_t nc = (int64_t)NCH * nB[l - 1];
     const int64_t nb_l = (l <= ltop) ? nB[l] : 0;
     DevBuf<uint64_t> codes;
@@ -890,6 +1066,9 @@ static void build_tree_d(dmk_plan_s* P, const double* dpts) {
     DMK_LAUNCH_CHECK();
   }
   if (D == 3) {
+    P->box_c4.alloc(nbox, s);
+    k_box_c4<<<nblk(nbox), TPB, 0, s>>>(P->box_code.p, P->box_level.p, nbox, P->box_c4.p);
+    DMK_LAUNCH_CHECK();
     P->xl4.alloc(n ? n : 1, s);
     P->xl4lo.alloc(n ? n : 1, s);
     k_leaf_local4<<<nblk(32 * nbox), TPB, 0, s>>>(P->box_code.p, P->box_level.p, P->box_start.p, P->box_end.p,
