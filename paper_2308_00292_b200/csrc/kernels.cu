@@ -133,6 +133,172 @@ __global__ void __launch_bounds__(Cfg<P>::TA * Cfg<P>::TB)
     for (int k = 0; k < C::RB; ++k) out[(ta + i * C::TA) * P + tb + k * C::TB] = acc[i][k];
 }
 
+// ---- fp32 tier (reading R16, p <= 18): anterpolation and evaluation on the FP32 pipes
+// (2x the fp64 rate).  Chebyshev values are computed in fp64 and rounded once; partial
+// sums run in fp32 over at most 32 points (anterpolation) or one Chebyshev index pair
+// (evaluation, 2 x p terms), then are added in fp64, so the relative error of a moment
+// or a potential stays at a few fp32 roundings (~2e-7), below the fp32 rounding of the
+// stored plane waves that R16 already accepts.
+//
+// k_anterp32: mu[n1][n2][n3] = sum_j (rho_j Tx_j[n1] Ty_j[n2]) Tz_j[n3]; thread (n1, n2)
+// keeps the p values over n3.
+template <int P>
+struct Ant32 {
+  static constexpr int P2 = P * P, NT = (P2 + 31) / 32 * 32, CH = 128, PZ = (P + 3) & ~3;
+};
+template <int P>
+__global__ void __launch_bounds__(Ant32<P>::NT, 2) k_anterp32(DevTree t, const int32_t* __restrict__ boxes,
+                                                           const double* __restrict__ q, double* __restrict__ mom) {
+  using A_ = Ant32<P>;
+  constexpr int P2 = A_::P2, NT = A_::NT, CH = A_::CH, PZ = A_::PZ;
+  __shared__ float sx[CH][P], sy[CH][P];
+  __shared__ __align__(16) float sz[CH][PZ];
+  __shared__ int2 rg[8];
+  __shared__ int nr_s, tot_s;
+  const int b = boxes[blockIdx.x], tid = threadIdx.x;
+  if (tid == 0) {
+    nr_s = box_ranges<false>(t, b, rg);
+    int tot = 0;
+    for (int r = 0; r < nr_s; ++r) tot += rg[r].y - rg[r].x;
+    tot_s = tot;
+  }
+  __syncthreads();
+  const int nr = nr_s, tot = tot_s;
+  if (tot == 0) return;   // moments were zeroed by the caller
+  double cen[3], ih;
+  box_geom(t.code[b], t.level[b], cen, ih);
+  const int n1 = tid / P, n2 = tid % P;
+  const bool own = tid < P2;
+  double acc[P];
+#pragma unroll
+  for (int n = 0; n < P; ++n) acc[n] = 0.0;
+  for (int c0 = 0; c0 < tot; c0 += CH) {
+    const int nc = min(CH, tot - c0);
+    for (int w = tid; w < CH * 3; w += NT) {
+      const int j = w / 3, d = w % 3;
+      double T[P];
+      if (j < nc) {
+        const int pi = range_point(rg, nr, c0 + j);
+        const double x = (d == 0 ? t.xs[pi] : d == 1 ? t.ys[pi] : t.zs[pi]);
+        cheb_vec((x - cen[d]) * ih, T, P, d == 0 ? q[pi] : 1.0);
+      } else {
+#pragma unroll
+        for (int n = 0; n < P; ++n) T[n] = 0.0;
+      }
+      if (d == 2) {
+#pragma unroll
+        for (int n = 0; n < PZ; ++n) sz[j][n] = n < P ? (float)T[n] : 0.0f;
+      } else {
+        float* dst = d == 0 ? sx[j] : sy[j];
+#pragma unroll
+        for (int n = 0; n < P; ++n) dst[n] = (float)T[n];
+      }
+    }
+    __syncthreads();
+    if (own) {
+      for (int j0 = 0; j0 < nc; j0 += 32) {   // fp32 partial sums over <= 32 points
+        float a32[PZ];
+#pragma unroll
+        for (int n = 0; n < PZ; ++n) a32[n] = 0.0f;
+        const int j1 = min(nc, j0 + 32);
+        for (int j = j0; j < j1; ++j) {
+          const float wv = sx[j][n1] * sy[j][n2];
+          const float4* zr = reinterpret_cast<const float4*>(sz[j]);
+#pragma unroll
+          for (int v = 0; v < PZ / 4; ++v) {
+            const float4 z = zr[v];
+            a32[4 * v] = fmaf(wv, z.x, a32[4 * v]);
+            a32[4 * v + 1] = fmaf(wv, z.y, a32[4 * v + 1]);
+            a32[4 * v + 2] = fmaf(wv, z.z, a32[4 * v + 2]);
+            a32[4 * v + 3] = fmaf(wv, z.w, a32[4 * v + 3]);
+          }
+        }
+#pragma unroll
+        for (int n = 0; n < P; ++n) acc[n] += (double)a32[n];
+      }
+    }
+    __syncthreads();
+  }
+  if (own) {
+    double* out = mom + (size_t)t.fout_rank[b] * P * P2 + (size_t)tid * P;
+#pragma unroll
+    for (int n = 0; n < P; ++n) out[n] = acc[n];
+  }
+}
+
+// k_eval32: u_i = sum_n1 T_n1(x_i) sum_n2 T_n2(y_i) sum_n3 Lambda[n1 n2 n3] T_n3(z_i), one
+// target per thread, Lambda in shared memory (fp32, broadcast reads), T_n1 by the
+// recurrence in fp64, the n1 sum in fp64.
+template <int P>
+struct Ev32 {
+  static constexpr int NT = 128, PZ = (P + 3) & ~3;
+  static constexpr size_t smem = sizeof(float) * (size_t)P * P * PZ;
+};
+template <int P>
+__global__ void __launch_bounds__(Ev32<P>::NT) k_eval32(DevTree t, const int32_t* __restrict__ boxes,
+                                                        const double* __restrict__ lam, double* __restrict__ ufar) {
+  using E = Ev32<P>;
+  constexpr int NT = E::NT, PZ = E::PZ, P2 = P * P;
+  extern __shared__ float4 sl4[];   // [P2][PZ/4]
+  float* sl = reinterpret_cast<float*>(sl4);
+  __shared__ int2 rg[8];
+  __shared__ int nr_s, tot_s;
+  const int b = boxes[blockIdx.x], tid = threadIdx.x;
+  if (tid == 0) {
+    nr_s = box_ranges<true>(t, b, rg);
+    int tot = 0;
+    for (int r = 0; r < nr_s; ++r) tot += rg[r].y - rg[r].x;
+    tot_s = tot;
+  }
+  __syncthreads();
+  const int nr = nr_s, tot = tot_s;
+  if (tot == 0) return;
+  const double* src = lam + (size_t)t.exp_rank[b] * P * P2;
+  for (int i = tid; i < P2 * PZ; i += NT) {
+    const int r = i / PZ, c = i - r * PZ;
+    sl[i] = c < P ? (float)src[r * P + c] : 0.0f;
+  }
+  double cen[3], ih;
+  box_geom(t.code[b], t.level[b], cen, ih);
+  __syncthreads();
+  for (int k = tid; k < tot; k += NT) {
+    const int pi = range_point(rg, nr, k);
+    const double x = (t.xs[pi] - cen[0]) * ih;
+    double ty[P], tz[P];
+    cheb_vec((t.ys[pi] - cen[1]) * ih, ty, P, 1.0);
+    cheb_vec((t.zs[pi] - cen[2]) * ih, tz, P, 1.0);
+    float fy[P], fz[PZ];
+#pragma unroll
+    for (int n = 0; n < P; ++n) fy[n] = (float)ty[n];
+#pragma unroll
+    for (int n = 0; n < PZ; ++n) fz[n] = n < P ? (float)tz[n] : 0.0f;
+    double u = 0.0, ta = 1.0, tb = x;   // T_n1(x), T_{n1+1}(x)
+#pragma unroll 1
+    for (int n1 = 0; n1 < P; ++n1) {
+      const float4* row = sl4 + (size_t)n1 * P * (PZ / 4);
+      float s1 = 0.0f;
+#pragma unroll
+      for (int n2 = 0; n2 < P; ++n2) {
+        float s = 0.0f;
+#pragma unroll
+        for (int v = 0; v < PZ / 4; ++v) {
+          const float4 l4 = row[n2 * (PZ / 4) + v];
+          s = fmaf(l4.x, fz[4 * v], s);
+          s = fmaf(l4.y, fz[4 * v + 1], s);
+          s = fmaf(l4.z, fz[4 * v + 2], s);
+          s = fmaf(l4.w, fz[4 * v + 3], s);
+        }
+        s1 = fmaf(s, fy[n2], s1);
+      }
+      u = fma((double)s1, ta, u);
+      const double tn = 2.0 * x * tb - ta;
+      ta = tb;
+      tb = tn;
+    }
+    ufar[pi] = u;
+  }
+}
+
 // ---------------------------------------------------------------- c2p / p2c
 // ---- c2p / p2c by parent groups on fp64 tensor cores (Lemmas 2.2-2.3).
 // The 8 children of a parent share the axis factors: with octant o = (o1 o2 o3),
@@ -1413,13 +1579,15 @@ static void run_eval(dmk_plan_s* PL, int phase = PH_UP | PH_DOWN, int top = 0) {
     // ---- Step 2: upward pass
     tm.begin("anterp");
     DMK_CUDA(cudaMemsetAsync(PL->mom.p, 0, PL->mom.bytes(), s));
-    {
-      size_t sm = AntMma<P>::smem;
-      set_smem(k_anterp_mma<P>, sm);
-      if (PL->nfout) {
+    if (PL->nfout) {
+      if constexpr (P <= 18) {   // fp32 tier (R16)
+        k_anterp32<P><<<(int)PL->nfout, Ant32<P>::NT, 0, s>>>(dt, PL->fout_list.p, PL->q.p, PL->mom.p);
+      } else {
+        size_t sm = AntMma<P>::smem;
+        set_smem(k_anterp_mma<P>, sm);
         k_anterp_mma<P><<<(int)PL->nfout, AntMma<P>::NW * 32, sm, s>>>(dt, PL->fout_list.p, PL->q.p, PL->mom.p);
-        DMK_LAUNCH_CHECK();
       }
+      DMK_LAUNCH_CHECK();
     }
     tm.end();
   }
@@ -1502,10 +1670,9 @@ static void run_eval(dmk_plan_s* PL, int phase = PH_UP | PH_DOWN, int top = 0) {
     tm.begin("eval");
     {
       if (PL->nexp) {
-        if constexpr (P <= 18) {
-          size_t sm = EvalPad<P>::smem;
-          set_smem(k_eval_pad<P>, sm);
-          k_eval_pad<P><<<(int)PL->nexp, 256, sm, s>>>(dt, PL->exp_list.p, PL->lam.p, PL->ufar.p);
+        if constexpr (P <= 18) {   // fp32 tier (R16)
+          set_smem(k_eval32<P>, Ev32<P>::smem);
+          k_eval32<P><<<(int)PL->nexp, Ev32<P>::NT, Ev32<P>::smem, s>>>(dt, PL->exp_list.p, PL->lam.p, PL->ufar.p);
         } else {
           size_t sm = EvalMma<P>::smem;
           set_smem(k_eval_mma<P>, sm);

@@ -82,7 +82,9 @@ def test_moments_match_oracle_proxies(case):
     for i in np.nonzero(T.fout)[0]:
         ref = cheb.apply3([Vt, Vt, Vt], st["proxy"][i])
         got = mom[fout[i]]
-        assert np.max(np.abs(got - ref)) <= 1e-11 * max(1.0, np.max(np.abs(ref)))
+        # p <= 18: fp32 anterpolation (reading R16): a few fp32 roundings, ~2e-7 relative
+        tol = 1e-11 if p >= 28 else 1e-6
+        assert np.max(np.abs(got - ref)) <= tol * max(1.0, np.max(np.abs(ref)))
 
 
 def phi_from_parity_split(F, nf):
@@ -118,7 +120,8 @@ def test_outgoing_matches_oracle(case):
         else:
             got = phi_from_parity_split(phi[s0 + (r - 1) * s1: s0 + r * s1], nf)
         ref = st["Phi"][i]
-        assert np.max(np.abs(got - ref)) <= (1e-11 if inf.p >= 28 else 2e-7) * np.max(np.abs(ref))
+        # p <= 18: fp32 moments (anterpolation) and fp32-stored plane waves (reading R16)
+        assert np.max(np.abs(got - ref)) <= fp_tol(inf.p) * np.max(np.abs(ref))
 
 
 def test_local_expansions_match_oracle(case):
@@ -241,5 +244,6 @@ def test_linearity():
     plan = dmk.dmk_plan(cuda(x), eps=1e-6, leaf_capacity=100)
     a, b, c = (plan.eval(cuda(v)).cpu().numpy() for v in (q1, q2, q1 + q2))
     plan.close()
-    # linear up to the rounding of the fp32-stored plane waves (reading R16, p = 18)
-    assert np.max(np.abs(a + b - c)) <= 1e-7 * np.max(np.abs(c))
+    # linear up to fp32 roundings (reading R16, p = 18: fp32 anterpolation, plane waves,
+    # translation, evaluation and P2P pairs, each a few 2^-24 relative)
+    assert np.max(np.abs(a + b - c)) <= 1e-6 * np.max(np.abs(c))
