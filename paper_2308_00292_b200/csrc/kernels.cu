@@ -820,6 +820,88 @@ __global__ void __launch_bounds__(PWS_NT, 3)
   }
 }
 
+// fp32 tier: T_pw2poly (Eqs. 3.43-3.44) of every non-root local box from the weighted
+// incoming expansion T[a][pi][b][c] written by k_pwshift, as three axis contractions
+// over the whole box (no slab chunking, two barriers): axis 3 rows (a, pi12, b) from
+// global memory into U[a][pi12][b][n3], axis 2 columns into V[a][pi1][n2][n3], axis 1
+// into Lambda[n1][n2][n3] (fp64, global).  The output index n of each axis picks the
+// input parity n mod 2, so output pairs (2k, 2k+1) take (Gr[2k][.], Gr[2k+1][.]) times
+// (parity-0, parity-1) inputs: one packed FFMA2 per input index.
+template <int P, int H>
+struct Pw2p {
+  static constexpr int NT = 256, PH = (P + 1) / 2, PE = 2 * PH, HH = (H + 1) & ~1;
+  static constexpr int NU = H * 4 * H * PE, NV = H * 2 * PE * P;
+  static constexpr size_t smem = sizeof(float2) * (size_t)H * PH + sizeof(float) * (size_t)(NU + NV);
+};
+template <int P, int H>
+__global__ void __launch_bounds__(Pw2p<P, H>::NT, 2)
+    k_pw2poly32(DevTree t, const int32_t* __restrict__ boxes, const double* __restrict__ Gr,
+                const float* __restrict__ Tin, double* __restrict__ lam) {
+  using C = Pw2p<P, H>;
+  constexpr int NT = C::NT, PH = C::PH, PE = C::PE, HH = C::HH, HSQ = H * H, SLAB = 8 * HSQ, P2 = P * P;
+  extern __shared__ float2 smp[];
+  float2* GP = smp;                                        // [c][k] = (Gr[2k][c], Gr[2k+1][c])
+  float* U = reinterpret_cast<float*>(GP + H * PH);        // [a][pi12][b][PE]
+  float* V = U + C::NU;                                    // [a][pi1][PE][P]
+  const int b = boxes[blockIdx.x], tid = threadIdx.x;
+  for (int i = tid; i < H * PH; i += NT) {
+    const int c = i / PH, k = i - c * PH;
+    GP[i] = make_float2((float)Gr[(2 * k) * HH + c], 2 * k + 1 < P ? (float)Gr[(2 * k + 1) * HH + c] : 0.0f);
+  }
+  __syncthreads();
+  const float* tb = Tin + (size_t)t.exp_rank[b] * H * SLAB;
+  // axis 3: U[a][g][bb][n3] = sum_c Gr[n3][c] T[a][2 g + n3%2][bb][c]
+  for (int u = tid; u < H * 4 * H; u += NT) {
+    const int a = u / (4 * H), g = (u / H) % 4, bb = u % H;
+    const float* r0 = tb + (size_t)a * SLAB + (2 * g) * HSQ + bb * H;
+    float2 tv[H];
+#pragma unroll
+    for (int c = 0; c < H; ++c) tv[c] = make_float2(__ldg(r0 + c), __ldg(r0 + HSQ + c));
+    float2* dst = reinterpret_cast<float2*>(U + (size_t)u * PE);
+#pragma unroll 1
+    for (int k = 0; k < PH; ++k) {
+      float2 acc = make_float2(0.0f, 0.0f);
+#pragma unroll
+      for (int c = 0; c < H; ++c) acc = __ffma2_rn(GP[c * PH + k], tv[c], acc);
+      dst[k] = acc;
+    }
+  }
+  __syncthreads();
+  // axis 2: V[a][p1][n2][n3] = sum_bb Gr[n2][bb] U[a][2 p1 + n2%2][bb][n3]
+  for (int u = tid; u < H * 2 * P; u += NT) {
+    const int a = u / (2 * P), p1 = (u / P) % 2, n3 = u % P;
+    const float* c0 = U + ((size_t)(a * 4 + 2 * p1) * H) * PE + n3;
+    float2 uv[H];
+#pragma unroll
+    for (int bb = 0; bb < H; ++bb) uv[bb] = make_float2(c0[bb * PE], c0[(H + bb) * PE]);
+    float* dst = V + ((size_t)(a * 2 + p1) * PE) * P + n3;
+#pragma unroll 1
+    for (int k = 0; k < PH; ++k) {
+      float2 acc = make_float2(0.0f, 0.0f);
+#pragma unroll
+      for (int bb = 0; bb < H; ++bb) acc = __ffma2_rn(GP[bb * PH + k], uv[bb], acc);
+      dst[(2 * k) * P] = acc.x;
+      dst[(2 * k + 1) * P] = acc.y;
+    }
+  }
+  __syncthreads();
+  // axis 1: Lambda[n1][n2][n3] = sum_a Gr[n1][a] V[a][n1%2][n2][n3]
+  double* out = lam + (size_t)t.exp_rank[b] * P * P2;
+  for (int u = tid; u < P2; u += NT) {
+    float2 vv[H];
+#pragma unroll
+    for (int a = 0; a < H; ++a) vv[a] = make_float2(V[(size_t)(a * 2) * PE * P + u], V[(size_t)(a * 2 + 1) * PE * P + u]);
+#pragma unroll 1
+    for (int k = 0; k < PH; ++k) {
+      float2 acc = make_float2(0.0f, 0.0f);
+#pragma unroll
+      for (int a = 0; a < H; ++a) acc = __ffma2_rn(GP[a * PH + k], vv[a], acc);
+      out[(size_t)(2 * k) * P2 + u] = (double)acc.x;
+      if (2 * k + 1 < P) out[(size_t)(2 * k + 1) * P2 + u] = (double)acc.y;
+    }
+  }
+}
+
 // Incoming expansion + conversion to Chebyshev coefficients of one local-expansion box
 // (Eq. 3.39 fused with Eqs. 3.43-3.44): per chunk of AC slabs a, the 27-colleague
 // translation (separable rotations: three nested 3-point sums), the weights, then the
@@ -1713,10 +1795,10 @@ static void run_eval(dmk_plan_s* PL, int phase = PH_UP | PH_DOWN, int top = 0) {
           }
           tm.end();
           tm.begin("pw2poly");
-          set_smem(k_pwlocal<P, H, AC, false, true>, K1::smem);
-          k_pwlocal<P, H, AC, false, true><<<(int)(PL->nexp - 1), K1::NT, K1::smem, s>>>(
-              dt, PL->exp_list.p + 1, T.dGr1, T.dW, T.wstride, Fp, PL->phi_size0, PL->phi_size1, PL->lam.p,
-              PL->pwt.p);
+          using K2 = Pw2p<P, H>;
+          set_smem(k_pw2poly32<P, H>, K2::smem);
+          k_pw2poly32<P, H><<<(int)(PL->nexp - 1), K2::NT, K2::smem, s>>>(dt, PL->exp_list.p + 1, T.dGr1, PL->pwt.p,
+                                                                         PL->lam.p);
         } else {
           k_pwlocal<P, H, AC, false><<<(int)(PL->nexp - 1), K1::NT, K1::smem, s>>>(
               dt, PL->exp_list.p + 1, T.dGr1, T.dW, T.wstride, Fp, PL->phi_size0, PL->phi_size1, PL->lam.p);
