@@ -655,6 +655,95 @@ __global__ void __launch_bounds__(256) k_prox2pw(DevTree t, const int32_t* __res
   }
 }
 
+// fp32 tier: T_prox2pw (Eq. 3.42) of every F_out box as three whole-box axis
+// contractions with packed FFMA2: an axis contraction over n of one parity class is a
+// sum over the input pairs (2j, 2j+1), and (Qr[m][2j], Qr[m][2j+1]) x (v[2j], v[2j+1])
+// accumulates the parity-0 and parity-1 outputs in the two halves of one register:
+//   axis 3: X1[n1][n2][c]  = (sum_{n3 even}, sum_{n3 odd}) Qr[c][n3] mu[n1][n2][n3]
+//   axis 2: X2[n1][pi3][b][c] = (pi2 = 0, 1) halves over n2
+//   axis 1: F[a][pi][b][c] (fp32, global) over n1.
+template <int P, int H>
+struct Px32 {
+  static constexpr int NT = 256, PH = (P + 1) / 2, PP = 2 * PH;
+  static constexpr size_t smem =
+      sizeof(float2) * ((size_t)H * PH + (size_t)P * P * H + (size_t)P * 2 * H * H);
+};
+template <int P, int H>
+__global__ void __launch_bounds__(Px32<P, H>::NT) k_prox2pw32(DevTree t, const int32_t* __restrict__ boxes,
+                                                              const double* __restrict__ Qr,
+                                                              const double* __restrict__ mom, float* __restrict__ F,
+                                                              size_t base, size_t stride) {
+  using C = Px32<P, H>;
+  constexpr int NT = C::NT, PH = C::PH, PP = C::PP, HSQ = H * H, P2 = P * P;
+  extern __shared__ float2 smx[];
+  float2* QP = smx;              // [m][j] = (Qr[m][2j], Qr[m][2j+1])
+  float2* X1 = QP + H * PH;      // [n1][n2][c]      (pi3 halves)
+  float2* X2 = X1 + P2 * H;      // [n1][pi3][b][c]  (pi2 halves)
+  const int b = boxes[blockIdx.x], tid = threadIdx.x;
+  const int r = t.fout_rank[b];
+  const double* mu = mom + (size_t)r * P * P2;
+  float* out = F + base + (size_t)(r == 0 ? 0 : r - 1) * stride;
+  for (int i = tid; i < H * PH; i += NT) {
+    const int m = i / PH, j = i - m * PH;
+    QP[i] = make_float2((float)Qr[m * PP + 2 * j], (float)Qr[m * PP + 2 * j + 1]);   // Qr rows are zero-padded
+  }
+  __syncthreads();
+  // axis 3: one (n1, n2) row of mu per unit
+  for (int u = tid; u < P2; u += NT) {
+    float2 v[PH];
+#pragma unroll
+    for (int j = 0; j < PH; ++j)
+      v[j] = make_float2((float)mu[(size_t)u * P + 2 * j], 2 * j + 1 < P ? (float)mu[(size_t)u * P + 2 * j + 1] : 0.0f);
+#pragma unroll 1
+    for (int c = 0; c < H; ++c) {
+      float2 acc = make_float2(0.0f, 0.0f);
+#pragma unroll
+      for (int j = 0; j < PH; ++j) acc = __ffma2_rn(QP[c * PH + j], v[j], acc);
+      X1[u * H + c] = acc;
+    }
+  }
+  __syncthreads();
+  // axis 2: unit (n1, pi3, c): inputs X1[n1][n2][c].pi3 over n2
+  for (int u = tid; u < P * 2 * H; u += NT) {
+    const int n1 = u / (2 * H), p3 = (u / H) % 2, c = u % H;
+    float2 v[PH];
+#pragma unroll
+    for (int j = 0; j < PH; ++j) {
+      const float2 e0 = X1[(n1 * P + 2 * j) * H + c];
+      const float2 e1 = 2 * j + 1 < P ? X1[(n1 * P + 2 * j + 1) * H + c] : make_float2(0.0f, 0.0f);
+      v[j] = p3 ? make_float2(e0.y, e1.y) : make_float2(e0.x, e1.x);
+    }
+#pragma unroll 1
+    for (int bb = 0; bb < H; ++bb) {
+      float2 acc = make_float2(0.0f, 0.0f);
+#pragma unroll
+      for (int j = 0; j < PH; ++j) acc = __ffma2_rn(QP[bb * PH + j], v[j], acc);
+      X2[((n1 * 2 + p3) * H + bb) * H + c] = acc;
+    }
+  }
+  __syncthreads();
+  // axis 1: unit (pi2, pi3, b, c): inputs X2[n1][pi3][b][c].pi2 over n1 -> F[a][pi][b][c]
+  for (int u = tid; u < 4 * HSQ; u += NT) {
+    const int g = u / HSQ, bc = u - g * HSQ, p2 = g >> 1, p3 = g & 1;
+    float2 v[PH];
+#pragma unroll
+    for (int j = 0; j < PH; ++j) {
+      const float2 e0 = X2[((2 * j) * 2 + p3) * HSQ + bc];
+      const float2 e1 = 2 * j + 1 < P ? X2[((2 * j + 1) * 2 + p3) * HSQ + bc] : make_float2(0.0f, 0.0f);
+      v[j] = p2 ? make_float2(e0.y, e1.y) : make_float2(e0.x, e1.x);
+    }
+#pragma unroll 1
+    for (int a = 0; a < H; ++a) {
+      float2 acc = make_float2(0.0f, 0.0f);
+#pragma unroll
+      for (int j = 0; j < PH; ++j) acc = __ffma2_rn(QP[a * PH + j], v[j], acc);
+      float* o = out + (size_t)a * 8 * HSQ + bc;
+      o[(2 * p2 + p3) * HSQ] = acc.x;         // pi1 = 0
+      o[(4 + 2 * p2 + p3) * HSQ] = acc.y;     // pi1 = 1
+    }
+  }
+}
+
 // Rotation-accumulate along one axis (bit ST of the parity index): acc += R(delta phi) g.
 template <int ST, int DELTA>
 __device__ __forceinline__ void rot_acc(double* acc, const double* g, double C, double S) {
@@ -1758,15 +1847,32 @@ static void run_eval(dmk_plan_s* PL, int phase = PH_UP | PH_DOWN, int top = 0) {
       constexpr int H = NF + 1, H0 = NF0 + 1, AC = px_ch(P, H), AC0 = px_ch(P, H0);
       using K1 = Prox2pw<P, H, AC>;
       using K0 = Prox2pw<P, H0, AC0>;
-      set_smem(k_prox2pw<P, H0, AC0>, K0::smem);
-      set_smem(k_prox2pw<P, H, AC>, K1::smem);
+      if constexpr (P > 18) {
+        set_smem(k_prox2pw<P, H0, AC0>, K0::smem);
+        set_smem(k_prox2pw<P, H, AC>, K1::smem);
+      }
       FStore<P>* Fp = reinterpret_cast<FStore<P>*>(PL->phi.p);
-      k_prox2pw<P, H0, AC0><<<1, K0::NT, K0::smem, s>>>(dt, PL->fout_list.p, T.dQr0, PL->mom.p, Fp, 0, 0);
-      DMK_LAUNCH_CHECK();
-      if (PL->nfout > 1) {
-        k_prox2pw<P, H, AC><<<(int)(PL->nfout - 1), K1::NT, K1::smem, s>>>(dt, PL->fout_list.p + 1, T.dQr1, PL->mom.p,
-                                                                           Fp, PL->phi_size0, PL->phi_size1);
+      if constexpr (P <= 18) {   // fp32 tier (R16)
+        using X0 = Px32<P, H0>;
+        using X1 = Px32<P, H>;
+        set_smem(k_prox2pw32<P, H0>, X0::smem);
+        set_smem(k_prox2pw32<P, H>, X1::smem);
+        k_prox2pw32<P, H0><<<1, X0::NT, X0::smem, s>>>(dt, PL->fout_list.p, T.dQr0, PL->mom.p, Fp, 0, 0);
         DMK_LAUNCH_CHECK();
+        if (PL->nfout > 1) {
+          k_prox2pw32<P, H><<<(int)(PL->nfout - 1), X1::NT, X1::smem, s>>>(dt, PL->fout_list.p + 1, T.dQr1, PL->mom.p,
+                                                                          Fp, PL->phi_size0, PL->phi_size1);
+          DMK_LAUNCH_CHECK();
+        }
+      } else {
+        k_prox2pw<P, H0, AC0><<<1, K0::NT, K0::smem, s>>>(dt, PL->fout_list.p, T.dQr0, PL->mom.p, Fp, 0, 0);
+        DMK_LAUNCH_CHECK();
+        if (PL->nfout > 1) {
+          k_prox2pw<P, H, AC><<<(int)(PL->nfout - 1), K1::NT, K1::smem, s>>>(dt, PL->fout_list.p + 1, T.dQr1,
+                                                                             PL->mom.p, Fp, PL->phi_size0,
+                                                                             PL->phi_size1);
+          DMK_LAUNCH_CHECK();
+        }
       }
     }
     tm.end();
