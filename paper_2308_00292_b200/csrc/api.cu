@@ -2,6 +2,7 @@
 // placement (host <-> device), plan lifetime, introspection.
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <exception>
 
 #include "common.cuh"
@@ -45,6 +46,52 @@ static void require_device() {
   DMK_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
 }
 
+// ---- stream/event pool (per device, process-wide, thread-safe)
+namespace {
+struct StreamSet {
+  int dev;
+  cudaStream_t side, hi, root;
+  cudaEvent_t fork, join, rootev;
+};
+std::mutex g_pool_mu;
+std::vector<StreamSet> g_pool;
+}  // namespace
+
+static void acquire_streams(dmk_plan_s* P) {
+  int dev = 0;
+  DMK_CUDA(cudaGetDevice(&dev));
+  StreamSet ss{};
+  bool found = false;
+  {
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    for (size_t i = 0; i < g_pool.size(); ++i)
+      if (g_pool[i].dev == dev) {
+        ss = g_pool[i];
+        g_pool.erase(g_pool.begin() + i);
+        found = true;
+        break;
+      }
+  }
+  if (!found) {
+    int prio_lo = 0, prio_hi = 0;
+    ss.dev = dev;
+    DMK_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+    DMK_CUDA(cudaStreamCreateWithPriority(&ss.side, cudaStreamNonBlocking, prio_lo));
+    DMK_CUDA(cudaStreamCreateWithPriority(&ss.hi, cudaStreamNonBlocking, prio_hi));
+    DMK_CUDA(cudaStreamCreateWithPriority(&ss.root, cudaStreamNonBlocking, prio_hi));
+    DMK_CUDA(cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming));
+    DMK_CUDA(cudaEventCreateWithFlags(&ss.join, cudaEventDisableTiming));
+    DMK_CUDA(cudaEventCreateWithFlags(&ss.rootev, cudaEventDisableTiming));
+  }
+  P->pool_dev = dev;
+  P->side_stream = ss.side;
+  P->hi_stream = ss.hi;
+  P->root_stream = ss.root;
+  P->ev_fork = ss.fork;
+  P->ev_join = ss.join;
+  P->ev_root = ss.rootev;
+}
+
 static void alloc_eval_buffers(dmk_plan_s* P) {
   const Tables& T = *P->tab;
   cudaStream_t s = P->stream;
@@ -71,6 +118,15 @@ static void alloc_eval_buffers(dmk_plan_s* P) {
 }  // namespace dmk
 
 using namespace dmk;
+
+// the streams go back to the pool once idle (dmk_destroy synchronises them first)
+dmk_plan_s::~dmk_plan_s() {
+  for (auto e : ev_pool) cudaEventDestroy(e);
+  if (pool_dev >= 0 && side_stream) {
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    g_pool.push_back(StreamSet{pool_dev, side_stream, hi_stream, root_stream, ev_fork, ev_join, ev_root});
+  }
+}
 
 extern "C" {
 
@@ -117,12 +173,7 @@ int dmk_plan(int dim, int kernel, double eps, int64_t n, const double* points, i
           P->side = opt->root[dim];
         }
       }
-      int prio_lo = 0, prio_hi = 0;
-      DMK_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
-      DMK_CUDA(cudaStreamCreateWithPriority(&P->side_stream, cudaStreamNonBlocking, prio_lo));
-      DMK_CUDA(cudaStreamCreateWithPriority(&P->hi_stream, cudaStreamNonBlocking, prio_hi));
-      DMK_CUDA(cudaEventCreateWithFlags(&P->ev_fork, cudaEventDisableTiming));
-      DMK_CUDA(cudaEventCreateWithFlags(&P->ev_join, cudaEventDisableTiming));
+      acquire_streams(P);
       const char* ps = std::getenv("DMK_SERIAL");
       P->serial = ps && ps[0] == '1';
       const char* pe = std::getenv("DMK_PROFILE");
@@ -239,6 +290,7 @@ int dmk_destroy(dmk_plan_t P) {
     if (P->p2p_pending) cudaStreamWaitEvent(s, P->ev_join, 0);   // near-field branch still running
     if (P->side_stream) cudaStreamSynchronize(P->side_stream);
     if (P->hi_stream) cudaStreamSynchronize(P->hi_stream);
+    if (P->root_stream) cudaStreamSynchronize(P->root_stream);
     delete P;   // DevBuf destructors enqueue cudaFreeAsync on the plan stream
     cudaStreamSynchronize(s);
   });

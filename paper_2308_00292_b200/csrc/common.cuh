@@ -164,18 +164,15 @@ struct dmk_plan_s {
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
   // near-field branch: side stream + fork/join events (created with the plan)
-  cudaStream_t side_stream = nullptr;   // near field, lowest priority
-  cudaStream_t hi_stream = nullptr;     // far field, highest priority
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // streams and events from a process-wide pool (creating them costs more than a
+  // small evaluation): near field (lowest priority), far field and the root-box chain
+  // (highest priority), fork/join events
+  cudaStream_t side_stream = nullptr, hi_stream = nullptr, root_stream = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_root = nullptr;
+  int pool_dev = -1;
   bool p2p_pending = false;   // a near-field branch was forked and not yet joined
   bool serial = false;        // DMK_SERIAL=1: near field on the plan stream (no overlap)
-  ~dmk_plan_s() {
-    for (auto e : ev_pool) cudaEventDestroy(e);
-    if (ev_fork) cudaEventDestroy(ev_fork);
-    if (ev_join) cudaEventDestroy(ev_join);
-    if (side_stream) cudaStreamDestroy(side_stream);
-    if (hi_stream) cudaStreamDestroy(hi_stream);
-  }
+  ~dmk_plan_s();
 };
 
 namespace dmk {

@@ -1842,6 +1842,13 @@ static void run_eval(dmk_plan_s* PL, int phase = PH_UP | PH_DOWN, int top = 0) {
   }
   if (nl > 1 && (phase & PH_DOWN)) {
     // ---- Step 3: downward pass
+    // the root box's chain (prox2pw, pwlocal: one CTA each, H0 > H) runs on its own
+    // stream beside the other boxes' launches; joined before p2c
+    cudaStream_t sr = PL->serial ? s : PL->root_stream;
+    if (!PL->serial) {
+      DMK_CUDA(cudaEventRecord(PL->ev_fork, s));
+      DMK_CUDA(cudaStreamWaitEvent(sr, PL->ev_fork, 0));
+    }
     tm.begin("prox2pw");
     {
       constexpr int H = NF + 1, H0 = NF0 + 1, AC = px_ch(P, H), AC0 = px_ch(P, H0);
@@ -1857,7 +1864,7 @@ static void run_eval(dmk_plan_s* PL, int phase = PH_UP | PH_DOWN, int top = 0) {
         using X1 = Px32<P, H>;
         set_smem(k_prox2pw32<P, H0>, X0::smem);
         set_smem(k_prox2pw32<P, H>, X1::smem);
-        k_prox2pw32<P, H0><<<1, X0::NT, X0::smem, s>>>(dt, PL->fout_list.p, T.dQr0, PL->mom.p, Fp, 0, 0);
+        k_prox2pw32<P, H0><<<1, X0::NT, X0::smem, sr>>>(dt, PL->fout_list.p, T.dQr0, PL->mom.p, Fp, 0, 0);
         DMK_LAUNCH_CHECK();
         if (PL->nfout > 1) {
           k_prox2pw32<P, H><<<(int)(PL->nfout - 1), X1::NT, X1::smem, s>>>(dt, PL->fout_list.p + 1, T.dQr1, PL->mom.p,
@@ -1865,7 +1872,7 @@ static void run_eval(dmk_plan_s* PL, int phase = PH_UP | PH_DOWN, int top = 0) {
           DMK_LAUNCH_CHECK();
         }
       } else {
-        k_prox2pw<P, H0, AC0><<<1, K0::NT, K0::smem, s>>>(dt, PL->fout_list.p, T.dQr0, PL->mom.p, Fp, 0, 0);
+        k_prox2pw<P, H0, AC0><<<1, K0::NT, K0::smem, sr>>>(dt, PL->fout_list.p, T.dQr0, PL->mom.p, Fp, 0, 0);
         DMK_LAUNCH_CHECK();
         if (PL->nfout > 1) {
           k_prox2pw<P, H, AC><<<(int)(PL->nfout - 1), K1::NT, K1::smem, s>>>(dt, PL->fout_list.p + 1, T.dQr1,
@@ -1885,9 +1892,10 @@ static void run_eval(dmk_plan_s* PL, int phase = PH_UP | PH_DOWN, int top = 0) {
       set_smem(k_pwlocal<P, H, AC, false>, K1::smem);
       // root: exp rank 0, F_out rank 0
       const FStore<P>* Fp = reinterpret_cast<const FStore<P>*>(PL->phi.p);
-      k_pwlocal<P, H0, AC0, true><<<1, K0::NT, K0::smem, s>>>(dt, PL->exp_list.p, T.dGr0, T.dW0, 0, Fp, 0, 0,
-                                                              PL->lam.p);
+      k_pwlocal<P, H0, AC0, true><<<1, K0::NT, K0::smem, sr>>>(dt, PL->exp_list.p, T.dGr0, T.dW0, 0, Fp, 0, 0,
+                                                               PL->lam.p);
       DMK_LAUNCH_CHECK();
+      if (!PL->serial) DMK_CUDA(cudaEventRecord(PL->ev_root, sr));
       if (PL->nexp > 1) {
         if constexpr (P <= 18) {
           // parent-group translation (k_pwshift) into T, then the back transforms
@@ -1913,6 +1921,7 @@ static void run_eval(dmk_plan_s* PL, int phase = PH_UP | PH_DOWN, int top = 0) {
       }
     }
     tm.end();
+    if (!PL->serial) DMK_CUDA(cudaStreamWaitEvent(s, PL->ev_root, 0));
     tm.begin("p2c");
     {
       // parents at level l-1 push their local expansions into their level-l children
