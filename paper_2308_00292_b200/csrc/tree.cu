@@ -139,12 +139,54 @@ __global__ void k_bbox_partial(const double* __restrict__ pts, int64_t n, double
   if (threadIdx.x < 6) out[blockIdx.x * 6 + threadIdx.x] = s[threadIdx.x][0];
 }
 
+// root cube on the device (reading R5): lo = per-axis minimum, side = max extent (1 if
+// 0), scale = 2^21/side; bad = non-finite coordinates.  Read by the key and gather
+// kernels without a host round trip; the host copy is read at the next synchronisation.
+struct Geo {
+  double lo[3], side, scale;
+  int bad;
+};
 template <int D>
-__global__ void k_keys(const double* __restrict__ pts, int64_t n, double lo0, double lo1, double lo2,
-                       double scale, uint64_t* keys, int32_t* idx) {
+__global__ void __launch_bounds__(TPB) k_bbox_final(const double* __restrict__ part, int nb, Geo* g) {
+  __shared__ double sm[6][TPB];
+  double mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
+  for (int b = threadIdx.x; b < nb; b += TPB)
+    for (int d = 0; d < D; ++d) {
+      mn[d] = fmin(mn[d], part[6 * b + d]);
+      mx[d] = fmax(mx[d], part[6 * b + 3 + d]);
+    }
+  for (int d = 0; d < 3; ++d) {
+    sm[d][threadIdx.x] = mn[d];
+    sm[3 + d][threadIdx.x] = mx[d];
+  }
+  __syncthreads();
+  for (int w = TPB / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w)
+      for (int d = 0; d < 3; ++d) {
+        sm[d][threadIdx.x] = fmin(sm[d][threadIdx.x], sm[d][threadIdx.x + w]);
+        sm[3 + d][threadIdx.x] = fmax(sm[3 + d][threadIdx.x], sm[3 + d][threadIdx.x + w]);
+      }
+    __syncthreads();
+  }
+  if (threadIdx.x != 0) return;
+  for (int d = 0; d < 3; ++d) {
+    mn[d] = sm[d][0];
+    mx[d] = sm[3 + d][0];
+  }
+  double ext = 0;
+  for (int d = 0; d < 3; ++d) g->lo[d] = d < D ? mn[d] : 0.0;
+  for (int d = 0; d < D; ++d) ext = fmax(ext, mx[d] - mn[d]);
+  g->bad = isfinite(ext) ? 0 : 1;
+  g->side = ext > 0 ? ext : 1.0;
+  g->scale = (double)(1 << NBITS) / g->side;
+}
+
+template <int D>
+__global__ void k_keys(const double* __restrict__ pts, int64_t n, const Geo* __restrict__ g, uint64_t* keys,
+                       int32_t* idx) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
-  const double lo[3] = {lo0, lo1, lo2};
+  const double lo[3] = {g->lo[0], g->lo[1], g->lo[2]}, scale = g->scale;
   int q[3];
   for (int d = 0; d < D; ++d) {
     double t = floor(__dmul_rn(__dsub_rn(pts[D * i + d], lo[d]), scale));
@@ -157,10 +199,10 @@ __global__ void k_keys(const double* __restrict__ pts, int64_t n, double lo0, do
 
 template <int D>
 __global__ void k_gather_pts(const double* __restrict__ pts, const int32_t* __restrict__ perm, int64_t n,
-                             double lo0, double lo1, double lo2, double side, double* xs, double* ys,
-                             double* zs) {
+                             const Geo* __restrict__ g, double* xs, double* ys, double* zs) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
+  const double lo0 = g->lo[0], lo1 = g->lo[1], lo2 = g->lo[2], side = g->side;
   int64_t j = perm[i];
   xs[i] = __ddiv_rn(__dsub_rn(pts[D * j + 0], lo0), side);
   ys[i] = __ddiv_rn(__dsub_rn(pts[D * j + 1], lo1), side);
@@ -362,6 +404,26 @@ __global__ void k_read_at(const int32_t* __restrict__ a, const int32_t* __restri
   }
 }
 
+struct ReadIdx {   // by value
+  int64_t v[LMAX + 3];
+  int m;
+};
+// out[i] = fscan[v[i]], out[m + i] = escan[v[i]] (i < m), out[2m] = dlist_off[nbox],
+// out[2m + 1] = poff[nbox]: every host-side size of the plan in one read-back
+__global__ void k_read_totals(const int32_t* __restrict__ fscan, const int32_t* __restrict__ escan, ReadIdx ri,
+                              const int32_t* __restrict__ doff, const int32_t* __restrict__ poff, int64_t nbox,
+                              int64_t* out) {
+  const int i = threadIdx.x;
+  if (i < ri.m) {
+    out[i] = fscan[ri.v[i]];
+    out[ri.m + i] = escan[ri.v[i]];
+  }
+  if (i == 0) {
+    out[2 * ri.m] = doff[nbox];
+    out[2 * ri.m + 1] = poff[nbox];
+  }
+}
+
 __global__ void k_iota_u64(uint64_t* out, int64_t n) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < n) out[i] = (uint64_t)i;
@@ -372,16 +434,27 @@ __global__ void k_fill_level(int32_t* lev, int64_t a, int64_t b, int l) {
   if (i < b) lev[i] = l;
 }
 
-struct BoxCtx {
+struct BoxCtx {   // passed by value (no host-to-device copies)
   const uint64_t* code;
   const int32_t* level;
-  const int64_t* loff;      // device level offsets [nlevels+1]
+  int64_t loff[LMAX + 2];   // level offsets [nlevels+1]
   const uint64_t* B;        // concatenated non-leaf sets
-  const int64_t* boff;      // offsets of B per level [nlevels+1]
+  int64_t boff[LMAX + 2];   // offsets of B per level [nlevels+1]
   int nlevels;
   const uint64_t* keys;
   int64_t n;
+  // coarse levels (<= lbc): B and E bitmaps and the exclusive scan of the E words, so a
+  // box's index is a rank (one word and one popcount) instead of a binary search
+  int lbc;
+  int64_t woff[12];         // word offsets per coarse level
+  const uint32_t* bmB;
+  const uint32_t* bmE;
+  const int32_t* posE;
 };
+__device__ __forceinline__ int64_t bm_rank(const BoxCtx& c, int l, uint64_t code) {
+  const int64_t w0 = c.woff[l], w = w0 + (int64_t)(code >> 5);
+  return (int64_t)(c.posE[w] - c.posE[w0]) + __popc(c.bmE[w] & ((1u << (code & 31)) - 1u));
+}
 
 template <int D>
 __global__ void k_box_attrs(BoxCtx c, int64_t nbox, int32_t* start, int32_t* end, int32_t* parent,
@@ -398,6 +471,29 @@ __global__ void k_box_attrs(BoxCtx c, int64_t nbox, int32_t* start, int32_t* end
   int64_t e = (l == 0) ? c.n : lower_bound_u64(c.keys, c.n, hiv);
   start[i] = (int32_t)s;
   end[i] = (int32_t)e;
+  if (l <= c.lbc) {
+    flags[i] = bm_get(c.bmB + c.woff[l], code) ? 0 : 1;
+    parent[i] = l > 0 ? (int32_t)(c.loff[l - 1] + bm_rank(c, l - 1, code >> D)) : -1;
+    int x[3];
+    decode<D>(code, x);
+    const int n1 = 1 << l;
+    for (int k = 0; k < NCOL; ++k) {
+      int cc[3], rem = k;
+      bool ok = true;
+      for (int d = D - 1; d >= 0; --d) {
+        cc[d] = x[d] + (rem % 3) - 1;
+        rem /= 3;
+        ok = ok && cc[d] >= 0 && cc[d] < n1;
+      }
+      int32_t r = -1;
+      if (ok) {
+        const uint64_t nb = encode<D>(cc);
+        if (bm_get(c.bmE + c.woff[l], nb)) r = (int32_t)(c.loff[l] + bm_rank(c, l, nb));
+      }
+      coll[NCOL * i + k] = r;
+    }
+    return;
+  }
   bool leaf = bsearch_u64(c.B + c.boff[l], c.boff[l + 1] - c.boff[l], code) < 0;
   flags[i] = leaf ? 1 : 0;
   if (l > 0) {
@@ -702,33 +798,29 @@ static void build_tree_d(dmk_plan_s* P, const double* dpts) {
     t_last = now;
   };
 
-  // ---- root cube (reading R5), or the caller's (distributed plans share one root)
+  // ---- root cube (reading R5), or the caller's (distributed plans share one root):
+  // computed on the device; the host copy (pinned) is read after the next round trip
+  static thread_local Geo* hgeo = nullptr;
+  if (!hgeo) DMK_CUDA(cudaHostAlloc((void**)&hgeo, sizeof(Geo), cudaHostAllocDefault));
+  DevBuf<Geo> dgeo;
+  dgeo.alloc(1, s);
   if (P->root_fixed) {
     if (!(P->side > 0) || !std::isfinite(P->side)) fail(DMK_ERR_ARG, "fixed root side must be > 0");
+    Geo g{};
+    for (int d = 0; d < 3; ++d) g.lo[d] = d < D ? P->lo[d] : 0.0;
+    g.side = P->side;
+    g.scale = (double)(1 << NBITS) / P->side;
+    *hgeo = g;
+    DMK_CUDA(cudaMemcpyAsync(dgeo.p, hgeo, sizeof(Geo), cudaMemcpyHostToDevice, s));
   } else {
     int nb = std::min(nblk(n), 1024);
     DevBuf<double> part;
     part.alloc(6 * nb, s);
     k_bbox_partial<D><<<nb, TPB, 0, s>>>(dpts, n, part.p);
+    k_bbox_final<D><<<1, TPB, 0, s>>>(part.p, nb, dgeo.p);
     DMK_LAUNCH_CHECK();
-    std::vector<double> h(6 * nb);
-    DMK_CUDA(cudaMemcpyAsync(h.data(), part.p, h.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
-    DMK_CUDA(cudaStreamSynchronize(s));
-    double mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
-    for (int b = 0; b < nb; ++b)
-      for (int d = 0; d < D; ++d) {
-        mn[d] = std::fmin(mn[d], h[6 * b + d]);
-        mx[d] = std::fmax(mx[d], h[6 * b + 3 + d]);
-      }
-    double ext = 0;
-    for (int d = 0; d < D; ++d) {
-      P->lo[d] = mn[d];
-      ext = std::fmax(ext, mx[d] - mn[d]);
-    }
-    if (!std::isfinite(ext)) fail(DMK_ERR_ARG, "points contain non-finite coordinates");
-    P->side = ext > 0 ? ext : 1.0;
+    DMK_CUDA(cudaMemcpyAsync(hgeo, dgeo.p, sizeof(Geo), cudaMemcpyDeviceToHost, s));
   }
-  const double scale = (double)(1 << NBITS) / P->side;
   mark("bbox");
 
   // ---- Morton keys, stable sort, sorted normalised coordinates
@@ -737,7 +829,7 @@ static void build_tree_d(dmk_plan_s* P, const double* dpts) {
     DevBuf<int32_t> i0;
     k0.alloc(n, s);
     i0.alloc(n, s);
-    k_keys<D><<<nblk(n), TPB, 0, s>>>(dpts, n, P->lo[0], P->lo[1], P->lo[2], scale, k0.p, i0.p);
+    k_keys<D><<<nblk(n), TPB, 0, s>>>(dpts, n, dgeo.p, k0.p, i0.p);
     DMK_LAUNCH_CHECK();
     P->keys.alloc(n, s);
     P->perm.alloc(n, s);
@@ -747,8 +839,7 @@ static void build_tree_d(dmk_plan_s* P, const double* dpts) {
     P->xs.alloc(n, s);
     P->ys.alloc(n, s);
     if (D == 3) P->zs.alloc(n, s);
-    k_gather_pts<D><<<nblk(n), TPB, 0, s>>>(dpts, P->perm.p, n, P->lo[0], P->lo[1], P->lo[2], P->side, P->xs.p,
-                                         P->ys.p, P->zs.p);
+    k_gather_pts<D><<<nblk(n), TPB, 0, s>>>(dpts, P->perm.p, n, dgeo.p, P->xs.p, P->ys.p, P->zs.p);
     DMK_LAUNCH_CHECK();
   }
 
@@ -786,6 +877,11 @@ static void build_tree_d(dmk_plan_s* P, const double* dpts) {
     unsigned long long hc[LMAX];
     DMK_CUDA(cudaMemcpyAsync(hc, dcnt.p, sizeof(hc), cudaMemcpyDeviceToHost, s));
     DMK_CUDA(cudaStreamSynchronize(s));
+    if (!P->root_fixed) {   // the root cube computed on the device
+      if (hgeo->bad) fail(DMK_ERR_ARG, "points contain non-finite coordinates");
+      for (int d = 0; d < D; ++d) P->lo[d] = hgeo->lo[d];
+      P->side = hgeo->side;
+    }
     DevBuf<uint64_t> codes;
     DevBuf<uint8_t> flags;
     DevBuf<int64_t> nsel;
@@ -854,18 +950,19 @@ static void build_tree_d(dmk_plan_s* P, const double* dpts) {
   // ---- box sets per level: E_l = B_l + non-empty children of B_{l-1}
   std::vector<DevBuf<uint64_t>> E(nlevels);
   std::vector<int64_t> nE(nlevels, 0);
+  DevBuf<int32_t> bm_cnt, bm_pos;   // popcounts and exclusive scan of [B | E] bitmap words
   {
     // coarse levels: E bitmaps, then all coarse B and E lists from one scan and one
     // round trip for their sizes
-    const uint32_t one = 1u;
-    DMK_CUDA(cudaMemcpyAsync(bmE, &one, sizeof(uint32_t), cudaMemcpyHostToDevice, s));   // E_0 = {root}
+    DMK_CUDA(cudaMemsetAsync(bmE, 1, 1, s));   // E_0 = {root}: first word = 1 (little endian)
     const int lc = std::min(LBC, nlevels - 1);
     for (int l = 1; l <= lc; ++l) {
       k_E_bm<D><<<nblk(nbits(l) / 32 + 1), TPB, 0, s>>>(bmB + cs.woff[l], bmNE + cs.woff[l], bmB + cs.woff[l - 1],
                                                        nbits(l), bmE + cs.woff[l]);
       DMK_LAUNCH_CHECK();
     }
-    DevBuf<int32_t> cnt, pos;
+    DevBuf<int32_t>& cnt = bm_cnt;
+    DevBuf<int32_t>& pos = bm_pos;
     DevBuf<int64_t> tot;
     cnt.alloc(2 * W + 1, s);
     pos.alloc(2 * W + 1, s);
@@ -929,11 +1026,6 @@ static void build_tree_d(dmk_plan_s* P, const double* dpts) {
   for (int l = 0; l <= ltop; ++l)
     if (nB[l])
       DMK_CUDA(cudaMemcpyAsync(Bcat.p + boff[l], B[l].p, nB[l] * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
-  DevBuf<int64_t> dloff, dboff;
-  dloff.alloc(nlevels + 1, s);
-  dboff.alloc(nlevels + 1, s);
-  DMK_CUDA(cudaMemcpyAsync(dloff.p, th.level_off.data(), (nlevels + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s));
-  DMK_CUDA(cudaMemcpyAsync(dboff.p, boff.data(), (nlevels + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s));
 
   P->box_start.alloc(nbox, s);
   P->box_end.alloc(nbox, s);
@@ -941,7 +1033,23 @@ static void build_tree_d(dmk_plan_s* P, const double* dpts) {
   P->box_coll.alloc(NCOL * nbox, s);
   P->box_child.alloc(NCH * nbox, s);
   P->box_flags.alloc(nbox, s);
-  BoxCtx ctx{P->box_code.p, P->box_level.p, dloff.p, Bcat.p, dboff.p, nlevels, P->keys.p, n};
+  static_assert(LBC + 2 <= 12, "BoxCtx::woff");
+  BoxCtx ctx{};
+  ctx.code = P->box_code.p;
+  ctx.level = P->box_level.p;
+  ctx.B = Bcat.p;
+  ctx.nlevels = nlevels;
+  ctx.keys = P->keys.p;
+  ctx.n = n;
+  ctx.lbc = LBC;
+  ctx.bmB = bmB;
+  ctx.bmE = bmE;
+  ctx.posE = bm_pos.p + W;
+  for (int l = 0; l <= nlevels; ++l) {
+    ctx.loff[l] = th.level_off[l];
+    ctx.boff[l] = boff[l];
+  }
+  for (int l = 0; l <= LBC + 1; ++l) ctx.woff[l] = cs.woff[l];
   k_box_attrs<D><<<nblk(nbox), TPB, 0, s>>>(ctx, nbox, P->box_start.p, P->box_end.p, P->box_parent.p,
                                          P->box_coll.p, P->box_flags.p);
   DMK_LAUNCH_CHECK();
@@ -986,20 +1094,35 @@ static void build_tree_d(dmk_plan_s* P, const double* dpts) {
   k_rank<<<nblk(nbox), TPB, 0, s>>>(fscan.p, fsel.p, nbox, P->fout_rank.p);
   k_rank<<<nblk(nbox), TPB, 0, s>>>(escan.p, esel.p, nbox, P->exp_rank.p);
   DMK_LAUNCH_CHECK();
+  // direct lists (CSR over boxes) and P2P work items: counts and scans, then the flag
+  // totals, per-level rank offsets and list sizes in ONE round trip, then the fills
+  DevBuf<int32_t> dcnt, pcnt, poff;
+  dcnt.alloc(nbox + 1, s);
+  pcnt.alloc(nbox + 1, s);
+  poff.alloc(nbox + 1, s);
+  DMK_CUDA(cudaMemsetAsync(dcnt.p, 0, (nbox + 1) * sizeof(int32_t), s));
+  DMK_CUDA(cudaMemsetAsync(pcnt.p, 0, (nbox + 1) * sizeof(int32_t), s));
+  k_dlist<D, false><<<nblk(32 * nbox), TPB, 0, s>>>(P->box_start.p, P->box_end.p, P->box_parent.p, P->box_child.p,
+                                                    P->box_coll.p, P->box_flags.p, P->box_code.p, P->box_level.p,
+                                                    nbox, dcnt.p, nullptr, nullptr);
+  DMK_LAUNCH_CHECK();
+  k_p2p_count<<<nblk(nbox), TPB, 0, s>>>(P->box_start.p, P->box_end.p, P->box_flags.p, nbox, pcnt.p);
+  DMK_LAUNCH_CHECK();
+  P->dlist_off.alloc(nbox + 1, s);
+  exclusive_scan(s, dcnt.p, P->dlist_off.p, nbox + 1);
+  exclusive_scan(s, pcnt.p, poff.p, nbox + 1);
   {
-    // totals and per-level rank offsets in one round trip
-    std::vector<int64_t> idx(nlevels + 1);
-    for (int l = 0; l < nlevels; ++l) idx[l] = th.level_off[l];
-    idx[nlevels] = nbox;
+    ReadIdx ri{};
     const int m = nlevels + 1;
-    DevBuf<int64_t> didx, dout;
-    didx.alloc(m, s);
-    dout.alloc(2 * m, s);
-    DMK_CUDA(cudaMemcpyAsync(didx.p, idx.data(), m * sizeof(int64_t), cudaMemcpyHostToDevice, s));
-    k_read_at<<<1, 64, 0, s>>>(fscan.p, escan.p, didx.p, m, dout.p);
+    for (int l = 0; l < nlevels; ++l) ri.v[l] = th.level_off[l];
+    ri.v[nlevels] = nbox;
+    ri.m = m;
+    DevBuf<int64_t> dout;
+    dout.alloc(2 * m + 2, s);
+    k_read_totals<<<1, 64, 0, s>>>(fscan.p, escan.p, ri, P->dlist_off.p, poff.p, nbox, dout.p);
     DMK_LAUNCH_CHECK();
-    std::vector<int64_t> h(2 * m);
-    DMK_CUDA(cudaMemcpyAsync(h.data(), dout.p, 2 * m * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    std::vector<int64_t> h(2 * m + 2);
+    DMK_CUDA(cudaMemcpyAsync(h.data(), dout.p, h.size() * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     DMK_CUDA(cudaStreamSynchronize(s));
     P->nfout = h[nlevels];
     P->nexp = h[m + nlevels];
@@ -1009,6 +1132,8 @@ static void build_tree_d(dmk_plan_s* P, const double* dpts) {
       th.fout_off[l] = h[l];
       th.exp_off[l] = h[m + l];
     }
+    P->ndlist = h[2 * m];
+    P->np2p = h[2 * m + 1];
   }
   {
     cub::CountingInputIterator<int32_t> cnt_it(0);
@@ -1023,48 +1148,16 @@ static void build_tree_d(dmk_plan_s* P, const double* dpts) {
       return cub::DeviceSelect::Flagged(t, b, cnt_it, esel.p, P->exp_list.p, nsel.p, nbox, s);
     });
   }
-
   mark("flags");
-  // ---- direct lists (CSR over boxes) and P2P work items: counts, scans, one round trip
-  // for both totals, fills
-  {
-    DevBuf<int32_t> cnt, pcnt, poff;
-    cnt.alloc(nbox + 1, s);
-    pcnt.alloc(nbox + 1, s);
-    poff.alloc(nbox + 1, s);
-    DMK_CUDA(cudaMemsetAsync(cnt.p, 0, (nbox + 1) * sizeof(int32_t), s));
-    DMK_CUDA(cudaMemsetAsync(pcnt.p, 0, (nbox + 1) * sizeof(int32_t), s));
-    k_dlist<D, false><<<nblk(32 * nbox), TPB, 0, s>>>(P->box_start.p, P->box_end.p, P->box_parent.p, P->box_child.p,
-                                              P->box_coll.p, P->box_flags.p, P->box_code.p, P->box_level.p, nbox,
-                                              cnt.p, nullptr, nullptr);
-    DMK_LAUNCH_CHECK();
-    k_p2p_count<<<nblk(nbox), TPB, 0, s>>>(P->box_start.p, P->box_end.p, P->box_flags.p, nbox, pcnt.p);
-    DMK_LAUNCH_CHECK();
-    P->dlist_off.alloc(nbox + 1, s);
-    exclusive_scan(s, cnt.p, P->dlist_off.p, nbox + 1);
-    exclusive_scan(s, pcnt.p, poff.p, nbox + 1);
-    DevBuf<int64_t> didx, dout;
-    didx.alloc(1, s);
-    dout.alloc(2, s);
-    const int64_t last = nbox;
-    DMK_CUDA(cudaMemcpyAsync(didx.p, &last, sizeof(int64_t), cudaMemcpyHostToDevice, s));
-    k_read_at<<<1, 32, 0, s>>>(P->dlist_off.p, poff.p, didx.p, 1, dout.p);
-    DMK_LAUNCH_CHECK();
-    int64_t h[2];
-    DMK_CUDA(cudaMemcpyAsync(h, dout.p, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-    DMK_CUDA(cudaStreamSynchronize(s));
-    P->ndlist = h[0];
-    P->np2p = h[1];
-    P->dlist.alloc(P->ndlist ? P->ndlist : 1, s);
-    k_dlist<D, true><<<nblk(32 * nbox), TPB, 0, s>>>(P->box_start.p, P->box_end.p, P->box_parent.p, P->box_child.p,
-                                             P->box_coll.p, P->box_flags.p, P->box_code.p, P->box_level.p, nbox,
-                                             nullptr, P->dlist_off.p, P->dlist.p);
-    DMK_LAUNCH_CHECK();
-    mark("dlists");
-    P->p2p_items.alloc(2 * (P->np2p ? P->np2p : 1), s);
-    k_p2p_fill<<<nblk(nbox), TPB, 0, s>>>(P->box_start.p, pcnt.p, poff.p, nbox, P->p2p_items.p);
-    DMK_LAUNCH_CHECK();
-  }
+  P->dlist.alloc(P->ndlist ? P->ndlist : 1, s);
+  k_dlist<D, true><<<nblk(32 * nbox), TPB, 0, s>>>(P->box_start.p, P->box_end.p, P->box_parent.p, P->box_child.p,
+                                                   P->box_coll.p, P->box_flags.p, P->box_code.p, P->box_level.p,
+                                                   nbox, nullptr, P->dlist_off.p, P->dlist.p);
+  DMK_LAUNCH_CHECK();
+  mark("dlists");
+  P->p2p_items.alloc(2 * (P->np2p ? P->np2p : 1), s);
+  k_p2p_fill<<<nblk(nbox), TPB, 0, s>>>(P->box_start.p, pcnt.p, poff.p, nbox, P->p2p_items.p);
+  DMK_LAUNCH_CHECK();
   if (D == 3) {
     P->box_c4.alloc(nbox, s);
     k_box_c4<<<nblk(nbox), TPB, 0, s>>>(P->box_code.p, P->box_level.p, nbox, P->box_c4.p);
