@@ -357,7 +357,8 @@ __global__ void __launch_bounds__(256) k_c2p_grp(DevTree t, const int32_t* __res
   double* xi = sA + 2 * P2;         // [(o2 o3)][MT][P2]
   double* eta = xi + 4 * MT * P2;   // [o3][MT][P2]
   __shared__ const double* ch[8];
-  const int b = parents[blockIdx.x], tid = threadIdx.x, m0 = blockIdx.y * MT;
+  // 1D grid, the tiles of a parent adjacent (they read the same children: L2 reuse)
+  const int b = parents[blockIdx.x / C::NTILE], tid = threadIdx.x, m0 = (blockIdx.x % C::NTILE) * MT;
   if (tid < 8) {
     const int c = t.child[8 * (int64_t)b + tid];
     ch[tid] = (c >= 0 && (t.flags[c] & F_OUT)) ? mom + (size_t)t.fout_rank[c] * P3 : nullptr;
@@ -445,7 +446,8 @@ __global__ void __launch_bounds__(256) k_p2c_grp(DevTree t, const int32_t* __res
   double* zeta = sA + 2 * P2;        // [o1][MT][P2]        (k1 m2 m3)
   double* zeta2 = zeta + 2 * MT * P2;   // [o1][o2][MT][P2]  (k1 k2 m3)
   __shared__ double* ch[8];
-  const int b = parents[blockIdx.x], tid = threadIdx.x, k0 = blockIdx.y * MT;
+  // 1D grid, the tiles of a parent adjacent (they read the same parent: L2 reuse)
+  const int b = parents[blockIdx.x / C::NTILE], tid = threadIdx.x, k0 = (blockIdx.x % C::NTILE) * MT;
   if (tid < 8) {
     const int c = t.child[8 * (int64_t)b + tid];
     ch[tid] = (c >= 0 && (t.flags[c] & F_EXP)) ? lam + (size_t)t.exp_rank[c] * P3 : nullptr;
@@ -818,7 +820,8 @@ __global__ void __launch_bounds__(PWS_NT, 3)
   __shared__ const float* win[64];   // window box (w1 w2 w3), null: absent or not F_out
   __shared__ int rank[8];            // exp rank of child o = (o1 o2 o3), -1: none
   __shared__ int lvl;
-  const int pb = parents[blockIdx.x], tid = threadIdx.x;
+  // 1D grid, the PWS_GY mode slices of a parent adjacent (same window: L2 reuse)
+  const int pb = parents[blockIdx.x / PWS_GY], slice = blockIdx.x % PWS_GY, tid = threadIdx.x;
   if (tid < 64) {
     const int w1 = tid >> 4, w2 = (tid >> 2) & 3, w3 = tid & 3;
     // window index w = 2 D + c + 1 for the child c of the parent colleague B + D
@@ -843,7 +846,7 @@ __global__ void __launch_bounds__(PWS_NT, 3)
   for (int o = 0; o < 8; ++o) any |= rank[o] >= 0;
   if (!any) return;
   const double* Wl = W + (size_t)lvl * wstride;
-  for (int m = blockIdx.y * PWS_NT + tid; m < NM; m += gridDim.y * PWS_NT) {
+  for (int m = slice * PWS_NT + tid; m < NM; m += PWS_GY * PWS_NT) {
     const int a = m / HSQ, bc = m - a * HSQ;
     float Ca, Sa, Cb, Sb, Cc, Sc;
     rot_csf(a, Ca, Sa);
@@ -1798,7 +1801,7 @@ static void run_c2p_level(dmk_plan_s* PL, const DevTree& dt, int l) {
   const int64_t ca = th.fout_off[l + 1], cb = th.fout_off[l + 2];
   if (b <= a || cb <= ca) return;
   set_smem(k_c2p_grp<P, MT>, G::smem_c2p);
-  dim3 grid((unsigned)(b - a), G::NTILE);
+  const unsigned grid = (unsigned)((b - a) * G::NTILE);
   k_c2p_grp<P, MT><<<grid, 256, G::smem_c2p, s>>>(dt, PL->fout_list.p + a, PL->tab->dA, PL->mom.p);
   DMK_LAUNCH_CHECK();
 }
@@ -1902,7 +1905,7 @@ static void run_eval(dmk_plan_s* PL, int phase = PH_UP | PH_DOWN, int top = 0) {
           tm.end();
           tm.begin("pwshift");
           if (PL->nfout > 0) {
-            dim3 grid((unsigned)PL->nfout, PWS_GY);
+            const unsigned grid = (unsigned)(PL->nfout * PWS_GY);
             k_pwshift<H><<<grid, PWS_NT, 0, s>>>(dt, PL->fout_list.p, reinterpret_cast<const float*>(Fp),
                                                   PL->phi_size0, PL->phi_size1, T.dW, T.wstride, PL->pwt.p);
             DMK_LAUNCH_CHECK();
@@ -1931,7 +1934,7 @@ static void run_eval(dmk_plan_s* PL, int phase = PH_UP | PH_DOWN, int top = 0) {
       for (int l = 1; l < nl; ++l) {
         const int64_t a = th.exp_off[l - 1], b = th.exp_off[l];
         if (b <= a || th.exp_off[l + 1] <= th.exp_off[l]) continue;
-        dim3 grid((unsigned)(b - a), G::NTILE);
+        const unsigned grid = (unsigned)((b - a) * G::NTILE);
         k_p2c_grp<P, MT><<<grid, 256, G::smem_p2c, s>>>(dt, PL->exp_list.p + a, T.dA, PL->lam.p);
         DMK_LAUNCH_CHECK();
       }
