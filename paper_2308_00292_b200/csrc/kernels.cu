@@ -182,25 +182,27 @@ __global__ void __launch_bounds__(Ant32<P>::NT) k_anterp32(DevTree t, const int3
   for (int c0 = 0; c0 < tot; c0 += CH) {
     const int nc = min(CH, tot - c0);
     for (int w = tid; w < CH * 3; w += NT) {
+      // Chebyshev values by the recurrence in fp64, rounded once (no register array)
       const int j = w / 3, d = w % 3;
-      double T[P];
+      float* dst = d == 0 ? sx + j * P : (d == 1 ? sy + j * PY : sz + j * PZ);
+      const int len = d == 0 ? P : (d == 1 ? PY : PZ);
       if (j < nc) {
         const int pi = range_point(rg, nr, c0 + j);
-        const double x = (d == 0 ? t.xs[pi] : d == 1 ? t.ys[pi] : t.zs[pi]);
-        cheb_vec((x - cen[d]) * ih, T, P, d == 0 ? q[pi] : 1.0);
+        const double xx = ((d == 0 ? t.xs[pi] : d == 1 ? t.ys[pi] : t.zs[pi]) - cen[d]) * ih;
+        const double sc = d == 0 ? q[pi] : 1.0;
+        double ta = 1.0, tb = xx;
+        dst[0] = (float)sc;
+        if (P > 1) dst[1] = (float)(sc * xx);
+#pragma unroll 4
+        for (int n = 2; n < P; ++n) {
+          const double tn = 2.0 * xx * tb - ta;
+          dst[n] = (float)(sc * tn);
+          ta = tb;
+          tb = tn;
+        }
+        for (int n = P; n < len; ++n) dst[n] = 0.0f;
       } else {
-#pragma unroll
-        for (int n = 0; n < P; ++n) T[n] = 0.0;
-      }
-      if (d == 0) {
-#pragma unroll
-        for (int n = 0; n < P; ++n) sx[j * P + n] = (float)T[n];
-      } else if (d == 1) {
-#pragma unroll
-        for (int n = 0; n < PY; ++n) sy[j * PY + n] = n < P ? (float)T[n] : 0.0f;
-      } else {
-#pragma unroll
-        for (int n = 0; n < PZ; ++n) sz[j * PZ + n] = n < P ? (float)T[n] : 0.0f;
+        for (int n = 0; n < len; ++n) dst[n] = 0.0f;
       }
     }
     __syncthreads();
@@ -210,6 +212,7 @@ __global__ void __launch_bounds__(Ant32<P>::NT) k_anterp32(DevTree t, const int3
 #pragma unroll
         for (int v = 0; v < PZ / 2; ++v) aa[v] = ab[v] = make_float2(0.0f, 0.0f);
         const int j1 = min(nc, j0 + 32);
+#pragma unroll 2
         for (int j = j0; j < j1; ++j) {
           const float2 wy = *reinterpret_cast<const float2*>(sy + j * PY + 2 * m);
           const float wx = sx[j * P + n1];
@@ -1711,7 +1714,7 @@ __global__ void __launch_bounds__(128) k_p2p32(DevTree t, const int32_t* __restr
         fD[2 * j + 1] = 0.0f;
       }
       __syncwarp();
-#pragma unroll 2
+#pragma unroll 4
       for (int jp = ph; jp < npair; jp += f) {
         const float4 A = sA[warp][jp], Bv = sB[warp][jp], C = sC[warp][jp];
         const float2 Dv = sD[warp][jp];

@@ -16,13 +16,14 @@ import paper_2308_00292_b200 as dmk  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 1_000_000
 kind = sys.argv[2] if len(sys.argv) > 2 else "uniform"
+eps = float(sys.argv[3]) if len(sys.argv) > 3 else 1e-6
 x, q = dmk_inputs.make(kind, n, seed=1)
 X = torch.as_tensor(x, device="cuda")
 Q = torch.as_tensor(q, device="cuda")
 for r in range(4):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    plan = dmk.dmk_plan(X, eps=1e-6, leaf_capacity=200)
+    plan = dmk.dmk_plan(X, eps=eps, leaf_capacity=200)
     torch.cuda.synchronize()
     t1 = time.perf_counter()
     plan.eval(Q)
