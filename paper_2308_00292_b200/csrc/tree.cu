@@ -386,6 +386,30 @@ __global__ void k_bm_fill(const uint32_t* __restrict__ bm, const int32_t* __rest
     x &= x - 1;
   }
 }
+// all-coarse trees: the box arrays (code, level) straight from the E bitmaps, every
+// level in one launch (box index = level offset + rank within the level)
+struct CoarseFill {   // by value
+  int64_t woff[12], loff[12];
+  int nl;
+};
+__global__ void k_coarse_boxes(const uint32_t* __restrict__ bmE, const int32_t* __restrict__ posE, CoarseFill cf,
+                               uint64_t* code, int32_t* level) {
+  const int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (w >= cf.woff[cf.nl]) return;
+  int l = 0;
+  while (w >= cf.woff[l + 1]) ++l;
+  uint32_t x = bmE[w];
+  int64_t p = cf.loff[l] + (posE[w] - posE[cf.woff[l]]);
+  const uint64_t base = (uint64_t)(w - cf.woff[l]) * 32;
+  while (x) {
+    const int b = __ffs(x) - 1;
+    code[p] = base + b;
+    level[p] = l;
+    ++p;
+    x &= x - 1;
+  }
+}
+
 // per-level totals of a scanned bitmap: tot[l] = pos[woff[l+1]] - pos[woff[l]] (pos has
 // one extra trailing entry)
 template <int D>
@@ -950,6 +974,7 @@ static void build_tree_d(dmk_plan_s* P, const double* dpts) {
   // ---- box sets per level: E_l = B_l + non-empty children of B_{l-1}
   std::vector<DevBuf<uint64_t>> E(nlevels);
   std::vector<int64_t> nE(nlevels, 0);
+  const bool all_coarse = nlevels - 1 <= LBC;
   DevBuf<int32_t> bm_cnt, bm_pos;   // popcounts and exclusive scan of [B | E] bitmap words
   {
     // coarse levels: E bitmaps, then all coarse B and E lists from one scan and one
@@ -977,15 +1002,16 @@ static void build_tree_d(dmk_plan_s* P, const double* dpts) {
     int64_t ht[2 * (LBC + 1)];
     DMK_CUDA(cudaMemcpyAsync(ht, tot.p, sizeof(ht), cudaMemcpyDeviceToHost, s));
     DMK_CUDA(cudaStreamSynchronize(s));
-    for (int l = 0; l <= std::min(LBC, ltop); ++l) {
-      nB[l] = ht[l];
+    for (int l = 0; l <= std::min(LBC, ltop); ++l) nB[l] = ht[l];
+    for (int l = 0; l <= lc; ++l) nE[l] = ht[LBC + 1 + l];
+    // all levels coarse: the box arrays come straight from the bitmaps (no lists)
+    for (int l = 0; l <= std::min(LBC, ltop) && !all_coarse; ++l) {
       B[l].alloc(nB[l] ? nB[l] : 1, s);
       const int64_t nw = cs.woff[l + 1] - cs.woff[l];
       k_bm_fill<<<nblk(nw), TPB, 0, s>>>(bmB + cs.woff[l], pos.p + cs.woff[l], nw, B[l].p);
       DMK_LAUNCH_CHECK();
     }
-    for (int l = 0; l <= lc; ++l) {
-      nE[l] = ht[LBC + 1 + l];
+    for (int l = 0; l <= lc && !all_coarse; ++l) {
       E[l].alloc(nE[l] ? nE[l] : 1, s);
       const int64_t nw = cs.woff[l + 1] - cs.woff[l];
       k_bm_fill<<<nblk(nw), TPB, 0, s>>>(bmE + cs.woff[l], pos.p + W + cs.woff[l], nw, E[l].p);
@@ -1013,19 +1039,31 @@ static void build_tree_d(dmk_plan_s* P, const double* dpts) {
   const int64_t nbox = P->nbox = th.level_off[nlevels];
   P->box_code.alloc(nbox, s);
   P->box_level.alloc(nbox, s);
-  for (int l = 0; l < nlevels; ++l) {
-    DMK_CUDA(cudaMemcpyAsync(P->box_code.p + th.level_off[l], E[l].p, nE[l] * sizeof(uint64_t),
-                             cudaMemcpyDeviceToDevice, s));
-    k_fill_level<<<nblk(nE[l]), TPB, 0, s>>>(P->box_level.p, th.level_off[l], th.level_off[l + 1], l);
-    DMK_LAUNCH_CHECK();
-  }
   std::vector<int64_t> boff(nlevels + 1, 0);
-  for (int l = 0; l < nlevels; ++l) boff[l + 1] = boff[l] + ((l <= ltop) ? nB[l] : 0);
   DevBuf<uint64_t> Bcat;
-  Bcat.alloc(boff[nlevels] ? boff[nlevels] : 1, s);
-  for (int l = 0; l <= ltop; ++l)
-    if (nB[l])
-      DMK_CUDA(cudaMemcpyAsync(Bcat.p + boff[l], B[l].p, nB[l] * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
+  if (all_coarse) {
+    CoarseFill cf{};
+    for (int l = 0; l <= nlevels; ++l) {
+      cf.woff[l] = cs.woff[l];
+      cf.loff[l] = th.level_off[l];
+    }
+    cf.nl = nlevels;
+    k_coarse_boxes<<<nblk(cs.woff[nlevels]), TPB, 0, s>>>(bmE, bm_pos.p + W, cf, P->box_code.p, P->box_level.p);
+    DMK_LAUNCH_CHECK();
+    Bcat.alloc(1, s);   // unused: every level answers from the bitmaps
+  } else {
+    for (int l = 0; l < nlevels; ++l) {
+      DMK_CUDA(cudaMemcpyAsync(P->box_code.p + th.level_off[l], E[l].p, nE[l] * sizeof(uint64_t),
+                               cudaMemcpyDeviceToDevice, s));
+      k_fill_level<<<nblk(nE[l]), TPB, 0, s>>>(P->box_level.p, th.level_off[l], th.level_off[l + 1], l);
+      DMK_LAUNCH_CHECK();
+    }
+    for (int l = 0; l < nlevels; ++l) boff[l + 1] = boff[l] + ((l <= ltop) ? nB[l] : 0);
+    Bcat.alloc(boff[nlevels] ? boff[nlevels] : 1, s);
+    for (int l = 0; l <= ltop; ++l)
+      if (nB[l])
+        DMK_CUDA(cudaMemcpyAsync(Bcat.p + boff[l], B[l].p, nB[l] * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
+  }
 
   P->box_start.alloc(nbox, s);
   P->box_end.alloc(nbox, s);
