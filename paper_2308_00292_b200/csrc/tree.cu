@@ -605,10 +605,18 @@ __global__ void k_flag_targets(const int32_t* start, const int32_t* end, const i
   if (tgt) flags[i] |= 16;
 }
 
-__global__ void k_rank(const int32_t* scan, const uint8_t* sel, int64_t nbox, int32_t* rank) {
+// ranks in the compact F_out / local-expansion arrays and the compact box lists
+// themselves (scatter by rank), both kinds in one pass
+__global__ void k_ranks_lists(const int32_t* __restrict__ fscan, const uint8_t* __restrict__ fsel,
+                              const int32_t* __restrict__ escan, const uint8_t* __restrict__ esel, int64_t nbox,
+                              int32_t* frank, int32_t* erank, int32_t* flist, int32_t* elist) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= nbox) return;
-  rank[i] = sel[i] ? scan[i] : -1;
+  const bool f = fsel[i], e = esel[i];
+  frank[i] = f ? fscan[i] : -1;
+  erank[i] = e ? escan[i] : -1;
+  if (f) flist[fscan[i]] = (int32_t)i;
+  if (e) elist[escan[i]] = (int32_t)i;
 }
 
 // direct lists: pass 0 counts, pass 1 fills; one warp per box, lanes over the colleague
@@ -1129,8 +1137,10 @@ static void build_tree_d(dmk_plan_s* P, const double* dpts) {
   exclusive_scan_u8(s, esel.p, escan.p, nbox + 1);
   P->fout_rank.alloc(nbox, s);
   P->exp_rank.alloc(nbox, s);
-  k_rank<<<nblk(nbox), TPB, 0, s>>>(fscan.p, fsel.p, nbox, P->fout_rank.p);
-  k_rank<<<nblk(nbox), TPB, 0, s>>>(escan.p, esel.p, nbox, P->exp_rank.p);
+  P->fout_list.alloc(nbox, s);   // capacity nbox: filled before the sizes are known on the host
+  P->exp_list.alloc(nbox, s);
+  k_ranks_lists<<<nblk(nbox), TPB, 0, s>>>(fscan.p, fsel.p, escan.p, esel.p, nbox, P->fout_rank.p, P->exp_rank.p,
+                                           P->fout_list.p, P->exp_list.p);
   DMK_LAUNCH_CHECK();
   // direct lists (CSR over boxes) and P2P work items: counts and scans, then the flag
   // totals, per-level rank offsets and list sizes in ONE round trip, then the fills
@@ -1172,19 +1182,6 @@ static void build_tree_d(dmk_plan_s* P, const double* dpts) {
     }
     P->ndlist = h[2 * m];
     P->np2p = h[2 * m + 1];
-  }
-  {
-    cub::CountingInputIterator<int32_t> cnt_it(0);
-    DevBuf<int64_t> nsel;
-    nsel.alloc(1, s);
-    P->fout_list.alloc(P->nfout ? P->nfout : 1, s);
-    P->exp_list.alloc(P->nexp ? P->nexp : 1, s);
-    cub_run(s, [&](void* t, size_t& b) {
-      return cub::DeviceSelect::Flagged(t, b, cnt_it, fsel.p, P->fout_list.p, nsel.p, nbox, s);
-    });
-    cub_run(s, [&](void* t, size_t& b) {
-      return cub::DeviceSelect::Flagged(t, b, cnt_it, esel.p, P->exp_list.p, nsel.p, nbox, s);
-    });
   }
   mark("flags");
   P->dlist.alloc(P->ndlist ? P->ndlist : 1, s);
