@@ -125,6 +125,9 @@ class Plan:
                               ctypes.byref(h)), "dmk_plan")
         self._h = h
         self.n = int(n)
+        # the plan's stream may still read the points after dmk_plan returns (no
+        # synchronisation there): keep them alive until close()
+        self._points = keep
 
     def eval(self, charges, out=None):
         """Potentials u_i = sum_{j: x_j != x_i} K(|x_i - x_j|) rho_j (caller order)."""
@@ -204,6 +207,7 @@ class Plan:
         if getattr(self, "_h", None):
             lib().dmk_destroy(self._h)
             self._h = None
+        self._points = None
 
     def __del__(self):
         try:

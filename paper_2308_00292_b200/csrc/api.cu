@@ -192,7 +192,9 @@ int dmk_plan(int dim, int kernel, double eps, int64_t n, const double* points, i
       // lambda' = lambda * side (K(side r') = exp(-lambda' r')/(side r'))
       P->tab = &get_tables(kernel, eps, kernel == DMK_KERNEL_YUKAWA ? P->lambda * P->side : 0.0);
       alloc_eval_buffers(P);
-      DMK_CUDA(cudaStreamSynchronize(P->stream));
+      // no synchronisation: the plan's device work is ordered on P->stream before any
+      // evaluation or read-back (all of which run on P->stream)
+      DMK_CUDA(cudaGetLastError());
     } catch (...) {
       delete P;
       throw;
