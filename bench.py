@@ -209,7 +209,7 @@ def run_reference(a):
         cores = os.cpu_count()
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "points/s", "n_gpus": a.gpus,
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64+f32" if info.p <= 18 else "f64", "data": "synthetic",
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": WORKLOAD, "sample_points": n_s, "eps": a.eps, "leaf_capacity": a.ns},
             "cpu_baseline": {"value": value, "unit": "points/s", "cores": cores, "kind": "oracle",
                              "sample": f"each step: oracle DMK on {n_s} points of the config-1 distribution"},
@@ -305,7 +305,7 @@ def run_distributed(a):
         line = {
             "metric": METRIC, "value": a.n * world / (t_step * 1e-3), "unit": "points/s", "n_gpus": world,
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": t_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64+f32" if info.p <= 18 else "f64", "data": "synthetic",
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64+f32" if a.eps > 5e-7 else "f64", "data": "synthetic",
             "config": {"workload": f"uniform iid in [0,1]^3, {a.n} points per GPU, one global problem of "
                                    f"{a.n * world} points, 3D Laplace, eps={a.eps}, leaf capacity {a.ns}",
                        "N_per_gpu": a.n, "eps": a.eps, "leaf_capacity": a.ns,
