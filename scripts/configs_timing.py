@@ -18,6 +18,7 @@ import paper_2308_00292_b200 as dmk  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--only", default="")
 a = ap.parse_args()
 CONFIGS = [
     ("config0 laplace uniform 1e4 eps1e-6", "uniform", 10_000, 1e-6, "laplace", 0.0),
@@ -29,6 +30,8 @@ CONFIGS = [
     ("config4 yukawa uniform 1e8 eps1e-6 (1 GPU)", "uniform", 100_000_000, 1e-6, "yukawa", 10.0),
 ]
 for name, kind, n, eps, kernel, lam in CONFIGS:
+    if a.only and a.only not in name:
+        continue
     x, q = dmk_inputs.make(kind, n, seed=1)
     X, Q = torch.as_tensor(x, device="cuda"), torch.as_tensor(q, device="cuda")
     del x, q
