@@ -100,21 +100,25 @@ class Clocks:
 
 
 def stage_models(info, n, pairs, K, inball):
-    """Algorithmic work per phase: (bound, amount, unit)."""
+    """Algorithmic work per phase: (bound, amount, unit, precision)."""
     P, nf, nf0 = info.p, info.nf, info.nf0
     p3 = P ** 3
-    # outgoing expansions, real parity-split form: 8 (nf+1)^3 doubles per box
-    phi_bytes = 8 * 8 * ((nf0 + 1) ** 3 + (info.nfout - 1) * (nf + 1) ** 3)
+    fp32 = P <= 18   # precision tier (reading R16)
+    # outgoing expansions, real parity-split form: 8 (nf+1)^3 values per box, stored in
+    # fp32 (4 bytes) for p <= 18, fp64 otherwise
+    phi_bytes = 8 * (4 if fp32 else 8) * ((nf0 + 1) ** 3 + (info.nfout - 1) * (nf + 1) ** 3)
+    alu = "fp32" if fp32 else "fp64"
     return {
-        "anterp": ("alu", 2.0 * p3 * n, "flop"),
-        "c2p": ("alu", 2.0 * 3 * P ** 4 * (info.nfout - 1), "flop"),
-        "prox2pw": ("hbm", 8.0 * p3 * info.nfout + phi_bytes, "byte"),
-        "pwlocal": ("hbm", phi_bytes + 8.0 * p3 * info.nexp, "byte"),
-        "p2c": ("alu", 2.0 * 3 * P ** 4 * (info.nexp - 1), "flop"),
-        "eval": ("alu", 2.0 * p3 * n, "flop"),
+        "anterp": ("alu", 2.0 * p3 * n, "flop", alu),
+        # c2p / p2c by parent groups: 14 p^4 FMA per parent of 8 children = 3.5 p^4 flop per child
+        "c2p": ("alu", 3.5 * P ** 4 * (info.nfout - 1), "flop", "fp64"),
+        "prox2pw": ("hbm", 8.0 * p3 * info.nfout + phi_bytes, "byte", None),
+        "pwlocal": ("hbm", phi_bytes + 8.0 * p3 * info.nexp, "byte", None),
+        "p2c": ("alu", 3.5 * P ** 4 * (info.nexp - 1), "flop", "fp64"),
+        "eval": ("alu", 2.0 * p3 * n, "flop", alu),
         # every list pair: distance test (9 flop); pairs inside the residual's ball
         # r < r_L: polynomial (2K), rsqrt (~6), s and the accumulate (6)
-        "p2p": ("alu", 9.0 * pairs + (2.0 * K + 12.0) * inball, "flop"),
+        "p2p": ("alu", 9.0 * pairs + (2.0 * K + 12.0) * inball, "flop", alu),
     }
 
 
@@ -465,20 +469,19 @@ def main():
     fp64_peak = N_SM * FP64_FMA_PER_CLK_SM * 2 * pk.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
     # fp32 tier (reading R16, p <= 18): the P2P pairs run in single precision
     fp32_peak = N_SM * FP32_FMA_PER_CLK_SM * 2 * pk.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
-    p2p32 = info.p <= 18
     models = stage_models(info, a.n, pairs, info.respoly_degree, inball)
     stages = {}
-    for name, (bound, amount, unit) in models.items():
+    for name, (bound, amount, unit, prec) in models.items():
         ms = stage_ms.get(name)
         if not ms:
             continue
         if bound == "hbm":
             ach, peak, u_ = amount / (ms * 1e-3) / 1e9, pk["hbm_gbs"], "GB/s"
         else:
-            pk_ = fp32_peak if (name == "p2p" and p2p32) else fp64_peak
+            pk_ = fp32_peak if prec == "fp32" else fp64_peak
             ach, peak, u_ = amount / (ms * 1e-3) / 1e12, pk_, "TFLOP/s"
         stages[name] = {"ms": round(ms, 4), "bound": bound, "achieved": round(ach, 3), "peak": round(peak, 1),
-                        "unit": u_, "frac": round(ach / peak, 4)}
+                        "unit": u_, "frac": round(ach / peak, 4), **({"precision": prec} if prec else {})}
     tree_ms = float(np.mean(plan_ms))          # dmk_plan: tree, lists, tables (cached)
     dom = max(stages, key=lambda s: stages[s]["ms"])
     roof = dict(stages[dom])
@@ -491,7 +494,7 @@ def main():
                  "traffic_source": "profiles/r01_traffic.json (ncu --set full, dram bytes per launch)",
                  "peak_source": ("MEASURED_PEAKS.json hbm_gbs" if roof["bound"] == "hbm" else
                                  "derived: 148 SM x 128 fp32 FMA/clk x 2 x sm_max_mhz (DESIGN.md 8(d))"
-                                 if (dom == "p2p" and p2p32) else
+                                 if roof.get("precision") == "fp32" else
                                  "derived: 148 SM x 64 fp64 FMA/clk x 2 x sm_max_mhz (DESIGN.md 8(d))")})
     line = {
         "metric": METRIC, "value": value, "unit": "points/s", "n_gpus": world, "steps": a.steps,
