@@ -21,7 +21,7 @@
 //   k_pwlocal<P,H>    translation (p = 28) or its k_pwshift result, then T_pw2poly
 //                  Lambda_own(B) = (Gr (x) Gr (x) Gr) Psi_l(B)
 //   k_p2c_grp<P>   Lambda(children) += (A^T)^{(x)3} Lambda(parent) by parent groups
-//   k_eval_pad<P> / k_eval_mma<P>   far field at targets from Lambda (DMMA)
+//   k_eval32<P> / k_eval_mma<P>   far field at targets from Lambda (fp32 tier / DMMA)
 //   k_p2p<K> / k_p2p32<K>   residual kernel R_{L_S} over the direct lists (warp per
 //                  item of <= 32 targets, fp64 or the fp32 tier), self terms
 //   k_combine      (u_far + u_near)/side, scattered to the caller's order
@@ -31,22 +31,6 @@
 #include "device.cuh"
 
 namespace dmk {
-
-// ---------------------------------------------------------------- tiling configs
-template <int P>
-struct Cfg;
-template <>
-struct Cfg<9> {
-  static constexpr int TB = 3, RB = 3, TA = 27, RA = 3, CH = 32, ECH = 16;
-};
-template <>
-struct Cfg<18> {
-  static constexpr int TB = 3, RB = 6, TA = 54, RA = 6, CH = 32, ECH = 16;
-};
-template <>
-struct Cfg<28> {
-  static constexpr int TB = 4, RB = 7, TA = 98, RA = 8, CH = 16, ECH = 8;
-};
 
 // ---------------------------------------------------------------- gather
 // q[i] = charges[perm[i]] (Morton order, fp64); with the fp32 P2P tier also the charge
@@ -58,79 +42,6 @@ __global__ void k_gather_q(const double* __restrict__ charges, const int32_t* __
   const double v = charges[perm[i]];
   q[i] = v;
   if (xl4) xl4[i].w = (float)v;
-}
-
-// ---------------------------------------------------------------- anterpolation
-// mu[a=(n1,n2)][b=n3] += sum_j (rho_j Tx_j[n1] Ty_j[n2]) Tz_j[n3]
-template <int P>
-__global__ void __launch_bounds__(Cfg<P>::TA * Cfg<P>::TB)
-    k_anterp(DevTree t, const int32_t* __restrict__ boxes, const double* __restrict__ q, double* __restrict__ mom) {
-  using C = Cfg<P>;
-  constexpr int NT = C::TA * C::TB, P2 = P * P, CH = C::CH;
-  extern __shared__ double sm[];
-  double* sU = sm;                 // [CH][P2]
-  double* sV = sU + CH * P2;       // [CH][P]
-  double* sT = sV + CH * P;        // [CH][2][P] (rho Tx, Ty)
-  __shared__ int2 rg[8];
-  __shared__ int nr_s, tot_s;
-  const int b = boxes[blockIdx.x];
-  if (threadIdx.x == 0) {
-    nr_s = box_ranges<false>(t, b, rg);
-    int tot = 0;
-    for (int r = 0; r < nr_s; ++r) tot += rg[r].y - rg[r].x;
-    tot_s = tot;
-  }
-  __syncthreads();
-  const int nr = nr_s, tot = tot_s;
-  if (tot == 0) return;   // moments were zeroed by the caller
-  double cen[3], ih;
-  box_geom(t.code[b], t.level[b], cen, ih);
-  const int tid = threadIdx.x, tb = tid % C::TB, ta = tid / C::TB;
-  double acc[C::RA][C::RB];
-#pragma unroll
-  for (int i = 0; i < C::RA; ++i)
-#pragma unroll
-    for (int k = 0; k < C::RB; ++k) acc[i][k] = 0.0;
-
-  for (int c0 = 0; c0 < tot; c0 += CH) {
-    const int nc = min(CH, tot - c0);
-    for (int w = tid; w < CH * 3; w += NT) {   // Chebyshev vectors
-      int j = w / 3, d = w % 3;
-      double T[P];
-      if (j < nc) {
-        int pi = range_point(rg, nr, c0 + j);
-        double x = (d == 0 ? t.xs[pi] : d == 1 ? t.ys[pi] : t.zs[pi]);
-        cheb_vec((x - cen[d]) * ih, T, P, d == 0 ? q[pi] : 1.0);
-      } else {
-        for (int n = 0; n < P; ++n) T[n] = 0.0;
-      }
-      double* dst = (d == 2) ? (sV + j * P) : (sT + (j * 2 + d) * P);
-      for (int n = 0; n < P; ++n) dst[n] = T[n];
-    }
-    __syncthreads();
-    for (int w = tid; w < CH * P2; w += NT) {
-      int j = w / P2, a = w % P2;
-      sU[w] = sT[(j * 2) * P + a / P] * sT[(j * 2 + 1) * P + a % P];
-    }
-    __syncthreads();
-    for (int j = 0; j < nc; ++j) {
-      double u[C::RA], v[C::RB];
-#pragma unroll
-      for (int i = 0; i < C::RA; ++i) u[i] = sU[j * P2 + ta + i * C::TA];
-#pragma unroll
-      for (int k = 0; k < C::RB; ++k) v[k] = sV[j * P + tb + k * C::TB];
-#pragma unroll
-      for (int i = 0; i < C::RA; ++i)
-#pragma unroll
-        for (int k = 0; k < C::RB; ++k) acc[i][k] = fma(u[i], v[k], acc[i][k]);
-    }
-    __syncthreads();
-  }
-  double* out = mom + (size_t)t.fout_rank[b] * P * P2;
-#pragma unroll
-  for (int i = 0; i < C::RA; ++i)
-#pragma unroll
-    for (int k = 0; k < C::RB; ++k) out[(ta + i * C::TA) * P + tb + k * C::TB] = acc[i][k];
 }
 
 // ---- fp32 tier (reading R16, p <= 18): anterpolation and evaluation on the FP32 pipes
@@ -1184,86 +1095,7 @@ __global__ void __launch_bounds__(PwLocal<P, H, AC>::NT, PwLocal<P, H, AC>::MINB
   }
 }
 
-// ---------------------------------------------------------------- evaluation
-template <int P>
-__global__ void __launch_bounds__(Cfg<P>::TA * Cfg<P>::TB)
-    k_eval(DevTree t, const int32_t* __restrict__ boxes, const double* __restrict__ lam, double* __restrict__ ufar) {
-  using C = Cfg<P>;
-  constexpr int NT = C::TA * C::TB, P2 = P * P, CH = C::ECH;
-  extern __shared__ double sm[];
-  double* sU = sm;                 // [CH][P2]
-  double* sV = sU + CH * P2;       // [CH][P]
-  double* sT = sV + CH * P;        // [CH][2][P]
-  double* red = sT + CH * 2 * P;   // [NT][CH]
-  __shared__ int2 rg[8];
-  __shared__ int nr_s, tot_s;
-  const int b = boxes[blockIdx.x];
-  if (threadIdx.x == 0) {
-    nr_s = box_ranges<true>(t, b, rg);
-    int tot = 0;
-    for (int r = 0; r < nr_s; ++r) tot += rg[r].y - rg[r].x;
-    tot_s = tot;
-  }
-  __syncthreads();
-  const int nr = nr_s, tot = tot_s;
-  if (tot == 0) return;
-  double cen[3], ih;
-  box_geom(t.code[b], t.level[b], cen, ih);
-  const int tid = threadIdx.x, tb = tid % C::TB, ta = tid / C::TB;
-  double L[C::RA][C::RB];
-  const double* src = lam + (size_t)t.exp_rank[b] * P * P2;
-#pragma unroll
-  for (int i = 0; i < C::RA; ++i)
-#pragma unroll
-    for (int k = 0; k < C::RB; ++k) L[i][k] = src[(ta + i * C::TA) * P + tb + k * C::TB];
-  // reduction uses only complete warps (NT need not be a multiple of 32)
-  const int lane = tid & 31, warp = tid >> 5, nwarp = NT / 32;
-  for (int c0 = 0; c0 < tot; c0 += CH) {
-    const int nc = min(CH, tot - c0);
-    for (int w = tid; w < CH * 3; w += NT) {
-      int j = w / 3, d = w % 3;
-      double T[P];
-      if (j < nc) {
-        int pi = range_point(rg, nr, c0 + j);
-        double x = (d == 0 ? t.xs[pi] : d == 1 ? t.ys[pi] : t.zs[pi]);
-        cheb_vec((x - cen[d]) * ih, T, P, 1.0);
-      } else {
-        for (int n = 0; n < P; ++n) T[n] = 0.0;
-      }
-      double* dst = (d == 2) ? (sV + j * P) : (sT + (j * 2 + d) * P);
-      for (int n = 0; n < P; ++n) dst[n] = T[n];
-    }
-    __syncthreads();
-    for (int w = tid; w < CH * P2; w += NT) {
-      int j = w / P2, a = w % P2;
-      sU[w] = sT[(j * 2) * P + a / P] * sT[(j * 2 + 1) * P + a % P];
-    }
-    __syncthreads();
-    for (int j = 0; j < CH; ++j) {
-      double part = 0.0;
-      if (j < nc) {
-#pragma unroll
-        for (int i = 0; i < C::RA; ++i) {
-          double g = 0.0;
-#pragma unroll
-          for (int k = 0; k < C::RB; ++k) g = fma(L[i][k], sV[j * P + tb + k * C::TB], g);
-          part = fma(g, sU[j * P2 + ta + i * C::TA], part);
-        }
-      }
-      red[tid * CH + j] = part;
-    }
-    __syncthreads();
-    for (int j = warp; j < nc && warp < nwarp; j += nwarp) {
-      double s = 0.0;
-      for (int i = lane; i < NT; i += 32) s += red[i * CH + j];
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-      if (lane == 0) ufar[range_point(rg, nr, c0 + j)] = s;
-    }
-    __syncthreads();
-  }
-}
-
+// ---------------------------------------------------------------- evaluation (p = 28)
 // Far-field evaluation: u_j = sum_a (Tx_j[n1] Ty_j[n2]) G[j][a],  G = V Lambda^T,
 // V[j][b] = Tz_j[b]  (a = n1 P + n2, b = n3).  One CTA per local-expansion box,
 // Lambda in smem in DMMA-fragment order, each warp evaluates tiles of 8 targets.
@@ -1343,98 +1175,6 @@ __global__ void __launch_bounds__(256) k_eval_mma(DevTree t, const int32_t* __re
       a += 8;
       if (two && a < P2) part = fma(d0, Tx[a / P] * Ty[a % P], part);
       if (two && a + 1 < P2) part = fma(d1, Tx[(a + 1) / P] * Ty[(a + 1) % P], part);
-    }
-    part += __shfl_xor_sync(0xffffffffu, part, 1);
-    part += __shfl_xor_sync(0xffffffffu, part, 2);
-    if (q4 == 0 && g < nv) ufar[range_point(rg, nr, tt + g)] = part;
-    __syncwarp();
-  }
-}
-
-// Far-field evaluation, padded-tile form (P <= 18): the DMMA n dimension runs over
-// (n1, n2) with n2 padded to NB blocks of 8, so every output tile has a single n1 and
-// the epilogue u_j += Tx_j[n1] (c0 Ty_j[n2] + c1 Ty_j[n2+1]) needs no index division
-// (the unpadded version spends most of its issue slots there).
-template <int P>
-struct EvalPad {
-  static constexpr int KS = (P + 3) / 4, NB = (P + 7) / 8, NTL = P * NB, NW = 8;
-  static constexpr size_t smem = sizeof(double) * ((size_t)NTL * KS * 32 + (size_t)NW * 8 * 3 * P);
-};
-template <int P>
-__global__ void __launch_bounds__(256) k_eval_pad(DevTree t, const int32_t* __restrict__ boxes,
-                                                  const double* __restrict__ lam, double* __restrict__ ufar) {
-  using E = EvalPad<P>;
-  constexpr int P2 = P * P, KS = E::KS, NB = E::NB, NTL = E::NTL, NW = E::NW;
-  extern __shared__ double sm[];
-  double* lamF = sm;                        // [NTL][KS][32] B fragments, tile nt = n1*NB + blk
-  double* Tv = lamF + NTL * KS * 32;        // [NW][8 targets][3 dims][P]
-  __shared__ int2 rg[8];
-  __shared__ int nr_s, tot_s;
-  const int b = boxes[blockIdx.x], tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) {
-    nr_s = box_ranges<true>(t, b, rg);
-    int tot = 0;
-    for (int r = 0; r < nr_s; ++r) tot += rg[r].y - rg[r].x;
-    tot_s = tot;
-  }
-  const double* src = lam + (size_t)t.exp_rank[b] * P * P2;
-  for (int i = tid; i < NTL * KS * 32; i += NW * 32) {
-    const int ln = i & 31, ks = (i >> 5) % KS, nt = (i >> 5) / KS;
-    const int n1 = nt / NB, n2 = (nt % NB) * 8 + (ln >> 2), n3 = ks * 4 + (ln & 3);
-    lamF[i] = (n2 < P && n3 < P) ? src[(n1 * P + n2) * P + n3] : 0.0;
-  }
-  __syncthreads();
-  const int nr = nr_s, tot = tot_s;
-  if (tot == 0) return;
-  double cen[3], ih;
-  box_geom(t.code[b], t.level[b], cen, ih);
-  double* T = Tv + warp * 8 * 3 * P;
-  const int g = lane >> 2, q4 = lane & 3;
-  for (int tt = warp * 8; tt < tot; tt += NW * 8) {
-    const int nv = min(8, tot - tt);
-    if (lane < 24) {
-      const int j = lane / 3, d = lane % 3;
-      double Tl[P];
-      if (j < nv) {
-        const int pi = range_point(rg, nr, tt + j);
-        const double x = (d == 0 ? t.xs[pi] : d == 1 ? t.ys[pi] : t.zs[pi]);
-        cheb_vec((x - cen[d]) * ih, Tl, P, 1.0);
-      } else {
-#pragma unroll
-        for (int n = 0; n < P; ++n) Tl[n] = 0.0;
-      }
-#pragma unroll
-      for (int n = 0; n < P; ++n) T[(j * 3 + d) * P + n] = Tl[n];
-    }
-    __syncwarp();
-    double af[KS], ty[NB][2];
-#pragma unroll
-    for (int ks = 0; ks < KS; ++ks) {
-      const int n3 = ks * 4 + q4;
-      af[ks] = n3 < P ? T[(g * 3 + 2) * P + n3] : 0.0;
-    }
-#pragma unroll
-    for (int bl = 0; bl < NB; ++bl)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int n2 = bl * 8 + 2 * q4 + e;
-        ty[bl][e] = n2 < P ? T[(g * 3 + 1) * P + n2] : 0.0;
-      }
-    const double* Tx = T + (g * 3 + 0) * P;
-    double part = 0.0;
-#pragma unroll 1
-    for (int n1 = 0; n1 < P; ++n1) {
-      double c[NB][2];
-#pragma unroll
-      for (int bl = 0; bl < NB; ++bl) c[bl][0] = c[bl][1] = 0.0;
-#pragma unroll
-      for (int ks = 0; ks < KS; ++ks)
-#pragma unroll
-        for (int bl = 0; bl < NB; ++bl) dmma(c[bl][0], c[bl][1], af[ks], lamF[((n1 * NB + bl) * KS + ks) * 32 + lane]);
-      double v = 0.0;
-#pragma unroll
-      for (int bl = 0; bl < NB; ++bl) v = fma(c[bl][0], ty[bl][0], fma(c[bl][1], ty[bl][1], v));
-      part = fma(Tx[n1], v, part);
     }
     part += __shfl_xor_sync(0xffffffffu, part, 1);
     part += __shfl_xor_sync(0xffffffffu, part, 2);
@@ -1811,7 +1551,6 @@ static void run_c2p_level(dmk_plan_s* PL, const DevTree& dt, int l) {
 
 template <int P, int NF, int NF0>
 static void run_eval(dmk_plan_s* PL, int phase = PH_UP | PH_DOWN, int top = 0) {
-  using C = Cfg<P>;
   cudaStream_t s = PL->stream;
   const Tables& T = *PL->tab;
   DevTree dt = dev_tree(PL);

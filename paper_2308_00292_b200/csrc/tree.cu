@@ -266,18 +266,6 @@ __global__ void k_touch(const uint64_t* __restrict__ Bq, int64_t nq, int l, uint
   if (flags) flags[t] = ok ? 1 : 0;
 }
 
-// non-empty level-l boxes whose parent is non-leaf
-template <int D>
-__global__ void k_nonempty(const uint64_t* __restrict__ keys, int64_t n, int l, const uint64_t* __restrict__ Bp,
-                           int64_t nBp, uint64_t* codes, uint8_t* flags) {
-  int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (a >= n) return;
-  int sh = D * (NBITS - l);
-  uint64_t c = keys[a] >> sh;
-  bool start = (a == 0) || ((keys[a - 1] >> sh) != c);
-  codes[a] = c;
-  flags[a] = (start && bsearch_u64(Bp, nBp, c >> D) >= 0) ? 1 : 0;
-}
 
 // box set of level l: children of the level-(l-1) non-leaf boxes that hold points or are
 // themselves non-leaf (candidates enumerated in Morton order, so the selection is sorted)
@@ -418,15 +406,6 @@ __global__ void k_bm_totals(const int32_t* __restrict__ pos, Coarse<D> cs, int64
   if (l <= Coarse<D>::LBC) tot[l] = pos[base + cs.woff[l + 1]] - pos[base + cs.woff[l]];
 }
 
-// out[i] = a[idx[i]], out[m + i] = b[idx[i]]: many scalar reads, one round trip
-__global__ void k_read_at(const int32_t* __restrict__ a, const int32_t* __restrict__ b,
-                          const int64_t* __restrict__ idx, int m, int64_t* out) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < m) {
-    out[i] = a[idx[i]];
-    out[m + i] = b[idx[i]];
-  }
-}
 
 struct ReadIdx {   // by value
   int64_t v[LMAX + 3];
@@ -448,10 +427,6 @@ __global__ void k_read_totals(const int32_t* __restrict__ fscan, const int32_t* 
   }
 }
 
-__global__ void k_iota_u64(uint64_t* out, int64_t n) {
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i < n) out[i] = (uint64_t)i;
-}
 
 __global__ void k_fill_level(int32_t* lev, int64_t a, int64_t b, int l) {
   int64_t i = a + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;

@@ -1,3 +1,3 @@
 timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/t.log 2>&1; tail -2 gpurun_out/t.log
 python scripts/tree_prof.py 2>&1 | tail -1
-python bench.py --steps 10 --warmup 3 > gpurun_out/bench_r22.json 2> gpurun_out/bench_r22.err; tail -2 gpurun_out/bench_r22.err
+python bench.py --steps 10 --warmup 3 > gpurun_out/bench_r23.json 2> gpurun_out/bench_r23.err; tail -2 gpurun_out/bench_r23.err
