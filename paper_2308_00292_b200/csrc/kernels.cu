@@ -256,13 +256,16 @@ __global__ void __launch_bounds__(Ev32<P>::NT) k_eval32(DevTree t, const int32_t
 // memory, each contraction a DMMA GEMM (mma_tiles).
 template <int P, int MT>
 struct GrpCfg {
+  // p = 28: one CTA per SM fits (shared memory), so 16 warps instead of 8 keep more
+  // tiles' operand loads in flight
+  static constexpr int NT = P > 18 ? 512 : 256;
   static constexpr int P2 = P * P, NTILE = (P + MT - 1) / MT;
   static constexpr int KS2 = (2 * P + 3) / 4, KS1 = (P + 3) / 4;
   static constexpr size_t smem_c2p = sizeof(double) * ((size_t)2 * P2 + 6 * (size_t)MT * P2);
   static constexpr size_t smem_p2c = sizeof(double) * ((size_t)2 * P2 + 6 * (size_t)MT * P2);
 };
 template <int P, int MT>
-__global__ void __launch_bounds__(256) k_c2p_grp(DevTree t, const int32_t* __restrict__ parents,
+__global__ void __launch_bounds__(GrpCfg<P, MT>::NT) k_c2p_grp(DevTree t, const int32_t* __restrict__ parents,
                                                  const double* __restrict__ A, double* __restrict__ mom) {
   using C = GrpCfg<P, MT>;
   constexpr int P2 = C::P2, P3 = P2 * P, KS2 = C::KS2;
@@ -277,7 +280,7 @@ __global__ void __launch_bounds__(256) k_c2p_grp(DevTree t, const int32_t* __res
     const int c = t.child[8 * (int64_t)b + tid];
     ch[tid] = (c >= 0 && (t.flags[c] & F_OUT)) ? mom + (size_t)t.fout_rank[c] * P3 : nullptr;
   }
-  for (int i = tid; i < 2 * P2; i += 256) sA[i] = A[i];
+  for (int i = tid; i < 2 * P2; i += C::NT) sA[i] = A[i];
   __syncthreads();
   bool any = false;
 #pragma unroll
@@ -351,7 +354,7 @@ __global__ void __launch_bounds__(256) k_c2p_grp(DevTree t, const int32_t* __res
 }
 
 template <int P, int MT>
-__global__ void __launch_bounds__(256) k_p2c_grp(DevTree t, const int32_t* __restrict__ parents,
+__global__ void __launch_bounds__(GrpCfg<P, MT>::NT) k_p2c_grp(DevTree t, const int32_t* __restrict__ parents,
                                                  const double* __restrict__ A, double* __restrict__ lam) {
   using C = GrpCfg<P, MT>;
   constexpr int P2 = C::P2, P3 = P2 * P, KS1 = C::KS1, KS2 = C::KS2;
@@ -366,7 +369,7 @@ __global__ void __launch_bounds__(256) k_p2c_grp(DevTree t, const int32_t* __res
     const int c = t.child[8 * (int64_t)b + tid];
     ch[tid] = (c >= 0 && (t.flags[c] & F_EXP)) ? lam + (size_t)t.exp_rank[c] * P3 : nullptr;
   }
-  for (int i = tid; i < 2 * P2; i += 256) sA[i] = A[i];
+  for (int i = tid; i < 2 * P2; i += C::NT) sA[i] = A[i];
   __syncthreads();
   bool any = false;
 #pragma unroll
@@ -490,11 +493,12 @@ __device__ __forceinline__ double dot_par(const double* __restrict__ row, const 
 template <int P, int H, int CH>
 struct Prox2pw {
   using G = PwGeom<P, H>;
-  static constexpr int NT = 256, KS = ((P + 1) / 2 + 3) / 4, HP = (H + 7) / 8 * 8;
+  // p = 28: one CTA per SM (shared memory), 16 warps to keep more DMMA tiles in flight
+  static constexpr int NT = P > 18 ? 512 : 256, KS = ((P + 1) / 2 + 3) / 4, HP = (H + 7) / 8 * 8;
   static constexpr size_t smem = sizeof(double) * ((size_t)2 * HP * KS * 4 + (size_t)P * P * CH + (size_t)H * P * CH);
 };
 template <int P, int H, int CH>
-__global__ void __launch_bounds__(256) k_prox2pw(DevTree t, const int32_t* __restrict__ boxes,
+__global__ void __launch_bounds__(Prox2pw<P, H, CH>::NT) k_prox2pw(DevTree t, const int32_t* __restrict__ boxes,
                                                  const double* __restrict__ Qr, const double* __restrict__ mom,
                                                  FStore<P>* __restrict__ F, size_t base, size_t stride) {
   using G = PwGeom<P, H>;
@@ -1545,7 +1549,7 @@ static void run_c2p_level(dmk_plan_s* PL, const DevTree& dt, int l) {
   if (b <= a || cb <= ca) return;
   set_smem(k_c2p_grp<P, MT>, G::smem_c2p);
   const unsigned grid = (unsigned)((b - a) * G::NTILE);
-  k_c2p_grp<P, MT><<<grid, 256, G::smem_c2p, s>>>(dt, PL->fout_list.p + a, PL->tab->dA, PL->mom.p);
+  k_c2p_grp<P, MT><<<grid, G::NT, G::smem_c2p, s>>>(dt, PL->fout_list.p + a, PL->tab->dA, PL->mom.p);
   DMK_LAUNCH_CHECK();
 }
 
@@ -1677,7 +1681,7 @@ static void run_eval(dmk_plan_s* PL, int phase = PH_UP | PH_DOWN, int top = 0) {
         const int64_t a = th.exp_off[l - 1], b = th.exp_off[l];
         if (b <= a || th.exp_off[l + 1] <= th.exp_off[l]) continue;
         const unsigned grid = (unsigned)((b - a) * G::NTILE);
-        k_p2c_grp<P, MT><<<grid, 256, G::smem_p2c, s>>>(dt, PL->exp_list.p + a, T.dA, PL->lam.p);
+        k_p2c_grp<P, MT><<<grid, G::NT, G::smem_p2c, s>>>(dt, PL->exp_list.p + a, T.dA, PL->lam.p);
         DMK_LAUNCH_CHECK();
       }
     }
