@@ -138,6 +138,11 @@ struct dmk_plan_s {
   // work list for the P2P kernel: (leaf box, first target) items of <= 32 targets
   dmk::DevBuf<int32_t> p2p_items;
   int64_t np2p = 0;
+  // Sec. 3.4 form (3D): octant offsets of every leaf, octant work items (leaf, octant,
+  // t0, t1), number of target leaves (the form is chosen for big leaves)
+  dmk::DevBuf<int32_t> leaf_oct;
+  dmk::DevBuf<int4> p2p_items_o;
+  int64_t np2p_o = 0, nleaf_t = 0;
   // fp32 P2P tier (p <= 18): leaf-local double-single source records, Morton order:
   // (x, y, z, rho) high parts and (x, y, z, 0) low parts
   dmk::DevBuf<float4> xl4, xl4lo;

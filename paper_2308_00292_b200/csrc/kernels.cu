@@ -25,6 +25,7 @@
 //   k_p2p<K> / k_p2p32<K>   residual kernel R_{L_S} over the direct lists (warp per
 //                  item of <= 32 targets, fp64 or the fp32 tier), self terms
 //   k_combine      (u_far + u_near)/side, scattered to the caller's order
+#include <cstdlib>
 #include <cstring>
 #include <type_traits>
 
@@ -1494,6 +1495,170 @@ __global__ void __launch_bounds__(128) k_p2p32(DevTree t, const int32_t* __restr
   }
 }
 
+template <int K, int KER>
+__global__ void __launch_bounds__(128) k_p2p32o(DevTree t, const int4* __restrict__ items, int64_t nitems,
+                                                const int32_t* __restrict__ oct,
+                                               const int32_t* __restrict__ doff, const int32_t* __restrict__ dlist,
+                                               const float4* __restrict__ boxc, const float4* __restrict__ src,
+                                               const float4* __restrict__ srclo, ResPoly rp,
+                                               const double* __restrict__ lvpoly, float lam,
+                                               double* __restrict__ unear) {
+  __shared__ float4 sA[4][16], sB[4][16], sC[4][16];   // (-x, -y) hi, (-z hi, rho), (-x, -y) lo
+  __shared__ float2 sD[4][16];                         // -z lo
+  __shared__ double red[4][32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t it = (int64_t)blockIdx.x * 4 + warp;
+  if (it >= nitems) return;
+  const int4 itm = items[it];
+  const int B = itm.x, o = itm.y, t0 = itm.z;
+  const int nt = itm.w - itm.z;
+  // an item of nt < 16 targets (the tail of a leaf) splits each source tile over
+  // f = 32/nt lane groups: lane = target + nt * phase, phase strides the source pairs
+  const int f = 32 / nt, tj = lane % nt, ph = lane / nt;
+  const float4 tp = src[t0 + tj], tl = srclo[t0 + tj];
+  const float4 cB = boxc[B];
+  // the target octant's box (Sec. 3.4: one more level of refinement for the culling)
+  const float hT = 0.25f * cB.w;
+  const float ox = cB.x + ((o >> 2) & 1 ? hT : -hT), oy = cB.y + ((o >> 1) & 1 ? hT : -hT),
+              oz = cB.z + (o & 1 ? hT : -hT);
+  __shared__ int sOa[4][8], sOx[4][8];   // selected source octants: first point, exclusive prefix
+  float2 a2[K + 1];
+  if (KER == KER_LAPLACE) {
+#pragma unroll
+    for (int j = 0; j <= K; ++j) a2[j] = make_float2((float)rp.a[j], (float)rp.a[j]);
+  }
+  float* fA = reinterpret_cast<float*>(sA[warp]);
+  float* fB = reinterpret_cast<float*>(sB[warp]);
+  float* fC = reinterpret_cast<float*>(sC[warp]);
+  float* fD = reinterpret_cast<float*>(sD[warp]);
+  const float2 m1 = make_float2(-1.0f, -1.0f);
+  double acc = 0.0;
+  for (int e = doff[B]; e < doff[B + 1]; ++e) {
+    const int S = dlist[e];
+    const float4 cS = boxc[S];   // centre and side 2^-L (fp32, exact)
+    // c_T - c_S, exact: both are dyadic with <= 22 significant bits
+    float xt, yt, zt, xe, ye, ze;
+    two_sum(tp.x, cB.x - cS.x, xt, xe);
+    two_sum(tp.y, cB.y - cS.y, yt, ye);
+    two_sum(tp.z, cB.z - cS.z, zt, ze);
+    xe += tl.x;
+    ye += tl.y;
+    ze += tl.z;
+    const float2 xt2 = make_float2(xt, xt), yt2 = make_float2(yt, yt), zt2 = make_float2(zt, zt);
+    const float2 xe2 = make_float2(xe, xe), ye2 = make_float2(ye, ye), ze2 = make_float2(ze, ze);
+    const float irl = __int_as_float(0x7F000000 - __float_as_int(cS.w));   // 2^L
+    const float rl2 = cS.w * cS.w;
+    const float2 tw2 = make_float2(2.0f * irl * irl, 2.0f * irl * irl), nirl2 = make_float2(-irl, -irl);
+    if (KER == KER_YUKAWA) {
+      const int L = t.level[S];
+#pragma unroll
+      for (int j = 0; j <= K; ++j) {
+        const float c = (float)__ldg(lvpoly + L * (K + 1) + j);
+        a2[j] = make_float2(c, c);
+      }
+    }
+    // source octants of S within r_L of the target octant (closed boxes: every pair of a
+    // culled octant has r >= r_L, where R_L = 0): lanes 0-7 test one octant each
+    bool sel = false;
+    int oa = 0, oc = 0;
+    if (lane < 8) {
+      oa = oct[8 * (int64_t)S + lane];
+      oc = (lane < 7 ? oct[8 * (int64_t)S + lane + 1] : t.end[S]) - oa;
+      if (oc > 0) {
+        const float hS = 0.25f * cS.w;
+        const float gx = fmaxf(0.0f, fabsf(ox - (cS.x + ((lane >> 2) & 1 ? hS : -hS))) - hT - hS);
+        const float gy = fmaxf(0.0f, fabsf(oy - (cS.y + ((lane >> 1) & 1 ? hS : -hS))) - hT - hS);
+        const float gz = fmaxf(0.0f, fabsf(oz - (cS.z + (lane & 1 ? hS : -hS))) - hT - hS);
+        sel = fmaf(gx, gx, fmaf(gy, gy, gz * gz)) < rl2 * 1.000001f;
+      }
+    }
+    if (!__any_sync(0xffffffffu, sel)) continue;
+    int c = sel ? oc : 0, incl = c;
+#pragma unroll
+    for (int d = 1; d < 8; d <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= d) incl += v;
+    }
+    const int total = __shfl_sync(0xffffffffu, incl, 7);
+    if (lane < 8) {
+      sOa[warp][lane] = oa;
+      sOx[warp][lane] = sel ? incl - c : 0x7fffffff;   // unselected: never matched
+    }
+    __syncwarp();
+    float2 part = make_float2(0.0f, 0.0f);
+    for (int s0 = 0; s0 < total; s0 += 32) {
+      const int ns = min(32, total - s0), npair = (ns + 1) >> 1;
+      const int j = lane >> 1, h = lane & 1;
+      if (lane < ns) {
+        const int g = s0 + lane;
+        int kk = 0, best = -1;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int x0 = sOx[warp][k];
+          if (x0 <= g && x0 >= best) {
+            best = x0;
+            kk = k;
+          }
+        }
+        const int si = sOa[warp][kk] + (g - best);
+        const float4 hi = src[si], lo = srclo[si];
+        fA[4 * j + h] = -hi.x;
+        fA[4 * j + 2 + h] = -hi.y;
+        fB[4 * j + h] = -hi.z;
+        fB[4 * j + 2 + h] = hi.w;
+        fC[4 * j + h] = -lo.x;
+        fC[4 * j + 2 + h] = -lo.y;
+        fD[2 * j + h] = -lo.z;
+      } else if (lane == ns && h == 1) {
+        // odd tail: a chargeless source at (4, 4, 4) r_L, outside the ball of every
+        // target (|x_t| <= 2.5 r_L per axis) yet close enough that the polynomial of
+        // its packed partner lane stays finite (s < 260)
+        const float pad = -4.0f * cS.w;
+        fA[4 * j + 1] = pad;
+        fA[4 * j + 3] = pad;
+        fB[4 * j + 1] = pad;
+        fB[4 * j + 3] = 0.0f;
+        fC[4 * j + 1] = 0.0f;
+        fC[4 * j + 3] = 0.0f;
+        fD[2 * j + 1] = 0.0f;
+      }
+      __syncwarp();
+#pragma unroll 4
+      for (int jp = ph; jp < npair; jp += f) {
+        const float4 A = sA[warp][jp], Bv = sB[warp][jp], C = sC[warp][jp];
+        const float2 Dv = sD[warp][jp];
+        const float2 dx = __fadd2_rn(__fadd2_rn(xt2, make_float2(A.x, A.y)), __fadd2_rn(xe2, make_float2(C.x, C.y)));
+        const float2 dy = __fadd2_rn(__fadd2_rn(yt2, make_float2(A.z, A.w)), __fadd2_rn(ye2, make_float2(C.z, C.w)));
+        const float2 dz = __fadd2_rn(__fadd2_rn(zt2, make_float2(Bv.x, Bv.y)), __fadd2_rn(ze2, Dv));
+        const float2 r2 = __ffma2_rn(dx, dx, __ffma2_rn(dy, dy, __fmul2_rn(dz, dz)));
+        const bool i0 = r2.x < rl2, i1 = r2.y < rl2;
+        if (i0 || i1) {
+          const float2 s2 = __ffma2_rn(r2, tw2, m1);
+          float2 pv = a2[K];
+#pragma unroll
+          for (int q = K - 1; q >= 0; --q) pv = __ffma2_rn(pv, s2, a2[q]);
+          // r^2 below FLT_MIN (|x_t - x_s| < 1e-19 r_L) counts as coincident
+          const float ri0 = rsqrt_approx(r2.x), ri1 = rsqrt_approx(r2.y);
+          float k0 = (KER == KER_YUKAWA) ? expf(-lam * r2.x * ri0) * ri0 : ri0;
+          float k1 = (KER == KER_YUKAWA) ? expf(-lam * r2.y * ri1) * ri1 : ri1;
+          const float2 kv = make_float2(r2.x >= 1.17549435e-38f ? k0 : 0.0f, r2.y >= 1.17549435e-38f ? k1 : 0.0f);
+          const float2 w = make_float2(i0 ? Bv.z : 0.0f, i1 ? Bv.w : 0.0f);
+          part = __ffma2_rn(w, __ffma2_rn(pv, nirl2, kv), part);
+        }
+      }
+      __syncwarp();
+    }
+    acc += (double)part.x + (double)part.y;
+  }
+  red[warp][lane] = ph < f ? acc : 0.0;
+  __syncwarp();
+  if (lane < nt) {
+    double u = 0.0;
+    for (int k = 0; k < f; ++k) u += red[warp][lane + k * nt];
+    unear[t0 + lane] = u;
+  }
+}
+
 // u = (u_far + u_near)/side, scattered to the caller's order (after both branches)
 __global__ void k_combine(const double* __restrict__ ufar, const double* __restrict__ unear,
                           const int32_t* __restrict__ perm, int64_t n, double inv_side, double* __restrict__ out) {
@@ -1748,6 +1913,37 @@ static void run_p2p32_deg(dmk_plan_s* PL, const ResPoly& rp, int K, cudaStream_t
   DMK_LAUNCH_CHECK();
 }
 
+// Sec. 3.4 form: octant items and per-octant source culling (58% of the pairs of a
+// uniform tree).  Opt-in (DMK_P2P_FORM=octant): measured slower than k_p2p32 on both
+// config 1 (3.36 vs 1.23 ms, ~30-point leaves) and config 2 (43 vs 26 ms, mean 52
+// points per leaf): octants of ~4-8 targets leave a warp's lanes with one or two source
+// pairs per list entry, so the per-entry culling and gather cost more than the pairs
+// saved.  Kept as a tested alternative for much bigger leaves.
+static bool use_octant_form(const dmk_plan_s* PL) {
+  const char* e = std::getenv("DMK_P2P_FORM");
+  return e && std::strcmp(e, "octant") == 0 && PL->np2p_o > 0;
+}
+template <int KER>
+static void run_p2p32o_deg(dmk_plan_s* PL, const ResPoly& rp, int K, cudaStream_t st) {
+  DevTree dt = dev_tree(PL);
+  int nb = (int)((PL->np2p_o + 3) / 4);
+  if (nb == 0) return;
+  const Tables& T = *PL->tab;
+#define DMK_P2P_CASE(KK)                                                                                    \
+  case KK:                                                                                                  \
+    k_p2p32o<KK, KER><<<nb, 128, 0, st>>>(dt, PL->p2p_items_o.p, PL->np2p_o, PL->leaf_oct.p, PL->dlist_off.p, \
+                                          PL->dlist.p, PL->box_c4.p, PL->xl4.p, PL->xl4lo.p, rp, T.dRespoly,  \
+                                          (float)T.lam, PL->unear.p);                                       \
+    break;
+  switch (K) {
+    DMK_P2P_CASE(4) DMK_P2P_CASE(6) DMK_P2P_CASE(8) DMK_P2P_CASE(10) DMK_P2P_CASE(12) DMK_P2P_CASE(14)
+    DMK_P2P_CASE(16) DMK_P2P_CASE(18) DMK_P2P_CASE(20) DMK_P2P_CASE(22) DMK_P2P_CASE(24)
+    default: fail(DMK_ERR_UNSUPPORTED, "residual polynomial degree out of range");
+  }
+#undef DMK_P2P_CASE
+  DMK_LAUNCH_CHECK();
+}
+
 template <class F>
 static void dispatch_p(dmk_plan_s* PL, F f) {
   switch (PL->tab->p) {
@@ -1801,11 +1997,13 @@ void eval_upward(dmk_plan_s* PL, const double* dcharges) {
   const bool full = PL->th.nlevels == 1;
   if (PL->tab->kernel == DMK_KERNEL_YUKAWA) {
     K = PL->tab->respoly_deg;
-    if (p2p32) run_p2p32_deg<KER_YUKAWA>(PL, rp, K, slo);
+    if (p2p32 && use_octant_form(PL)) run_p2p32o_deg<KER_YUKAWA>(PL, rp, K, slo);
+    else if (p2p32) run_p2p32_deg<KER_YUKAWA>(PL, rp, K, slo);
     else if (full) run_p2p_deg<KER_YUKAWA, true>(PL, nullptr, rp, K, slo);
     else run_p2p_deg<KER_YUKAWA, false>(PL, nullptr, rp, K, slo);
   } else {
-    if (p2p32) run_p2p32_deg<KER_LAPLACE>(PL, rp, K, slo);
+    if (p2p32 && use_octant_form(PL)) run_p2p32o_deg<KER_LAPLACE>(PL, rp, K, slo);
+    else if (p2p32) run_p2p32_deg<KER_LAPLACE>(PL, rp, K, slo);
     else if (full) run_p2p_deg<KER_LAPLACE, true>(PL, nullptr, rp, K, slo);
     else run_p2p_deg<KER_LAPLACE, false>(PL, nullptr, rp, K, slo);
   }

@@ -414,8 +414,9 @@ struct ReadIdx {   // by value
 // out[i] = fscan[v[i]], out[m + i] = escan[v[i]] (i < m), out[2m] = dlist_off[nbox],
 // out[2m + 1] = poff[nbox]: every host-side size of the plan in one read-back
 __global__ void k_read_totals(const int32_t* __restrict__ fscan, const int32_t* __restrict__ escan, ReadIdx ri,
-                              const int32_t* __restrict__ doff, const int32_t* __restrict__ poff, int64_t nbox,
-                              int64_t* out) {
+                              const int32_t* __restrict__ doff, const int32_t* __restrict__ poff,
+                              const int32_t* __restrict__ poff_o, const unsigned long long* __restrict__ nleaf,
+                              int64_t nbox, int64_t* out) {
   const int i = threadIdx.x;
   if (i < ri.m) {
     out[i] = fscan[ri.v[i]];
@@ -424,6 +425,8 @@ __global__ void k_read_totals(const int32_t* __restrict__ fscan, const int32_t* 
   if (i == 0) {
     out[2 * ri.m] = doff[nbox];
     out[2 * ri.m + 1] = poff[nbox];
+    out[2 * ri.m + 2] = poff_o ? poff_o[nbox] : 0;
+    out[2 * ri.m + 3] = nleaf ? (int64_t)*nleaf : 0;
   }
 }
 
@@ -653,6 +656,59 @@ __global__ void k_p2p_count(const int32_t* start, const int32_t* end, const uint
   if (i >= nbox) return;
   int n_ = end[i] - start[i];
   cnt[i] = ((flags[i] & 1) && (flags[i] & 16) && n_ > 0) ? (n_ + 31) / 32 : 0;
+}
+// Sec. 3.4, 3D: the octants of every leaf (its points are Morton
+// sorted, so octant k is a contiguous range): oct[8 b + k] = first point of octant k.
+__global__ void k_leaf_oct(const uint64_t* __restrict__ keys, const uint64_t* __restrict__ code,
+                           const int32_t* __restrict__ level, const int32_t* __restrict__ start,
+                           const int32_t* __restrict__ end, const uint8_t* __restrict__ flags, int64_t nbox,
+                           int32_t* oct) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t b = t >> 3;
+  const int k = (int)(t & 7);
+  if (b >= nbox) return;
+  if (!(flags[b] & 1)) return;
+  const int l = level[b];
+  int64_t lo = start[b], hi = end[b];
+  if (k > 0 && l < NBITS) {
+    const int sh = 3 * (NBITS - l - 1);
+    const uint64_t v = ((code[b] << 3) | (uint64_t)k) << sh;
+    while (lo < hi) {   // first point of the leaf with key >= v
+      const int64_t mid = (lo + hi) >> 1;
+      if (keys[mid] < v) lo = mid + 1; else hi = mid;
+    }
+  } else if (k > 0) {
+    lo = end[b];        // level-NBITS leaf: one octant
+  }
+  oct[8 * b + k] = (int32_t)lo;
+}
+// octant work items of the target leaves: (leaf, octant, t0, t1), <= 32 targets each;
+// also counts the target leaves (for the host's choice of the P2P form)
+__global__ void k_p2p_count_o(const int32_t* __restrict__ start, const int32_t* __restrict__ end,
+                              const uint8_t* __restrict__ flags, const int32_t* __restrict__ oct, int64_t nbox,
+                              int32_t* cnt, unsigned long long* nleaf) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= nbox) return;
+  int c = 0;
+  if ((flags[i] & 1) && (flags[i] & 16) && end[i] > start[i]) {
+    for (int k = 0; k < 8; ++k) {
+      const int a = oct[8 * i + k], e = k < 7 ? oct[8 * i + k + 1] : end[i];
+      c += (e - a + 31) / 32;
+    }
+    atomicAdd(nleaf, 1ull);
+  }
+  cnt[i] = c;
+}
+__global__ void k_p2p_fill_o(const int32_t* __restrict__ end, const int32_t* __restrict__ oct,
+                             const int32_t* __restrict__ cnt, const int32_t* __restrict__ off, int64_t nbox,
+                             int4* items) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= nbox || cnt[i] == 0) return;
+  int p = off[i];
+  for (int k = 0; k < 8; ++k) {
+    const int a = oct[8 * i + k], e = k < 7 ? oct[8 * i + k + 1] : end[i];
+    for (int t0 = a; t0 < e; t0 += 32) items[p++] = make_int4((int)i, k, t0, min(e, t0 + 32));
+  }
 }
 __global__ void k_p2p_fill(const int32_t* start, const int32_t* cnt, const int32_t* off, int64_t nbox,
                            int32_t* items) {
@@ -1134,6 +1190,24 @@ static void build_tree_d(dmk_plan_s* P, const double* dpts) {
   P->dlist_off.alloc(nbox + 1, s);
   exclusive_scan(s, dcnt.p, P->dlist_off.p, nbox + 1);
   exclusive_scan(s, pcnt.p, poff.p, nbox + 1);
+  // octant items (Sec. 3.4 P2P form, 3D), chosen at evaluation for big leaves
+  DevBuf<int32_t> ocnt, ooff;
+  DevBuf<unsigned long long> nleaf;
+  if (D == 3) {
+    P->leaf_oct.alloc(8 * nbox, s);
+    k_leaf_oct<<<nblk(8 * nbox), TPB, 0, s>>>(P->keys.p, P->box_code.p, P->box_level.p, P->box_start.p,
+                                              P->box_end.p, P->box_flags.p, nbox, P->leaf_oct.p);
+    DMK_LAUNCH_CHECK();
+    ocnt.alloc(nbox + 1, s);
+    ooff.alloc(nbox + 1, s);
+    nleaf.alloc(1, s);
+    DMK_CUDA(cudaMemsetAsync(ocnt.p + nbox, 0, sizeof(int32_t), s));
+    DMK_CUDA(cudaMemsetAsync(nleaf.p, 0, sizeof(unsigned long long), s));
+    k_p2p_count_o<<<nblk(nbox), TPB, 0, s>>>(P->box_start.p, P->box_end.p, P->box_flags.p, P->leaf_oct.p, nbox,
+                                             ocnt.p, nleaf.p);
+    DMK_LAUNCH_CHECK();
+    exclusive_scan(s, ocnt.p, ooff.p, nbox + 1);
+  }
   {
     ReadIdx ri{};
     const int m = nlevels + 1;
@@ -1141,10 +1215,11 @@ static void build_tree_d(dmk_plan_s* P, const double* dpts) {
     ri.v[nlevels] = nbox;
     ri.m = m;
     DevBuf<int64_t> dout;
-    dout.alloc(2 * m + 2, s);
-    k_read_totals<<<1, 64, 0, s>>>(fscan.p, escan.p, ri, P->dlist_off.p, poff.p, nbox, dout.p);
+    dout.alloc(2 * m + 4, s);
+    k_read_totals<<<1, 64, 0, s>>>(fscan.p, escan.p, ri, P->dlist_off.p, poff.p, D == 3 ? ooff.p : nullptr,
+                                   D == 3 ? nleaf.p : nullptr, nbox, dout.p);
     DMK_LAUNCH_CHECK();
-    std::vector<int64_t> h(2 * m + 2);
+    std::vector<int64_t> h(2 * m + 4);
     DMK_CUDA(cudaMemcpyAsync(h.data(), dout.p, h.size() * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     DMK_CUDA(cudaStreamSynchronize(s));
     P->nfout = h[nlevels];
@@ -1157,6 +1232,8 @@ static void build_tree_d(dmk_plan_s* P, const double* dpts) {
     }
     P->ndlist = h[2 * m];
     P->np2p = h[2 * m + 1];
+    P->np2p_o = h[2 * m + 2];
+    P->nleaf_t = h[2 * m + 3];
   }
   mark("flags");
   P->dlist.alloc(P->ndlist ? P->ndlist : 1, s);
@@ -1168,6 +1245,11 @@ static void build_tree_d(dmk_plan_s* P, const double* dpts) {
   P->p2p_items.alloc(2 * (P->np2p ? P->np2p : 1), s);
   k_p2p_fill<<<nblk(nbox), TPB, 0, s>>>(P->box_start.p, pcnt.p, poff.p, nbox, P->p2p_items.p);
   DMK_LAUNCH_CHECK();
+  if (D == 3) {
+    P->p2p_items_o.alloc(P->np2p_o ? P->np2p_o : 1, s);
+    k_p2p_fill_o<<<nblk(nbox), TPB, 0, s>>>(P->box_end.p, P->leaf_oct.p, ocnt.p, ooff.p, nbox, P->p2p_items_o.p);
+    DMK_LAUNCH_CHECK();
+  }
   if (D == 3) {
     P->box_c4.alloc(nbox, s);
     k_box_c4<<<nblk(nbox), TPB, 0, s>>>(P->box_code.p, P->box_level.p, nbox, P->box_c4.p);

@@ -247,3 +247,24 @@ def test_linearity():
     # linear up to fp32 roundings (reading R16, p = 18: fp32 anterpolation, plane waves,
     # translation, evaluation and P2P pairs, each a few 2^-24 relative)
     assert np.max(np.abs(a + b - c)) <= 1e-6 * np.max(np.abs(c))
+
+
+@pytest.mark.parametrize("kernel", ["laplace", "yukawa"])
+def test_p2p_octant_form(kernel, monkeypatch):
+    """The Sec. 3.4 form of the near field (octant work items, source octants culled by
+    their distance to the target octant) against the leaf form and
+    the direct sum: culled pairs have r >= r_L where R_L = 0 (1/r; Yukawa culls r >= r_L
+    in both forms, reading R13), so the two agree to fp32 summation order."""
+    x, q = dmk_inputs.clusters(30000, seed=31)
+    lam = 10.0 if kernel == "yukawa" else 0.0
+    res = {}
+    for form in ("leaf", "octant"):
+        monkeypatch.setenv("DMK_P2P_FORM", form)
+        plan = dmk.dmk_plan(cuda(x), eps=1e-6, leaf_capacity=200, kernel=kernel, lam=lam)
+        u = plan.eval(cuda(q)).cpu().numpy()
+        res[form] = (u, plan.stage("unear"))
+        plan.close()
+    (ul, nl), (uo, no) = res["leaf"], res["octant"]
+    assert np.max(np.abs(no - nl)) <= 1e-6 * np.max(np.abs(nl))
+    ref = direct.yukawa3d(x, q, lam) if kernel == "yukawa" else direct.laplace3d(x, q)
+    assert direct.rel_l2(uo, ref) <= 2e-6
