@@ -13,6 +13,8 @@
 //   level is < LMAX; 2:1 balance over closed-box contact, built bottom-up; keep all
 //   non-leaf boxes and all non-empty leaves, numbered by (level, Morton code).
 #include <chrono>
+#include <cstdlib>
+#include <cstring>
 
 #include <cub/cub.cuh>
 
@@ -1193,7 +1195,9 @@ static void build_tree_d(dmk_plan_s* P, const double* dpts) {
   // octant items (Sec. 3.4 P2P form, 3D), chosen at evaluation for big leaves
   DevBuf<int32_t> ocnt, ooff;
   DevBuf<unsigned long long> nleaf;
-  if (D == 3) {
+  const char* pform = std::getenv("DMK_P2P_FORM");
+  const bool build_oct = D == 3 && pform && std::strcmp(pform, "octant") == 0;   // opt-in form
+  if (build_oct) {
     P->leaf_oct.alloc(8 * nbox, s);
     k_leaf_oct<<<nblk(8 * nbox), TPB, 0, s>>>(P->keys.p, P->box_code.p, P->box_level.p, P->box_start.p,
                                               P->box_end.p, P->box_flags.p, nbox, P->leaf_oct.p);
@@ -1216,8 +1220,8 @@ static void build_tree_d(dmk_plan_s* P, const double* dpts) {
     ri.m = m;
     DevBuf<int64_t> dout;
     dout.alloc(2 * m + 4, s);
-    k_read_totals<<<1, 64, 0, s>>>(fscan.p, escan.p, ri, P->dlist_off.p, poff.p, D == 3 ? ooff.p : nullptr,
-                                   D == 3 ? nleaf.p : nullptr, nbox, dout.p);
+    k_read_totals<<<1, 64, 0, s>>>(fscan.p, escan.p, ri, P->dlist_off.p, poff.p, build_oct ? ooff.p : nullptr,
+                                   build_oct ? nleaf.p : nullptr, nbox, dout.p);
     DMK_LAUNCH_CHECK();
     std::vector<int64_t> h(2 * m + 4);
     DMK_CUDA(cudaMemcpyAsync(h.data(), dout.p, h.size() * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
@@ -1245,7 +1249,7 @@ static void build_tree_d(dmk_plan_s* P, const double* dpts) {
   P->p2p_items.alloc(2 * (P->np2p ? P->np2p : 1), s);
   k_p2p_fill<<<nblk(nbox), TPB, 0, s>>>(P->box_start.p, pcnt.p, poff.p, nbox, P->p2p_items.p);
   DMK_LAUNCH_CHECK();
-  if (D == 3) {
+  if (build_oct) {
     P->p2p_items_o.alloc(P->np2p_o ? P->np2p_o : 1, s);
     k_p2p_fill_o<<<nblk(nbox), TPB, 0, s>>>(P->box_end.p, P->leaf_oct.p, ocnt.p, ooff.p, nbox, P->p2p_items_o.p);
     DMK_LAUNCH_CHECK();
