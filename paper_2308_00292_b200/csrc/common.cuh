@@ -154,6 +154,7 @@ struct dmk_plan_s {
 
   // eval buffers
   dmk::DevBuf<double> q, mom, phi, lam, ufar, unear;
+  dmk::DevBuf<double> lamc;               // 3D: local expansions inherited through p2c (lam: own part)
   dmk::DevBuf<float> pwt;                 // fp32 tier: translated + weighted plane waves per local box
   dmk::DevBuf<double> scalar;             // device scratch scalar (2D: total charge)
   int64_t phi_size0 = 0, phi_size1 = 0;   // doubles per root / per other box

@@ -168,7 +168,8 @@ struct Ev32 {
 };
 template <int P>
 __global__ void __launch_bounds__(Ev32<P>::NT) k_eval32(DevTree t, const int32_t* __restrict__ boxes,
-                                                        const double* __restrict__ lam, double* __restrict__ ufar) {
+                                                        const double* __restrict__ lam,
+                                                        const double* __restrict__ lamc, double* __restrict__ ufar) {
   using E = Ev32<P>;
   constexpr int NT = E::NT, PZ = E::PZ, P2 = P * P;
   extern __shared__ float4 sl4[];   // [P2][PZ/4]
@@ -185,10 +186,12 @@ __global__ void __launch_bounds__(Ev32<P>::NT) k_eval32(DevTree t, const int32_t
   __syncthreads();
   const int nr = nr_s, tot = tot_s;
   if (tot == 0) return;
+  // the box's own local expansion plus the one inherited through p2c
   const double* src = lam + (size_t)t.exp_rank[b] * P * P2;
+  const double* srcc = lamc + (size_t)t.exp_rank[b] * P * P2;
   for (int i = tid; i < P2 * PZ; i += NT) {
     const int r = i / PZ, c = i - r * PZ;
-    sl[i] = c < P ? (float)src[r * P + c] : 0.0f;
+    sl[i] = c < P ? (float)(src[r * P + c] + srcc[r * P + c]) : 0.0f;
   }
   double cen[3], ih;
   box_geom(t.code[b], t.level[b], cen, ih);
@@ -356,7 +359,8 @@ __global__ void __launch_bounds__(GrpCfg<P, MT>::NT) k_c2p_grp(DevTree t, const 
 
 template <int P, int MT>
 __global__ void __launch_bounds__(GrpCfg<P, MT>::NT) k_p2c_grp(DevTree t, const int32_t* __restrict__ parents,
-                                                 const double* __restrict__ A, double* __restrict__ lam) {
+                                                 const double* __restrict__ A, const double* __restrict__ lam,
+                                                 double* __restrict__ lamc) {
   using C = GrpCfg<P, MT>;
   constexpr int P2 = C::P2, P3 = P2 * P, KS1 = C::KS1, KS2 = C::KS2;
   extern __shared__ double sm[];
@@ -368,7 +372,7 @@ __global__ void __launch_bounds__(GrpCfg<P, MT>::NT) k_p2c_grp(DevTree t, const 
   const int b = parents[blockIdx.x / C::NTILE], tid = threadIdx.x, k0 = (blockIdx.x % C::NTILE) * MT;
   if (tid < 8) {
     const int c = t.child[8 * (int64_t)b + tid];
-    ch[tid] = (c >= 0 && (t.flags[c] & F_EXP)) ? lam + (size_t)t.exp_rank[c] * P3 : nullptr;
+    ch[tid] = (c >= 0 && (t.flags[c] & F_EXP)) ? lamc + (size_t)t.exp_rank[c] * P3 : nullptr;
   }
   for (int i = tid; i < 2 * P2; i += C::NT) sA[i] = A[i];
   __syncthreads();
@@ -376,7 +380,9 @@ __global__ void __launch_bounds__(GrpCfg<P, MT>::NT) k_p2c_grp(DevTree t, const 
 #pragma unroll
   for (int o = 0; o < 8; ++o) any |= ch[o] != nullptr;
   if (!any) return;
+  // the parent's full local expansion: its own part plus what it inherited
   const double* src = lam + (size_t)t.exp_rank[b] * P3;
+  const double* srcc = lamc + (size_t)t.exp_rank[b] * P3;
   // axis 1: zeta[o1][i][m2m3] = sum_m1 A_o1[m1][k0+i] Lambda_P[m1][m2m3]
   mma_tiles<KS1>(
       (2 * MT + 7) / 8, (P2 + 7) / 8,
@@ -384,7 +390,9 @@ __global__ void __launch_bounds__(GrpCfg<P, MT>::NT) k_p2c_grp(DevTree t, const 
         const int o1 = m >= MT, i = m - o1 * MT;
         return (m < 2 * MT && k0 + i < P && k < P) ? sA[(o1 * P + k) * P + k0 + i] : 0.0;
       },
-      [&](int k, int n) { return (k < P && n < P2) ? __ldg(src + (size_t)k * P2 + n) : 0.0; },
+      [&](int k, int n) {
+        return (k < P && n < P2) ? __ldg(src + (size_t)k * P2 + n) + __ldg(srcc + (size_t)k * P2 + n) : 0.0;
+      },
       [&](int m, int n, double v0, double v1) {
         if (m < 2 * MT) {
           if (n < P2) zeta[m * P2 + n] = v0;
@@ -435,7 +443,7 @@ __global__ void __launch_bounds__(GrpCfg<P, MT>::NT) k_p2c_grp(DevTree t, const 
           if (nn >= 2 * P) continue;
           const int o3 = nn >= P, k3 = nn - o3 * P;
           double* c = ch[g * 2 + o3];
-          if (c) atomicAdd(c + (size_t)(k0 + i) * P2 + k2 * P + k3, e ? v1 : v0);   // one writer: RED
+          if (c) c[(size_t)(k0 + i) * P2 + k2 * P + k3] = e ? v1 : v0;   // inherited part: one writer
         }
       });
 }
@@ -1111,7 +1119,8 @@ struct EvalMma {
 };
 template <int P>
 __global__ void __launch_bounds__(256) k_eval_mma(DevTree t, const int32_t* __restrict__ boxes,
-                                                  const double* __restrict__ lam, double* __restrict__ ufar) {
+                                                  const double* __restrict__ lam, const double* __restrict__ lamc,
+                                                  double* __restrict__ ufar) {
   using E = EvalMma<P>;
   constexpr int P2 = E::P2, KS = E::KS, NT8 = E::NT8, NW = E::NW;
   extern __shared__ double sm[];
@@ -1126,11 +1135,12 @@ __global__ void __launch_bounds__(256) k_eval_mma(DevTree t, const int32_t* __re
     for (int r = 0; r < nr_s; ++r) tot += rg[r].y - rg[r].x;
     tot_s = tot;
   }
-  const double* src = lam + (size_t)t.exp_rank[b] * P * P2;
+  const double* src = lam + (size_t)t.exp_rank[b] * P * P2;   // own + inherited (p2c) expansions
+  const double* srcc = lamc + (size_t)t.exp_rank[b] * P * P2;
   for (int i = tid; i < NT8 * KS * 32; i += NW * 32) {
     int ln = i & 31, ks = (i >> 5) % KS, nt = (i >> 5) / KS;
     int a = nt * 8 + (ln >> 2), bb = ks * 4 + (ln & 3);
-    lamF[i] = (a < P2 && bb < P) ? src[a * P + bb] : 0.0;
+    lamF[i] = (a < P2 && bb < P) ? src[a * P + bb] + srcc[a * P + bb] : 0.0;
   }
   __syncthreads();
   const int nr = nr_s, tot = tot_s;
@@ -1836,6 +1846,9 @@ static void run_eval(dmk_plan_s* PL, int phase = PH_UP | PH_DOWN, int top = 0) {
     }
     tm.end();
     if (!PL->serial) DMK_CUDA(cudaStreamWaitEvent(s, PL->ev_root, 0));
+    // inherited local expansions: the root inherits nothing; every other local box gets
+    // its part written (not added) by its parent's k_p2c_grp
+    DMK_CUDA(cudaMemsetAsync(PL->lamc.p, 0, (size_t)P3 * sizeof(double), s));
     tm.begin("p2c");
     {
       // parents at level l-1 push their local expansions into their level-l children
@@ -1846,7 +1859,7 @@ static void run_eval(dmk_plan_s* PL, int phase = PH_UP | PH_DOWN, int top = 0) {
         const int64_t a = th.exp_off[l - 1], b = th.exp_off[l];
         if (b <= a || th.exp_off[l + 1] <= th.exp_off[l]) continue;
         const unsigned grid = (unsigned)((b - a) * G::NTILE);
-        k_p2c_grp<P, MT><<<grid, G::NT, G::smem_p2c, s>>>(dt, PL->exp_list.p + a, T.dA, PL->lam.p);
+        k_p2c_grp<P, MT><<<grid, G::NT, G::smem_p2c, s>>>(dt, PL->exp_list.p + a, T.dA, PL->lam.p, PL->lamc.p);
         DMK_LAUNCH_CHECK();
       }
     }
@@ -1856,11 +1869,12 @@ static void run_eval(dmk_plan_s* PL, int phase = PH_UP | PH_DOWN, int top = 0) {
       if (PL->nexp) {
         if constexpr (P <= 18) {   // fp32 tier (R16)
           set_smem(k_eval32<P>, Ev32<P>::smem);
-          k_eval32<P><<<(int)PL->nexp, Ev32<P>::NT, Ev32<P>::smem, s>>>(dt, PL->exp_list.p, PL->lam.p, PL->ufar.p);
+          k_eval32<P><<<(int)PL->nexp, Ev32<P>::NT, Ev32<P>::smem, s>>>(dt, PL->exp_list.p, PL->lam.p, PL->lamc.p,
+                                                                          PL->ufar.p);
         } else {
           size_t sm = EvalMma<P>::smem;
           set_smem(k_eval_mma<P>, sm);
-          k_eval_mma<P><<<(int)PL->nexp, 256, sm, s>>>(dt, PL->exp_list.p, PL->lam.p, PL->ufar.p);
+          k_eval_mma<P><<<(int)PL->nexp, 256, sm, s>>>(dt, PL->exp_list.p, PL->lam.p, PL->lamc.p, PL->ufar.p);
         }
         DMK_LAUNCH_CHECK();
       }
