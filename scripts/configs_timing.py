@@ -30,7 +30,7 @@ CONFIGS = [
     ("config4 yukawa uniform 1e8 eps1e-6 (1 GPU)", "uniform", 100_000_000, 1e-6, "yukawa", 10.0),
 ]
 for name, kind, n, eps, kernel, lam in CONFIGS:
-    if a.only and a.only not in name:
+    if a.only and not any(o in name for o in a.only.split("|")):
         continue
     x, q = dmk_inputs.make(kind, n, seed=1)
     X, Q = torch.as_tensor(x, device="cuda"), torch.as_tensor(q, device="cuda")
