@@ -1,5 +1,7 @@
-timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/t.log 2>&1; tail -2 gpurun_out/t.log
-python scripts/tree_prof.py 2>&1 | tail -1
-python scripts/tree_prof.py 1000000 uniform 1e-9 2>&1 | tail -1
-python bench.py --steps 10 --warmup 3 > gpurun_out/bench_r26.json 2> gpurun_out/bench_r26.err; tail -2 gpurun_out/bench_r26.err
-python scripts/configs_timing.py --only config2 --reps 3
+# scratch helper for one gpurun call (edited per experiment): launch lists of the
+# eps = 1e-9 (p = 28) tier and of config 2 (1e7 clustered points)
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_p28_v9.csv \
+    python scripts/prof_step.py --reps 2 --eps 1e-9 > gpurun_out/ncu_p28.log 2>&1
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c2_v9.csv \
+    python scripts/prof_step.py --reps 2 --n 10000000 --kind clusters > gpurun_out/ncu_c2.log 2>&1
+tail -1 gpurun_out/ncu_p28.log; tail -1 gpurun_out/ncu_c2.log
