@@ -11,9 +11,11 @@ max over ranks.  Prints ONE JSON line (rank 0).
 
 --impl reference times the CPU oracle (oracle/dmk.py, fp64 numpy, as it stands) on a
 bounded sample of the same workload on the host cores; under torchrun only rank 0
-runs it.  N > 1 (torchrun, one rank per GPU, NCCL) runs the partitioned DMK of
-paper_2308_00292_b200/parallel.py on one global problem of N x (--n) uniform points (weak
-scaling: --n points per GPU): Morton partition, particle halo, coarse-moment all-reduce.
+runs it.  --gpus N > 1: the script relaunches itself under torchrun (one NCCL rank per
+GPU, 127.0.0.1) unless it already runs under one, and every rank runs the partitioned
+DMK of paper_2308_00292_b200/parallel.py on one global problem of N x (--n) uniform
+points (weak scaling: --n points per GPU): Morton partition, particle halo,
+coarse-moment all-reduce.  DMK_BENCH_DISTRIBUTED=1 takes that path at N = 1 too.
 """
 from __future__ import annotations
 
@@ -221,10 +223,25 @@ def run_reference(a):
     print(json.dumps(line), flush=True)
 
 
-def run_distributed(a):
+def torchrun_command(a, port):
+    """The relaunch of this script with one rank per GPU (the driver's own launch line)."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={a.gpus}",
+            "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+
+
+def free_port():
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def run_distributed(a, backend=None, device=None, pg="nccl"):
     """N > 1: one global uniform problem of world * a.n points, a.n generated per rank,
     evaluated by the partitioned DMK (weak scaling).  Device-event timing on each rank
-    between barriers, max over ranks."""
+    between barriers, max over ranks.  `backend` / `device` / `pg` are for the CPU test
+    of this path (tests/test_bench_distributed.py runs it under gloo with its own
+    backend); the product run is libdmk on this rank's GPU over NCCL."""
     import numpy as np
     import torch
     import torch.distributed as dist
@@ -239,61 +256,95 @@ def run_distributed(a):
     os.environ.setdefault("WORLD_SIZE", str(world))
     os.environ.setdefault("RANK", str(rank))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    dist.init_process_group("nccl", device_id=dev)
+    if world != a.gpus:
+        raise SystemExit(f"bench.py: --gpus {a.gpus} but WORLD_SIZE={world}")
+    cuda = device is None
+    if cuda:
+        torch.cuda.set_device(local)
+        dev = torch.device("cuda", local)
+        dist.init_process_group(pg, device_id=dev)
+        backend = par.GpuBackend(dev)
+    else:
+        dev = torch.device(device)
+        dist.init_process_group(pg)
     comm = par.TorchComm()
-    backend = par.GpuBackend(dev)
     x, q = dmk_inputs.uniform(a.n, seed=1 + rank)
     X, Q = torch.as_tensor(x, device=dev), torch.as_tensor(q, device=dev)
-    flush = torch.empty(256 * 2 ** 20 // 4, dtype=torch.float32, device=dev)
-    stream = torch.cuda.current_stream(dev)
+    flush = torch.empty(256 * 2 ** 20 // 4, dtype=torch.float32, device=dev) if cuda else None
+    stream = torch.cuda.current_stream(dev) if cuda else None
     st = {}
+
+    def sync():
+        if cuda:
+            torch.cuda.synchronize(dev)
+
+    class Span:   # device events on the launching stream (host clock in the CPU test)
+        def __init__(self):
+            if cuda:
+                self.e0, self.e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+        def start(self):
+            if cuda:
+                self.e0.record(stream)
+            else:
+                self.t0 = time.perf_counter()
+
+        def stop(self):
+            if cuda:
+                self.e1.record(stream)
+            else:
+                self.t1 = time.perf_counter()
+
+        def ms(self):
+            return self.e0.elapsed_time(self.e1) if cuda else 1e3 * (self.t1 - self.t0)
 
     def step(Xs, Qs):
         return par.dmk_eval_distributed(Xs, Qs, comm, backend, eps=a.eps, ns=a.ns, stats=st)
 
     for _ in range(a.warmup):
         step(X, Q)
-    torch.cuda.synchronize(dev)
+    sync()
     L = dmk.lib()
     import ctypes
     L.dmk_kernel_launches.restype = ctypes.c_int64
     L.dmk_kernel_launches.argtypes = [ctypes.c_void_p]
     launches0 = L.dmk_kernel_launches(None)
     clk = Clocks(local)
-    clk.start()
+    if cuda:
+        clk.start()
     times = []
     for _ in range(a.steps):
-        flush.zero_()
-        torch.cuda.synchronize(dev)
+        if flush is not None:
+            flush.zero_()
+        sync()
         dist.barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
+        sp = Span()
+        sp.start()
         u = step(X, Q)
-        e1.record(stream)
-        torch.cuda.synchronize(dev)
+        sp.stop()
+        sync()
         dist.barrier()
-        times.append(e0.elapsed_time(e1))
-    clocks = clk.stop()
+        times.append(sp.ms())
+    clocks = clk.stop() if cuda else {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["cpu test run"]}
     launches = (L.dmk_kernel_launches(None) - launches0) // a.steps
-    t = torch.tensor([float(np.mean(times))], device=dev)
+    t = torch.tensor([float(np.mean(times))], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     t_step = float(t.item())
     # end to end: host points/charges copied in and potentials copied out every step
-    Xh, Qh = torch.as_tensor(x).pin_memory(), torch.as_tensor(q).pin_memory()
+    Xh, Qh = (torch.as_tensor(x).pin_memory(), torch.as_tensor(q).pin_memory()) if cuda else \
+        (torch.as_tensor(x), torch.as_tensor(q))
     e2e = []
     for k in range(a.warmup + a.steps):
-        torch.cuda.synchronize(dev)
+        sync()
         dist.barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
+        sp = Span()
+        sp.start()
         uh = step(Xh.to(dev, non_blocking=True), Qh.to(dev, non_blocking=True)).cpu()
-        e1.record(stream)
-        torch.cuda.synchronize(dev)
+        sp.stop()
+        sync()
         if k >= a.warmup:
-            e2e.append(e0.elapsed_time(e1))
-    te = torch.tensor([float(np.mean(e2e))], device=dev)
+            e2e.append(sp.ms())
+    te = torch.tensor([float(np.mean(e2e))], dtype=torch.float64, device=dev)
     dist.all_reduce(te, op=dist.ReduceOp.MAX)
     # accuracy: direct sum over all ranks' points at 100 of rank 0's targets
     xa = [torch.zeros_like(X) for _ in range(world)]
@@ -302,7 +353,7 @@ def run_distributed(a):
     dist.all_gather(qa, Q)
     if rank == 0:
         xs, qs = torch.cat(xa).cpu().numpy(), torch.cat(qa).cpu().numpy()
-        idx = np.random.default_rng(7).choice(a.n, 100, replace=False)
+        idx = np.random.default_rng(7).choice(a.n, min(100, a.n), replace=False)
         ref = np.array([np.sum(np.delete(qs, i) / np.linalg.norm(np.delete(xs, i, axis=0) - xs[i], axis=1))
                         for i in idx])
         rel = float(np.linalg.norm(u.cpu().numpy()[idx] - ref) / np.linalg.norm(ref))
@@ -316,7 +367,7 @@ def run_distributed(a):
                        "step": "partitioned DMK: root all-reduce, Morton partition, all-to-all, halo, "
                                "coarse-moment all-reduce, plan + upward x2 + downward, return all-to-all",
                        "l2": "flushed by a 256 MiB write between timed steps",
-                       "parallelism": f"Morton partition over {world} ranks (NCCL)",
+                       "parallelism": f"Morton partition over {world} ranks ({pg})",
                        "partition_level": st.get("level"), "halo_points_rank0": st.get("n_halo"),
                        "own_points_rank0": st.get("n_own")},
             "rel_l2_err_sampled": rel, "clocks": clocks,
@@ -325,6 +376,8 @@ def run_distributed(a):
                     "api": "paper_2308_00292_b200.parallel.dmk_eval_distributed(host tensors copied in/out)"},
             "gpu_launches": int(launches),
         }
+        if not cuda:
+            line["backend"] = f"test: {type(backend).__name__} on {device} (not a measurement)"
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
 
@@ -333,6 +386,9 @@ def main():
     a = parse()
     if a.impl == "reference":
         return run_reference(a)
+    if a.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one NCCL rank per GPU: relaunch under torchrun (the driver's own launch line)
+        raise SystemExit(subprocess.call(torchrun_command(a, free_port())))
     if int(os.environ.get("WORLD_SIZE", "1")) > 1 or os.environ.get("DMK_BENCH_DISTRIBUTED") == "1":
         return run_distributed(a)
     os.environ.setdefault("DMK_PROFILE", "1")
@@ -342,19 +398,9 @@ def main():
     import dmk_inputs
     import paper_2308_00292_b200 as dmk
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    world, rank, local = 1, 0, int(os.environ.get("LOCAL_RANK", "0"))   # N > 1 runs run_distributed
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
-
-    def barrier():
-        if dist is not None:
-            dist.barrier()
 
     x, q = dmk_inputs.uniform(a.n, seed=1 + rank)
     X = torch.as_tensor(x, device=dev)
@@ -387,14 +433,12 @@ def main():
     for k in range(a.steps):
         flush.zero_()
         torch.cuda.synchronize(dev)
-        barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         em = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         plan, u = step(em)
         e1.record(stream)
         torch.cuda.synchronize(dev)
-        barrier()
         times.append(e0.elapsed_time(e1))
         plan_ms.append(e0.elapsed_time(em))
         if k == a.steps - 1:
@@ -425,10 +469,6 @@ def main():
     pw_parts = {k: round(stage_ms.pop(k), 4) for k in ("pwshift", "pw2poly") if k in stage_ms}
     if pw_parts:
         stage_ms["pwlocal"] = stage_ms.get("pwlocal", 0.0) + sum(pw_parts.values())
-    if dist is not None:
-        t = torch.tensor([t_step], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        t_step = float(t.item())
     value = a.n * world / (t_step * 1e-3)
 
     # ---- end to end through the public API, pinned host buffers
@@ -439,7 +479,6 @@ def main():
     for k in range(a.warmup + a.steps):
         flush.zero_()
         torch.cuda.synchronize(dev)
-        barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         plan = dmk.dmk_plan(Xh, eps=a.eps, leaf_capacity=a.ns, stream=sptr)
@@ -450,15 +489,6 @@ def main():
         if k >= a.warmup:
             e2e_times.append(e0.elapsed_time(e1))
     t_e2e = float(np.mean(e2e_times))
-    if dist is not None:
-        t = torch.tensor([t_e2e], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        t_e2e = float(t.item())
-
-    if rank != 0:
-        if dist is not None:
-            dist.destroy_process_group()
-        return
 
     # ---- accuracy on this run's output: direct sum at 200 sampled targets
     idx = np.random.default_rng(7).choice(a.n, 200, replace=False)
@@ -503,7 +533,7 @@ def main():
         "config": {"workload": WORKLOAD, "N_per_gpu": a.n, "eps": a.eps, "leaf_capacity": a.ns,
                    "step": "dmk_plan (tree+lists) + dmk_eval, device-resident inputs",
                    "l2": "flushed by a 256 MiB write between timed steps",
-                   "parallelism": "single" if world == 1 else f"replicas x{world} (independent problems)"},
+                   "parallelism": "single"},
         "rel_l2_err_sampled": rel,
         "clocks": clocks,
         "e2e": {"value": a.n * world / (t_e2e * 1e-3), "unit": "points/s",
@@ -519,11 +549,9 @@ def main():
         "tree": {"nbox": info.nbox, "nlevels": info.nlevels, "nfout": info.nfout, "nexp": info.nexp,
                  "p2p_pairs": pairs, "p2p_pairs_in_ball": inball},
     }
-    if world == 1 and not a.no_cpu_baseline:
+    if not a.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(a.cpu_sample, a.eps, a.ns)
     print(json.dumps(line), flush=True)
-    if dist is not None:
-        dist.destroy_process_group()
 
 
 if __name__ == "__main__":

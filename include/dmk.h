@@ -6,11 +6,20 @@
  *
  *     u_i = sum_{j : x_j != x_i} K(x_i - x_j) rho_j ,   i = 1..N      (Eq. 1.1)
  *
- * with sources = targets, for K(r) = 1/r in 3D (Eq. 3.1), by the
- * discrete DMK algorithm of Sec. 3.5 with the PSWF kernel split
- * of Sec. 3.6 (Eq. 3.66) and the parameters of Table 1
- * (PAPER.md:2010-2035).  Coincident pairs (x_j == x_i, including j == i) are omitted,
- * as the paper's self-interaction rule prescribes.
+ * with sources = targets, by the discrete DMK algorithm of Sec. 3.5
+ * with the PSWF kernel split of Sec. 3.6 (Eq. 3.66) and the
+ * parameters of Table 1.  Coincident pairs (x_j == x_i, including
+ * j == i) are omitted, as the paper's self-interaction rule prescribes (PAPER.md:524-541,
+ * 1192-1195).
+ *
+ * Supported (dim, kernel) pairs -- anything else returns DMK_ERR_UNSUPPORTED:
+ *   dim = 3, DMK_KERNEL_LAPLACE  K(r) = 1/r                (Eq. 3.1)
+ *   dim = 3, DMK_KERNEL_YUKAWA   K(r) = exp(-lambda r)/r   (Sec. 4.6, Eqs. 4.17-4.18,
+ *                                PAPER.md:2395-2440); needs opt->lambda > 0 and
+ *                                lambda * side < 2 c (side = the root cube's side, c of
+ *                                Table 1), else DMK_ERR_ARG / DMK_ERR_UNSUPPORTED
+ *   dim = 2, DMK_KERNEL_LOG      K(r) = -log r             (Sec. 4.6 at lambda = 0 in 2D,
+ *                                PAPER.md:2441-2447)
  *
  * Conventions for every entry point
  *   - Return value: DMK_OK (0) on success, a negative DMK_ERR_* code otherwise.  The
@@ -21,11 +30,29 @@
  *     The library never takes ownership of caller buffers.  A plan owns its device
  *     memory until dmk_destroy().
  *   - Streams: all device work of a plan is ordered on the stream given at plan time
- *     (0 = legacy default stream).  dmk_plan() synchronises that stream before it
- *     returns.  dmk_eval() with DMK_MEM_DEVICE buffers is asynchronous with respect
- *     to the host; with DMK_MEM_HOST buffers it returns after the result is in host
- *     memory.
- *   - Precision: all arithmetic is IEEE fp64.
+ *     (0 = legacy default stream).  Everything is stream-ordered: dmk_plan() waits for
+ *     one read-back of the tree sizes in the middle of the build, then enqueues the rest
+ *     and returns WITHOUT a final synchronisation, so DMK_MEM_DEVICE points must stay
+ *     valid until the plan's stream reaches that work (the Python binding keeps them
+ *     alive until close()).  dmk_eval() / dmk_upward() / dmk_downward() with
+ *     DMK_MEM_DEVICE buffers are asynchronous with respect to the host; with DMK_MEM_HOST
+ *     buffers they return after the result is in host memory.  An error raised by
+ *     asynchronous device work surfaces on a later call.  Internally a plan forks onto
+ *     pooled side streams (near field at low priority, far field at high priority) and
+ *     joins back into the plan stream before any result is visible there.
+ *   - Precision (reading R16 of DESIGN.md; the north star's "FP64 or FP32 chosen per
+ *     precision tier").  eps = 1e-9 (p = 28) and every 2D plan: all arithmetic and
+ *     storage in IEEE fp64.  3D with eps in {1e-3, 1e-6} (p <= 18): the tree, the
+ *     moments after anterpolation, c2p/p2c, prox2pw and the local expansions are fp64;
+ *     the outgoing plane waves are STORED in fp32; anterpolation, the colleague
+ *     translation, the back transforms, the leaf evaluation and the P2P pairs compute
+ *     in fp32 (double-single point coordinates for P2P) with fp64 accumulation across
+ *     blocks.  Contract: the potentials match the fp64 direct sum to relative l2 error
+ *     <= 2 eps on every tier (tests/test_gpu_*.py).
+ *   - Step-1 tables (Sec. 3.5 Step 1) are computed on the host on first use and cached
+ *     per (device, kernel, Table 1 row, lambda * side); the Yukawa entries, which depend
+ *     on the data's extent, are bounded (least recently used evicted; live plans keep
+ *     theirs).
  *   - There is no CPU fallback: without a usable CUDA device every call fails with
  *     DMK_ERR_CUDA.
  */
@@ -47,8 +74,7 @@ extern "C" {
 #define DMK_MEM_DEVICE 0
 #define DMK_MEM_HOST 1
 
-/* Kernels.  DMK_KERNEL_LAPLACE: K(r) = 1/r in 3D (Eq. 3.1).  Others are reserved
- * (2D log, 3D Yukawa: Sec. 4.6, Eqs. 4.17-4.18) and return DMK_ERR_UNSUPPORTED. */
+/* Kernels (see the (dim, kernel) table above). */
 #define DMK_KERNEL_LAPLACE 0
 #define DMK_KERNEL_YUKAWA 1
 #define DMK_KERNEL_LOG 2
@@ -74,18 +100,19 @@ typedef struct dmk_options {
 } dmk_options;
 
 /* dmk_plan: build the plan for N points in `dim` dimensions.
- *   dim      must be 3.
- *   kernel   DMK_KERNEL_*.
+ *   dim      3 (DMK_KERNEL_LAPLACE, DMK_KERNEL_YUKAWA) or 2 (DMK_KERNEL_LOG).
+ *   kernel   DMK_KERNEL_*; other (dim, kernel) pairs: DMK_ERR_UNSUPPORTED.
  *   eps      requested precision; snapped to the next tighter Table 1 row among
  *            {1e-3, 1e-6, 1e-9}.  eps < 1e-9: DMK_ERR_UNSUPPORTED.
  *   n        number of points, 1 <= n < 2^31.
- *   points   n x dim row-major fp64 (point i at points[dim*i .. dim*i+dim-1]), in `mem`.
+ *   points   n x dim row-major fp64 (point i at points[dim*i .. dim*i+dim-1]), in `mem`;
+ *            must be finite (DMK_ERR_ARG otherwise).
  *   opt      see dmk_options (may be NULL).
- *   out      receives the plan handle.
+ *   out      receives the plan handle (NULL on failure).
  * Work done (Sec. 3.5 Step 0 and Step 1): bounding cube, Morton keys, stable sort,
- * adaptive 2:1-balanced octree, colleague / plane-wave / direct interaction lists --
- * all in CUDA kernels on the device -- plus the per-precision tables of Step 1
- * (computed once on the host per precision and cached).  */
+ * adaptive 2:1-balanced 2^dim-tree, colleague / plane-wave / direct interaction lists --
+ * all in CUDA kernels on the device -- plus the Step-1 tables (host, cached, see the
+ * conventions above).  */
 int dmk_plan(int dim, int kernel, double eps, int64_t n, const double* points, int mem,
              const dmk_options* opt, dmk_plan_t* out);
 

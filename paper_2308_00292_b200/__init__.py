@@ -201,6 +201,8 @@ class Plan:
         ms = (ctypes.c_double * 32)()
         names = (ctypes.c_char_p * 32)()
         k = lib().dmk_eval_timings(self._h, ms, names, 32)
+        if k < 0:
+            raise DmkError(f"dmk_eval_timings failed ({k}): {lib().dmk_last_error().decode()}")
         return {names[i].decode(): ms[i] for i in range(max(k, 0))}
 
     def close(self):

@@ -108,7 +108,9 @@ static void alloc_eval_buffers(dmk_plan_s* P) {
   P->scalar.alloc(1, s);
   if (P->th.nlevels > 1) {
     P->mom.alloc(P->nfout * pd, s);
-    P->phi.alloc(P->phi_size0 + (P->nfout - 1) * P->phi_size1, s);
+    P->phi_count = P->phi_size0 + (P->nfout - 1) * P->phi_size1;
+    P->phi_f32 = P->dim == 3 && T.p <= 18;
+    P->phi.alloc(P->phi_f32 ? (P->phi_count + 1) / 2 : P->phi_count, s);
     P->lam.alloc(P->nexp * pd, s);
     if (P->dim == 3) P->lamc.alloc(P->nexp * pd, s);
     // fp32 tier (p <= 18, 3D): weighted incoming plane waves of every local box (k_pwshift)
@@ -132,7 +134,8 @@ dmk_plan_s::~dmk_plan_s() {
 extern "C" {
 
 const char* dmk_last_error(void) { return g_err.c_str(); }
-const char* dmk_version(void) { return "libdmk 0.1 (sm_100a, fp64, 3D Laplace PSWF split)"; }
+const char* dmk_version(void) { return "libdmk 0.2 (sm_100a; 3D Laplace, 3D Yukawa, 2D log; PSWF split; "
+         "eps 1e-3/1e-6: fp32 tier with fp64 accumulation, eps 1e-9: fp64)"; }
 
 int dmk_plan(int dim, int kernel, double eps, int64_t n, const double* points, int mem, const dmk_options* opt,
              dmk_plan_t* out) {
@@ -191,7 +194,8 @@ int dmk_plan(int dim, int kernel, double eps, int64_t n, const double* points, i
       build_tree(P, dpts);
       // tables after the tree: the Yukawa split runs in unit-root-cube coordinates,
       // lambda' = lambda * side (K(side r') = exp(-lambda' r')/(side r'))
-      P->tab = &get_tables(kernel, eps, kernel == DMK_KERNEL_YUKAWA ? P->lambda * P->side : 0.0);
+      P->tab_ref = get_tables(kernel, eps, kernel == DMK_KERNEL_YUKAWA ? P->lambda * P->side : 0.0);
+      P->tab = P->tab_ref.get();
       alloc_eval_buffers(P);
       // no synchronisation: the plan's device work is ordered on P->stream before any
       // evaluation or read-back (all of which run on P->stream)
@@ -369,8 +373,8 @@ int dmk_stage_copy(dmk_plan_t P, int which, double* out, int64_t count) {
     switch (which) {
       case DMK_STAGE_MOMENTS: b = &P->mom; break;
       case DMK_STAGE_OUTGOING:
-        if (P->dim == 3 && P->tab->p <= 18) {   // stored in fp32 (reading R16): widen
-          if (count != (int64_t)P->phi.n) fail(DMK_ERR_ARG, "count must equal the stage size");
+        if (count != P->phi_count) fail(DMK_ERR_ARG, "count must equal the stage size " + std::to_string(P->phi_count));
+        if (P->phi_f32) {   // stored in fp32 (reading R16): widen
           std::vector<float> h(count);
           DMK_CUDA(cudaMemcpyAsync(h.data(), P->phi.p, count * sizeof(float), cudaMemcpyDeviceToHost, P->stream));
           DMK_CUDA(cudaStreamSynchronize(P->stream));
@@ -400,7 +404,7 @@ int64_t dmk_stage_size(dmk_plan_t P, int which) {
   if (!P) return DMK_ERR_ARG;
   switch (which) {
     case DMK_STAGE_MOMENTS: return (int64_t)P->mom.n;
-    case DMK_STAGE_OUTGOING: return (int64_t)P->phi.n;
+    case DMK_STAGE_OUTGOING: return P->phi_count;
     case DMK_STAGE_LOCAL: return (int64_t)P->lam.n;
     case DMK_STAGE_UFAR: return (int64_t)P->ufar.n;
     case DMK_STAGE_UNEAR: return (int64_t)P->unear.n;

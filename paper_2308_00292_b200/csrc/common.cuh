@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -85,8 +86,15 @@ struct Tables {
   double *dQr1 = nullptr, *dQr0 = nullptr, *dGr1 = nullptr, *dGr0 = nullptr, *dA = nullptr, *dW = nullptr,
          *dW0 = nullptr, *dRespoly = nullptr;
   size_t wstride = 0;
+  int dev = -1;   // device holding the d* arrays (freed with the last reference)
+  Tables() = default;
+  Tables(const Tables&) = delete;
+  Tables& operator=(const Tables&) = delete;
+  ~Tables();
 };
-const Tables& get_tables(int kernel, double eps, double lam);  // cached; throws via fail()
+// cached per (device, kernel, precision row, lambda'); throws via fail()
+std::shared_ptr<const Tables> get_tables(int kernel, double eps, double lam);
+size_t tables_cached();   // number of cached table sets (tests)
 double snap_eps(double eps);
 
 // ---------------------------------------------------------------- plan
@@ -104,6 +112,7 @@ struct dmk_plan_s {
   double eps = 0, lambda = 0;   // lambda: Yukawa parameter in the caller's units
   int64_t n = 0;
   cudaStream_t stream = 0;
+  std::shared_ptr<const dmk::Tables> tab_ref;   // keeps the tables alive (cache may evict)
   const dmk::Tables* tab = nullptr;
   bool profile = false;        // DMK_PROFILE=1: per-phase CUDA events in dmk_eval (no host syncs)
   bool profile_tree = false;   // DMK_PROFILE_TREE=1: synchronising phase marks in dmk_plan
@@ -153,7 +162,12 @@ struct dmk_plan_s {
   std::vector<int64_t> c2p_off, p2c_off;   // per-level ranges into fout_list / exp_list
 
   // eval buffers
-  dmk::DevBuf<double> q, mom, phi, lam, ufar, unear;
+  dmk::DevBuf<double> q, mom, lam, ufar, unear;
+  // outgoing plane waves: phi_count values, stored as fp32 (phi_f32, the 3D p <= 18 tier,
+  // reading R16) or fp64; the buffer is sized in bytes for the stored type
+  dmk::DevBuf<double> phi;
+  int64_t phi_count = 0;
+  bool phi_f32 = false;
   dmk::DevBuf<double> lamc;               // 3D: local expansions inherited through p2c (lam: own part)
   dmk::DevBuf<float> pwt;                 // fp32 tier: translated + weighted plane waves per local box
   dmk::DevBuf<double> scalar;             // device scratch scalar (2D: total charge)

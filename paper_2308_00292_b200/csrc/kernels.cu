@@ -30,6 +30,7 @@
 #include <type_traits>
 
 #include "device.cuh"
+#include "umma.cuh"
 
 namespace dmk {
 
@@ -156,6 +157,182 @@ __global__ void __launch_bounds__(Ant32<P>::NT) k_anterp32(DevTree t, const int3
   }
   double* out = mom + (size_t)t.fout_rank[b] * P3;
   for (int i = tid; i < P3; i += NT) out[i] = cube[i];
+}
+
+// ---- fp32 tier on the 5th-generation tensor cores (tcgen05, kind::tf32 with the 3xTF32
+// split): the same contraction as a GEMM per F_out box with the points as K,
+//   mu[(n1 n2)][n3] = sum_j W[(n1 n2)][j] Tz[n3][j],   W[(n1 n2)][j] = rho_j Tx_j[n1] Ty_j[n2],
+// M = p^2 rows in MT tiles of 128 (TMEM lanes), N = p padded to NP (a multiple of 16),
+// K = the points in chunks of KC = 32.  Per chunk the CTA writes W and Tz, each split
+// as hi = tf32(v), lo = tf32(v - hi), into shared memory in the K-major no-swizzle
+// layout of umma.cuh; one thread issues A_hi B_hi + A_lo B_hi + A_hi B_lo (MT x 4 k-steps
+// x 3 MMAs) into one of two TMEM accumulators and commits them to an mbarrier; while the
+// tensor core runs, the threads compute the next chunk's Chebyshev values, then read the
+// previous chunk's accumulator (tcgen05.ld) into fp64 registers -- one thread per row
+// (n1, n2), fp32 sums over at most KC points as in k_anterp32, fp64 across chunks.
+template <int P>
+struct AntTC {
+  static constexpr int P2 = P * P, MT = (P2 + 127) / 128, NP = (P + 15) / 16 * 16, KC = 32;
+  static constexpr int NT = 128 * MT;                     // one thread per accumulator row
+  static constexpr int ACOLS = MT * NP;                   // TMEM columns per accumulator
+  static constexpr int TCOLS = 2 * ACOLS <= 32 ? 32 : (2 * ACOLS <= 64 ? 64 : (2 * ACOLS <= 128 ? 128 : 256));
+  static constexpr size_t A_WORDS = (size_t)MT * 128 * KC, B_WORDS = (size_t)NP * KC;
+  static constexpr size_t smem = sizeof(float) * (2 * A_WORDS + 2 * B_WORDS + (size_t)3 * KC * P) + 128;
+};
+__device__ __forceinline__ int umma_koff(int row, int k, int kc) {   // K-major, no swizzle (umma.cuh)
+  return (row >> 3) * (kc / 4) * 32 + (k >> 2) * 32 + (row & 7) * 4 + (k & 3);
+}
+template <int P>
+__global__ void __launch_bounds__(AntTC<P>::NT) k_anterp_tc(DevTree t, const int32_t* __restrict__ boxes,
+                                                            const double* __restrict__ q, double* __restrict__ mom) {
+  using C = AntTC<P>;
+  constexpr int P2 = C::P2, MT = C::MT, NP = C::NP, KC = C::KC, NT = C::NT, ACOLS = C::ACOLS;
+  extern __shared__ __align__(128) float smf[];
+  float* Ah = smf;                       // [MT*128][KC] K-major, hi
+  float* Al = Ah + C::A_WORDS;           // lo
+  float* Bh = Al + C::A_WORDS;           // [NP][KC]
+  float* Bl = Bh + C::B_WORDS;
+  float* sx = Bl + C::B_WORDS;           // [KC][P] rho T_n1(x)
+  float* sy = sx + KC * P;               // [KC][P]
+  float* sz = sy + KC * P;               // [KC][P]
+  __shared__ __align__(8) uint64_t mbar;
+  __shared__ uint32_t tbase;
+  __shared__ int2 rg[8];
+  __shared__ int nr_s, tot_s;
+  const int b = boxes[blockIdx.x], tid = threadIdx.x, warp = tid >> 5;
+  if (tid == 0) {
+    nr_s = box_ranges<false>(t, b, rg);
+    int tot = 0;
+    for (int r = 0; r < nr_s; ++r) tot += rg[r].y - rg[r].x;
+    tot_s = tot;
+  }
+  __syncthreads();
+  const int nr = nr_s, tot = tot_s;
+  if (tot == 0) return;   // moments were zeroed by the caller
+  // zero the padding rows / columns once (never rewritten): A rows >= p^2, B rows >= p
+  for (int i = tid; i < (int)(2 * C::A_WORDS); i += NT) smf[i] = 0.0f;
+  for (int i = tid; i < (int)(2 * C::B_WORDS); i += NT) Bh[i] = 0.0f;
+  if (warp == 0) umma::tmem_alloc<C::TCOLS>(&tbase);
+  if (tid == 0) umma::mbar_init(&mbar, 1);
+  umma::fence_before_sync();
+  __syncthreads();
+  umma::fence_after_sync();
+  const uint32_t tmem = tbase;
+  double cen[3], ih;
+  box_geom(t.code[b], t.level[b], cen, ih);
+  // this thread's accumulator row m = (n1, n2): tile tm = warp / 4, TMEM lane quarter warp % 4
+  const int m = tid;                        // rows 0..MT*128-1, row m lives in tile m/128, lane m%128
+  const int n1 = m / P, n2 = m - n1 * P;
+  const bool real = m < P2;
+  double acc[P];
+#pragma unroll
+  for (int n = 0; n < P; ++n) acc[n] = 0.0;
+  const uint32_t idesc = umma::idesc_tf32(128, NP);
+  const int nch = (tot + KC - 1) / KC;
+  auto flush = [&](int c) {   // accumulator of chunk c -> fp64 registers
+    umma::mbar_wait(&mbar, (uint32_t)(c & 1));
+    umma::fence_after_sync();
+    float v[32];
+    const uint32_t col = (uint32_t)((c & 1) * ACOLS + (m >> 7) * NP);
+    if constexpr (NP >= 32) umma::ld32x32b_x32(tmem + ((uint32_t)(32 * (warp & 3)) << 16) + col, v);
+    else umma::ld32x32b_x16(tmem + ((uint32_t)(32 * (warp & 3)) << 16) + col, v);
+#pragma unroll
+    for (int n = 0; n < P; ++n) acc[n] += (double)v[n];
+  };
+  for (int c = 0; c < nch; ++c) {
+    const int c0 = c * KC, nc = min(KC, tot - c0);
+    // ---- Chebyshev values of the chunk (fp64 recurrence, rounded once)
+    for (int w = tid; w < KC * 3; w += NT) {
+      const int j = w / 3, d = w % 3;
+      float* dst = (d == 0 ? sx : d == 1 ? sy : sz) + j * P;
+      if (j < nc) {
+        const int pi = range_point(rg, nr, c0 + j);
+        const double xx = ((d == 0 ? t.xs[pi] : d == 1 ? t.ys[pi] : t.zs[pi]) - cen[d]) * ih;
+        const double sc = d == 0 ? q[pi] : 1.0;
+        double ta = 1.0, tb = xx;
+        dst[0] = (float)sc;
+        if (P > 1) dst[1] = (float)(sc * xx);
+#pragma unroll 4
+        for (int n = 2; n < P; ++n) {
+          const double tn = 2.0 * xx * tb - ta;
+          dst[n] = (float)(sc * tn);
+          ta = tb;
+          tb = tn;
+        }
+      } else {
+        for (int n = 0; n < P; ++n) dst[n] = 0.0f;
+      }
+    }
+    // ---- the previous chunk's accumulator (its MMAs also free the operand buffers)
+    if (c > 0) flush(c - 1);
+    __syncthreads();
+    // ---- operands of this chunk: W row m over the KC points, Tz rows n3 < p
+    if (real) {
+#pragma unroll
+      for (int k4 = 0; k4 < KC; k4 += 4) {
+        float4 h, l;
+        float* hv = &h.x;
+        float* lv = &l.x;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float w = sx[(k4 + e) * P + n1] * sy[(k4 + e) * P + n2];
+          hv[e] = umma::tf32_rna(w);
+          lv[e] = umma::tf32_rna(w - hv[e]);
+        }
+        const int o = umma_koff(m, k4, KC);
+        *reinterpret_cast<float4*>(Ah + o) = h;
+        *reinterpret_cast<float4*>(Al + o) = l;
+      }
+    }
+    for (int w = tid; w < P * (KC / 4); w += NT) {
+      const int n3 = w / (KC / 4), k4 = 4 * (w % (KC / 4));
+      float4 h, l;
+      float* hv = &h.x;
+      float* lv = &l.x;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float z = sz[(k4 + e) * P + n3];
+        hv[e] = umma::tf32_rna(z);
+        lv[e] = umma::tf32_rna(z - hv[e]);
+      }
+      const int o = umma_koff(n3, k4, KC);
+      *reinterpret_cast<float4*>(Bh + o) = h;
+      *reinterpret_cast<float4*>(Bl + o) = l;
+    }
+    umma::fence_smem_to_async();
+    umma::fence_before_sync();
+    __syncthreads();
+    if (tid == 0) {
+      umma::fence_after_sync();
+      const uint32_t dbase = tmem + (uint32_t)((c & 1) * ACOLS);
+      bool accum = false;
+#pragma unroll
+      for (int pr = 0; pr < 3; ++pr) {   // hi.hi, lo.hi, hi.lo
+        const float* A = pr == 1 ? Al : Ah;
+        const float* Bm = pr == 2 ? Bl : Bh;
+#pragma unroll
+        for (int s = 0; s < KC / 8; ++s) {
+          const uint64_t db = umma::sdesc_kmajor(Bm + s * 64, 128, 32 * KC);
+#pragma unroll
+          for (int tm = 0; tm < MT; ++tm) {
+            const uint64_t da = umma::sdesc_kmajor(A + (size_t)tm * 128 * KC + s * 64, 128, 32 * KC);
+            umma::mma_tf32(dbase + tm * NP, da, db, idesc, accum || pr > 0 || s > 0);
+          }
+        }
+        accum = true;
+      }
+      umma::commit(&mbar);
+    }
+  }
+  flush(nch - 1);
+  umma::fence_before_sync();
+  __syncthreads();
+  if (warp == 0) umma::tmem_free<C::TCOLS>(tmem);
+  if (real) {
+    double* out = mom + (size_t)t.fout_rank[b] * P * P2 + (size_t)m * P;
+#pragma unroll
+    for (int n = 0; n < P; ++n) out[n] = acc[n];
+  }
 }
 
 // k_eval32: u_i = sum_n1 T_n1(x_i) sum_n2 T_n2(y_i) sum_n3 Lambda[n1 n2 n3] T_n3(z_i), two
@@ -1380,6 +1557,9 @@ __device__ __forceinline__ float rsqrt_approx(float x) {   // MUFU.RSQ, flush-to
   asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+__device__ __forceinline__ void sts_f32(uint32_t addr, float v) {
+  asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
+}
 __device__ __forceinline__ void two_sum(float a, float b, float& s, float& e) {
   s = __fadd_rn(a, b);
   const float bb = __fsub_rn(s, a);
@@ -1504,6 +1684,268 @@ __global__ void __launch_bounds__(P2P32_NW * 32) k_p2p32(DevTree t, const int32_
   if (lane < nt) {
     double u = 0.0;
     for (int k = 0; k < f; ++k) u += red[warp][lane + k * nt];
+    unear[t0 + lane] = u;
+  }
+}
+
+// ---- fp32 tier, queue form (the default).  k_p2p32 is issue-bound on divergence: the
+// residual polynomial runs whenever ANY lane of the warp holds an in-ball pair, which is
+// almost every iteration although only ~16% of the list pairs of a uniform tree lie
+// inside r_L (ball 4 pi/3 out of 27 boxes).  Here the pass over
+// the list (phase A) only measures the pairs -- coordinates in units of the source leaf's
+// r_L (an exact power-of-two scaling) -- and appends each in-ball pair to a lane-private
+// queue in shared memory as two floats: u = r^2 / r_L^2 and w = rho_j / r_L.  When a
+// lane's queue is nearly full, and at the end of the item, the warp drains the queues
+// (phase B): with s = 2u - 1,
+//   R_L(r) rho_j = (rho_j / r_L) (u^{-1/2} - m_L(s))               (Laplace, Eq. 3.66)
+//   R_L(r) rho_j = (rho_j / r_L) (e^{-lam r} u^{-1/2} - m_L(s))    (Yukawa, Eq. 4.18)
+// two queue entries per packed FFMA2, every lane busy except for the tail of the
+// longest queue.  u = 0 (coincident pair, self term) gives -w m_L(-1) = -M_L(0) rho_j
+// (Step 5).  Yukawa's polynomial and kernel depend on the source
+// level: its queue holds one level at a time (drained when the level changes).
+// Phase A measures with the high parts of the double-single coordinates only (error
+// <= ~2^-24 * 2.5 r_L per coordinate, i.e. <= ~1.5e-7 r_L / r relative on r): a pair
+// closer than sqrt(tc) r_L -- rare, a warp-uniform branch over CHK iterations --
+// is re-measured with the full double-single difference (hi + lo) like k_p2p32.
+// The list's entries are read 32 at a time into registers (lane k holds entry k's
+// range and box) and broadcast by shuffles; the source tile k+1 is loaded into
+// registers while tile k is measured.
+template <int K, int KER, int QC>
+struct P2PQ {
+  // resident one-warp CTAs per SM that the shared memory allows (queue + staging + the
+  // 1 KB per-CTA reservation); the register allocation is held to the same count
+  static constexpr int MINB = (228 * 1024) / (256 * QC + 1400 + 1024);
+  static constexpr int CHK = 4;   // pair iterations between queue-capacity votes
+  static_assert(QC >= 4 * CHK + 2, "queue too small");   // drained at QC - 2 CHK
+};
+struct ResPoly32 {
+  float a[25];   // the residual polynomial's coefficients in fp32 (kernel parameter space)
+};
+// u = r^2 / r_L^2 (queued), w = rho_j / r_L; s = 2u - 1; coefficients c[q] (Laplace: the
+// kernel parameter, constant bank; Yukawa: the queued level's, registers)
+template <int K, int KER, class CF>
+__device__ __forceinline__ float2 p2pq_term(float2 u, float2 w, const CF& c, float lam_rl, bool v0, bool v1) {
+  const float2 s = __ffma2_rn(u, make_float2(2.0f, 2.0f), make_float2(-1.0f, -1.0f));
+  float2 pv = make_float2(c[K], c[K]);
+#pragma unroll
+  for (int q = K - 1; q >= 0; --q) pv = __ffma2_rn(pv, s, make_float2(c[q], c[q]));
+  // r_L / r; u below FLT_MIN (|x_t - x_s| < 1e-19 r_L) counts as coincident
+  float k0 = rsqrt_approx(u.x), k1 = rsqrt_approx(u.y);
+  if (KER == KER_YUKAWA) {   // e^{-lam r}, r = r_L sqrt(u) = r_L u (r_L/r)
+    k0 *= __expf(-lam_rl * u.x * k0);
+    k1 *= __expf(-lam_rl * u.y * k1);
+  }
+  const float2 kv = make_float2(u.x >= 1.17549435e-38f ? k0 : 0.0f, u.y >= 1.17549435e-38f ? k1 : 0.0f);
+  const float2 r = __fmul2_rn(w, __fadd2_rn(kv, make_float2(-pv.x, -pv.y)));
+  return make_float2(v0 ? r.x : 0.0f, v1 ? r.y : 0.0f);
+}
+template <int K, int KER, int QC>
+__global__ void __launch_bounds__(32, P2PQ<K, KER, QC>::MINB) k_p2p32q(DevTree t, const int32_t* __restrict__ items, int64_t nitems,
+                                               const int32_t* __restrict__ doff, const int32_t* __restrict__ dlist,
+                                               const float4* __restrict__ boxc, const float4* __restrict__ src,
+                                               const float4* __restrict__ srclo, ResPoly32 rp,
+                                               const double* __restrict__ lvpoly, float lam, float tc,
+                                               double* __restrict__ unear) {
+  constexpr int CHK = P2PQ<K, KER, QC>::CHK;
+  // staged tile as 16 source pairs + slot 16, a permanent pad; slots past the tile's pairs
+  // are pads too (a chargeless source at (4, 4, 4) r_L, outside every target's ball)
+  __shared__ float4 sA[17], sB[17], sC[17];   // (-x, -y) hi, (-z hi, rho/r_L), (-x, -y) lo
+  __shared__ float2 sD[17];                   // -z lo
+  __shared__ float qT[2 * QC * 32];           // lane-private queues: t at [slot][lane], w QC slots later
+  __shared__ double red[32];
+  const int lane = threadIdx.x;
+  const int64_t it = blockIdx.x;
+  if (it >= nitems) return;
+  const int B = items[2 * it], t0 = items[2 * it + 1];
+  const int nt = min(32, t.end[B] - t0);
+  // an item of nt < 16 targets (the tail of a leaf) splits each source tile over
+  // f = 32/nt lane groups: lane = target + nt * phase, phase strides the source pairs
+  const int f = 32 / nt, tj = lane % nt, ph = lane / nt;
+  const bool act = ph < f;
+  const float4 tp = src[t0 + tj], tl = srclo[t0 + tj];
+  const float4 cB = boxc[B];
+  float cy[KER == KER_YUKAWA ? K + 1 : 1];   // Yukawa: the queued level's coefficients
+  float* fA = reinterpret_cast<float*>(sA);
+  float* fB = reinterpret_cast<float*>(sB);
+  float* fC = reinterpret_cast<float*>(sC);
+  float* fD = reinterpret_cast<float*>(sD);
+  if (lane == 0) {
+    sA[16] = make_float4(-1e30f, -1e30f, -1e30f, -1e30f);
+    sB[16] = make_float4(-1e30f, -1e30f, 0.0f, 0.0f);
+    sC[16] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+    sD[16] = make_float2(0.0f, 0.0f);
+  }
+  // next free slot of this lane's queue as a shared-memory byte address (t; w at +128 QC)
+  const uint32_t qa0 = (uint32_t)__cvta_generic_to_shared(qT + lane);
+  uint32_t qa = qa0;
+  const uint32_t qlim = qa0 + 128 * (QC - 2 * CHK);
+  int qlev = -1;
+  float qlam = 0.0f;   // Yukawa: lam * r_L of the queued level
+  double acc = 0.0;
+  auto drain = [&]() {
+    const int cnt = (int)(qa - qa0) >> 7;
+    const int mx = __reduce_max_sync(0xffffffffu, cnt);
+    float2 ap = make_float2(0.0f, 0.0f);
+    for (int i = 0; i < mx; i += 2) {
+      const float2 tt = make_float2(qT[32 * i + lane], qT[32 * (i + 1) + lane]);
+      const float2 ww = make_float2(qT[32 * (QC + i) + lane], qT[32 * (QC + i + 1) + lane]);
+      if constexpr (KER == KER_YUKAWA)
+        ap = __fadd2_rn(ap, p2pq_term<K, KER>(tt, ww, cy, qlam, i < cnt, i + 1 < cnt));
+      else
+        ap = __fadd2_rn(ap, p2pq_term<K, KER>(tt, ww, rp.a, qlam, i < cnt, i + 1 < cnt));
+    }
+    acc += (double)ap.x + (double)ap.y;
+    qa = qa0;
+  };
+  // ---- the list in batches of 32 entries: lane k holds entry e0 + k
+  const int e_beg = doff[B], e_end = doff[B + 1];
+  int eb = e_beg;   // first entry of the batch in registers
+  int m_start = 0, m_end = 0, m_lev = 0;
+  float4 m_c = cB;
+  auto load_batch = [&](int e0) {
+    eb = e0;
+    if (e0 + lane < e_end) {
+      const int S = dlist[e0 + lane];
+      m_start = t.start[S];
+      m_end = t.end[S];
+      m_c = boxc[S];
+      if (KER == KER_YUKAWA) m_lev = t.level[S];
+    }
+  };
+  load_batch(e_beg);
+  int e = e_beg;
+  int s0 = __shfl_sync(0xffffffffu, m_start, 0), sE = __shfl_sync(0xffffffffu, m_end, 0);
+  float4 rh = make_float4(0.0f, 0.0f, 0.0f, 0.0f), rl = rh;
+  if (s0 + lane < sE) {
+    rh = src[s0 + lane];
+    rl = srclo[s0 + lane];
+  }
+  while (true) {
+    const int k = e - eb;
+    const float4 cS = make_float4(__shfl_sync(0xffffffffu, m_c.x, k), __shfl_sync(0xffffffffu, m_c.y, k),
+                                  __shfl_sync(0xffffffffu, m_c.z, k), __shfl_sync(0xffffffffu, m_c.w, k));
+    const int L = KER == KER_YUKAWA ? __shfl_sync(0xffffffffu, m_lev, k) : 0;
+    const int ns = min(32, sE - s0), npair = (ns + 1) >> 1;
+    const float irl = __int_as_float(0x7F000000 - __float_as_int(cS.w));   // 2^L
+    // ---- stage the current tile (all lanes finished reading the previous one)
+    __syncwarp();
+    {
+      const bool real = lane < ns;
+      const int j = lane >> 1, h = lane & 1;
+      const float pad = -4.0f * cS.w;
+      const float nirl = -irl;   // coordinates in units of r_L, negated
+      fA[4 * j + h] = real ? rh.x * nirl : pad;
+      fA[4 * j + 2 + h] = real ? rh.y * nirl : pad;
+      fB[4 * j + h] = real ? rh.z * nirl : pad;
+      fB[4 * j + 2 + h] = real ? rh.w * irl : 0.0f;
+      fC[4 * j + h] = real ? rl.x * nirl : 0.0f;
+      fC[4 * j + 2 + h] = real ? rl.y * nirl : 0.0f;
+      fD[2 * j + h] = real ? rl.z * nirl : 0.0f;
+    }
+    __syncwarp();
+    // ---- advance the cursor and prefetch the next tile into registers
+    int ns0 = s0 + 32, nsE = sE;
+    bool more = true;
+    if (ns0 >= sE) {
+      ++e;
+      if (e < e_end) {
+        if (e - eb == 32) load_batch(e);
+        ns0 = __shfl_sync(0xffffffffu, m_start, e - eb);
+        nsE = __shfl_sync(0xffffffffu, m_end, e - eb);
+      } else {
+        more = false;
+      }
+    }
+    if (more && ns0 + lane < nsE) {
+      rh = src[ns0 + lane];
+      rl = srclo[ns0 + lane];
+    }
+    // ---- level constants (Yukawa: the queue holds one level)
+    if (KER == KER_YUKAWA) {
+      if (L != qlev) {
+        if (__any_sync(0xffffffffu, qa != qa0)) drain();
+        qlev = L;
+        qlam = lam * cS.w;
+#pragma unroll
+        for (int j = 0; j <= K; ++j) cy[KER == KER_YUKAWA ? j : 0] = (float)__ldg(lvpoly + L * (K + 1) + j);
+      }
+    }
+    // ---- the target in the source leaf's frame (exact centre difference + TwoSum), in
+    // units of r_L (exact power-of-two scaling, as the staged sources)
+    float xt, yt, zt, xe, ye, ze;
+    two_sum(tp.x, cB.x - cS.x, xt, xe);
+    two_sum(tp.y, cB.y - cS.y, yt, ye);
+    two_sum(tp.z, cB.z - cS.z, zt, ze);
+    xe = (xe + tl.x) * irl;
+    ye = (ye + tl.y) * irl;
+    ze = (ze + tl.z) * irl;
+    xt *= irl;
+    yt *= irl;
+    zt *= irl;
+    // ---- phase A: measure, queue the in-ball pairs.  f == 1 (warp-uniform): every lane
+    // walks the same pair slots, padded to a multiple of CHK (pads never enter the ball)
+    const float lim = act ? 1.0f : -1.0f;   // in-ball test u < 1; idle lanes queue nothing
+    auto phase_a = [&](auto uni_) {
+      constexpr bool UNI = decltype(uni_)::value;
+      const int kmax = UNI ? npair : (npair + f - 1) / f;   // warp-uniform trip count
+      for (int k0 = 0; k0 < kmax; k0 += CHK) {
+        if (__any_sync(0xffffffffu, qa > qlim)) drain();
+        float2 tt[CHK], ww[CHK];
+        int jj[CHK];
+        bool close = false;
+#pragma unroll
+        for (int kk = 0; kk < CHK; ++kk) {
+          const int jp = UNI ? k0 + kk : ph + (k0 + kk) * f;
+          jj[kk] = UNI ? jp : (act && jp < npair ? jp : 16);
+          const float4 A = sA[jj[kk]], Bv = sB[jj[kk]];
+          const float2 dx = __fadd2_rn(make_float2(xt, xt), make_float2(A.x, A.y));
+          const float2 dy = __fadd2_rn(make_float2(yt, yt), make_float2(A.z, A.w));
+          const float2 dz = __fadd2_rn(make_float2(zt, zt), make_float2(Bv.x, Bv.y));
+          tt[kk] = __ffma2_rn(dx, dx, __ffma2_rn(dy, dy, __fmul2_rn(dz, dz)));
+          ww[kk] = make_float2(Bv.z, Bv.w);
+          close |= fminf(tt[kk].x, tt[kk].y) < tc;
+        }
+        if (__any_sync(0xffffffffu, close)) {   // rare: close pairs need the low parts
+#pragma unroll
+          for (int kk = 0; kk < CHK; ++kk) {
+            const float4 A = sA[jj[kk]], Bv = sB[jj[kk]], C = sC[jj[kk]];
+            const float2 Dv = sD[jj[kk]];
+            const float2 dx = __fadd2_rn(__fadd2_rn(make_float2(xt, xt), make_float2(A.x, A.y)),
+                                         __fadd2_rn(make_float2(xe, xe), make_float2(C.x, C.y)));
+            const float2 dy = __fadd2_rn(__fadd2_rn(make_float2(yt, yt), make_float2(A.z, A.w)),
+                                         __fadd2_rn(make_float2(ye, ye), make_float2(C.z, C.w)));
+            const float2 dz = __fadd2_rn(__fadd2_rn(make_float2(zt, zt), make_float2(Bv.x, Bv.y)),
+                                         __fadd2_rn(make_float2(ze, ze), Dv));
+            tt[kk] = __ffma2_rn(dx, dx, __ffma2_rn(dy, dy, __fmul2_rn(dz, dz)));
+          }
+        }
+#pragma unroll
+        for (int kk = 0; kk < CHK; ++kk) {
+          if (tt[kk].x < lim) {
+            sts_f32(qa, tt[kk].x);
+            sts_f32(qa + 128 * QC, ww[kk].x);
+            qa += 128;
+          }
+          if (tt[kk].y < lim) {
+            sts_f32(qa, tt[kk].y);
+            sts_f32(qa + 128 * QC, ww[kk].y);
+            qa += 128;
+          }
+        }
+      }
+    };
+    if (f == 1) phase_a(std::true_type{});
+    else phase_a(std::false_type{});
+    if (!more) break;
+    s0 = ns0;
+    sE = nsE;
+  }
+  drain();
+  red[lane] = act ? acc : 0.0;
+  __syncwarp();
+  if (lane < nt) {
+    double u = 0.0;
+    for (int k = 0; k < f; ++k) u += red[lane + k * nt];
     unear[t0 + lane] = u;
   }
 }
@@ -1682,15 +2124,19 @@ __global__ void k_combine(const double* __restrict__ ufar, const double* __restr
 // ---------------------------------------------------------------- host launchers
 void resolve_timings(dmk_plan_s* P) {
   if (P->ev_marks.empty()) return;
-  DMK_CUDA(cudaEventSynchronize(P->ev_marks.back().e1));
+  // marks live on several streams (the near field on the side stream): wait for every
+  // one, and commit the sums only when all of them resolved
+  for (auto& m : P->ev_marks) DMK_CUDA(cudaEventSynchronize(m.e1));
+  std::vector<std::pair<const char*, double>> acc(P->timings);
   for (auto& m : P->ev_marks) {
     float ms = 0;
     DMK_CUDA(cudaEventElapsedTime(&ms, m.e0, m.e1));
     bool found = false;
-    for (auto& pr : P->timings)
+    for (auto& pr : acc)
       if (std::strcmp(pr.first, m.name) == 0) { pr.second += ms; found = true; }
-    if (!found) P->timings.push_back({m.name, (double)ms});
+    if (!found) acc.push_back({m.name, (double)ms});
   }
+  P->timings.swap(acc);
   P->ev_marks.clear();
 }
 
@@ -1708,6 +2154,11 @@ constexpr int px_ch(int P, int H) {
   return (H + nchunk - 1) / nchunk;
 }
 constexpr int pw_ac(int H) { return 2 * H * H <= 1024 ? 2 : 1; }
+
+static bool anterp_tc() {   // validation in progress: opt-in (DMK_ANTERP=tc)
+  const char* e = std::getenv("DMK_ANTERP");
+  return e && std::strcmp(e, "tc") == 0;
+}
 
 // Phases of run_eval: UP = anterpolation + c2p (Step 2), DOWN = Step 3; C2P_ONLY =
 // c2p for the levels above `top` only (after dmk_level_moments injected level `top`).
@@ -1753,9 +2204,16 @@ static void run_eval(dmk_plan_s* PL, int phase = PH_UP | PH_DOWN, int top = 0) {
     tm.begin("anterp");
     DMK_CUDA(cudaMemsetAsync(PL->mom.p, 0, PL->mom.bytes(), s));
     if (PL->nfout) {
-      if constexpr (P <= 18) {   // fp32 tier (R16)
-        set_smem(k_anterp32<P>, Ant32<P>::smem);
-        k_anterp32<P><<<(int)PL->nfout, Ant32<P>::NT, Ant32<P>::smem, s>>>(dt, PL->fout_list.p, PL->q.p, PL->mom.p);
+      if constexpr (P <= 18) {   // fp32 tier (R16): tensor cores (tcgen05), or FFMA2 (DMK_ANTERP=ffma)
+        if (anterp_tc()) {
+          set_smem(k_anterp_tc<P>, AntTC<P>::smem);
+          k_anterp_tc<P><<<(int)PL->nfout, AntTC<P>::NT, AntTC<P>::smem, s>>>(dt, PL->fout_list.p, PL->q.p,
+                                                                              PL->mom.p);
+        } else {
+          set_smem(k_anterp32<P>, Ant32<P>::smem);
+          k_anterp32<P><<<(int)PL->nfout, Ant32<P>::NT, Ant32<P>::smem, s>>>(dt, PL->fout_list.p, PL->q.p,
+                                                                            PL->mom.p);
+        }
       } else {
         size_t sm = AntMma<P>::smem;
         set_smem(k_anterp_mma<P>, sm);
@@ -1933,16 +2391,56 @@ static void run_p2p32_deg(dmk_plan_s* PL, const ResPoly& rp, int K, cudaStream_t
   DMK_LAUNCH_CHECK();
 }
 
+// queue form (default): DMK_P2P_QC selects the queue capacity, DMK_P2P_TC the u = r^2/r_L^2
+// below which a pair is re-measured with the double-single low parts (tuning)
+static float p2p_tc() {
+  const char* e = std::getenv("DMK_P2P_TC");
+  return e ? (float)std::atof(e) : 0.04f;
+}
+template <int KER, int QC>
+static void run_p2p32q_deg(dmk_plan_s* PL, const ResPoly& rp64, int K, cudaStream_t st) {
+  DevTree dt = dev_tree(PL);
+  ResPoly32 rp{};
+  for (int k = 0; k < 25; ++k) rp.a[k] = (float)rp64.a[k];
+  const int64_t nb = PL->np2p;
+  if (nb == 0) return;
+  const Tables& T = *PL->tab;
+#define DMK_P2P_CASE(KK)                                                                                   \
+  case KK:                                                                                                 \
+    k_p2p32q<KK, KER, QC><<<(unsigned)nb, 32, 0, st>>>(dt, PL->p2p_items.p, PL->np2p, PL->dlist_off.p,      \
+                                                      PL->dlist.p, PL->box_c4.p, PL->xl4.p, PL->xl4lo.p, rp, \
+                                                      T.dRespoly, (float)T.lam, p2p_tc(), PL->unear.p);     \
+    break;
+  switch (K) {
+    DMK_P2P_CASE(4) DMK_P2P_CASE(6) DMK_P2P_CASE(8) DMK_P2P_CASE(10) DMK_P2P_CASE(12) DMK_P2P_CASE(14)
+    DMK_P2P_CASE(16) DMK_P2P_CASE(18) DMK_P2P_CASE(20) DMK_P2P_CASE(22) DMK_P2P_CASE(24)
+    default: fail(DMK_ERR_UNSUPPORTED, "residual polynomial degree out of range");
+  }
+#undef DMK_P2P_CASE
+  DMK_LAUNCH_CHECK();
+}
+template <int KER>
+static void run_p2p32q(dmk_plan_s* PL, const ResPoly& rp, int K, cudaStream_t st) {
+  const char* e = std::getenv("DMK_P2P_QC");
+  const int qc = e ? std::atoi(e) : 32;
+  if (qc == 48) run_p2p32q_deg<KER, 48>(PL, rp, K, st);
+  else if (qc == 24) run_p2p32q_deg<KER, 24>(PL, rp, K, st);
+  else run_p2p32q_deg<KER, 32>(PL, rp, K, st);
+}
+static int p2p_form(const dmk_plan_s* PL) {   // 0 queue (default), 1 leaf (k_p2p32), 2 octant
+  const char* e = std::getenv("DMK_P2P_FORM");
+  if (!e) return 0;
+  if (std::strcmp(e, "leaf") == 0) return 1;
+  if (std::strcmp(e, "octant") == 0 && PL->np2p_o > 0) return 2;
+  return 0;
+}
+
 // Sec. 3.4 form: octant items and per-octant source culling (58% of the pairs of a
 // uniform tree).  Opt-in (DMK_P2P_FORM=octant): measured slower than k_p2p32 on both
 // config 1 (3.36 vs 1.23 ms, ~30-point leaves) and config 2 (43 vs 26 ms, mean 52
 // points per leaf): octants of ~4-8 targets leave a warp's lanes with one or two source
 // pairs per list entry, so the per-entry culling and gather cost more than the pairs
 // saved.  Kept as a tested alternative for much bigger leaves.
-static bool use_octant_form(const dmk_plan_s* PL) {
-  const char* e = std::getenv("DMK_P2P_FORM");
-  return e && std::strcmp(e, "octant") == 0 && PL->np2p_o > 0;
-}
 template <int KER>
 static void run_p2p32o_deg(dmk_plan_s* PL, const ResPoly& rp, int K, cudaStream_t st) {
   DevTree dt = dev_tree(PL);
@@ -2015,15 +2513,18 @@ void eval_upward(dmk_plan_s* PL, const double* dcharges) {
   for (int k = 0; k <= K && k < 25; ++k) rp.a[k] = poly[k];
   tm.begin("p2p", slo);
   const bool full = PL->th.nlevels == 1;
+  const int form = p2p32 ? p2p_form(PL) : -1;
   if (PL->tab->kernel == DMK_KERNEL_YUKAWA) {
     K = PL->tab->respoly_deg;
-    if (p2p32 && use_octant_form(PL)) run_p2p32o_deg<KER_YUKAWA>(PL, rp, K, slo);
-    else if (p2p32) run_p2p32_deg<KER_YUKAWA>(PL, rp, K, slo);
+    if (form == 2) run_p2p32o_deg<KER_YUKAWA>(PL, rp, K, slo);
+    else if (form == 1) run_p2p32_deg<KER_YUKAWA>(PL, rp, K, slo);
+    else if (form == 0) run_p2p32q<KER_YUKAWA>(PL, rp, K, slo);
     else if (full) run_p2p_deg<KER_YUKAWA, true>(PL, nullptr, rp, K, slo);
     else run_p2p_deg<KER_YUKAWA, false>(PL, nullptr, rp, K, slo);
   } else {
-    if (p2p32 && use_octant_form(PL)) run_p2p32o_deg<KER_LAPLACE>(PL, rp, K, slo);
-    else if (p2p32) run_p2p32_deg<KER_LAPLACE>(PL, rp, K, slo);
+    if (form == 2) run_p2p32o_deg<KER_LAPLACE>(PL, rp, K, slo);
+    else if (form == 1) run_p2p32_deg<KER_LAPLACE>(PL, rp, K, slo);
+    else if (form == 0) run_p2p32q<KER_LAPLACE>(PL, rp, K, slo);
     else if (full) run_p2p_deg<KER_LAPLACE, true>(PL, nullptr, rp, K, slo);
     else run_p2p_deg<KER_LAPLACE, false>(PL, nullptr, rp, K, slo);
   }

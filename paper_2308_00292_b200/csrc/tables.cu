@@ -525,9 +525,29 @@ Tables* build_log2d_tables(double eps) {
 }
 
 std::mutex g_mu;
-std::map<std::tuple<int, double, double>, Tables*> g_cache;
+// Cache of Step-1 tables, keyed by (device, kernel, Table 1 row, lambda').  Laplace and
+// log tables are one per device and row.  The Yukawa tables depend on lambda' =
+// lambda * side, i.e. on the data's bounding cube, so almost every point set gets its own:
+// at most YUKAWA_CACHE of them stay cached per process (least recently used evicted);
+// plans hold a reference, so an evicted table lives until its last plan is destroyed.
+constexpr size_t YUKAWA_CACHE = 8;
+struct Entry {
+  std::shared_ptr<const Tables> t;
+  uint64_t last_use;
+};
+std::map<std::tuple<int, int, double, double>, Entry> g_cache;
+uint64_t g_tick = 0;
 
 }  // namespace
+
+Tables::~Tables() {
+  int cur = -1;
+  if (cudaGetDevice(&cur) != cudaSuccess) return;
+  if (dev >= 0 && dev != cur) cudaSetDevice(dev);
+  for (double* d : {dQr1, dQr0, dGr1, dGr0, dA, dW, dW0, dRespoly})
+    if (d) cudaFree(d);
+  if (dev >= 0 && dev != cur) cudaSetDevice(cur);
+}
 
 double snap_eps(double eps) {
   for (const Row& r : TABLE1)
@@ -535,14 +555,36 @@ double snap_eps(double eps) {
   return 0;
 }
 
-const Tables& get_tables(int kernel, double eps, double lam) {
+std::shared_ptr<const Tables> get_tables(int kernel, double eps, double lam) {
+  int dev = 0;
+  DMK_CUDA(cudaGetDevice(&dev));
   std::lock_guard<std::mutex> lk(g_mu);
-  auto key = std::make_tuple(kernel, snap_eps(eps), kernel == DMK_KERNEL_YUKAWA ? lam : 0.0);
+  const bool yuk = kernel == DMK_KERNEL_YUKAWA;
+  auto key = std::make_tuple(dev, kernel, snap_eps(eps), yuk ? lam : 0.0);
   auto it = g_cache.find(key);
-  if (it != g_cache.end()) return *it->second;
-  Tables* T = build_tables(kernel, eps, lam);
-  g_cache[key] = T;
-  return *T;
+  if (it != g_cache.end()) {
+    it->second.last_use = ++g_tick;
+    return it->second.t;
+  }
+  std::shared_ptr<Tables> T(build_tables(kernel, eps, lam));
+  T->dev = dev;
+  if (yuk) {
+    size_t ny = 0;
+    auto lru = g_cache.end();
+    for (auto e = g_cache.begin(); e != g_cache.end(); ++e)
+      if (std::get<1>(e->first) == DMK_KERNEL_YUKAWA) {
+        ++ny;
+        if (lru == g_cache.end() || e->second.last_use < lru->second.last_use) lru = e;
+      }
+    if (ny >= YUKAWA_CACHE) g_cache.erase(lru);
+  }
+  g_cache[key] = Entry{T, ++g_tick};
+  return T;
+}
+
+size_t tables_cached() {
+  std::lock_guard<std::mutex> lk(g_mu);
+  return g_cache.size();
 }
 
 }  // namespace dmk

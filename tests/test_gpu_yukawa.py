@@ -25,12 +25,18 @@ def run(x, q, eps, ns, lam=LAM):
     return plan, u
 
 
-@pytest.fixture(scope="module")
-def staged():
+# far-field stage tolerances per tier: the Laplace tier tolerances of
+# tests/test_gpu_parity.py (about 3x the measured fp32 / fp64 rounding error)
+STAGE_TOL = {18: dict(local=5e-7, ufar=1e-6), 28: dict(local=2e-14, ufar=5e-14)}
+
+
+@pytest.fixture(scope="module", params=[1e-6, 1e-9], ids=["eps1e-6", "eps1e-9"])
+def staged(request):
+    eps = request.param
     x, q = dmk_inputs.clusters(2500, seed=11)
-    ref_u, st = dmk_yukawa3d(x, q, 1e-6, 40, LAM, return_stages=True)
-    plan, u = run(x, q, 1e-6, 40)
-    yield dict(x=x, q=q, st=st, plan=plan, u=u, ref_u=ref_u)
+    ref_u, st = dmk_yukawa3d(x, q, eps, 40, LAM, return_stages=True)
+    plan, u = run(x, q, eps, 40)
+    yield dict(x=x, q=q, st=st, plan=plan, u=u, ref_u=ref_u, eps=eps)
     plan.close()
 
 
@@ -42,27 +48,27 @@ def test_yukawa_tree_matches_oracle(staged):
 
 
 def test_yukawa_local_expansions_and_fields(staged):
-    st, plan = staged["st"], staged["plan"]
+    st, plan, eps = staged["st"], staged["plan"], staged["eps"]
     p = plan.info().p
+    tl = STAGE_TOL[p]
     lam = plan.stage("local").reshape(-1, p, p, p)
     exp = plan.tree("exp")
     scale = max(np.max(np.abs(st["local"][i])) for i in st["local"])
-    # p = 18: plane waves stored in fp32 (reading R16)
     for i in np.nonzero(exp >= 0)[0]:
-        assert np.max(np.abs(lam[exp[i]] - st["local"][i])) <= 1e-6 * scale
+        assert np.max(np.abs(lam[exp[i]] - st["local"][i])) <= tl["local"] * scale
     ufar, unear = plan.stage("ufar"), plan.stage("unear")
-    assert np.max(np.abs(ufar - st["u_far"])) <= 1e-6 * np.max(np.abs(st["u_far"]))
+    assert np.max(np.abs(ufar - st["u_far"])) <= tl["ufar"] * np.max(np.abs(st["u_far"]))
     ref_near = st["u_near"] + st["u_self"]
     # The device culls list pairs with r >= r_L, where R_L = K - M_L is below eps M_L(0)
     # but (unlike 1/r) not exactly 0 (reading R13); the
     # oracle evaluates K - M_L over the whole list.  The two agree to that eps tail.
-    assert np.max(np.abs(unear - ref_near)) <= 1e-6 * np.max(np.abs(ref_near))
+    assert np.max(np.abs(unear - ref_near)) <= eps * np.max(np.abs(ref_near))
 
 
 def test_yukawa_potential_vs_oracle_and_direct(staged):
-    u, ref_u = staged["u"], staged["ref_u"]
-    assert np.max(np.abs(u - ref_u)) <= 1e-6 * np.max(np.abs(ref_u))   # reading R13
-    assert direct.rel_l2(u, direct.yukawa3d(staged["x"], staged["q"], LAM)) <= 2e-6
+    u, ref_u, eps = staged["u"], staged["ref_u"], staged["eps"]
+    assert np.max(np.abs(u - ref_u)) <= eps * np.max(np.abs(ref_u))   # reading R13
+    assert direct.rel_l2(u, direct.yukawa3d(staged["x"], staged["q"], LAM)) <= 2 * eps
 
 
 @pytest.mark.parametrize("eps", [1e-3, 1e-6, 1e-9])
