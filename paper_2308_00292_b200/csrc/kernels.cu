@@ -183,7 +183,7 @@ __device__ __forceinline__ int umma_koff(int row, int k, int kc) {   // K-major,
   return (row >> 3) * (kc / 4) * 32 + (k >> 2) * 32 + (row & 7) * 4 + (k & 3);
 }
 template <int P>
-__global__ void __launch_bounds__(AntTC<P>::NT) k_anterp_tc(DevTree t, const int32_t* __restrict__ boxes,
+__global__ void __launch_bounds__(AntTC<P>::NT, 2) k_anterp_tc(DevTree t, const int32_t* __restrict__ boxes,
                                                             const double* __restrict__ q, double* __restrict__ mom) {
   using C = AntTC<P>;
   constexpr int P2 = C::P2, MT = C::MT, NP = C::NP, KC = C::KC, NT = C::NT, ACOLS = C::ACOLS;
@@ -209,9 +209,17 @@ __global__ void __launch_bounds__(AntTC<P>::NT) k_anterp_tc(DevTree t, const int
   __syncthreads();
   const int nr = nr_s, tot = tot_s;
   if (tot == 0) return;   // moments were zeroed by the caller
-  // zero the padding rows / columns once (never rewritten): A rows >= p^2, B rows >= p
-  for (int i = tid; i < (int)(2 * C::A_WORDS); i += NT) smf[i] = 0.0f;
-  for (int i = tid; i < (int)(2 * C::B_WORDS); i += NT) Bh[i] = 0.0f;
+  // zero the padding once (never rewritten): A rows >= p^2, B rows >= p (hi and lo)
+  for (int i = tid; i < (MT * 128 - P2) * KC; i += NT) {
+    const int r = P2 + i / KC, k = i % KC;
+    Ah[umma_koff(r, k, KC)] = 0.0f;
+    Al[umma_koff(r, k, KC)] = 0.0f;
+  }
+  for (int i = tid; i < (NP - P) * KC; i += NT) {
+    const int r = P + i / KC, k = i % KC;
+    Bh[umma_koff(r, k, KC)] = 0.0f;
+    Bl[umma_koff(r, k, KC)] = 0.0f;
+  }
   if (warp == 0) umma::tmem_alloc<C::TCOLS>(&tbase);
   if (tid == 0) umma::mbar_init(&mbar, 1);
   umma::fence_before_sync();
@@ -220,14 +228,18 @@ __global__ void __launch_bounds__(AntTC<P>::NT) k_anterp_tc(DevTree t, const int
   const uint32_t tmem = tbase;
   double cen[3], ih;
   box_geom(t.code[b], t.level[b], cen, ih);
-  // this thread's accumulator row m = (n1, n2): tile tm = warp / 4, TMEM lane quarter warp % 4
-  const int m = tid;                        // rows 0..MT*128-1, row m lives in tile m/128, lane m%128
+  // this thread's accumulator row m = (n1, n2): tile m / 128, TMEM lane m % 128
+  const int m = tid;
   const int n1 = m / P, n2 = m - n1 * P;
   const bool real = m < P2;
   double acc[P];
 #pragma unroll
   for (int n = 0; n < P; ++n) acc[n] = 0.0;
   const uint32_t idesc = umma::idesc_tf32(128, NP);
+  // descriptors of the k-step-0, tile-0 operands; the others differ only in the start
+  // address field (16-byte units): + s * 256 B along K, + tm * 128 * KC * 4 B along M
+  const uint64_t dAh = umma::sdesc_kmajor(Ah, 128, 32 * KC), dAl = umma::sdesc_kmajor(Al, 128, 32 * KC);
+  const uint64_t dBh = umma::sdesc_kmajor(Bh, 128, 32 * KC), dBl = umma::sdesc_kmajor(Bl, 128, 32 * KC);
   const int nch = (tot + KC - 1) / KC;
   auto flush = [&](int c) {   // accumulator of chunk c -> fp64 registers
     umma::mbar_wait(&mbar, (uint32_t)(c & 1));
@@ -239,20 +251,32 @@ __global__ void __launch_bounds__(AntTC<P>::NT) k_anterp_tc(DevTree t, const int
 #pragma unroll
     for (int n = 0; n < P; ++n) acc[n] += (double)v[n];
   };
+  // Chebyshev work item of this thread: point j = tid / 3 of the chunk, axis d = tid % 3;
+  // its coordinate (and charge) are loaded one chunk ahead
+  const int jw = tid / 3, dw = tid % 3;
+  const bool cw = tid < 3 * KC;
+  const double* coord = dw == 0 ? t.xs : (dw == 1 ? t.ys : t.zs);
+  double xn = 0.0, qn = 1.0;
+  auto load_pt = [&](int c) {
+    if (cw && c * KC + jw < tot) {
+      const int pi = range_point(rg, nr, c * KC + jw);
+      xn = (coord[pi] - cen[dw]) * ih;
+      qn = dw == 0 ? q[pi] : 1.0;
+    } else {
+      xn = 2.0;   // outside [-1, 1]: marks a padding point
+    }
+  };
+  load_pt(0);
   for (int c = 0; c < nch; ++c) {
-    const int c0 = c * KC, nc = min(KC, tot - c0);
     // ---- Chebyshev values of the chunk (fp64 recurrence, rounded once)
-    for (int w = tid; w < KC * 3; w += NT) {
-      const int j = w / 3, d = w % 3;
-      float* dst = (d == 0 ? sx : d == 1 ? sy : sz) + j * P;
-      if (j < nc) {
-        const int pi = range_point(rg, nr, c0 + j);
-        const double xx = ((d == 0 ? t.xs[pi] : d == 1 ? t.ys[pi] : t.zs[pi]) - cen[d]) * ih;
-        const double sc = d == 0 ? q[pi] : 1.0;
+    if (cw) {
+      float* dst = (dw == 0 ? sx : dw == 1 ? sy : sz) + jw * P;
+      if (xn <= 1.5) {
+        const double xx = xn, sc = qn;
         double ta = 1.0, tb = xx;
         dst[0] = (float)sc;
         if (P > 1) dst[1] = (float)(sc * xx);
-#pragma unroll 4
+#pragma unroll 6
         for (int n = 2; n < P; ++n) {
           const double tn = 2.0 * xx * tb - ta;
           dst[n] = (float)(sc * tn);
@@ -260,9 +284,11 @@ __global__ void __launch_bounds__(AntTC<P>::NT) k_anterp_tc(DevTree t, const int
           tb = tn;
         }
       } else {
+#pragma unroll
         for (int n = 0; n < P; ++n) dst[n] = 0.0f;
       }
     }
+    if (c + 1 < nch) load_pt(c + 1);
     // ---- the previous chunk's accumulator (its MMAs also free the operand buffers)
     if (c > 0) flush(c - 1);
     __syncthreads();
@@ -305,21 +331,16 @@ __global__ void __launch_bounds__(AntTC<P>::NT) k_anterp_tc(DevTree t, const int
     if (tid == 0) {
       umma::fence_after_sync();
       const uint32_t dbase = tmem + (uint32_t)((c & 1) * ACOLS);
-      bool accum = false;
 #pragma unroll
       for (int pr = 0; pr < 3; ++pr) {   // hi.hi, lo.hi, hi.lo
-        const float* A = pr == 1 ? Al : Ah;
-        const float* Bm = pr == 2 ? Bl : Bh;
+        const uint64_t da0 = pr == 1 ? dAl : dAh, db0 = pr == 2 ? dBl : dBh;
 #pragma unroll
         for (int s = 0; s < KC / 8; ++s) {
-          const uint64_t db = umma::sdesc_kmajor(Bm + s * 64, 128, 32 * KC);
 #pragma unroll
-          for (int tm = 0; tm < MT; ++tm) {
-            const uint64_t da = umma::sdesc_kmajor(A + (size_t)tm * 128 * KC + s * 64, 128, 32 * KC);
-            umma::mma_tf32(dbase + tm * NP, da, db, idesc, accum || pr > 0 || s > 0);
-          }
+          for (int tm = 0; tm < MT; ++tm)
+            umma::mma_tf32(dbase + tm * NP, da0 + (uint64_t)(s * 16 + tm * 32 * KC), db0 + (uint64_t)(s * 16), idesc,
+                           pr > 0 || s > 0);
         }
-        accum = true;
       }
       umma::commit(&mbar);
     }

@@ -307,3 +307,25 @@ def test_p2p_queue_capacities(qc, monkeypatch):
         out[c] = plan.stage("unear")
         plan.close()
     assert np.max(np.abs(out[qc] - out["32"])) <= 1e-6 * np.max(np.abs(out["32"]))
+
+
+@pytest.mark.parametrize("eps", [1e-3, 1e-6])
+def test_anterp_tensor_core_form(eps, monkeypatch):
+    """Anterpolation on the 5th-generation tensor cores (tcgen05 kind::tf32, 3xTF32 split,
+    TMEM accumulators flushed to fp64 every 32 points; DMK_ANTERP=tc) against the oracle's
+    proxy charges (Def. 2.1, mu = V^T rho~) on a deep adaptive tree.  The 3xTF32 products
+    carry ~2^-21 relative error: measured 6.8e-7 (profiles/r02_anterp_forms_v1.jsonl)."""
+    monkeypatch.setenv("DMK_ANTERP", "tc")
+    x, q = dmk_inputs.make("clusters", 12000, seed=21)
+    _, st = dmk_laplace3d(x, q, eps, 40, return_stages=True)
+    T = st["tree"]
+    plan, u = gpu_run(x, q, eps, 40)
+    p = plan.info().p
+    mom = plan.stage("moments").reshape(-1, p, p, p)
+    fout = plan.tree("fout")
+    plan.close()
+    Vt = cheb.V(p).T
+    for i in np.nonzero(T.fout)[0]:
+        ref = cheb.apply3([Vt, Vt, Vt], st["proxy"][i])
+        assert np.max(np.abs(mom[fout[i]] - ref)) <= 2e-6 * max(1.0, np.max(np.abs(ref)))
+    assert direct.rel_l2(u, direct.laplace3d(x, q)) <= 2 * eps
