@@ -111,6 +111,42 @@ __device__ int box_ranges(const DevTree& t, int b, int2* rg) {
   }
   return nr;
 }
+// the same ranges collected by one warp (lanes 0..NCH-1 examine one child each, in
+// parallel: one round of dependent loads instead of NCH), in child order; also writes
+// the number of ranges and the total point count.  Call with all 32 lanes of a warp.
+template <bool EVAL, int NCH = 8>
+__device__ __forceinline__ void box_ranges_w(const DevTree& t, int b, int2* rg, int& nr_out, int& tot_out) {
+  const int lane = threadIdx.x & 31;
+  const uint8_t f = t.flags[b];
+  if (EVAL && (f & F_LEAF)) {
+    if (lane == 0) {
+      rg[0] = make_int2(t.start[b], t.end[b]);
+      nr_out = 1;
+      tot_out = t.end[b] - t.start[b];
+    }
+    return;
+  }
+  bool keep = false;
+  int2 r = make_int2(0, 0);
+  if (lane < NCH) {
+    const int ch = t.child[NCH * (int64_t)b + lane];
+    if (ch >= 0) {
+      const uint8_t fc = t.flags[ch];
+      r = make_int2(t.start[ch], t.end[ch]);
+      keep = (fc & F_LEAF) && r.y > r.x;
+      if (EVAL && ((fc & F_IN) || !(fc & F_TGT))) keep = false;
+    }
+  }
+  const unsigned m = __ballot_sync(0xffffffffu, keep);
+  if (keep) rg[__popc(m & ((1u << lane) - 1))] = r;
+  int len = keep ? r.y - r.x : 0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) len += __shfl_xor_sync(0xffffffffu, len, o);
+  if (lane == 0) {
+    nr_out = __popc(m);
+    tot_out = len;
+  }
+}
 __device__ __forceinline__ int range_point(const int2* rg, int nr, int idx) {
   for (int r = 0; r < nr; ++r) {
     int len = rg[r].y - rg[r].x;

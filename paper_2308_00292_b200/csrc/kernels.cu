@@ -77,12 +77,7 @@ __global__ void __launch_bounds__(Ant32<P>::NT) k_anterp32(DevTree t, const int3
   __shared__ int2 rg[8];
   __shared__ int nr_s, tot_s;
   const int b = boxes[blockIdx.x], tid = threadIdx.x;
-  if (tid == 0) {
-    nr_s = box_ranges<false>(t, b, rg);
-    int tot = 0;
-    for (int r = 0; r < nr_s; ++r) tot += rg[r].y - rg[r].x;
-    tot_s = tot;
-  }
+  if (tid < 32) box_ranges_w<false>(t, b, rg, nr_s, tot_s);
   for (int i = tid; i < P3; i += NT) cube[i] = 0.0;
   __syncthreads();
   const int nr = nr_s, tot = tot_s;
@@ -200,12 +195,7 @@ __global__ void __launch_bounds__(AntTC<P>::NT, 2) k_anterp_tc(DevTree t, const 
   __shared__ int2 rg[8];
   __shared__ int nr_s, tot_s;
   const int b = boxes[blockIdx.x], tid = threadIdx.x, warp = tid >> 5;
-  if (tid == 0) {
-    nr_s = box_ranges<false>(t, b, rg);
-    int tot = 0;
-    for (int r = 0; r < nr_s; ++r) tot += rg[r].y - rg[r].x;
-    tot_s = tot;
-  }
+  if (tid < 32) box_ranges_w<false>(t, b, rg, nr_s, tot_s);
   __syncthreads();
   const int nr = nr_s, tot = tot_s;
   if (tot == 0) return;   // moments were zeroed by the caller
@@ -356,6 +346,173 @@ __global__ void __launch_bounds__(AntTC<P>::NT, 2) k_anterp_tc(DevTree t, const 
   }
 }
 
+// ---- fp32 tier far-field evaluation on the tensor cores (tcgen05 kind::tf32, 3xTF32):
+//   G[j][(n1 n2)] = sum_n3 Tz_j[n3] Lambda[(n1 n2)][n3]          (UMMA: M = 128 targets,
+//   u_j = sum_n1 Tx_j[n1] sum_n2 Ty_j[n2] G[j][(n1 n2)]           N = p^2 in chunks, K = p)
+// One CTA per local-expansion box, one thread per target of a 128-target tile (its
+// Chebyshev values in fp64, rounded once; Tz split hi/lo into its A row).  Lambda (own +
+// inherited part) is split into hi/lo B rows once per box.  The p^2 columns run in NCH
+// chunks of NCW through two TMEM accumulators: chunk c + 2 is issued as soon as the
+// threads have read chunk c, so the tensor core works while the threads contract.
+template <int P>
+struct EvTC {
+  static constexpr int P2 = P * P, KP = (P + 7) / 8 * 8, NB = (P2 + 15) / 16 * 16;
+  static constexpr int NCH = NB <= 128 ? 1 : (NB + 111) / 112, NCW = NB <= 128 ? NB : 112;
+  static constexpr int NT = 128;
+  static constexpr int TCOLS = (NCH > 1 ? 2 : 1) * NCW <= 128 ? 128 : 256;
+  static constexpr size_t A_WORDS = (size_t)128 * KP, B_WORDS = (size_t)NCH * NCW * KP;
+  static constexpr size_t smem = sizeof(float) * (2 * A_WORDS + 2 * B_WORDS) + 128;
+};
+template <int P>
+__global__ void __launch_bounds__(EvTC<P>::NT, 2) k_eval_tc(DevTree t, const int32_t* __restrict__ boxes,
+                                                            const double* __restrict__ lam,
+                                                            const double* __restrict__ lamc,
+                                                            double* __restrict__ ufar) {
+  using C = EvTC<P>;
+  constexpr int P2 = C::P2, KP = C::KP, NCH = C::NCH, NCW = C::NCW, NT = C::NT;
+  extern __shared__ __align__(128) float smf[];
+  float* Ah = smf;                  // [128][KP]  Tz of the tile's targets
+  float* Al = Ah + C::A_WORDS;
+  float* Bh = Al + C::A_WORDS;      // [NCH*NCW][KP]  Lambda rows (n1 n2)
+  float* Bl = Bh + C::B_WORDS;
+  __shared__ __align__(8) uint64_t mbar[2];
+  __shared__ uint32_t tbase;
+  __shared__ int2 rg[8];
+  __shared__ int nr_s, tot_s;
+  const int b = boxes[blockIdx.x], tid = threadIdx.x, warp = tid >> 5;
+  if (tid < 32) box_ranges_w<true>(t, b, rg, nr_s, tot_s);
+  __syncthreads();
+  const int nr = nr_s, tot = tot_s;
+  if (tot == 0) return;
+  // ---- B: the box's local expansion (own + inherited) as hi/lo tf32 rows, zero padded
+  {
+    const double* src = lam + (size_t)t.exp_rank[b] * P * P2;
+    const double* srcc = lamc + (size_t)t.exp_rank[b] * P * P2;
+    // one row (n1 n2) of p values per thread and pass: all its loads in flight together
+    for (int r = tid; r < NCH * NCW; r += NT) {
+      double v[KP];
+#pragma unroll
+      for (int k = 0; k < KP; ++k) v[k] = 0.0;
+      if (r < P2) {
+#pragma unroll
+        for (int k = 0; k < P; ++k) v[k] = __ldg(src + (size_t)r * P + k) + __ldg(srcc + (size_t)r * P + k);
+      }
+#pragma unroll
+      for (int k4 = 0; k4 < KP; k4 += 4) {
+        float4 h, l;
+        float* hv = &h.x;
+        float* lv = &l.x;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float f = (float)v[k4 + e];
+          hv[e] = umma::tf32_rna(f);
+          lv[e] = umma::tf32_rna(f - hv[e]);
+        }
+        const int o = umma_koff(r, k4, KP);
+        *reinterpret_cast<float4*>(Bh + o) = h;
+        *reinterpret_cast<float4*>(Bl + o) = l;
+      }
+    }
+  }
+  if (warp == 0) umma::tmem_alloc<C::TCOLS>(&tbase);
+  if (tid == 0) {
+    umma::mbar_init(&mbar[0], 1);
+    umma::mbar_init(&mbar[1], 1);
+  }
+  umma::fence_before_sync();
+  __syncthreads();
+  umma::fence_after_sync();
+  const uint32_t tmem = tbase;
+  double cen[3], ih;
+  box_geom(t.code[b], t.level[b], cen, ih);
+  const uint32_t idesc = umma::idesc_tf32(128, NCW);
+  const uint64_t dAh = umma::sdesc_kmajor(Ah, 128, 32 * KP), dAl = umma::sdesc_kmajor(Al, 128, 32 * KP);
+  const uint64_t dBh = umma::sdesc_kmajor(Bh, 128, 32 * KP), dBl = umma::sdesc_kmajor(Bl, 128, 32 * KP);
+  uint32_t ph0 = 0, ph1 = 0;   // completed phases of the two accumulators' mbarriers
+  auto issue = [&](int c) {    // chunk c of the p^2 columns into accumulator c % 2
+    umma::fence_after_sync();
+    const uint32_t d = tmem + (uint32_t)((c & 1) * NCW);
+    const uint64_t boff = (uint64_t)(c * NCW / 8) * (32 * KP / 16);   // rows c NCW.. (16-byte units)
+#pragma unroll
+    for (int pr = 0; pr < 3; ++pr) {   // hi.hi, lo.hi, hi.lo
+      const uint64_t da = pr == 1 ? dAl : dAh, db = (pr == 2 ? dBl : dBh) + boff;
+#pragma unroll
+      for (int s = 0; s < KP / 8; ++s) umma::mma_tf32(d, da + (uint64_t)(s * 16), db + (uint64_t)(s * 16), idesc, pr > 0 || s > 0);
+    }
+    umma::commit(&mbar[c & 1]);
+  };
+  for (int t0 = 0; t0 < tot; t0 += 128) {
+    const int j = t0 + tid;
+    const bool real = j < tot;
+    const int pi = real ? range_point(rg, nr, j) : 0;
+    float tx[P], ty[P];
+    {
+      double tz[P];
+      cheb_vec(real ? (t.xs[pi] - cen[0]) * ih : 0.0, tz, P, 1.0);
+#pragma unroll
+      for (int n = 0; n < P; ++n) tx[n] = (float)tz[n];
+      cheb_vec(real ? (t.ys[pi] - cen[1]) * ih : 0.0, tz, P, 1.0);
+#pragma unroll
+      for (int n = 0; n < P; ++n) ty[n] = (float)tz[n];
+      cheb_vec(real ? (t.zs[pi] - cen[2]) * ih : 0.0, tz, P, real ? 1.0 : 0.0);
+#pragma unroll
+      for (int k4 = 0; k4 < KP; k4 += 4) {
+        float4 h, l;
+        float* hv = &h.x;
+        float* lv = &l.x;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float z = k4 + e < P ? (float)tz[k4 + e] : 0.0f;
+          hv[e] = umma::tf32_rna(z);
+          lv[e] = umma::tf32_rna(z - hv[e]);
+        }
+        const int o = umma_koff(tid, k4, KP);
+        *reinterpret_cast<float4*>(Ah + o) = h;
+        *reinterpret_cast<float4*>(Al + o) = l;
+      }
+    }
+    umma::fence_smem_to_async();
+    umma::fence_before_sync();
+    __syncthreads();
+    if (tid == 0) {
+      issue(0);
+      if (NCH > 1) issue(1);
+    }
+    float s[P];
+#pragma unroll
+    for (int n = 0; n < P; ++n) s[n] = 0.0f;
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) {
+      umma::mbar_wait(&mbar[c & 1], (c & 1) ? ph1 : ph0);
+      if (c & 1) ph1 ^= 1;
+      else ph0 ^= 1;
+      umma::fence_after_sync();
+      const uint32_t base = tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)((c & 1) * NCW);
+#pragma unroll
+      for (int c32 = 0; c32 < NCW; c32 += 32) {
+        float g[32];
+        if (c32 + 32 <= NCW) umma::ld32x32b_x32(base + c32, g);
+        else umma::ld32x32b_x16(base + c32, g);
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          const int r = c * NCW + c32 + e;   // row (n1 n2), compile-time after unrolling
+          if (c32 + e < NCW && r < P2) s[r / P] = fmaf(ty[r % P], g[e], s[r / P]);
+        }
+      }
+      umma::fence_before_sync();
+      __syncthreads();   // accumulator c % 2 read by every thread
+      if (tid == 0 && c + 2 < NCH) issue(c + 2);
+    }
+    double u = 0.0;
+#pragma unroll
+    for (int n = 0; n < P; ++n) u = fma((double)tx[n], (double)s[n], u);
+    if (real) ufar[pi] = u;
+  }
+  umma::fence_before_sync();
+  __syncthreads();
+  if (warp == 0) umma::tmem_free<C::TCOLS>(tmem);
+}
+
 // k_eval32: u_i = sum_n1 T_n1(x_i) sum_n2 T_n2(y_i) sum_n3 Lambda[n1 n2 n3] T_n3(z_i), two
 // targets per thread (each Lambda row read from shared memory serves both), the n3 sums
 // as packed FFMA2 (even/odd n3 halves), T_n1 by the recurrence in fp64, the n1 sum in fp64.
@@ -375,12 +532,7 @@ __global__ void __launch_bounds__(Ev32<P>::NT) k_eval32(DevTree t, const int32_t
   __shared__ int2 rg[8];
   __shared__ int nr_s, tot_s;
   const int b = boxes[blockIdx.x], tid = threadIdx.x;
-  if (tid == 0) {
-    nr_s = box_ranges<true>(t, b, rg);
-    int tot = 0;
-    for (int r = 0; r < nr_s; ++r) tot += rg[r].y - rg[r].x;
-    tot_s = tot;
-  }
+  if (tid < 32) box_ranges_w<true>(t, b, rg, nr_s, tot_s);
   __syncthreads();
   const int nr = nr_s, tot = tot_s;
   if (tot == 0) return;
@@ -1327,12 +1479,7 @@ __global__ void __launch_bounds__(256) k_eval_mma(DevTree t, const int32_t* __re
   __shared__ int2 rg[8];
   __shared__ int nr_s, tot_s;
   const int b = boxes[blockIdx.x], tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) {
-    nr_s = box_ranges<true>(t, b, rg);
-    int tot = 0;
-    for (int r = 0; r < nr_s; ++r) tot += rg[r].y - rg[r].x;
-    tot_s = tot;
-  }
+  if (tid < 32) box_ranges_w<true>(t, b, rg, nr_s, tot_s);
   const double* src = lam + (size_t)t.exp_rank[b] * P * P2;   // own + inherited (p2c) expansions
   const double* srcc = lamc + (size_t)t.exp_rank[b] * P * P2;
   for (int i = tid; i < NT8 * KS * 32; i += NW * 32) {
@@ -1419,12 +1566,7 @@ __global__ void __launch_bounds__(AntMma<P>::NW * 32)
   __shared__ int2 rg[8];
   __shared__ int nr_s, tot_s;
   const int b = boxes[blockIdx.x], tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) {
-    nr_s = box_ranges<false>(t, b, rg);
-    int tot = 0;
-    for (int r = 0; r < nr_s; ++r) tot += rg[r].y - rg[r].x;
-    tot_s = tot;
-  }
+  if (tid < 32) box_ranges_w<false>(t, b, rg, nr_s, tot_s);
   __syncthreads();
   const int nr = nr_s, tot = tot_s;
   if (tot == 0) return;   // moments were zeroed by the caller
@@ -2181,6 +2323,11 @@ static bool anterp_tc() {   // validation in progress: opt-in (DMK_ANTERP=tc)
   return e && std::strcmp(e, "tc") == 0;
 }
 
+static bool eval_tc() {   // default: tensor cores; DMK_EVAL=ffma selects k_eval32
+  const char* e = std::getenv("DMK_EVAL");
+  return !(e && std::strcmp(e, "ffma") == 0);
+}
+
 // Phases of run_eval: UP = anterpolation + c2p (Step 2), DOWN = Step 3; C2P_ONLY =
 // c2p for the levels above `top` only (after dmk_level_moments injected level `top`).
 constexpr int PH_ANTERP = 1, PH_DOWN = 2, PH_C2P_ONLY = 4, PH_C2P = 8, PH_UP = PH_ANTERP | PH_C2P;
@@ -2352,10 +2499,16 @@ static void run_eval(dmk_plan_s* PL, int phase = PH_UP | PH_DOWN, int top = 0) {
     tm.begin("eval");
     {
       if (PL->nexp) {
-        if constexpr (P <= 18) {   // fp32 tier (R16)
-          set_smem(k_eval32<P>, Ev32<P>::smem);
-          k_eval32<P><<<(int)PL->nexp, Ev32<P>::NT, Ev32<P>::smem, s>>>(dt, PL->exp_list.p, PL->lam.p, PL->lamc.p,
-                                                                          PL->ufar.p);
+        if constexpr (P <= 18) {   // fp32 tier (R16): tensor cores, or FFMA2 (DMK_EVAL=ffma)
+          if (eval_tc()) {
+            set_smem(k_eval_tc<P>, EvTC<P>::smem);
+            k_eval_tc<P><<<(int)PL->nexp, EvTC<P>::NT, EvTC<P>::smem, s>>>(dt, PL->exp_list.p, PL->lam.p,
+                                                                              PL->lamc.p, PL->ufar.p);
+          } else {
+            set_smem(k_eval32<P>, Ev32<P>::smem);
+            k_eval32<P><<<(int)PL->nexp, Ev32<P>::NT, Ev32<P>::smem, s>>>(dt, PL->exp_list.p, PL->lam.p,
+                                                                            PL->lamc.p, PL->ufar.p);
+          }
         } else {
           size_t sm = EvalMma<P>::smem;
           set_smem(k_eval_mma<P>, sm);

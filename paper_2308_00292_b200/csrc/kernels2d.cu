@@ -48,12 +48,7 @@ __global__ void __launch_bounds__(256) k_anterp2(DevTree t, const int32_t* __res
   __shared__ int2 rg[NCH2];
   __shared__ int nr_s, tot_s;
   const int b = boxes[blockIdx.x], tid = threadIdx.x;
-  if (tid == 0) {
-    nr_s = box_ranges<false, NCH2>(t, b, rg);
-    int tot = 0;
-    for (int r = 0; r < nr_s; ++r) tot += rg[r].y - rg[r].x;
-    tot_s = tot;
-  }
+  if (tid < 32) box_ranges_w<false, NCH2>(t, b, rg, nr_s, tot_s);
   __syncthreads();
   const int nr = nr_s, tot = tot_s;
   double* out = mom + (size_t)t.fout_rank[b] * P2;
@@ -296,12 +291,7 @@ __global__ void __launch_bounds__(128) k_eval2(DevTree t, const int32_t* __restr
   __shared__ int2 rg[NCH2];
   __shared__ int nr_s, tot_s;
   const int b = boxes[blockIdx.x], tid = threadIdx.x;
-  if (tid == 0) {
-    nr_s = box_ranges<true, NCH2>(t, b, rg);
-    int tot = 0;
-    for (int r = 0; r < nr_s; ++r) tot += rg[r].y - rg[r].x;
-    tot_s = tot;
-  }
+  if (tid < 32) box_ranges_w<true, NCH2>(t, b, rg, nr_s, tot_s);
   const double* src = lam + (size_t)t.exp_rank[b] * P2;
   for (int i = tid; i < P2; i += NT) L[i] = src[i];
   __syncthreads();

@@ -329,3 +329,19 @@ def test_anterp_tensor_core_form(eps, monkeypatch):
         ref = cheb.apply3([Vt, Vt, Vt], st["proxy"][i])
         assert np.max(np.abs(mom[fout[i]] - ref)) <= 2e-6 * max(1.0, np.max(np.abs(ref)))
     assert direct.rel_l2(u, direct.laplace3d(x, q)) <= 2 * eps
+
+
+@pytest.mark.parametrize("eps", [1e-3, 1e-6])
+def test_eval_forms_agree(eps, monkeypatch):
+    """Far-field evaluation on the tensor cores (default, k_eval_tc: tcgen05 kind::tf32,
+    3xTF32) and on packed FFMA2 (DMK_EVAL=ffma, k_eval32): both against the oracle's far
+    field (Step 3 leaf evaluation) on a deep adaptive tree."""
+    x, q = dmk_inputs.make("sphere", 8000, seed=21)
+    _, st = dmk_laplace3d(x, q, eps, 60, return_stages=True)
+    for form in ("tc", "ffma"):
+        monkeypatch.setenv("DMK_EVAL", form)
+        plan, u = gpu_run(x, q, eps, 60)
+        ufar = plan.stage("ufar")
+        plan.close()
+        assert np.max(np.abs(ufar - st["u_far"])) <= tol(18, "ufar") * np.max(np.abs(st["u_far"])), form
+        assert direct.rel_l2(u, direct.laplace3d(x, q)) <= 2 * eps, form
