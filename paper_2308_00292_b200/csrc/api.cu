@@ -8,6 +8,7 @@
 #include "common.cuh"
 
 namespace dmk {
+bool pw64_group_env();
 void build_tree(dmk_plan_s* P, const double* dpts);
 void eval_plan(dmk_plan_s* P, const double* dcharges, double* dout);
 
@@ -115,6 +116,7 @@ static void alloc_eval_buffers(dmk_plan_s* P) {
     if (P->dim == 3) P->lamc.alloc(P->nexp * pd, s);
     // fp32 tier (p <= 18, 3D): weighted incoming plane waves of every local box (k_pwshift)
     if (P->dim == 3 && T.p <= 18) P->pwt.alloc(P->nexp * P->phi_size1, s);
+    if (P->dim == 3 && T.p > 18 && pw64_group_env() && P->nexp > 1) P->pwt64.alloc(P->nexp * P->phi_size1, s);
   }
 }
 

@@ -1189,6 +1189,129 @@ __global__ void __launch_bounds__(PWS_NT, 3)
   }
 }
 
+// ---- eps = 1e-9 tier (p = 28, fp64): the same parent-group translation in double
+// precision.  The 8 x 8 fp64 window sums of one mode do not fit one thread's registers,
+// so a thread owns one mode and one half of the children (o1), and walks the 3 x 4 x 4
+// part of the window that half needs (48 instead of 64 reads of F per mode and half;
+// per child 24 instead of the 27 x 8 = 216 reads of the per-box form).  The weighted
+// incoming expansions go to T (fp64) for the back transforms (k_pwlocal<..., FROMT>).
+constexpr int PWS64_NT = 128;
+template <int H>
+__global__ void __launch_bounds__(PWS64_NT, 2)
+    k_pwshift64(DevTree t, const int32_t* __restrict__ parents, const double* __restrict__ F, size_t base,
+                size_t stride, const double* __restrict__ W, size_t wstride, double* __restrict__ Tout) {
+  constexpr int HSQ = H * H, NM = H * HSQ, SLAB = 8 * HSQ;
+  __shared__ const double* win[64];   // window box (w1 w2 w3), null: absent or not F_out
+  __shared__ int rank[8];             // exp rank of child o = (o1 o2 o3), -1: none
+  __shared__ int lvl;
+  const int pb = parents[blockIdx.x], tid = threadIdx.x;   // grid: (parent, mode block, o1)
+  if (tid < 64) {
+    const int w1 = tid >> 4, w2 = (tid >> 2) & 3, w3 = tid & 3;
+    const int D1 = w1 == 0 ? -1 : (w1 == 3 ? 1 : 0), D2 = w2 == 0 ? -1 : (w2 == 3 ? 1 : 0),
+              D3 = w3 == 0 ? -1 : (w3 == 3 ? 1 : 0);
+    const int c1 = w1 - 2 * D1 - 1, c2 = w2 - 2 * D2 - 1, c3 = w3 - 2 * D3 - 1;
+    const int S = t.coll[27 * (int64_t)pb + (D1 + 1) * 9 + (D2 + 1) * 3 + (D3 + 1)];
+    const double* ptr = nullptr;
+    if (S >= 0) {
+      const int ch = t.child[8 * (int64_t)S + (c1 << 2) + (c2 << 1) + c3];
+      if (ch >= 0 && (t.flags[ch] & F_OUT)) ptr = F + base + (size_t)(t.fout_rank[ch] - 1) * stride;
+    }
+    win[tid] = ptr;
+  } else if (tid < 72) {
+    const int ch = t.child[8 * (int64_t)pb + (tid - 64)];
+    rank[tid - 64] = (ch >= 0 && (t.flags[ch] & F_EXP)) ? t.exp_rank[ch] : -1;
+    if (tid == 64) lvl = t.level[pb] + 1;
+  }
+  __syncthreads();
+  const int o1 = blockIdx.z;
+  bool any = false;
+#pragma unroll
+  for (int o = 0; o < 4; ++o) any |= rank[o1 * 4 + o] >= 0;
+  if (!any) return;
+  const double* Wl = W + (size_t)lvl * wstride;
+  const int m = blockIdx.y * PWS64_NT + tid;
+  if (m >= NM) return;
+  const int a = m / HSQ, bc = m - a * HSQ;
+  double Ca, Sa, Cb, Sb, Cc, Sc;
+  rot_cs(a, Ca, Sa);
+  rot_cs(bc / H, Cb, Sb);
+  rot_cs(bc % H, Cc, Sc);
+  const size_t off = (size_t)a * SLAB + bc;
+  double X[2][2][8];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int p = 0; p < 8; ++p) X[i][j][p] = 0.0;
+#pragma unroll 1
+  for (int w1 = o1; w1 < o1 + 3; ++w1) {
+    double Y[2][2][8];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int p = 0; p < 8; ++p) Y[i][j][p] = 0.0;
+#pragma unroll
+    for (int w2 = 0; w2 < 4; ++w2) {
+      double Z[2][8];
+#pragma unroll
+      for (int p = 0; p < 8; ++p) Z[0][p] = Z[1][p] = 0.0;
+#pragma unroll
+      for (int w3 = 0; w3 < 4; ++w3) {
+        const double* sp = win[w1 * 16 + w2 * 4 + w3];
+        if (sp == nullptr) continue;
+        double g[8];
+#pragma unroll
+        for (int p = 0; p < 8; ++p) g[p] = __ldg(sp + off + p * HSQ);
+        // child o3 takes window w3 in o3..o3+2 with delta = o3 + 1 - w3
+        if (w3 <= 2) {
+          if (w3 == 0) rot_acc<1, 1>(Z[0], g, Cc, Sc);
+          else if (w3 == 1) rot_acc<1, 0>(Z[0], g, Cc, Sc);
+          else rot_acc<1, -1>(Z[0], g, Cc, Sc);
+        }
+        if (w3 >= 1) {
+          if (w3 == 1) rot_acc<1, 1>(Z[1], g, Cc, Sc);
+          else if (w3 == 2) rot_acc<1, 0>(Z[1], g, Cc, Sc);
+          else rot_acc<1, -1>(Z[1], g, Cc, Sc);
+        }
+      }
+#pragma unroll
+      for (int o2 = 0; o2 < 2; ++o2) {
+        if (w2 < o2 || w2 > o2 + 2) continue;
+        const int d = o2 + 1 - w2;
+#pragma unroll
+        for (int o3 = 0; o3 < 2; ++o3) {
+          if (d > 0) rot_acc<2, 1>(Y[o2][o3], Z[o3], Cb, Sb);
+          else if (d < 0) rot_acc<2, -1>(Y[o2][o3], Z[o3], Cb, Sb);
+          else rot_acc<2, 0>(Y[o2][o3], Z[o3], Cb, Sb);
+        }
+      }
+    }
+    const int d = o1 + 1 - w1;
+#pragma unroll
+    for (int o2 = 0; o2 < 2; ++o2)
+#pragma unroll
+      for (int o3 = 0; o3 < 2; ++o3) {
+        if (d > 0) rot_acc<4, 1>(X[o2][o3], Y[o2][o3], Ca, Sa);
+        else if (d < 0) rot_acc<4, -1>(X[o2][o3], Y[o2][o3], Ca, Sa);
+        else rot_acc<4, 0>(X[o2][o3], Y[o2][o3], Ca, Sa);
+      }
+  }
+  const double wt = __ldg(Wl + m);
+#pragma unroll
+  for (int o2 = 0; o2 < 2; ++o2)
+#pragma unroll
+    for (int o3 = 0; o3 < 2; ++o3) {
+      const int r = rank[o1 * 4 + o2 * 2 + o3];
+      if (r < 0) continue;
+      double* dst = Tout + (size_t)r * H * SLAB + off;
+#pragma unroll
+      for (int p = 0; p < 8; ++p) dst[p * HSQ] = wt * X[o2][o3][p];
+    }
+}
+
 // fp32 tier: T_pw2poly (Eqs. 3.43-3.44) of every non-root local box from the weighted
 // incoming expansion T[a][pi][b][c] written by k_pwshift, as three axis contractions
 // over the whole box (no slab chunking, two barriers): axis 3 rows (a, pi12, b) from
@@ -1290,11 +1413,11 @@ struct PwLocal {
                         (VSMEM ? (size_t)H * 2 * G::P2 : (size_t)AC * 2 * G::P2));
   static constexpr int MINB = (VSMEM && NT <= 352) ? 2 : 1;
 };
-template <int P, int H, int AC, bool ROOT, bool FROMT = false>
+template <int P, int H, int AC, bool ROOT, bool FROMT = false, class TT = float>
 __global__ void __launch_bounds__(PwLocal<P, H, AC>::NT, PwLocal<P, H, AC>::MINB)
     k_pwlocal(DevTree t, const int32_t* __restrict__ boxes, const double* __restrict__ Gr,
               const double* __restrict__ W, size_t wstride, const FStore<P>* __restrict__ F, size_t base,
-              size_t stride, double* __restrict__ lam, const float* __restrict__ Tin = nullptr) {
+              size_t stride, double* __restrict__ lam, const TT* __restrict__ Tin = nullptr) {
   using G = PwGeom<P, H>;
   using C = PwLocal<P, H, AC>;
   using TF = FStore<P>;
@@ -1336,7 +1459,7 @@ __global__ void __launch_bounds__(PwLocal<P, H, AC>::NT, PwLocal<P, H, AC>::MINB
       const size_t off = (size_t)a * SLAB + bc;
       double o[8];
       if (FROMT) {   // translated and weighted by k_pwshift
-        const float* tb = Tin + (size_t)t.exp_rank[b] * H * SLAB + off;
+        const TT* tb = Tin + (size_t)t.exp_rank[b] * H * SLAB + off;
 #pragma unroll
         for (int p = 0; p < 8; ++p) o[p] = (double)__ldg(tb + p * HSQ);
       } else if (ROOT) {
@@ -2328,6 +2451,16 @@ static bool eval_tc() {   // default: tensor cores; DMK_EVAL=ffma selects k_eval
   return !(e && std::strcmp(e, "ffma") == 0);
 }
 
+// eps = 1e-9 translation: the 27-colleague per-box form (default: measured 8.4 ms at
+// config 1) or parent groups + fp64 T + back transforms (DMK_PW64=group: 7.0 + 3.6 ms,
+// k_pwshift64 is latency-bound at 204 registers / 8 warps per SM; profiles/
+// r02_pw64_forms_v1.jsonl); chosen at plan time (the T buffer is sized then)
+bool pw64_group_env() {
+  const char* e = std::getenv("DMK_PW64");
+  return e && std::strcmp(e, "group") == 0;
+}
+#define pw64_group() (PL->pwt64.n > 0)
+
 // Phases of run_eval: UP = anterpolation + c2p (Step 2), DOWN = Step 3; C2P_ONLY =
 // c2p for the levels above `top` only (after dmk_level_moments injected level `top`).
 constexpr int PH_ANTERP = 1, PH_DOWN = 2, PH_C2P_ONLY = 4, PH_C2P = 8, PH_UP = PH_ANTERP | PH_C2P;
@@ -2469,6 +2602,22 @@ static void run_eval(dmk_plan_s* PL, int phase = PH_UP | PH_DOWN, int top = 0) {
           set_smem(k_pw2poly32<P, H>, K2::smem);
           k_pw2poly32<P, H><<<(int)(PL->nexp - 1), K2::NT, K2::smem, s>>>(dt, PL->exp_list.p + 1, T.dGr1, PL->pwt.p,
                                                                          PL->lam.p);
+        } else if (pw64_group()) {
+          // eps = 1e-9: fp64 parent-group translation into T, then the back transforms
+          tm.end();
+          tm.begin("pwshift");
+          if (PL->nfout > 0) {
+            const dim3 grid((unsigned)PL->nfout, (unsigned)((H * H * H + PWS64_NT - 1) / PWS64_NT), 2);
+            k_pwshift64<H><<<grid, PWS64_NT, 0, s>>>(dt, PL->fout_list.p, reinterpret_cast<const double*>(Fp),
+                                                     PL->phi_size0, PL->phi_size1, T.dW, T.wstride, PL->pwt64.p);
+            DMK_LAUNCH_CHECK();
+          }
+          tm.end();
+          tm.begin("pw2poly");
+          set_smem(k_pwlocal<P, H, AC, false, true, double>, K1::smem);
+          k_pwlocal<P, H, AC, false, true, double><<<(int)(PL->nexp - 1), K1::NT, K1::smem, s>>>(
+              dt, PL->exp_list.p + 1, T.dGr1, T.dW, T.wstride, Fp, PL->phi_size0, PL->phi_size1, PL->lam.p,
+              PL->pwt64.p);
         } else {
           k_pwlocal<P, H, AC, false><<<(int)(PL->nexp - 1), K1::NT, K1::smem, s>>>(
               dt, PL->exp_list.p + 1, T.dGr1, T.dW, T.wstride, Fp, PL->phi_size0, PL->phi_size1, PL->lam.p);

@@ -345,3 +345,26 @@ def test_eval_forms_agree(eps, monkeypatch):
         plan.close()
         assert np.max(np.abs(ufar - st["u_far"])) <= tol(18, "ufar") * np.max(np.abs(st["u_far"])), form
         assert direct.rel_l2(u, direct.laplace3d(x, q)) <= 2 * eps, form
+
+
+def test_pw64_parent_group_form(monkeypatch):
+    """eps = 1e-9 (p = 28, fp64): the parent-group translation (k_pwshift64: the 8 children
+    of a parent from the 4x4x4 window of outgoing expansions, Eq. 3.39, then the back
+    transforms from T, Eqs. 3.43-3.44; DMK_PW64=group) against the oracle's local
+    expansions and the default per-box form."""
+    x, q = dmk_inputs.make("sphere", 8000, seed=21)
+    _, st = dmk_laplace3d(x, q, 1e-9, 60, return_stages=True)
+    res = {}
+    for form in ("group", "box"):
+        monkeypatch.setenv("DMK_PW64", form)
+        plan, u = gpu_run(x, q, 1e-9, 60)
+        p = plan.info().p
+        lam = plan.stage("local").reshape(-1, p, p, p)
+        ex = plan.tree("exp")
+        plan.close()
+        scale = max(np.max(np.abs(st["local"][i])) for i in st["local"])
+        for i in np.nonzero(ex >= 0)[0]:
+            assert np.max(np.abs(lam[ex[i]] - st["local"][i])) <= tol(28, "local") * scale, form
+        res[form] = u
+    assert np.max(np.abs(res["group"] - res["box"])) <= 1e-13 * np.max(np.abs(res["box"]))
+    assert direct.rel_l2(res["group"], direct.laplace3d(x, q)) <= 2e-9
