@@ -34,6 +34,16 @@ sys.path.insert(0, ROOT)
 METRIC = "points/sec, 3D Laplace DMK, eps=1e-6, 1/2/4/8 B200; rel ℓ2 err vs direct"
 WORKLOAD = ("config1: 3D Laplace K=1/r, N=1e6 uniform iid in [0,1]^3, charges U[-1,1], "
             "eps=1e-6, leaf capacity 200, single B200 per rank")
+# The paper's own measurement context (context only, not a baseline: other hardware and a
+# single core).  Its throughput values are plotted, not printed: PAPER.md:2603-2606.
+PAPER_CONTEXT = {
+    "hardware": "single core of a 3.30 GHz Intel Xeon Gold 6234, single-threaded (PAPER.md:2518-2520)",
+    "software": "Fortran, Intel compiler, Intel MKL (PAPER.md:2518-2519)",
+    "workload": "3D Laplace, N = m 1e6 uniform in the unit box (m = 1..8) and on a sphere of radius "
+                "0.45; n_s = 280 for eps 1e-3/1e-6, 800 for 1e-9/1e-12 (PAPER.md:2531-2540)",
+    "throughput": "average throughput in units of 1e5 points/s, plotted per eps in the paper's "
+                  "throughput figure (PAPER.md:2603-2606); the values are not given in the text",
+}
 FP64_FMA_PER_CLK_SM = 64
 FP32_FMA_PER_CLK_SM = 128
 N_SM = 148
@@ -516,12 +526,16 @@ def main():
     dom = max(stages, key=lambda s: stages[s]["ms"])
     roof = dict(stages[dom])
     roof.pop("ms")
-    try:
-        traffic = json.load(open(os.path.join(ROOT, "profiles", "r01_traffic.json")))["bytes"].get(dom)
-    except Exception:
-        traffic = None
+    traffic, tsrc = None, None
+    for f in ("r02_traffic.json", "r01_traffic.json"):   # the latest committed capture
+        try:
+            traffic = json.load(open(os.path.join(ROOT, "profiles", f)))["bytes"].get(dom)
+            tsrc = f
+            break
+        except Exception:
+            pass
     roof.update({"kernel": dom, "traffic": traffic,
-                 "traffic_source": "profiles/r01_traffic.json (ncu --set full, dram bytes per launch)",
+                 "traffic_source": f"profiles/{tsrc} (ncu --set full, dram bytes per step)",
                  "peak_source": ("MEASURED_PEAKS.json hbm_gbs" if roof["bound"] == "hbm" else
                                  "derived: 148 SM x 128 fp32 FMA/clk x 2 x sm_max_mhz (DESIGN.md 8(d))"
                                  if roof.get("precision") == "fp32" else
@@ -549,6 +563,7 @@ def main():
         "tree": {"nbox": info.nbox, "nlevels": info.nlevels, "nfout": info.nfout, "nexp": info.nexp,
                  "p2p_pairs": pairs, "p2p_pairs_in_ball": inball},
     }
+    line["paper_context"] = PAPER_CONTEXT
     if not a.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(a.cpu_sample, a.eps, a.ns)
     print(json.dumps(line), flush=True)

@@ -113,7 +113,6 @@ static void alloc_eval_buffers(dmk_plan_s* P) {
     P->phi_f32 = P->dim == 3 && T.p <= 18;
     P->phi.alloc(P->phi_f32 ? (P->phi_count + 1) / 2 : P->phi_count, s);
     P->lam.alloc(P->nexp * pd, s);
-    if (P->dim == 3) P->lamc.alloc(P->nexp * pd, s);
     // fp32 tier (p <= 18, 3D): weighted incoming plane waves of every local box (k_pwshift)
     if (P->dim == 3 && T.p <= 18) P->pwt.alloc(P->nexp * P->phi_size1, s);
     if (P->dim == 3 && T.p > 18 && pw64_group_env() && P->nexp > 1) P->pwt64.alloc(P->nexp * P->phi_size1, s);
@@ -392,12 +391,6 @@ int dmk_stage_copy(dmk_plan_t P, int which, double* out, int64_t count) {
     }
     if (count != (int64_t)b->n) fail(DMK_ERR_ARG, "count must equal the stage size " + std::to_string(b->n));
     DMK_CUDA(cudaMemcpyAsync(out, b->p, count * sizeof(double), cudaMemcpyDeviceToHost, P->stream));
-    if (which == DMK_STAGE_LOCAL && P->dim == 3 && P->lamc.n == b->n) {   // own + inherited parts
-      std::vector<double> h(count);
-      DMK_CUDA(cudaMemcpyAsync(h.data(), P->lamc.p, count * sizeof(double), cudaMemcpyDeviceToHost, P->stream));
-      DMK_CUDA(cudaStreamSynchronize(P->stream));
-      for (int64_t i = 0; i < count; ++i) out[i] += h[i];
-    }
     DMK_CUDA(cudaStreamSynchronize(P->stream));
   });
 }

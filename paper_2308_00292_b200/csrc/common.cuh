@@ -168,7 +168,6 @@ struct dmk_plan_s {
   dmk::DevBuf<double> phi;
   int64_t phi_count = 0;
   bool phi_f32 = false;
-  dmk::DevBuf<double> lamc;               // 3D: local expansions inherited through p2c (lam: own part)
   dmk::DevBuf<float> pwt;                 // fp32 tier: translated + weighted plane waves per local box
   dmk::DevBuf<double> pwt64;              // eps = 1e-9 (p = 28): the same in fp64
   dmk::DevBuf<double> scalar;             // device scratch scalar (2D: total charge)

@@ -366,7 +366,6 @@ struct EvTC {
 template <int P>
 __global__ void __launch_bounds__(EvTC<P>::NT, 2) k_eval_tc(DevTree t, const int32_t* __restrict__ boxes,
                                                             const double* __restrict__ lam,
-                                                            const double* __restrict__ lamc,
                                                             double* __restrict__ ufar) {
   using C = EvTC<P>;
   constexpr int P2 = C::P2, KP = C::KP, NCH = C::NCH, NCW = C::NCW, NT = C::NT;
@@ -384,10 +383,9 @@ __global__ void __launch_bounds__(EvTC<P>::NT, 2) k_eval_tc(DevTree t, const int
   __syncthreads();
   const int nr = nr_s, tot = tot_s;
   if (tot == 0) return;
-  // ---- B: the box's local expansion (own + inherited) as hi/lo tf32 rows, zero padded
+  // ---- B: the box's local expansion (own + inherited, k_p2c_grp) as hi/lo tf32 rows
   {
     const double* src = lam + (size_t)t.exp_rank[b] * P * P2;
-    const double* srcc = lamc + (size_t)t.exp_rank[b] * P * P2;
     // one row (n1 n2) of p values per thread and pass: all its loads in flight together
     for (int r = tid; r < NCH * NCW; r += NT) {
       double v[KP];
@@ -395,7 +393,7 @@ __global__ void __launch_bounds__(EvTC<P>::NT, 2) k_eval_tc(DevTree t, const int
       for (int k = 0; k < KP; ++k) v[k] = 0.0;
       if (r < P2) {
 #pragma unroll
-        for (int k = 0; k < P; ++k) v[k] = __ldg(src + (size_t)r * P + k) + __ldg(srcc + (size_t)r * P + k);
+        for (int k = 0; k < P; ++k) v[k] = __ldg(src + (size_t)r * P + k);
       }
 #pragma unroll
       for (int k4 = 0; k4 < KP; k4 += 4) {
@@ -524,7 +522,7 @@ struct Ev32 {
 template <int P>
 __global__ void __launch_bounds__(Ev32<P>::NT) k_eval32(DevTree t, const int32_t* __restrict__ boxes,
                                                         const double* __restrict__ lam,
-                                                        const double* __restrict__ lamc, double* __restrict__ ufar) {
+                                                        double* __restrict__ ufar) {
   using E = Ev32<P>;
   constexpr int NT = E::NT, PZ = E::PZ, P2 = P * P;
   extern __shared__ float4 sl4[];   // [P2][PZ/4]
@@ -536,12 +534,11 @@ __global__ void __launch_bounds__(Ev32<P>::NT) k_eval32(DevTree t, const int32_t
   __syncthreads();
   const int nr = nr_s, tot = tot_s;
   if (tot == 0) return;
-  // the box's own local expansion plus the one inherited through p2c
+  // the box's local expansion (own + inherited, k_p2c_grp)
   const double* src = lam + (size_t)t.exp_rank[b] * P * P2;
-  const double* srcc = lamc + (size_t)t.exp_rank[b] * P * P2;
   for (int i = tid; i < P2 * PZ; i += NT) {
     const int r = i / PZ, c = i - r * PZ;
-    sl[i] = c < P ? (float)(src[r * P + c] + srcc[r * P + c]) : 0.0f;
+    sl[i] = c < P ? (float)src[r * P + c] : 0.0f;
   }
   double cen[3], ih;
   box_geom(t.code[b], t.level[b], cen, ih);
@@ -709,8 +706,7 @@ __global__ void __launch_bounds__(GrpCfg<P, MT>::NT) k_c2p_grp(DevTree t, const 
 
 template <int P, int MT>
 __global__ void __launch_bounds__(GrpCfg<P, MT>::NT) k_p2c_grp(DevTree t, const int32_t* __restrict__ parents,
-                                                 const double* __restrict__ A, const double* __restrict__ lam,
-                                                 double* __restrict__ lamc) {
+                                                 const double* __restrict__ A, double* __restrict__ lam) {
   using C = GrpCfg<P, MT>;
   constexpr int P2 = C::P2, P3 = P2 * P, KS1 = C::KS1, KS2 = C::KS2;
   extern __shared__ double sm[];
@@ -722,7 +718,7 @@ __global__ void __launch_bounds__(GrpCfg<P, MT>::NT) k_p2c_grp(DevTree t, const 
   const int b = parents[blockIdx.x / C::NTILE], tid = threadIdx.x, k0 = (blockIdx.x % C::NTILE) * MT;
   if (tid < 8) {
     const int c = t.child[8 * (int64_t)b + tid];
-    ch[tid] = (c >= 0 && (t.flags[c] & F_EXP)) ? lamc + (size_t)t.exp_rank[c] * P3 : nullptr;
+    ch[tid] = (c >= 0 && (t.flags[c] & F_EXP)) ? lam + (size_t)t.exp_rank[c] * P3 : nullptr;
   }
   for (int i = tid; i < 2 * P2; i += C::NT) sA[i] = A[i];
   __syncthreads();
@@ -730,9 +726,9 @@ __global__ void __launch_bounds__(GrpCfg<P, MT>::NT) k_p2c_grp(DevTree t, const 
 #pragma unroll
   for (int o = 0; o < 8; ++o) any |= ch[o] != nullptr;
   if (!any) return;
-  // the parent's full local expansion: its own part plus what it inherited
+  // the parent's full local expansion (its own part plus what it inherited: the level above
+  // was completed by the previous launch)
   const double* src = lam + (size_t)t.exp_rank[b] * P3;
-  const double* srcc = lamc + (size_t)t.exp_rank[b] * P3;
   // axis 1: zeta[o1][i][m2m3] = sum_m1 A_o1[m1][k0+i] Lambda_P[m1][m2m3]
   mma_tiles<KS1>(
       (2 * MT + 7) / 8, (P2 + 7) / 8,
@@ -741,7 +737,7 @@ __global__ void __launch_bounds__(GrpCfg<P, MT>::NT) k_p2c_grp(DevTree t, const 
         return (m < 2 * MT && k0 + i < P && k < P) ? sA[(o1 * P + k) * P + k0 + i] : 0.0;
       },
       [&](int k, int n) {
-        return (k < P && n < P2) ? __ldg(src + (size_t)k * P2 + n) + __ldg(srcc + (size_t)k * P2 + n) : 0.0;
+        return (k < P && n < P2) ? src[(size_t)k * P2 + n] : 0.0;
       },
       [&](int m, int n, double v0, double v1) {
         if (m < 2 * MT) {
@@ -793,7 +789,7 @@ __global__ void __launch_bounds__(GrpCfg<P, MT>::NT) k_p2c_grp(DevTree t, const 
           if (nn >= 2 * P) continue;
           const int o3 = nn >= P, k3 = nn - o3 * P;
           double* c = ch[g * 2 + o3];
-          if (c) c[(size_t)(k0 + i) * P2 + k2 * P + k3] = e ? v1 : v0;   // inherited part: one writer
+          if (c) c[(size_t)(k0 + i) * P2 + k2 * P + k3] += e ? v1 : v0;   // + own part: one writer
         }
       });
 }
@@ -1592,7 +1588,7 @@ struct EvalMma {
 };
 template <int P>
 __global__ void __launch_bounds__(256) k_eval_mma(DevTree t, const int32_t* __restrict__ boxes,
-                                                  const double* __restrict__ lam, const double* __restrict__ lamc,
+                                                  const double* __restrict__ lam,
                                                   double* __restrict__ ufar) {
   using E = EvalMma<P>;
   constexpr int P2 = E::P2, KS = E::KS, NT8 = E::NT8, NW = E::NW;
@@ -1603,12 +1599,11 @@ __global__ void __launch_bounds__(256) k_eval_mma(DevTree t, const int32_t* __re
   __shared__ int nr_s, tot_s;
   const int b = boxes[blockIdx.x], tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid < 32) box_ranges_w<true>(t, b, rg, nr_s, tot_s);
-  const double* src = lam + (size_t)t.exp_rank[b] * P * P2;   // own + inherited (p2c) expansions
-  const double* srcc = lamc + (size_t)t.exp_rank[b] * P * P2;
+  const double* src = lam + (size_t)t.exp_rank[b] * P * P2;   // own + inherited (p2c) expansion
   for (int i = tid; i < NT8 * KS * 32; i += NW * 32) {
     int ln = i & 31, ks = (i >> 5) % KS, nt = (i >> 5) / KS;
     int a = nt * 8 + (ln >> 2), bb = ks * 4 + (ln & 3);
-    lamF[i] = (a < P2 && bb < P) ? src[a * P + bb] + srcc[a * P + bb] : 0.0;
+    lamF[i] = (a < P2 && bb < P) ? src[a * P + bb] : 0.0;
   }
   __syncthreads();
   const int nr = nr_s, tot = tot_s;
@@ -2471,19 +2466,25 @@ constexpr int grp_mt() { return P <= 9 ? 9 : (P <= 18 ? 6 : 4); }
 // p2c tiles: smaller for p = 18 (6 tiles per parent; measured 0.30 -> 0.28 ms at config 1)
 template <int P>
 constexpr int grp_mt_p2c() { return P <= 9 ? 9 : (P <= 18 ? 3 : 4); }
+constexpr int64_t COARSE_PARENTS = 64;   // levels with at most this many parents: MT = 1
 template <int P>
 static void run_c2p_level(dmk_plan_s* PL, const DevTree& dt, int l) {
-  constexpr int MT = grp_mt<P>();
-  using G = GrpCfg<P, MT>;
   cudaStream_t s = PL->stream;
   const auto& th = PL->th;
   const int64_t a = th.fout_off[l], b = th.fout_off[l + 1];
   const int64_t ca = th.fout_off[l + 1], cb = th.fout_off[l + 2];
   if (b <= a || cb <= ca) return;
-  set_smem(k_c2p_grp<P, MT>, G::smem_c2p);
-  const unsigned grid = (unsigned)((b - a) * G::NTILE);
-  k_c2p_grp<P, MT><<<grid, G::NT, G::smem_c2p, s>>>(dt, PL->fout_list.p + a, PL->tab->dA, PL->mom.p);
-  DMK_LAUNCH_CHECK();
+  // coarse levels (few parents) are latency-bound: one parent row per CTA, p times the CTAs
+  auto go = [&](auto mt_) {
+    constexpr int MT = decltype(mt_)::value;
+    using G = GrpCfg<P, MT>;
+    set_smem(k_c2p_grp<P, MT>, G::smem_c2p);
+    const unsigned grid = (unsigned)((b - a) * G::NTILE);
+    k_c2p_grp<P, MT><<<grid, G::NT, G::smem_c2p, s>>>(dt, PL->fout_list.p + a, PL->tab->dA, PL->mom.p);
+    DMK_LAUNCH_CHECK();
+  };
+  if (b - a <= COARSE_PARENTS) go(std::integral_constant<int, 1>());
+  else go(std::integral_constant<int, grp_mt<P>()>());
 }
 
 template <int P, int NF, int NF0>
@@ -2627,21 +2628,25 @@ static void run_eval(dmk_plan_s* PL, int phase = PH_UP | PH_DOWN, int top = 0) {
     }
     tm.end();
     if (!PL->serial) DMK_CUDA(cudaStreamWaitEvent(s, PL->ev_root, 0));
-    // inherited local expansions: the root inherits nothing; every other local box gets
-    // its part written (not added) by its parent's k_p2c_grp
-    DMK_CUDA(cudaMemsetAsync(PL->lamc.p, 0, (size_t)P3 * sizeof(double), s));
+    // inherited local expansions: k_p2c_grp adds each parent's full expansion, split to
+    // its children (Lemma 2.3), into the children's own parts written by the back transforms
     tm.begin("p2c");
     {
       // parents at level l-1 push their local expansions into their level-l children
-      constexpr int MT = grp_mt_p2c<P>();
-      using G = GrpCfg<P, MT>;
-      set_smem(k_p2c_grp<P, MT>, G::smem_p2c);
+      auto go = [&](auto mt_, int64_t a, int64_t b) {
+        constexpr int MT = decltype(mt_)::value;
+        using G = GrpCfg<P, MT>;
+        set_smem(k_p2c_grp<P, MT>, G::smem_p2c);
+        const unsigned grid = (unsigned)((b - a) * G::NTILE);
+        k_p2c_grp<P, MT><<<grid, G::NT, G::smem_p2c, s>>>(dt, PL->exp_list.p + a, T.dA, PL->lam.p);
+        DMK_LAUNCH_CHECK();
+      };
       for (int l = 1; l < nl; ++l) {
         const int64_t a = th.exp_off[l - 1], b = th.exp_off[l];
         if (b <= a || th.exp_off[l + 1] <= th.exp_off[l]) continue;
-        const unsigned grid = (unsigned)((b - a) * G::NTILE);
-        k_p2c_grp<P, MT><<<grid, G::NT, G::smem_p2c, s>>>(dt, PL->exp_list.p + a, T.dA, PL->lam.p, PL->lamc.p);
-        DMK_LAUNCH_CHECK();
+        // coarse levels (few parents): one child row per CTA (latency-bound otherwise)
+        if (b - a <= COARSE_PARENTS) go(std::integral_constant<int, 1>(), a, b);
+        else go(std::integral_constant<int, grp_mt_p2c<P>()>(), a, b);
       }
     }
     tm.end();
@@ -2652,16 +2657,16 @@ static void run_eval(dmk_plan_s* PL, int phase = PH_UP | PH_DOWN, int top = 0) {
           if (eval_tc()) {
             set_smem(k_eval_tc<P>, EvTC<P>::smem);
             k_eval_tc<P><<<(int)PL->nexp, EvTC<P>::NT, EvTC<P>::smem, s>>>(dt, PL->exp_list.p, PL->lam.p,
-                                                                              PL->lamc.p, PL->ufar.p);
+                                                                              PL->ufar.p);
           } else {
             set_smem(k_eval32<P>, Ev32<P>::smem);
             k_eval32<P><<<(int)PL->nexp, Ev32<P>::NT, Ev32<P>::smem, s>>>(dt, PL->exp_list.p, PL->lam.p,
-                                                                            PL->lamc.p, PL->ufar.p);
+                                                                            PL->ufar.p);
           }
         } else {
           size_t sm = EvalMma<P>::smem;
           set_smem(k_eval_mma<P>, sm);
-          k_eval_mma<P><<<(int)PL->nexp, 256, sm, s>>>(dt, PL->exp_list.p, PL->lam.p, PL->lamc.p, PL->ufar.p);
+          k_eval_mma<P><<<(int)PL->nexp, 256, sm, s>>>(dt, PL->exp_list.p, PL->lam.p, PL->ufar.p);
         }
         DMK_LAUNCH_CHECK();
       }
