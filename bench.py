@@ -309,7 +309,7 @@ def run_distributed(a, backend=None, device=None, pg="nccl"):
             return self.e0.elapsed_time(self.e1) if cuda else 1e3 * (self.t1 - self.t0)
 
     def step(Xs, Qs):
-        return par.dmk_eval_distributed(Xs, Qs, comm, backend, eps=a.eps, ns=a.ns, stats=st)
+        return par.dmk_eval_let(Xs, Qs, comm, backend, eps=a.eps, ns=a.ns, stats=st)
 
     for _ in range(a.warmup):
         step(X, Q)
@@ -374,11 +374,13 @@ def run_distributed(a, backend=None, device=None, pg="nccl"):
             "config": {"workload": f"uniform iid in [0,1]^3, {a.n} points per GPU, one global problem of "
                                    f"{a.n * world} points, 3D Laplace, eps={a.eps}, leaf capacity {a.ns}",
                        "N_per_gpu": a.n, "eps": a.eps, "leaf_capacity": a.ns,
-                       "step": "partitioned DMK: root all-reduce, Morton partition, all-to-all, halo, "
-                               "coarse-moment all-reduce, plan + upward x2 + downward, return all-to-all",
+                       "step": "locally essential tree (parallel.dmk_eval_let): root all-reduce, sample-sort "
+                               "Morton partition, all-to-all, one-box particle halo, dense coarse-moment "
+                               "all-reduce + sparse boundary-moment all-to-all, plan + upward x2 + downward, "
+                               "return all-to-all",
                        "l2": "flushed by a 256 MiB write between timed steps",
                        "parallelism": f"Morton partition over {world} ranks ({pg})",
-                       "partition_level": st.get("level"), "halo_points_rank0": st.get("n_halo"),
+                       "halo_level": st.get("level"), "halo_points_rank0": st.get("n_halo"),
                        "own_points_rank0": st.get("n_own")},
             "rel_l2_err_sampled": rel, "clocks": clocks,
             "e2e": {"value": a.n * world / (float(te.item()) * 1e-3), "unit": "points/s",

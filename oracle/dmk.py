@@ -78,12 +78,17 @@ def _finish(T, us, rho, kernel, coinc_sum):
 
 
 def dmk(points, charges, eps: float, ns: int, kernel: str = "laplace", lam: float = 0.0,
-        return_stages: bool = False, root=None, min_level: int = 0, level_get=None, level_set=None):
+        return_stages: bool = False, root=None, min_level: int = 0, level_get=None, level_set=None,
+        box_get=None, box_set=None):
     """level_get = C: stop after Step 2 and return the proxy charges of every box of level
     C as a dense array [2^{dC}][p]*d indexed by Morton code (0 for absent boxes).
     level_set = (C, dense): after Step 2 replace the proxy charges of level C by `dense`
-    and rebuild the coarser levels by T_c2p.  Both need C < min_level; together with
-    root/min_level they are the hooks of a distributed evaluation."""
+    and rebuild the coarser levels by T_c2p.  box_get = (C, codes): stop after Step 2 and
+    return the proxy charges of the listed boxes of level C ([len(codes)][p]*d);
+    box_set = [(C, codes, values), ...]: after Step 2 replace the proxy charges of the
+    listed boxes (no rebuild), applied before level_set.  All need C < min_level; together
+    with root/min_level they are the hooks of a distributed evaluation (they only move
+    data: every value set is this function's own Step 2 output on some rank)."""
     T = Tree(points, ns, root=root, min_level=min_level)   # Step 0
     D = T.d
     prm = for_eps(eps, D)
@@ -160,6 +165,25 @@ def dmk(points, charges, eps: float, ns: int, kernel: str = "laplace", lam: floa
                 proxy[i] = acc
 
     c2p_levels(T.nlevels - 2)
+
+    def box_index(C):
+        return {int(T.box_code[i]): i for i in range(T.level_offset[C], T.level_offset[C + 1])}
+
+    if box_get is not None:
+        C, codes = int(box_get[0]), box_get[1]
+        ix = box_index(C)
+        out = np.zeros((len(codes),) + (p,) * D)
+        for k, c in enumerate(codes):
+            i = ix.get(int(c))
+            if i is not None and i in proxy:
+                out[k] = proxy[i]
+        return out
+    for C, codes, vals in (box_set or []):
+        ix = box_index(int(C))
+        for c, v in zip(codes, vals):
+            i = ix.get(int(c))
+            if i is not None and T.fout[i]:
+                proxy[i] = np.array(v)
     if level_get is not None:
         C = int(level_get)
         dense = np.zeros((2 ** (D * C),) + (p,) * D)

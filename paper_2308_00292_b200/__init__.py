@@ -67,6 +67,7 @@ def lib() -> ctypes.CDLL:
         L.dmk_upward.argtypes = [vp, vp, ci]
         L.dmk_downward.argtypes = [vp, vp, ci]
         L.dmk_level_moments.argtypes = [vp, ci, vp, i64, ci, ci]
+        L.dmk_box_moments.argtypes = [vp, ci, vp, i64, vp, ci, ci]
         L.dmk_destroy.argtypes = [vp]
         L.dmk_last_error.restype = ctypes.c_char_p
         L.dmk_version.restype = ctypes.c_char_p
@@ -76,7 +77,7 @@ def lib() -> ctypes.CDLL:
         L.dmk_stage_size.argtypes = [vp, ci]
         L.dmk_stage_size.restype = i64
         L.dmk_eval_timings.argtypes = [vp, ctypes.POINTER(dbl), ctypes.POINTER(ctypes.c_char_p), ci]
-        for f in ("dmk_plan", "dmk_eval", "dmk_upward", "dmk_downward", "dmk_level_moments",
+        for f in ("dmk_plan", "dmk_eval", "dmk_upward", "dmk_downward", "dmk_level_moments", "dmk_box_moments",
                   "dmk_destroy", "dmk_plan_info_get", "dmk_tree_copy",
                   "dmk_stage_copy", "dmk_eval_timings"):
             getattr(L, f).restype = ci
@@ -175,6 +176,18 @@ class Plan:
         _check(lib().dmk_level_moments(self._h, int(level), ptr, int(keep.numel() if hasattr(keep, "numel")
                                                                        else keep.size), mem, int(bool(set))),
                "dmk_level_moments")
+        return keep
+
+    def box_moments(self, level: int, codes, values=None, set: bool = False):
+        """Moments [len(codes), p, p, p] of the listed boxes (Morton codes at `level`): read,
+        or overwrite with set=True (no rebuild of other levels)."""
+        codes = np.ascontiguousarray(np.asarray(codes, dtype=np.int64))
+        p = self.info().p
+        if values is None:
+            values = np.empty((codes.size, p, p, p), dtype=np.float64)
+        ptr, mem, keep = _placement(values)
+        _check(lib().dmk_box_moments(self._h, int(level), codes.ctypes.data, int(codes.size), ptr, mem,
+                                     int(bool(set))), "dmk_box_moments")
         return keep
 
     def info(self) -> PlanInfo:

@@ -291,6 +291,36 @@ int dmk_level_moments(dmk_plan_t P, int level, double* dense, int64_t count, int
   });
 }
 
+int dmk_box_moments(dmk_plan_t P, int level, const int64_t* codes, int64_t nbox, double* values, int mem, int set) {
+  return guard([&] {
+    if (!P || (nbox > 0 && (!codes || !values))) fail(DMK_ERR_ARG, "null argument");
+    if (nbox < 0) fail(DMK_ERR_ARG, "nbox must be >= 0");
+    if (mem != DMK_MEM_DEVICE && mem != DMK_MEM_HOST) fail(DMK_ERR_ARG, "bad mem");
+    if (!P->upward_done) fail(DMK_ERR_STATE, "dmk_box_moments before dmk_upward");
+    if (level < 0 || level > 6) fail(DMK_ERR_ARG, "level out of range");
+    const int64_t nmax = (int64_t)1 << (3 * level);
+    const int64_t p3 = (int64_t)P->tab->p * P->tab->p * P->tab->p;
+    cudaStream_t s = P->stream;
+    DevBuf<int64_t> dc;
+    dc.alloc(nbox, s);
+    std::vector<int64_t> hc(codes, codes + nbox);   // codes are host memory
+    for (int64_t c : hc)
+      if (c < 0 || c >= nmax) fail(DMK_ERR_ARG, "box code out of range for the level");
+    if (nbox) DMK_CUDA(cudaMemcpyAsync(dc.p, hc.data(), nbox * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    if (mem == DMK_MEM_HOST) {
+      DevBuf<double> d;
+      d.alloc(nbox * p3, s);
+      if (set && nbox) DMK_CUDA(cudaMemcpyAsync(d.p, values, nbox * p3 * sizeof(double), cudaMemcpyHostToDevice, s));
+      box_moments(P, level, dc.p, nbox, d.p, set != 0);
+      if (!set && nbox) DMK_CUDA(cudaMemcpyAsync(values, d.p, nbox * p3 * sizeof(double), cudaMemcpyDeviceToHost, s));
+      DMK_CUDA(cudaStreamSynchronize(s));
+    } else {
+      box_moments(P, level, dc.p, nbox, values, set != 0);
+      DMK_CUDA(cudaStreamSynchronize(s));   // the host codes buffer is released on return
+    }
+  });
+}
+
 int dmk_destroy(dmk_plan_t P) {
   return guard([&] {
     if (!P) return;

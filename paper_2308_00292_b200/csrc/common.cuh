@@ -201,6 +201,7 @@ void eval_plan_2d(dmk_plan_s* PL, double* dout);
 void eval_upward(dmk_plan_s* PL, const double* dcharges);
 void eval_downward(dmk_plan_s* PL, double* dout);
 void level_moments(dmk_plan_s* PL, int level, double* ddense, bool set);
+void box_moments(dmk_plan_s* PL, int level, const int64_t* dcodes, int64_t nb, double* dvals, bool set);
 // cumulative number of libdmk kernel launches (this library's own kernels; the
 // CUB sort/scan/select kernels compiled into the library are counted separately)
 extern int64_t g_launches, g_cub_launches;

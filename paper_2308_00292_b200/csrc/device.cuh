@@ -90,6 +90,30 @@ __device__ __forceinline__ void mma_tiles(int mtiles, int ntiles, FA fa, FB fb, 
   }
 }
 
+// The same with an accumulate-into-memory epilogue: fpre(m, n, p0, p1) loads the two
+// existing values of the lane's outputs BEFORE the tile's DMMA chain (their latency
+// overlaps the MMAs), fc(m, n, c_n + p0, c_{n+1} + p1) stores the sums.
+template <int KS, class FA, class FB, class FP, class FC>
+__device__ __forceinline__ void mma_tiles_acc(int mtiles, int ntiles, FA fa, FB fb, FP fpre, FC fc) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int g = lane >> 2, q = lane & 3;
+  for (int t = warp; t < mtiles * ntiles; t += nw) {
+    const int m0 = (t / ntiles) * 8, n0 = (t % ntiles) * 8;
+    double p0 = 0.0, p1 = 0.0;
+    fpre(m0 + g, n0 + 2 * q, p0, p1);
+    double av[KS], bv[KS];
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      av[ks] = fa(m0 + g, ks * 4 + q);
+      bv[ks] = fb(ks * 4 + q, n0 + g);
+    }
+    double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) dmma(c0, c1, av[ks], bv[ks]);
+    fc(m0 + g, n0 + 2 * q, c0 + p0, c1 + p1);
+  }
+}
+
 // collect the point ranges a box works on:
 //   ANTERP: leaf children with points (F_out box)
 //   EVAL:   own points if the box is a leaf, else leaf children without F_in

@@ -771,26 +771,35 @@ __global__ void __launch_bounds__(GrpCfg<P, MT>::NT) k_p2c_grp(DevTree t, const 
       });
   __syncthreads();
   // axis 3: Lambda_(o1 o2 o3)[k0+i][k2][k3] += sum_m3 zeta2[o1][o2][i][k2][m3] A_o3[m3][k3]
-  mma_tiles<KS1>(
+  // (added to the child's own part written by the back transforms: the current values are
+  // loaded before each tile's DMMA chain)
+  auto out_ptr = [&](int m, int nn) -> double* {
+    const int r = m / P, k2 = m - r * P;   // r = (o1 o2) * MT + i
+    if (r >= 4 * MT || nn >= 2 * P) return nullptr;
+    const int g = r / MT, i = r - g * MT;
+    if (k0 + i >= P) return nullptr;
+    const int o3 = nn >= P, k3 = nn - o3 * P;
+    double* c = ch[g * 2 + o3];
+    return c ? c + (size_t)(k0 + i) * P2 + k2 * P + k3 : nullptr;
+  };
+  mma_tiles_acc<KS1>(
       (4 * MT * P + 7) / 8, (2 * P + 7) / 8,
       [&](int m, int k) { return (m < 4 * MT * P && k < P) ? zeta2[(size_t)(m / P) * P2 + (m % P) * P + k] : 0.0; },
       [&](int k, int n) {
         const int o3 = n >= P, k3 = n - o3 * P;
         return (k < P && n < 2 * P) ? sA[(o3 * P + k) * P + k3] : 0.0;
       },
+      [&](int m, int n, double& p0, double& p1) {
+        const double* a = out_ptr(m, n);
+        const double* b = out_ptr(m, n + 1);
+        p0 = a ? *a : 0.0;
+        p1 = b ? *b : 0.0;
+      },
       [&](int m, int n, double v0, double v1) {
-        const int r = m / P, k2 = m - r * P;   // r = (o1 o2) * MT + i
-        if (r >= 4 * MT) return;
-        const int g = r / MT, i = r - g * MT;
-        if (k0 + i >= P) return;
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int nn = n + e;
-          if (nn >= 2 * P) continue;
-          const int o3 = nn >= P, k3 = nn - o3 * P;
-          double* c = ch[g * 2 + o3];
-          if (c) c[(size_t)(k0 + i) * P2 + k2 * P + k3] += e ? v1 : v0;   // + own part: one writer
-        }
+        double* a = out_ptr(m, n);
+        double* b = out_ptr(m, n + 1);
+        if (a) *a = v0;   // one writer per element
+        if (b) *b = v1;
       });
 }
 
@@ -2466,7 +2475,6 @@ constexpr int grp_mt() { return P <= 9 ? 9 : (P <= 18 ? 6 : 4); }
 // p2c tiles: smaller for p = 18 (6 tiles per parent; measured 0.30 -> 0.28 ms at config 1)
 template <int P>
 constexpr int grp_mt_p2c() { return P <= 9 ? 9 : (P <= 18 ? 3 : 4); }
-constexpr int64_t COARSE_PARENTS = 64;   // levels with at most this many parents: MT = 1
 template <int P>
 static void run_c2p_level(dmk_plan_s* PL, const DevTree& dt, int l) {
   cudaStream_t s = PL->stream;
@@ -2474,7 +2482,6 @@ static void run_c2p_level(dmk_plan_s* PL, const DevTree& dt, int l) {
   const int64_t a = th.fout_off[l], b = th.fout_off[l + 1];
   const int64_t ca = th.fout_off[l + 1], cb = th.fout_off[l + 2];
   if (b <= a || cb <= ca) return;
-  // coarse levels (few parents) are latency-bound: one parent row per CTA, p times the CTAs
   auto go = [&](auto mt_) {
     constexpr int MT = decltype(mt_)::value;
     using G = GrpCfg<P, MT>;
@@ -2483,8 +2490,7 @@ static void run_c2p_level(dmk_plan_s* PL, const DevTree& dt, int l) {
     k_c2p_grp<P, MT><<<grid, G::NT, G::smem_c2p, s>>>(dt, PL->fout_list.p + a, PL->tab->dA, PL->mom.p);
     DMK_LAUNCH_CHECK();
   };
-  if (b - a <= COARSE_PARENTS) go(std::integral_constant<int, 1>());
-  else go(std::integral_constant<int, grp_mt<P>()>());
+  go(std::integral_constant<int, grp_mt<P>()>());
 }
 
 template <int P, int NF, int NF0>
@@ -2644,9 +2650,7 @@ static void run_eval(dmk_plan_s* PL, int phase = PH_UP | PH_DOWN, int top = 0) {
       for (int l = 1; l < nl; ++l) {
         const int64_t a = th.exp_off[l - 1], b = th.exp_off[l];
         if (b <= a || th.exp_off[l + 1] <= th.exp_off[l]) continue;
-        // coarse levels (few parents): one child row per CTA (latency-bound otherwise)
-        if (b - a <= COARSE_PARENTS) go(std::integral_constant<int, 1>(), a, b);
-        else go(std::integral_constant<int, grp_mt_p2c<P>()>(), a, b);
+        go(std::integral_constant<int, grp_mt_p2c<P>()>(), a, b);
       }
     }
     tm.end();
@@ -2912,6 +2916,32 @@ __global__ void k_level_set(const uint64_t* __restrict__ code, const int32_t* __
   const double* src = dense + (size_t)code[i] * p3;
   double* dst = mom + (size_t)r * p3;
   for (int k = threadIdx.x; k < p3; k += blockDim.x) dst[k] = src[k];
+}
+
+// sparse form (locally essential tree exchange): the boxes of a forced level are all
+// present in Morton order, so the box of code c is level_off[level] + c
+__global__ void k_box_moments(const int32_t* __restrict__ fout_rank, int64_t b0, const int64_t* __restrict__ codes,
+                              int p3, double* __restrict__ mom, double* __restrict__ vals, int set) {
+  const int64_t k = blockIdx.x;
+  const int r = fout_rank[b0 + codes[k]];
+  if (r < 0) return;
+  double* m = mom + (size_t)r * p3;
+  double* v = vals + (size_t)k * p3;
+  for (int i = threadIdx.x; i < p3; i += blockDim.x) {
+    if (set) m[i] = v[i];
+    else v[i] = m[i];
+  }
+}
+
+void box_moments(dmk_plan_s* PL, int level, const int64_t* dcodes, int64_t nb, double* dvals, bool set) {
+  if (PL->dim != 3) fail(DMK_ERR_UNSUPPORTED, "box moments are implemented for dim = 3");
+  if (level < 0 || level >= PL->min_level) fail(DMK_ERR_ARG, "level must be in [0, min_level)");
+  if (level >= PL->th.nlevels - 1) fail(DMK_ERR_STATE, "the tree has no non-leaf boxes at that level");
+  if (nb == 0) return;
+  const int p3 = PL->tab->p * PL->tab->p * PL->tab->p;
+  k_box_moments<<<(unsigned)nb, 256, 0, PL->stream>>>(PL->fout_rank.p, PL->th.level_off[level], dcodes, p3,
+                                                       PL->mom.p, dvals, set ? 1 : 0);
+  DMK_LAUNCH_CHECK();
 }
 
 void level_moments(dmk_plan_s* PL, int level, double* ddense, bool set) {

@@ -175,6 +175,15 @@ class GpuBackend:
     def set_level(self, plan, level, dense):
         plan.level_moments(level, dense.to(self.device).contiguous(), set=True)
 
+    def get_boxes(self, plan, level, codes):
+        p = plan.info().p
+        codes = np.asarray(codes, dtype=np.int64)
+        out = torch.empty((codes.size, p, p, p), dtype=torch.float64, device=self.device)
+        return plan.box_moments(level, codes, out)
+
+    def set_boxes(self, plan, level, codes, values):
+        plan.box_moments(level, np.asarray(codes, dtype=np.int64), values.to(self.device).contiguous(), set=True)
+
     def downward(self, plan):
         return plan.downward(device=self.device)
 
@@ -319,6 +328,258 @@ def dmk_eval_distributed(points: torch.Tensor, charges: torch.Tensor, comm: Comm
         u_own = u[:n_own]
         backend.close(plan)
     # 8. return to the source ranks
+    srank = own[:, 4].to(torch.int64)
+    back = torch.cat([own[:, 5:6], u_own[:, None]], 1)
+    got = torch.cat(comm.alltoallv([back[srank == d] for d in range(R)]), 0)
+    out = torch.empty(n_local, dtype=torch.float64, device=dev)
+    out[got[:, 0].to(torch.int64)] = got[:, 1]
+    return out
+
+
+# ---------------------------------------------------------------- locally essential tree
+def morton_encode(ix: torch.Tensor, iy: torch.Tensor, iz: torch.Tensor, level: int) -> torch.Tensor:
+    code = torch.zeros_like(ix)
+    for b in range(level):
+        code |= (((ix >> b) & 1) << (3 * b + 2)) | (((iy >> b) & 1) << (3 * b + 1)) | (((iz >> b) & 1) << (3 * b))
+    return code
+
+
+def morton_decode(code: torch.Tensor, level: int):
+    ix, iy, iz = torch.zeros_like(code), torch.zeros_like(code), torch.zeros_like(code)
+    for b in range(level):
+        ix |= ((code >> (3 * b + 2)) & 1) << b
+        iy |= ((code >> (3 * b + 1)) & 1) << b
+        iz |= ((code >> (3 * b)) & 1) << b
+    return ix, iy, iz
+
+
+def neighbour_codes(code: torch.Tensor, level: int) -> torch.Tensor:
+    """[n, 27] Morton codes of the colleagues (incl. itself) of boxes `code` at `level`,
+    -1 outside the root box; slot (dx+1)*9 + (dy+1)*3 + (dz+1)."""
+    ix, iy, iz = morton_decode(code, level)
+    n1 = 1 << level
+    out = []
+    for dx in (-1, 0, 1):
+        for dy in (-1, 0, 1):
+            for dz in (-1, 0, 1):
+                jx, jy, jz = ix + dx, iy + dy, iz + dz
+                ok = (jx >= 0) & (jx < n1) & (jy >= 0) & (jy < n1) & (jz >= 0) & (jz < n1)
+                c = morton_encode(jx.clamp(0, n1 - 1), jy.clamp(0, n1 - 1), jz.clamp(0, n1 - 1), level)
+                out.append(torch.where(ok, c, torch.full_like(c, -1)))
+    return torch.stack(out, 1)
+
+
+def choose_let_levels(n_total: int, ns: int, world: int) -> int:
+    """Halo level Lh = the plans' min_level <= 6: the particle halo is one level-Lh box
+    thick; as deep as the tree allows (one level above the leaves of a uniform cloud)."""
+    depth = max(1, math.ceil(math.log(max(n_total / max(ns, 1), 1.0), 8)))
+    return int(min(6, max(2, depth - 1)))
+
+
+KEY_BITS = 3 * NBITS   # 63-bit Morton keys, as the library sorts
+
+
+def box_rank_bits(code: torch.Tensor, level: int, splitters: torch.Tensor) -> torch.Tensor:
+    """Bitmask of the ranks whose Morton-key range meets box `code` of `level` (rank r
+    owns the keys in [splitters[r-1], splitters[r]))."""
+    span = 3 * (NBITS - level)
+    k0, k1 = code << span, ((code + 1) << span) - 1
+    r0 = torch.searchsorted(splitters, k0, right=True)
+    r1 = torch.searchsorted(splitters, k1, right=True)
+    one = torch.ones_like(code)
+    return ((one << (r1 + 1)) - 1) ^ ((one << r0) - 1)
+
+
+def key_splitters(keys: torch.Tensor, comm: Comm, samples: int = 256) -> torch.Tensor:
+    """R - 1 Morton-key splitters of all ranks' points by sample sort: every rank
+    contributes `samples` evenly spaced keys of its sorted keys; the merged sample's
+    R-quantiles split the points into R contiguous ranges of ~N/R points."""
+    R = comm.world
+    dev = keys.device
+    n = keys.shape[0]
+    ks = torch.sort(keys).values
+    cnt = comm.allreduce(torch.tensor([float(n)], dtype=torch.float64, device=dev), "sum")
+    # weights: each sample stands for n/samples local points
+    if n:
+        idx = torch.clamp(((torch.arange(samples, device=dev) + 0.5) * n / samples).to(torch.int64), max=n - 1)
+        smp = (ks[idx] >> 10).to(torch.float64)   # 53-bit: exact in float64
+        w = torch.full((samples,), n / samples, dtype=torch.float64, device=dev)
+    else:
+        smp = torch.zeros(samples, dtype=torch.float64, device=dev)
+        w = torch.zeros(samples, dtype=torch.float64, device=dev)
+    # gather every rank's (sample, weight) through the all-reduce of a rank-indexed table
+    tab = torch.zeros((R, 2, samples), dtype=torch.float64, device=dev)
+    tab[comm.rank, 0] = smp
+    tab[comm.rank, 1] = w
+    tab = comm.allreduce(tab, "sum")
+    allk, allw = tab[:, 0].reshape(-1), tab[:, 1].reshape(-1)
+    order = torch.argsort(allk)
+    allk, cw = allk[order], torch.cumsum(allw[order], 0)
+    tot = float(cnt.item())
+    pos = torch.searchsorted(cw, torch.arange(1, R, device=dev, dtype=torch.float64) * tot / R)
+    return allk[pos.clamp(max=allk.shape[0] - 1)].to(torch.int64) << 10
+
+
+def let_halo_fraction(hist_h: np.ndarray, Lh: int, world: int) -> np.ndarray:
+    """Halo points / owned points per rank for the point counts of every level-Lh box,
+    with the partition and halo rules of dmk_eval_let (no points needed): ranks own
+    contiguous Morton ranges of N/R points; a rank receives, as halo, the other ranks'
+    points in every level-Lh box equal or adjacent to a box holding its points."""
+    h = torch.as_tensor(hist_h, dtype=torch.float64)
+    cs = torch.cumsum(h, 0)
+    tot = float(cs[-1])
+    b0, b1 = cs - h, cs
+    code = torch.arange(8 ** Lh, dtype=torch.int64)
+    nb = neighbour_codes(code, Lh)
+    frac = np.zeros(world)
+    for r in range(world):
+        a, b = r * tot / world, (r + 1) * tot / world
+        mine = torch.clamp(torch.minimum(b1, torch.full_like(b1, b)) - torch.maximum(b0, torch.full_like(b0, a)), min=0)
+        has = mine > 0
+        need = torch.zeros(8 ** Lh, dtype=torch.bool)
+        for k in range(27):
+            ok = nb[:, k] >= 0
+            need[nb[ok, k][has[ok]]] = True
+        frac[r] = float((h[need] - mine[need]).sum()) / max(float(mine.sum()), 1.0)
+    return frac
+
+
+def dmk_eval_let(points: torch.Tensor, charges: torch.Tensor, comm: Comm, backend, eps: float = 1e-6,
+                 ns: int = 200, kernel: str = "laplace", lam: float = 0.0, levels=None,
+                 stats: dict | None = None) -> torch.Tensor:
+    """The distributed evaluation with a locally essential tree (north star's data plane):
+    potentials at this rank's points (same order) over the points of ALL ranks.
+
+      1. root box: all-reduce of the bounds (reading R5's single-process root cube).
+      2. ownership: contiguous Morton-key ranges of ~N/R points (sample-sort splitters,
+         all-reduced sample); every point goes to its owner (all-to-all).  Boxes on a
+         range boundary are shared.
+      3. particle halo, one level-Lh box thick: an owned point also goes to every rank with
+         points in its level-Lh box or in one of that box's colleagues (all-to-all) -- the
+         neighbour-halo particles: every level-Lh box holding owned points, its colleagues,
+         and so every colleague (level >= Lh) and direct-list source of an owned leaf (all
+         leaves are at level >= Lh, the plan's forced levels) are whole locally.
+      4. local plan over own + halo points, shared root, min_level = Lh, targets = own.
+      5. upward with the halo charges zeroed: exact owned-only (partial) moments.  Dense
+         level Gd = min(3, Lh - 1): all-reduce SUM (the replicated coarse levels).  Levels
+         Gd+1..Lh-1: the partial moments of each box holding owned points go to every rank
+         with points in one of its colleagues (all-to-all), which sums them -- the
+         boundary proxy data (sparse, one layer of boxes per level).
+      6. upward with all charges, then set the received boundary moments and the reduced
+         dense level (which rebuilds the levels above it by T_c2p), downward, and return
+         the own potentials to the ranks the points came from (all-to-all).
+    """
+    dev = points.device
+    x = points.to(torch.float64).reshape(-1, 3)
+    q = charges.to(torch.float64).reshape(-1)
+    n_local = x.shape[0]
+    R, me = comm.world, comm.rank
+    big = torch.tensor([1e300] * 3, dtype=torch.float64, device=dev)
+    mn = comm.allreduce(x.min(0).values if n_local else big, "min")
+    mx = comm.allreduce(x.max(0).values if n_local else -big, "max")
+    lo = mn.tolist()
+    ext = float((mx - mn).max())
+    side = ext if ext > 0 else 1.0
+    n_total = int(comm.allreduce(torch.tensor([float(n_local)], dtype=torch.float64, device=dev), "sum").item())
+    Lh = int(levels) if levels is not None else choose_let_levels(n_total, ns, R)
+    if not (1 <= Lh <= 6):
+        raise ValueError(f"LET halo level must be in [1, 6], got {Lh}")
+    if R == 1:
+        plan = backend.plan(x.contiguous(), eps, ns, kernel, lam, None, 0)
+        backend.upward(plan, q.contiguous())
+        u = torch.as_tensor(backend.downward(plan), device=dev)
+        backend.close(plan)
+        if stats is not None:
+            stats.update(level=0, n_own=n_local, n_halo=0, n_total=n_total)
+        return u
+    Gd = min(3, Lh - 1)   # dense all-reduce level
+    sh = 3 * (NBITS - Lh)
+    # 2. ownership: contiguous Morton-key ranges of ~N/R points (sample-sort splitters)
+    key = level_codes(x, lo, side, NBITS)
+    splitters = key_splitters(key, comm)
+    rows = torch.cat([x, q[:, None], torch.full((n_local, 1), float(me), dtype=torch.float64, device=dev),
+                      torch.arange(n_local, dtype=torch.float64, device=dev)[:, None]], 1)
+    dst = torch.searchsorted(splitters, key, right=True)
+    own = torch.cat(comm.alltoallv([rows[dst == d] for d in range(R)]), 0)
+    n_own = own.shape[0]
+    # 3. halo: every rank with points in a level-Lh colleague (or the box itself) of an
+    # owned point's box gets the point
+    ocode = (level_codes(own[:, :3], lo, side, NBITS) >> sh) if n_own else torch.zeros(0, dtype=torch.int64,
+                                                                                            device=dev)
+    ubox, inv = torch.unique(ocode, return_inverse=True)
+    nb = neighbour_codes(ubox, Lh)                                   # [nbox, 27]
+    dest = torch.zeros(len(ubox), dtype=torch.int64, device=dev)
+    for k in range(27):
+        bk = box_rank_bits(nb[:, k].clamp(min=0), Lh, splitters)
+        dest |= torch.where(nb[:, k] >= 0, bk, torch.zeros_like(bk))
+    sends = []
+    for d in range(R):
+        if d == me or n_own == 0:
+            sends.append(own[:0, :4])
+            continue
+        sends.append(own[((dest >> d) & 1).bool()[inv]][:, :4])
+    halo = torch.cat(comm.alltoallv(sends), 0)
+    n_halo = halo.shape[0]
+    if stats is not None:
+        stats.update(level=Lh, n_own=n_own, n_halo=n_halo, n_total=n_total)
+    # 4.-5. local plan, owned-only upward, dense + boundary exchanges
+    X = torch.cat([own[:, :3], halo[:, :3]], 0).contiguous()
+    Qall = torch.cat([own[:, 3], halo[:, 3]], 0).contiguous()
+    Qown = torch.cat([own[:, 3], torch.zeros(n_halo, dtype=torch.float64, device=dev)], 0).contiguous()
+    plan = backend.plan(X, eps, ns, kernel, lam, lo + [side], Lh, n_own) if n_own else None
+    if plan is not None:
+        backend.upward(plan, Qown)
+        dense = torch.as_tensor(backend.get_level(plan, Gd), device=dev)
+    else:
+        dense = None
+    shape = torch.tensor(list(dense.shape) if dense is not None else [0, 0, 0, 0], dtype=torch.float64, device=dev)
+    shape = comm.allreduce(shape, "max")
+    p = int(shape[1].item())
+    p3 = p ** 3
+    if dense is None:
+        dense = torch.zeros([int(v) for v in shape.tolist()], dtype=torch.float64, device=dev)
+    g_dense = comm.allreduce(dense, "sum")
+    # boundary exchange, levels Gd+1 .. Lh-1: the owned-only (partial) moments of every box
+    # holding owned points go to every rank with points in one of the box's colleagues;
+    # each rank sums what it receives with its own partial -> complete moments of every
+    # box it needs (colleagues of the ancestors of its points)
+    complete = {}
+    for lv in range(Gd + 1, Lh):
+        mine = torch.unique(ocode >> (3 * (Lh - lv))) if n_own else torch.zeros(0, dtype=torch.int64, device=dev)
+        vals = (torch.as_tensor(backend.get_boxes(plan, lv, mine.cpu().numpy()), device=dev).reshape(-1, p3)
+                if len(mine) else torch.zeros((0, p3), dtype=torch.float64, device=dev))
+        nbl = neighbour_codes(mine, lv)
+        dest = torch.zeros(len(mine), dtype=torch.int64, device=dev)
+        for k in range(27):
+            bk = box_rank_bits(nbl[:, k].clamp(min=0), lv, splitters)
+            dest |= torch.where(nbl[:, k] >= 0, bk, torch.zeros_like(bk))
+        sends = []
+        for d in range(R):
+            m = ((dest >> d) & 1).bool() if d != me else torch.zeros(len(mine), dtype=torch.bool, device=dev)
+            sends.append(torch.cat([mine[m].to(torch.float64)[:, None], vals[m]], 1))
+        got = torch.cat(comm.alltoallv(sends), 0)
+        need = torch.unique(nbl[nbl >= 0]) if len(mine) else torch.zeros(0, dtype=torch.int64, device=dev)
+        acc = torch.zeros((len(need), p3), dtype=torch.float64, device=dev)
+        if len(need):
+            pos = torch.searchsorted(need, mine)
+            acc.index_add_(0, pos, vals)
+            gc = got[:, 0].to(torch.int64)
+            pos = torch.searchsorted(need, gc)
+            ok = (pos < len(need)) & (need[pos.clamp(max=len(need) - 1)] == gc)
+            acc.index_add_(0, pos[ok], got[ok, 1:])
+        complete[lv] = (need, acc)
+    u_own = torch.zeros(0, dtype=torch.float64, device=dev)
+    if plan is not None:
+        backend.upward(plan, Qall)
+        for lv in range(Gd + 1, Lh):
+            need, acc = complete[lv]
+            if len(need):
+                backend.set_boxes(plan, lv, need.cpu().numpy(), acc.reshape(-1, p, p, p))
+        backend.set_level(plan, Gd, g_dense)
+        u = torch.as_tensor(backend.downward(plan), device=dev)
+        u_own = u[:n_own]
+        backend.close(plan)
+    # 6. return to the source ranks
     srank = own[:, 4].to(torch.int64)
     back = torch.cat([own[:, 5:6], u_own[:, None]], 1)
     got = torch.cat(comm.alltoallv([back[srank == d] for d in range(R)]), 0)

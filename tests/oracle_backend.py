@@ -27,8 +27,14 @@ class OracleBackend:
     def set_level(self, plan, level, dense):
         plan["set"] = (level, dense.cpu().numpy())
 
+    def get_boxes(self, plan, level, codes):
+        return torch.as_tensor(self._run(plan, box_get=(level, list(codes))))
+
+    def set_boxes(self, plan, level, codes, values):
+        plan.setdefault("bset", []).append((level, list(codes), values.cpu().numpy()))
+
     def downward(self, plan):
-        return torch.as_tensor(self._run(plan, level_set=plan["set"]))
+        return torch.as_tensor(self._run(plan, level_set=plan.get("set"), box_set=plan.get("bset")))
 
     def close(self, plan):
         pass
