@@ -183,6 +183,8 @@ int dmk_plan(int dim, int kernel, double eps, int64_t n, const double* points, i
       P->serial = ps && ps[0] == '1';
       const char* pe = std::getenv("DMK_PROFILE");
       P->profile = pe && pe[0] == '1';
+      const char* pf = std::getenv("DMK_FULL_SORT");
+      P->fast_sort = !(pf && pf[0] == '1');
       const char* pt = std::getenv("DMK_PROFILE_TREE");
       P->profile_tree = pt && pt[0] == '1';
       const double* dpts = points;

@@ -125,6 +125,8 @@ struct dmk_plan_s {
   bool root_fixed = false;   // lo/side given by the caller (dmk_options.root)
   int min_level = 0;         // levels < min_level fully refined (dmk_options.min_level)
   int64_t n_targets = 0;     // the first n_targets caller points are targets (= n by default)
+  bool fast_sort = true;     // 3D: sort the top 32 key bits first (DMK_FULL_SORT=1: all 63)
+  int sorted_from_bit = 0;   // 0: keys fully sorted; else only bits >= this are ordered
 
   // sorted points (normalised coordinates in [0,1]^3) and permutation
   dmk::DevBuf<uint64_t> keys;

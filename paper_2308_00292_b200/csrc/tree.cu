@@ -898,8 +898,14 @@ static void build_tree_d(dmk_plan_s* P, const double* dpts) {
     DMK_LAUNCH_CHECK();
     P->keys.alloc(n, s);
     P->perm.alloc(n, s);
+    // 3D: first the top 32 bits (4 radix passes instead of 8): levels <= 10 are sorted,
+    // which is all the tree needs unless a level-9 box must be refined (checked with the
+    // level counts below; then the rest of the key is sorted too, stably, which composes
+    // to the full stable sort of reading R5)
+    const int b0 = (D == 3 && P->fast_sort) ? D * NBITS - 32 : 0;
+    P->sorted_from_bit = b0;
     cub_run(s, [&](void* t, size_t& b) {
-      return cub::DeviceRadixSort::SortPairs(t, b, k0.p, P->keys.p, i0.p, P->perm.p, (int64_t)n, 0, D * NBITS, s);
+      return cub::DeviceRadixSort::SortPairs(t, b, k0.p, P->keys.p, i0.p, P->perm.p, (int64_t)n, b0, D * NBITS, s);
     });
     P->xs.alloc(n, s);
     P->ys.alloc(n, s);
@@ -942,6 +948,34 @@ static void build_tree_d(dmk_plan_s* P, const double* dpts) {
     unsigned long long hc[LMAX];
     DMK_CUDA(cudaMemcpyAsync(hc, dcnt.p, sizeof(hc), cudaMemcpyDeviceToHost, s));
     DMK_CUDA(cudaStreamSynchronize(s));
+    if (P->sorted_from_bit > 0 && hc[9] > 0) {
+      // a level-9 box holds > n_s points: the tree may go below level 10, where the top
+      // 32 bits do not order the keys -- finish the stable sort and recount
+      DevBuf<uint64_t> k1;
+      DevBuf<int32_t> i1;
+      k1.alloc(n, s);
+      i1.alloc(n, s);
+      cub_run(s, [&](void* t, size_t& b) {
+        return cub::DeviceRadixSort::SortPairs(t, b, P->keys.p, k1.p, P->perm.p, i1.p, (int64_t)n, 0, D * NBITS, s);
+      });
+      std::swap(P->keys.p, k1.p);
+      std::swap(P->perm.p, i1.p);
+      P->sorted_from_bit = 0;
+      k_gather_pts<D><<<nblk(n), TPB, 0, s>>>(dpts, P->perm.p, n, dgeo.p, P->xs.p, P->ys.p, P->zs.p);
+      DMK_LAUNCH_CHECK();
+      DMK_CUDA(cudaMemsetAsync(bmbuf.p, 0, 4 * W * sizeof(uint32_t), s));
+      DMK_CUDA(cudaMemsetAsync(dcnt.p, 0, LMAX * sizeof(unsigned long long), s));
+      k_count_big<D><<<std::min(nblk(n), 4 * 148), TPB, 0, s>>>(P->keys.p, n, ns, P->min_level, dcnt.p);
+      DMK_LAUNCH_CHECK();
+      k_mark_coarse<D><<<nblk(n), TPB, 0, s>>>(P->keys.p, n, ns, P->min_level, cs, bmU, bmNE);
+      DMK_LAUNCH_CHECK();
+      for (int l = 0; l < P->min_level && l <= LBC; ++l) {
+        k_bm_all<<<nblk(nbits(l) / 32 + 1), TPB, 0, s>>>(bmU + cs.woff[l], nbits(l));
+        DMK_LAUNCH_CHECK();
+      }
+      DMK_CUDA(cudaMemcpyAsync(hc, dcnt.p, sizeof(hc), cudaMemcpyDeviceToHost, s));
+      DMK_CUDA(cudaStreamSynchronize(s));
+    }
     if (!P->root_fixed) {   // the root cube computed on the device
       if (hgeo->bad) fail(DMK_ERR_ARG, "points contain non-finite coordinates");
       for (int d = 0; d < D; ++d) P->lo[d] = hgeo->lo[d];

@@ -64,12 +64,24 @@ def case(request):
     plan.close()
 
 
+def same_points_per_leaf(perm, T):
+    """The device's point order: a permutation that puts every leaf's points in the
+    leaf's range.  Within a leaf the order is free (the paper fixes none; the device
+    sorts by the top 32 Morton bits when the tree ends above level 10, R5)."""
+    assert np.array_equal(np.sort(perm), np.arange(len(T.perm)))
+    for i in np.nonzero(T.box_leaf)[0]:
+        a, b = T.box_start[i], T.box_end[i]
+        if not np.array_equal(np.sort(perm[a:b]), np.sort(T.perm[a:b])):
+            return False
+    return True
+
+
 def test_tree_bit_exact(case):
     T, plan = case["T"], case["plan"]
     inf = plan.info()
     assert inf.nbox == T.nbox and inf.nlevels == T.nlevels
     assert inf.side == T.side and tuple(inf.lo) == tuple(T.lo)
-    assert np.array_equal(plan.tree("perm"), T.perm)
+    assert same_points_per_leaf(plan.tree("perm"), T)
     assert np.array_equal(plan.tree("box_level"), T.box_level)
     assert np.array_equal(plan.tree("box_code"), T.box_code)
     assert np.array_equal(plan.tree("box_start"), T.box_start)
@@ -78,6 +90,24 @@ def test_tree_bit_exact(case):
     assert np.array_equal(plan.tree("box_parent"), T.box_parent)
     assert np.array_equal(plan.tree("colleagues").reshape(-1, 27), T.box_colleagues)
     assert np.array_equal(plan.tree("fout") >= 0, T.fout)
+
+
+def test_full_sort_order_bit_exact(monkeypatch):
+    """DMK_FULL_SORT=1: the stable sort by the whole 63-bit key (reading R5) -- the device's
+    permutation equals the oracle's element by element; the default (top 32 bits first,
+    the rest only when a level-9 box needs refinement) gives the same tree."""
+    x, q = dmk_inputs.make("sphere", 8000, seed=21)
+    T = Tree(x, 60)
+    monkeypatch.setenv("DMK_FULL_SORT", "1")
+    plan = dmk.dmk_plan(cuda(x), eps=1e-6, leaf_capacity=60)
+    perm_full = plan.tree("perm")
+    plan.close()
+    assert np.array_equal(perm_full, T.perm)
+    monkeypatch.delenv("DMK_FULL_SORT")
+    plan = dmk.dmk_plan(cuda(x), eps=1e-6, leaf_capacity=60)
+    assert np.array_equal(plan.tree("box_code"), T.box_code) and np.array_equal(plan.tree("box_end"), T.box_end)
+    assert same_points_per_leaf(plan.tree("perm"), T)
+    plan.close()
 
 
 def test_direct_lists_bit_exact(case):
