@@ -142,14 +142,16 @@ int dmk_downward(dmk_plan_t plan, double* potentials, int mem);
 int dmk_level_moments(dmk_plan_t plan, int level, double* dense, int64_t count, int mem, int set);
 
 /* dmk_box_moments: read (set = 0) or overwrite (set = 1) the Chebyshev moments of the
- * listed boxes of `level` (< the plan's min_level, 3D only): codes[nbox] (HOST int64) are
- * the boxes' Morton codes at that level, values[nbox][p][p][p] (fp64 in `mem`).  A box
+ * listed boxes of `level` (< the plan's min_level, 3D only): codes[nbox] (int64 in `mem`)
+ * are the boxes' Morton codes at that level (host codes outside [0, 8^level) fail with
+ * DMK_ERR_ARG, device codes outside it are skipped), values[nbox][p][p][p] (fp64 in
+ * `mem`).  With DMK_MEM_DEVICE the call is stream-ordered and does not synchronise.  A box
  * without an outgoing expansion reads nothing and ignores its values.  set = 1 does NOT
  * rebuild other levels (unlike dmk_level_moments): the sparse exchange of a locally
  * essential tree (paper_2308_00292_b200/parallel.py) -- every rank completes the moments
  * of the boundary boxes it needs at the levels between the dense all-reduce level and
  * min_level, then sets the dense level (which rebuilds the levels above it).  Call after
- * dmk_upward; returns after the copies (synchronises the plan stream). */
+ * dmk_upward. */
 int dmk_box_moments(dmk_plan_t plan, int level, const int64_t* codes, int64_t nbox, double* values, int mem, int set);
 
 /* dmk_destroy: free the plan (NULL is a no-op). */

@@ -181,13 +181,25 @@ class Plan:
     def box_moments(self, level: int, codes, values=None, set: bool = False):
         """Moments [len(codes), p, p, p] of the listed boxes (Morton codes at `level`): read,
         or overwrite with set=True (no rebuild of other levels)."""
-        codes = np.ascontiguousarray(np.asarray(codes, dtype=np.int64))
         p = self.info().p
+        try:
+            import torch
+            dev_codes = isinstance(codes, torch.Tensor) and codes.is_cuda
+        except ImportError:
+            dev_codes = False
+        if dev_codes:
+            codes = codes.to(torch.int64).contiguous()
+            cptr, nb = codes.data_ptr(), int(codes.numel())
+        else:
+            codes = np.ascontiguousarray(np.asarray(codes, dtype=np.int64))
+            cptr, nb = codes.ctypes.data, int(codes.size)
         if values is None:
-            values = np.empty((codes.size, p, p, p), dtype=np.float64)
+            values = np.empty((nb, p, p, p), dtype=np.float64)
         ptr, mem, keep = _placement(values)
-        _check(lib().dmk_box_moments(self._h, int(level), codes.ctypes.data, int(codes.size), ptr, mem,
-                                     int(bool(set))), "dmk_box_moments")
+        if (mem == DMK_MEM_DEVICE) != dev_codes:
+            raise DmkError("codes and values must live in the same memory")
+        _check(lib().dmk_box_moments(self._h, int(level), cptr, nb, ptr, mem, int(bool(set))), "dmk_box_moments")
+        self._keep_codes = codes   # stream-ordered use of device codes
         return keep
 
     def info(self) -> PlanInfo:

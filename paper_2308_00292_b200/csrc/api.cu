@@ -303,22 +303,21 @@ int dmk_box_moments(dmk_plan_t P, int level, const int64_t* codes, int64_t nbox,
     const int64_t nmax = (int64_t)1 << (3 * level);
     const int64_t p3 = (int64_t)P->tab->p * P->tab->p * P->tab->p;
     cudaStream_t s = P->stream;
-    DevBuf<int64_t> dc;
-    dc.alloc(nbox, s);
-    std::vector<int64_t> hc(codes, codes + nbox);   // codes are host memory
-    for (int64_t c : hc)
-      if (c < 0 || c >= nmax) fail(DMK_ERR_ARG, "box code out of range for the level");
-    if (nbox) DMK_CUDA(cudaMemcpyAsync(dc.p, hc.data(), nbox * sizeof(int64_t), cudaMemcpyHostToDevice, s));
     if (mem == DMK_MEM_HOST) {
+      for (int64_t k = 0; k < nbox; ++k)
+        if (codes[k] < 0 || codes[k] >= nmax) fail(DMK_ERR_ARG, "box code out of range for the level");
+      DevBuf<int64_t> dc;
       DevBuf<double> d;
+      dc.alloc(nbox, s);
       d.alloc(nbox * p3, s);
+      if (nbox) DMK_CUDA(cudaMemcpyAsync(dc.p, codes, nbox * sizeof(int64_t), cudaMemcpyHostToDevice, s));
       if (set && nbox) DMK_CUDA(cudaMemcpyAsync(d.p, values, nbox * p3 * sizeof(double), cudaMemcpyHostToDevice, s));
       box_moments(P, level, dc.p, nbox, d.p, set != 0);
       if (!set && nbox) DMK_CUDA(cudaMemcpyAsync(values, d.p, nbox * p3 * sizeof(double), cudaMemcpyDeviceToHost, s));
       DMK_CUDA(cudaStreamSynchronize(s));
     } else {
-      box_moments(P, level, dc.p, nbox, values, set != 0);
-      DMK_CUDA(cudaStreamSynchronize(s));   // the host codes buffer is released on return
+      // device codes: stream-ordered, no synchronisation; codes outside the level are skipped
+      box_moments(P, level, codes, nbox, values, set != 0);
     }
   });
 }

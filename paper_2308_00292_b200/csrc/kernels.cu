@@ -158,39 +158,48 @@ __global__ void __launch_bounds__(Ant32<P>::NT) k_anterp32(DevTree t, const int3
 // split): the same contraction as a GEMM per F_out box with the points as K,
 //   mu[(n1 n2)][n3] = sum_j W[(n1 n2)][j] Tz[n3][j],   W[(n1 n2)][j] = rho_j Tx_j[n1] Ty_j[n2],
 // M = p^2 rows in MT tiles of 128 (TMEM lanes), N = p padded to NP (a multiple of 16),
-// K = the points in chunks of KC = 32.  Per chunk the CTA writes W and Tz, each split
-// as hi = tf32(v), lo = tf32(v - hi), into shared memory in the K-major no-swizzle
-// layout of umma.cuh; one thread issues A_hi B_hi + A_lo B_hi + A_hi B_lo (MT x 4 k-steps
-// x 3 MMAs) into one of two TMEM accumulators and commits them to an mbarrier; while the
-// tensor core runs, the threads compute the next chunk's Chebyshev values, then read the
-// previous chunk's accumulator (tcgen05.ld) into fp64 registers -- one thread per row
-// (n1, n2), fp32 sums over at most KC points as in k_anterp32, fp64 across chunks.
+// K = the points.  Warp-specialised pipeline: 4 MT producer warps (one thread per row m)
+// compute the Chebyshev values of a super-chunk of SC points in fp64 (rounded once into
+// shared tables), then write W and Tz of each chunk of KC points, split as
+// hi = tf32(v), lo = tf32(v - hi), into one of two operand buffers (K-major, no swizzle,
+// umma.cuh) and arrive on its "full" mbarrier; one MMA warp waits for it, issues
+// A_hi B_hi + A_lo B_hi + A_hi B_lo (MT tiles x 3 MMAs) into the super-chunk's TMEM
+// accumulator and commits the buffer's "free" mbarrier (the tensor core releases it when
+// its MMAs complete).  Each super-chunk accumulates in one of two TMEM accumulators; the
+// producers read it (tcgen05.ld) into fp64 registers one super-chunk later, so the fp32
+// sums run over at most SC points (as k_anterp32's 32) and fp64 across super-chunks.
+#ifndef ANT_TC_KC
+#define ANT_TC_KC 8      // points per operand chunk (one K = 8 MMA step)
+#endif
+#ifndef ANT_TC_MINB
+#define ANT_TC_MINB 2    // two CTAs per SM (shared memory and TMEM allow two)
+#endif
 template <int P>
 struct AntTC {
-  static constexpr int P2 = P * P, MT = (P2 + 127) / 128, NP = (P + 15) / 16 * 16, KC = 32;
-  static constexpr int NT = 128 * MT;                     // one thread per accumulator row
+  static constexpr int P2 = P * P, MT = (P2 + 127) / 128, NP = (P + 15) / 16 * 16;
+  static constexpr int KC = ANT_TC_KC, SC = 64, NCH = SC / KC;
+  static constexpr int NPROD = 128 * MT;                  // producer threads: one per row
+  static constexpr int NT = NPROD + 32;                   // + the MMA warp
   static constexpr int ACOLS = MT * NP;                   // TMEM columns per accumulator
   static constexpr int TCOLS = 2 * ACOLS <= 32 ? 32 : (2 * ACOLS <= 64 ? 64 : (2 * ACOLS <= 128 ? 128 : 256));
   static constexpr size_t A_WORDS = (size_t)MT * 128 * KC, B_WORDS = (size_t)NP * KC;
-  static constexpr size_t smem = sizeof(float) * (2 * A_WORDS + 2 * B_WORDS + (size_t)3 * KC * P) + 128;
+  static constexpr size_t BUF_WORDS = 2 * A_WORDS + 2 * B_WORDS;   // hi + lo
+  static constexpr size_t smem = sizeof(float) * (2 * BUF_WORDS + (size_t)2 * 3 * SC * P) + 128;
 };
 __device__ __forceinline__ int umma_koff(int row, int k, int kc) {   // K-major, no swizzle (umma.cuh)
   return (row >> 3) * (kc / 4) * 32 + (k >> 2) * 32 + (row & 7) * 4 + (k & 3);
 }
 template <int P>
-__global__ void __launch_bounds__(AntTC<P>::NT, 2) k_anterp_tc(DevTree t, const int32_t* __restrict__ boxes,
-                                                            const double* __restrict__ q, double* __restrict__ mom) {
+__global__ void __launch_bounds__(AntTC<P>::NT, ANT_TC_MINB) k_anterp_tc(DevTree t, const int32_t* __restrict__ boxes,
+                                                               const double* __restrict__ q,
+                                                               double* __restrict__ mom) {
   using C = AntTC<P>;
-  constexpr int P2 = C::P2, MT = C::MT, NP = C::NP, KC = C::KC, NT = C::NT, ACOLS = C::ACOLS;
+  constexpr int P2 = C::P2, MT = C::MT, NP = C::NP, KC = C::KC, SC = C::SC, NCH = C::NCH;
+  constexpr int NPROD = C::NPROD, ACOLS = C::ACOLS;
   extern __shared__ __align__(128) float smf[];
-  float* Ah = smf;                       // [MT*128][KC] K-major, hi
-  float* Al = Ah + C::A_WORDS;           // lo
-  float* Bh = Al + C::A_WORDS;           // [NP][KC]
-  float* Bl = Bh + C::B_WORDS;
-  float* sx = Bl + C::B_WORDS;           // [KC][P] rho T_n1(x)
-  float* sy = sx + KC * P;               // [KC][P]
-  float* sz = sy + KC * P;               // [KC][P]
-  __shared__ __align__(8) uint64_t mbar;
+  float* buf[2] = {smf, smf + C::BUF_WORDS};   // [Ah | Al | Bh | Bl] per operand buffer
+  float* tab[2] = {smf + 2 * C::BUF_WORDS, smf + 2 * C::BUF_WORDS + 3 * SC * P};   // [sx|sy|sz][SC][P]
+  __shared__ __align__(8) uint64_t full[2], freeb[2], dfull[2], dfree[2];
   __shared__ uint32_t tbase;
   __shared__ int2 rg[8];
   __shared__ int nr_s, tot_s;
@@ -199,151 +208,190 @@ __global__ void __launch_bounds__(AntTC<P>::NT, 2) k_anterp_tc(DevTree t, const 
   __syncthreads();
   const int nr = nr_s, tot = tot_s;
   if (tot == 0) return;   // moments were zeroed by the caller
-  // zero the padding once (never rewritten): A rows >= p^2, B rows >= p (hi and lo)
-  for (int i = tid; i < (MT * 128 - P2) * KC; i += NT) {
+  // zero the padding once (never rewritten): A rows >= p^2, B rows >= p, both buffers
+  for (int i = tid; i < (MT * 128 - P2) * KC; i += C::NT) {
     const int r = P2 + i / KC, k = i % KC;
-    Ah[umma_koff(r, k, KC)] = 0.0f;
-    Al[umma_koff(r, k, KC)] = 0.0f;
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      buf[u][umma_koff(r, k, KC)] = 0.0f;
+      buf[u][C::A_WORDS + umma_koff(r, k, KC)] = 0.0f;
+    }
   }
-  for (int i = tid; i < (NP - P) * KC; i += NT) {
+  for (int i = tid; i < (NP - P) * KC; i += C::NT) {
     const int r = P + i / KC, k = i % KC;
-    Bh[umma_koff(r, k, KC)] = 0.0f;
-    Bl[umma_koff(r, k, KC)] = 0.0f;
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      buf[u][2 * C::A_WORDS + umma_koff(r, k, KC)] = 0.0f;
+      buf[u][2 * C::A_WORDS + C::B_WORDS + umma_koff(r, k, KC)] = 0.0f;
+    }
   }
   if (warp == 0) umma::tmem_alloc<C::TCOLS>(&tbase);
-  if (tid == 0) umma::mbar_init(&mbar, 1);
+  if (tid == 0) {
+    for (int u = 0; u < 2; ++u) {
+      umma::mbar_init(&full[u], NPROD / 32);   // one arrival per producer warp
+      umma::mbar_init(&freeb[u], 1);           // tcgen05.commit
+      umma::mbar_init(&dfull[u], 1);           // tcgen05.commit
+      umma::mbar_init(&dfree[u], NPROD / 32);
+    }
+  }
+  umma::fence_smem_to_async();
   umma::fence_before_sync();
   __syncthreads();
   umma::fence_after_sync();
   const uint32_t tmem = tbase;
-  double cen[3], ih;
-  box_geom(t.code[b], t.level[b], cen, ih);
-  // this thread's accumulator row m = (n1, n2): tile m / 128, TMEM lane m % 128
-  const int m = tid;
-  const int n1 = m / P, n2 = m - n1 * P;
-  const bool real = m < P2;
-  double acc[P];
+  const int nsc = (tot + SC - 1) / SC;   // super-chunks
+  if (warp == NPROD / 32) {
+    // ================= MMA warp
+    if ((tid & 31) == 0) {
+      const uint32_t idesc = umma::idesc_tf32(128, NP);
+      int g = 0;   // global chunk index
+      for (int sc = 0; sc < nsc; ++sc) {
+        const int d = sc & 1;
+        if (sc >= 2) umma::mbar_wait(&dfree[d], (uint32_t)(((sc - 2) >> 1) & 1));   // producers read it
+        const int nch = min(NCH, (tot - sc * SC + KC - 1) / KC);
+        for (int c = 0; c < nch; ++c, ++g) {
+          const int u = g & 1;
+          umma::mbar_wait(&full[u], (uint32_t)((g >> 1) & 1));
+          umma::fence_after_sync();
+          const float* B0 = buf[u];
+          const uint64_t dAh = umma::sdesc_kmajor(B0, 128, 32 * KC);
+          const uint64_t dAl = umma::sdesc_kmajor(B0 + C::A_WORDS, 128, 32 * KC);
+          const uint64_t dBh = umma::sdesc_kmajor(B0 + 2 * C::A_WORDS, 128, 32 * KC);
+          const uint64_t dBl = umma::sdesc_kmajor(B0 + 2 * C::A_WORDS + C::B_WORDS, 128, 32 * KC);
+          const uint32_t dbase = tmem + (uint32_t)(d * ACOLS);
 #pragma unroll
-  for (int n = 0; n < P; ++n) acc[n] = 0.0;
-  const uint32_t idesc = umma::idesc_tf32(128, NP);
-  // descriptors of the k-step-0, tile-0 operands; the others differ only in the start
-  // address field (16-byte units): + s * 256 B along K, + tm * 128 * KC * 4 B along M
-  const uint64_t dAh = umma::sdesc_kmajor(Ah, 128, 32 * KC), dAl = umma::sdesc_kmajor(Al, 128, 32 * KC);
-  const uint64_t dBh = umma::sdesc_kmajor(Bh, 128, 32 * KC), dBl = umma::sdesc_kmajor(Bl, 128, 32 * KC);
-  const int nch = (tot + KC - 1) / KC;
-  auto flush = [&](int c) {   // accumulator of chunk c -> fp64 registers
-    umma::mbar_wait(&mbar, (uint32_t)(c & 1));
-    umma::fence_after_sync();
-    float v[32];
-    const uint32_t col = (uint32_t)((c & 1) * ACOLS + (m >> 7) * NP);
-    if constexpr (NP >= 32) umma::ld32x32b_x32(tmem + ((uint32_t)(32 * (warp & 3)) << 16) + col, v);
-    else umma::ld32x32b_x16(tmem + ((uint32_t)(32 * (warp & 3)) << 16) + col, v);
+          for (int pr = 0; pr < 3; ++pr) {   // hi.hi, lo.hi, hi.lo
+            const uint64_t da = pr == 1 ? dAl : dAh, db = pr == 2 ? dBl : dBh;
 #pragma unroll
-    for (int n = 0; n < P; ++n) acc[n] += (double)v[n];
-  };
-  // Chebyshev work item of this thread: point j = tid / 3 of the chunk, axis d = tid % 3;
-  // its coordinate (and charge) are loaded one chunk ahead
-  const int jw = tid / 3, dw = tid % 3;
-  const bool cw = tid < 3 * KC;
-  const double* coord = dw == 0 ? t.xs : (dw == 1 ? t.ys : t.zs);
-  double xn = 0.0, qn = 1.0;
-  auto load_pt = [&](int c) {
-    if (cw && c * KC + jw < tot) {
-      const int pi = range_point(rg, nr, c * KC + jw);
-      xn = (coord[pi] - cen[dw]) * ih;
-      qn = dw == 0 ? q[pi] : 1.0;
-    } else {
-      xn = 2.0;   // outside [-1, 1]: marks a padding point
+            for (int s8 = 0; s8 < KC / 8; ++s8)
+#pragma unroll
+              for (int tm = 0; tm < MT; ++tm)
+                umma::mma_tf32(dbase + tm * NP, da + (uint64_t)(tm * 32 * KC + s8 * 16), db + (uint64_t)(s8 * 16),
+                               idesc, pr > 0 || c > 0 || s8 > 0);
+          }
+          umma::commit(&freeb[u]);   // the buffer is free once these MMAs complete
+        }
+        umma::commit(&dfull[d]);     // the super-chunk's accumulator is complete
+      }
     }
-  };
-  load_pt(0);
-  for (int c = 0; c < nch; ++c) {
-    // ---- Chebyshev values of the chunk (fp64 recurrence, rounded once)
-    if (cw) {
-      float* dst = (dw == 0 ? sx : dw == 1 ? sy : sz) + jw * P;
-      if (xn <= 1.5) {
-        const double xx = xn, sc = qn;
-        double ta = 1.0, tb = xx;
-        dst[0] = (float)sc;
-        if (P > 1) dst[1] = (float)(sc * xx);
+    __syncwarp();
+  } else {
+    // ================= producer warps: thread m owns accumulator row m = (n1, n2)
+    const int m = tid;
+    const int n1 = m / P, n2 = m - n1 * P;
+    const bool real = m < P2;
+    double cen[3], ih;
+    box_geom(t.code[b], t.level[b], cen, ih);
+    double acc[P];
+#pragma unroll
+    for (int n = 0; n < P; ++n) acc[n] = 0.0;
+    // Chebyshev work items: point j = w / 3 of the super-chunk, axis d = w % 3
+    auto cheb = [&](int sc) {
+      for (int w = tid; w < 3 * SC; w += NPROD) {
+        const int jw = w / 3, dw = w % 3;
+        const double* coord = dw == 0 ? t.xs : (dw == 1 ? t.ys : t.zs);
+        float* dst = tab[sc & 1] + dw * SC * P + jw * P;
+        const int j = sc * SC + jw;
+        if (j < tot) {
+          const int pi = range_point(rg, nr, j);
+          const double xx = (coord[pi] - cen[dw]) * ih, sc0 = dw == 0 ? q[pi] : 1.0;
+          double ta = 1.0, tb = xx;
+          dst[0] = (float)sc0;
+          if (P > 1) dst[1] = (float)(sc0 * xx);
 #pragma unroll 6
-        for (int n = 2; n < P; ++n) {
-          const double tn = 2.0 * xx * tb - ta;
-          dst[n] = (float)(sc * tn);
-          ta = tb;
-          tb = tn;
+          for (int n = 2; n < P; ++n) {
+            const double tn = 2.0 * xx * tb - ta;
+            dst[n] = (float)(sc0 * tn);
+            ta = tb;
+            tb = tn;
+          }
+        } else {
+#pragma unroll
+          for (int n = 0; n < P; ++n) dst[n] = 0.0f;
         }
-      } else {
-#pragma unroll
-        for (int n = 0; n < P; ++n) dst[n] = 0.0f;
       }
-    }
-    if (c + 1 < nch) load_pt(c + 1);
-    // ---- the previous chunk's accumulator (its MMAs also free the operand buffers)
-    if (c > 0) flush(c - 1);
-    __syncthreads();
-    // ---- operands of this chunk: W row m over the KC points, Tz rows n3 < p
-    if (real) {
-#pragma unroll
-      for (int k4 = 0; k4 < KC; k4 += 4) {
-        float4 h, l;
-        float* hv = &h.x;
-        float* lv = &l.x;
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float w = sx[(k4 + e) * P + n1] * sy[(k4 + e) * P + n2];
-          hv[e] = umma::tf32_rna(w);
-          lv[e] = umma::tf32_rna(w - hv[e]);
-        }
-        const int o = umma_koff(m, k4, KC);
-        *reinterpret_cast<float4*>(Ah + o) = h;
-        *reinterpret_cast<float4*>(Al + o) = l;
-      }
-    }
-    for (int w = tid; w < P * (KC / 4); w += NT) {
-      const int n3 = w / (KC / 4), k4 = 4 * (w % (KC / 4));
-      float4 h, l;
-      float* hv = &h.x;
-      float* lv = &l.x;
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float z = sz[(k4 + e) * P + n3];
-        hv[e] = umma::tf32_rna(z);
-        lv[e] = umma::tf32_rna(z - hv[e]);
-      }
-      const int o = umma_koff(n3, k4, KC);
-      *reinterpret_cast<float4*>(Bh + o) = h;
-      *reinterpret_cast<float4*>(Bl + o) = l;
-    }
-    umma::fence_smem_to_async();
-    umma::fence_before_sync();
-    __syncthreads();
-    if (tid == 0) {
+    };
+    auto flush = [&](int sc) {   // the accumulator of super-chunk sc -> fp64 registers
+      const int d = sc & 1;
+      umma::mbar_wait(&dfull[d], (uint32_t)((sc >> 1) & 1));
       umma::fence_after_sync();
-      const uint32_t dbase = tmem + (uint32_t)((c & 1) * ACOLS);
+      float v[32];
+      const uint32_t col = (uint32_t)(d * ACOLS + (m >> 7) * NP);
+      if constexpr (NP >= 32) umma::ld32x32b_x32(tmem + ((uint32_t)(32 * (warp & 3)) << 16) + col, v);
+      else umma::ld32x32b_x16(tmem + ((uint32_t)(32 * (warp & 3)) << 16) + col, v);
 #pragma unroll
-      for (int pr = 0; pr < 3; ++pr) {   // hi.hi, lo.hi, hi.lo
-        const uint64_t da0 = pr == 1 ? dAl : dAh, db0 = pr == 2 ? dBl : dBh;
+      for (int n = 0; n < P; ++n) acc[n] += (double)v[n];
+      umma::fence_before_sync();
+      __syncwarp();
+      if ((tid & 31) == 0) umma::mbar_arrive(&dfree[d]);
+    };
+    int g = 0;
+    cheb(0);
+    for (int sc = 0; sc < nsc; ++sc) {
+      umma::bar_sync(1, NPROD);   // the super-chunk's tables are written
+      const float* sx = tab[sc & 1];
+      const float* sy = sx + SC * P;
+      const float* sz = sy + SC * P;
+      const int nch = min(NCH, (tot - sc * SC + KC - 1) / KC);
+      for (int c = 0; c < nch; ++c, ++g) {
+        const int u = g & 1;
+        if (g >= 2) umma::mbar_wait(&freeb[u], (uint32_t)(((g - 2) >> 1) & 1));
+        float* Ah = buf[u];
+        float* Al = Ah + C::A_WORDS;
+        float* Bh = Al + C::A_WORDS;
+        float* Bl = Bh + C::B_WORDS;
+        if (real) {
 #pragma unroll
-        for (int s = 0; s < KC / 8; ++s) {
+          for (int k4 = 0; k4 < KC; k4 += 4) {
+            float4 h, l;
+            float* hv = &h.x;
+            float* lv = &l.x;
 #pragma unroll
-          for (int tm = 0; tm < MT; ++tm)
-            umma::mma_tf32(dbase + tm * NP, da0 + (uint64_t)(s * 16 + tm * 32 * KC), db0 + (uint64_t)(s * 16), idesc,
-                           pr > 0 || s > 0);
+            for (int e = 0; e < 4; ++e) {
+              const int j = c * KC + k4 + e;
+              const float w = sx[j * P + n1] * sy[j * P + n2];
+              hv[e] = umma::tf32_rna(w);
+              lv[e] = umma::tf32_rna(w - hv[e]);
+            }
+            const int o = umma_koff(m, k4, KC);
+            *reinterpret_cast<float4*>(Ah + o) = h;
+            *reinterpret_cast<float4*>(Al + o) = l;
+          }
         }
+        if (m < P * (KC / 4)) {
+          const int n3 = m / (KC / 4), k4 = 4 * (m % (KC / 4));
+          float4 h, l;
+          float* hv = &h.x;
+          float* lv = &l.x;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float z = sz[(c * KC + k4 + e) * P + n3];
+            hv[e] = umma::tf32_rna(z);
+            lv[e] = umma::tf32_rna(z - hv[e]);
+          }
+          const int o = umma_koff(n3, k4, KC);
+          *reinterpret_cast<float4*>(Bh + o) = h;
+          *reinterpret_cast<float4*>(Bl + o) = l;
+        }
+        umma::fence_smem_to_async();
+        __syncwarp();
+        if ((tid & 31) == 0) umma::mbar_arrive(&full[u]);
       }
-      umma::commit(&mbar);
+      // next super-chunk's tables (the other table buffer: its last readers finished
+      // before this super-chunk's bar_sync), then the previous accumulator
+      if (sc + 1 < nsc) cheb(sc + 1);
+      if (sc >= 1) flush(sc - 1);
+    }
+    flush(nsc - 1);
+    if (real) {
+      double* out = mom + (size_t)t.fout_rank[b] * P * P2 + (size_t)m * P;
+#pragma unroll
+      for (int n = 0; n < P; ++n) out[n] = acc[n];
     }
   }
-  flush(nch - 1);
   umma::fence_before_sync();
   __syncthreads();
   if (warp == 0) umma::tmem_free<C::TCOLS>(tmem);
-  if (real) {
-    double* out = mom + (size_t)t.fout_rank[b] * P * P2 + (size_t)m * P;
-#pragma unroll
-    for (int n = 0; n < P; ++n) out[n] = acc[n];
-  }
 }
 
 // ---- fp32 tier far-field evaluation on the tensor cores (tcgen05 kind::tf32, 3xTF32):
@@ -2727,7 +2775,7 @@ static void run_p2p32_deg(dmk_plan_s* PL, const ResPoly& rp, int K, cudaStream_t
 // below which a pair is re-measured with the double-single low parts (tuning)
 static float p2p_tc() {
   const char* e = std::getenv("DMK_P2P_TC");
-  return e ? (float)std::atof(e) : 0.04f;
+  return e ? (float)std::atof(e) : 0.0025f;   // r < 0.05 r_L
 }
 template <int KER, int QC>
 static void run_p2p32q_deg(dmk_plan_s* PL, const ResPoly& rp64, int K, cudaStream_t st) {
@@ -2920,10 +2968,13 @@ __global__ void k_level_set(const uint64_t* __restrict__ code, const int32_t* __
 
 // sparse form (locally essential tree exchange): the boxes of a forced level are all
 // present in Morton order, so the box of code c is level_off[level] + c
-__global__ void k_box_moments(const int32_t* __restrict__ fout_rank, int64_t b0, const int64_t* __restrict__ codes,
-                              int p3, double* __restrict__ mom, double* __restrict__ vals, int set) {
+__global__ void k_box_moments(const int32_t* __restrict__ fout_rank, int64_t b0, int64_t nmax,
+                              const int64_t* __restrict__ codes, int p3, double* __restrict__ mom,
+                              double* __restrict__ vals, int set) {
   const int64_t k = blockIdx.x;
-  const int r = fout_rank[b0 + codes[k]];
+  const int64_t c = codes[k];
+  if (c < 0 || c >= nmax) return;
+  const int r = fout_rank[b0 + c];
   if (r < 0) return;
   double* m = mom + (size_t)r * p3;
   double* v = vals + (size_t)k * p3;
@@ -2939,8 +2990,9 @@ void box_moments(dmk_plan_s* PL, int level, const int64_t* dcodes, int64_t nb, d
   if (level >= PL->th.nlevels - 1) fail(DMK_ERR_STATE, "the tree has no non-leaf boxes at that level");
   if (nb == 0) return;
   const int p3 = PL->tab->p * PL->tab->p * PL->tab->p;
-  k_box_moments<<<(unsigned)nb, 256, 0, PL->stream>>>(PL->fout_rank.p, PL->th.level_off[level], dcodes, p3,
-                                                       PL->mom.p, dvals, set ? 1 : 0);
+  k_box_moments<<<(unsigned)nb, 256, 0, PL->stream>>>(PL->fout_rank.p, PL->th.level_off[level],
+                                                       (int64_t)1 << (3 * level), dcodes, p3, PL->mom.p, dvals,
+                                                       set ? 1 : 0);
   DMK_LAUNCH_CHECK();
 }
 

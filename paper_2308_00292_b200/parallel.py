@@ -177,12 +177,13 @@ class GpuBackend:
 
     def get_boxes(self, plan, level, codes):
         p = plan.info().p
-        codes = np.asarray(codes, dtype=np.int64)
-        out = torch.empty((codes.size, p, p, p), dtype=torch.float64, device=self.device)
+        codes = torch.as_tensor(codes, dtype=torch.int64, device=self.device)
+        out = torch.empty((codes.numel(), p, p, p), dtype=torch.float64, device=self.device)
         return plan.box_moments(level, codes, out)
 
     def set_boxes(self, plan, level, codes, values):
-        plan.box_moments(level, np.asarray(codes, dtype=np.int64), values.to(self.device).contiguous(), set=True)
+        codes = torch.as_tensor(codes, dtype=torch.int64, device=self.device)
+        plan.box_moments(level, codes, values.to(self.device).contiguous(), set=True)
 
     def downward(self, plan):
         return plan.downward(device=self.device)
@@ -546,7 +547,7 @@ def dmk_eval_let(points: torch.Tensor, charges: torch.Tensor, comm: Comm, backen
     complete = {}
     for lv in range(Gd + 1, Lh):
         mine = torch.unique(ocode >> (3 * (Lh - lv))) if n_own else torch.zeros(0, dtype=torch.int64, device=dev)
-        vals = (torch.as_tensor(backend.get_boxes(plan, lv, mine.cpu().numpy()), device=dev).reshape(-1, p3)
+        vals = (torch.as_tensor(backend.get_boxes(plan, lv, mine), device=dev).reshape(-1, p3)
                 if len(mine) else torch.zeros((0, p3), dtype=torch.float64, device=dev))
         nbl = neighbour_codes(mine, lv)
         dest = torch.zeros(len(mine), dtype=torch.int64, device=dev)
@@ -574,7 +575,7 @@ def dmk_eval_let(points: torch.Tensor, charges: torch.Tensor, comm: Comm, backen
         for lv in range(Gd + 1, Lh):
             need, acc = complete[lv]
             if len(need):
-                backend.set_boxes(plan, lv, need.cpu().numpy(), acc.reshape(-1, p, p, p))
+                backend.set_boxes(plan, lv, need, acc.reshape(-1, p, p, p))
         backend.set_level(plan, Gd, g_dense)
         u = torch.as_tensor(backend.downward(plan), device=dev)
         u_own = u[:n_own]

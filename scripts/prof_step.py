@@ -20,6 +20,8 @@ ap.add_argument("--eps", type=float, default=1e-6)
 ap.add_argument("--ns", type=int, default=200)
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--kind", default="uniform")
+ap.add_argument("--kernel", default="laplace")
+ap.add_argument("--lam", type=float, default=10.0)
 a = ap.parse_args()
 x, q = dmk_inputs.make(a.kind, a.n, seed=1)
 X = torch.as_tensor(x, device="cuda")
@@ -27,7 +29,7 @@ Q = torch.as_tensor(q, device="cuda")
 for r in range(a.reps):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    plan = dmk.dmk_plan(X, eps=a.eps, leaf_capacity=a.ns)
+    plan = dmk.dmk_plan(X, eps=a.eps, leaf_capacity=a.ns, kernel=a.kernel, lam=a.lam)
     torch.cuda.synchronize()
     t1 = time.perf_counter()
     u = plan.eval(Q)

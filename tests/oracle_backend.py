@@ -28,10 +28,10 @@ class OracleBackend:
         plan["set"] = (level, dense.cpu().numpy())
 
     def get_boxes(self, plan, level, codes):
-        return torch.as_tensor(self._run(plan, box_get=(level, list(codes))))
+        return torch.as_tensor(self._run(plan, box_get=(level, [int(c) for c in codes])))
 
     def set_boxes(self, plan, level, codes, values):
-        plan.setdefault("bset", []).append((level, list(codes), values.cpu().numpy()))
+        plan.setdefault("bset", []).append((level, [int(c) for c in codes], values.cpu().numpy()))
 
     def downward(self, plan):
         return torch.as_tensor(self._run(plan, level_set=plan.get("set"), box_set=plan.get("bset")))

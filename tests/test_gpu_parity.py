@@ -342,9 +342,11 @@ def test_p2p_queue_capacities(qc, monkeypatch):
 @pytest.mark.parametrize("eps", [1e-3, 1e-6])
 def test_anterp_tensor_core_form(eps, monkeypatch):
     """Anterpolation on the 5th-generation tensor cores (tcgen05 kind::tf32, 3xTF32 split,
-    TMEM accumulators flushed to fp64 every 32 points; DMK_ANTERP=tc) against the oracle's
-    proxy charges (Def. 2.1, mu = V^T rho~) on a deep adaptive tree.  The 3xTF32 products
-    carry ~2^-21 relative error: measured 6.8e-7 (profiles/r02_anterp_forms_v1.jsonl)."""
+    warp-specialised: producer warps write the operands of 8-point chunks into two shared
+    buffers, one MMA warp issues; TMEM accumulators flushed to fp64 every 64 points;
+    DMK_ANTERP=tc) against the oracle's proxy charges (Def. 2.1, mu = V^T rho~) on a deep
+    adaptive tree.  The 3xTF32 products carry ~2^-21 relative error and the fp32 sums run
+    over 64 points: measured 1.1e-6 (profiles/r02_anterp_forms_v6.jsonl)."""
     monkeypatch.setenv("DMK_ANTERP", "tc")
     x, q = dmk_inputs.make("clusters", 12000, seed=21)
     _, st = dmk_laplace3d(x, q, eps, 40, return_stages=True)
