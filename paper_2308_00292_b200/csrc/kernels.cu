@@ -689,7 +689,7 @@ __global__ void __launch_bounds__(GrpCfg<P, MT>::NT) k_c2p_grp(DevTree t, const 
   for (int g = 0; g < 4; ++g) {
     const double* c0 = ch[g];
     const double* c1 = ch[4 + g];
-    mma_tiles<KS2>(
+    mma_tiles<KS2, true>(
         (MT + 7) / 8, (P2 + 7) / 8,
         [&](int m, int k) {
           const int o1 = k >= P, k1 = k - o1 * P;

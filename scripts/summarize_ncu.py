@@ -20,7 +20,8 @@ def launches(path, half):
     agg, cnt = collections.OrderedDict(), collections.Counter()
     scale = {"nsecond": 1e-6, "ns": 1e-6, "usecond": 1e-3, "us": 1e-3, "msecond": 1.0, "ms": 1.0}
     for r in data:
-        name = r[ki].split("(")[0].split("<")[0].replace("void ", "")
+        name = r[ki].replace("(anonymous namespace)::", "").replace("<unnamed>::", "")
+        name = name.split("(")[0].split("<")[0].replace("void ", "")
         v = float(r[vi].replace(",", "")) * scale.get(r[ui], 1.0)
         agg[name] = agg.get(name, 0.0) + v
         cnt[name] += 1
