@@ -318,13 +318,26 @@ __global__ void __launch_bounds__(128) k_eval2(DevTree t, const int32_t* __restr
 struct ResPoly2 {
   double a[25];
 };
-__global__ void k_sum(const double* __restrict__ q, int64_t n, double* out) {
+// total charge, deterministic: pass 1 gives SUMB fixed-order block partials, pass 2 adds
+// them in order (one block of SUMB threads)
+constexpr int SUMB = 512;
+__global__ void k_sum_part(const double* __restrict__ q, int64_t n, double* part) {
   __shared__ double s[256];
   double v = 0.0;
-  for (int64_t i = threadIdx.x; i < n; i += 256) v += q[i];
+  for (int64_t i = blockIdx.x * 256 + threadIdx.x; i < n; i += (int64_t)SUMB * 256) v += q[i];
   s[threadIdx.x] = v;
   __syncthreads();
   for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) s[threadIdx.x] += s[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = s[0];
+}
+__global__ void k_sum(const double* __restrict__ part, double* out) {
+  __shared__ double s[SUMB];
+  s[threadIdx.x] = part[threadIdx.x];
+  __syncthreads();
+  for (int w = SUMB / 2; w > 0; w >>= 1) {
     if (threadIdx.x < w) s[threadIdx.x] += s[threadIdx.x + w];
     __syncthreads();
   }
@@ -470,8 +483,14 @@ static void run_p2p2(dmk_plan_s* PL, double* out) {
   ResPoly2 rp{};
   const int K = T.respoly_deg;
   for (int k = 0; k <= K && k < 25; ++k) rp.a[k] = T.respoly[k];
-  k_sum<<<1, 256, 0, PL->stream>>>(PL->q.p, PL->n, PL->scalar.p);
-  DMK_LAUNCH_CHECK();
+  {
+    DevBuf<double> part;
+    part.alloc(SUMB, PL->stream);
+    k_sum_part<<<SUMB, 256, 0, PL->stream>>>(PL->q.p, PL->n, part.p);
+    DMK_LAUNCH_CHECK();
+    k_sum<<<1, SUMB, 0, PL->stream>>>(part.p, PL->scalar.p);
+    DMK_LAUNCH_CHECK();
+  }
   const double ls = std::log(PL->side);
 #define DMK_P2P2_CASE(KK)                                                                                          \
   case KK:                                                                                                         \

@@ -61,9 +61,15 @@ def stage_errors(kind, n, ns, eps):
     ex = plan.tree("exp")
     scale = max(np.max(np.abs(st["local"][i])) for i in st["local"])
     e_loc = max(np.max(np.abs(lam[ex[i]] - st["local"][i])) for i in np.nonzero(ex >= 0)[0]) / scale
-    ufar, unear = plan.stage("ufar"), plan.stage("unear")
-    e_far = np.max(np.abs(ufar - st["u_far"])) / np.max(np.abs(st["u_far"]))
-    ref_near = st["u_near"] + st["u_self"]
+    def caller(v, perm):
+        out = np.empty_like(v)
+        out[perm] = v
+        return out
+    dperm = plan.tree("perm")
+    ufar, unear = caller(plan.stage("ufar"), dperm), caller(plan.stage("unear"), dperm)
+    ref_far = caller(st["u_far"], T.perm)
+    e_far = np.max(np.abs(ufar - ref_far)) / np.max(np.abs(ref_far))
+    ref_near = caller(st["u_near"] + st["u_self"], T.perm)
     e_near_max = np.max(np.abs(unear - ref_near)) / np.max(np.abs(ref_near))
     e_near_l2 = np.linalg.norm(unear - ref_near) / np.linalg.norm(ref_near)
     e_tot_oracle = np.max(np.abs(u - ref_u)) / np.max(np.abs(ref_u))

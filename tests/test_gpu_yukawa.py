@@ -57,9 +57,12 @@ def test_yukawa_local_expansions_and_fields(staged):
     scale = max(np.max(np.abs(st["local"][i])) for i in st["local"])
     for i in np.nonzero(exp >= 0)[0]:
         assert np.max(np.abs(lam[exp[i]] - st["local"][i])) <= tl["local"] * scale
-    ufar, unear = plan.stage("ufar"), plan.stage("unear")
-    assert np.max(np.abs(ufar - st["u_far"])) <= tl["ufar"] * np.max(np.abs(st["u_far"]))
-    ref_near = st["u_near"] + st["u_self"]
+    from test_gpu_parity import caller_order
+    perm, Tp = plan.tree("perm"), st["tree"].perm
+    ufar, unear = caller_order(plan.stage("ufar"), perm), caller_order(plan.stage("unear"), perm)
+    ref_far = caller_order(st["u_far"], Tp)
+    assert np.max(np.abs(ufar - ref_far)) <= tl["ufar"] * np.max(np.abs(ref_far))
+    ref_near = caller_order(st["u_near"] + st["u_self"], Tp)
     # The device culls list pairs with r >= r_L, where R_L = K - M_L is below eps M_L(0)
     # but (unlike 1/r) not exactly 0 (reading R13); the
     # oracle evaluates K - M_L over the whole list.  The two agree to that eps tail.
