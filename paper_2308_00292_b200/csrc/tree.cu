@@ -722,30 +722,6 @@ __global__ void k_p2p_fill(const int32_t* start, const int32_t* cnt, const int32
   }
 }
 
-// P2P work of item k (targets x list sources), for the longest-first order of deep trees
-__global__ void k_item_work(const int32_t* __restrict__ items, int64_t nitems, const int32_t* __restrict__ start,
-                            const int32_t* __restrict__ end, const int32_t* __restrict__ doff,
-                            const int32_t* __restrict__ dlist, uint32_t* __restrict__ work,
-                            int32_t* __restrict__ idx) {
-  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (k >= nitems) return;
-  const int B = items[2 * k], t0 = items[2 * k + 1];
-  const int nt = min(32, end[B] - t0);
-  int64_t src = 0;
-  for (int e = doff[B]; e < doff[B + 1]; ++e) src += end[dlist[e]] - start[dlist[e]];
-  const int64_t wk = (int64_t)nt * src;
-  work[k] = (uint32_t)(wk < 0xFFFFFFFFll ? wk : 0xFFFFFFFFll);
-  idx[k] = (int32_t)k;
-}
-__global__ void k_items_permute(const int32_t* __restrict__ in, const int32_t* __restrict__ order, int64_t nitems,
-                                int32_t* __restrict__ out) {
-  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (k >= nitems) return;
-  const int32_t j = order[k];
-  out[2 * k] = in[2 * j];
-  out[2 * k + 1] = in[2 * j + 1];
-}
-
 // Leaf-local double-single source records for the fp32 P2P tier (reading R16): for the
 // leaf B holding point i, d = x_i - c_B (fp64, exact), hi = fl32(d), lo = fl32(d - hi);
 // xl4[i] = (hi_x, hi_y, hi_z, rho_i) (the charge slot is filled per evaluation) and
@@ -1307,27 +1283,6 @@ static void build_tree_d(dmk_plan_s* P, const double* dpts) {
   P->p2p_items.alloc(2 * (P->np2p ? P->np2p : 1), s);
   k_p2p_fill<<<nblk(nbox), TPB, 0, s>>>(P->box_start.p, pcnt.p, poff.p, nbox, P->p2p_items.p);
   DMK_LAUNCH_CHECK();
-  if (nlevels > 7 && P->np2p > 1) {
-    // deep adaptive trees: items of very different lengths -- longest first, so that the
-    // long items do not run alone at the end of the P2P launch (blocks start in order)
-    const int64_t ni = P->np2p;
-    DevBuf<uint32_t> w0, w1;
-    DevBuf<int32_t> i0, i1, sorted;
-    w0.alloc(ni, s);
-    w1.alloc(ni, s);
-    i0.alloc(ni, s);
-    i1.alloc(ni, s);
-    k_item_work<<<nblk(ni), TPB, 0, s>>>(P->p2p_items.p, ni, P->box_start.p, P->box_end.p, P->dlist_off.p,
-                                         P->dlist.p, w0.p, i0.p);
-    DMK_LAUNCH_CHECK();
-    cub_run(s, [&](void* t, size_t& b) {
-      return cub::DeviceRadixSort::SortPairsDescending(t, b, w0.p, w1.p, i0.p, i1.p, ni, 0, 32, s);
-    });
-    sorted.alloc(2 * ni, s);
-    k_items_permute<<<nblk(ni), TPB, 0, s>>>(P->p2p_items.p, i1.p, ni, sorted.p);
-    DMK_LAUNCH_CHECK();
-    std::swap(P->p2p_items.p, sorted.p);
-  }
   if (build_oct) {
     P->p2p_items_o.alloc(P->np2p_o ? P->np2p_o : 1, s);
     k_p2p_fill_o<<<nblk(nbox), TPB, 0, s>>>(P->box_end.p, P->leaf_oct.p, ocnt.p, ooff.p, nbox, P->p2p_items_o.p);
