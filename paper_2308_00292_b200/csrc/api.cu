@@ -14,6 +14,7 @@ void eval_plan(dmk_plan_s* P, const double* dcharges, double* dout);
 
 static thread_local std::string g_err;
 int64_t g_launches = 0, g_cub_launches = 0;
+thread_local int64_t g_alloc_bytes = 0;
 void set_error(const std::string& m) { g_err = m; }
 void fail(int code, const std::string& m) { throw Error{code, m}; }
 
@@ -45,6 +46,38 @@ static void require_device() {
   DMK_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
   uint64_t thr = UINT64_MAX;
   DMK_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+}
+
+// ---- stream-ordered pool reservation.  Plans allocate and free their buffers through the
+// device's default pool (release threshold: never).  When a plan needs more than the pool
+// holds, cudaMallocAsync maps new physical memory -- tens to hundreds of ms, at random
+// steps of a repeated evaluation (measured on config 2: 60-190 ms outliers in 24 steps,
+// none after a pre-grown pool, profiles/r02_repeat_c2c.json).  So the pool is grown
+// ahead, once per size class: to twice the bytes the largest plan so far requested.
+namespace {
+std::mutex g_res_mu;
+std::vector<std::pair<int, int64_t>> g_reserved;   // (device, bytes)
+}
+static void reserve_pool(int64_t bytes, cudaStream_t s) {
+  int dev = 0;
+  DMK_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(g_res_mu);
+  int64_t* have = nullptr;
+  for (auto& r : g_reserved)
+    if (r.first == dev) have = &r.second;
+  if (!have) {
+    g_reserved.push_back({dev, 0});
+    have = &g_reserved.back().second;
+  }
+  const int64_t want = 2 * bytes;
+  if (want <= *have) return;
+  void* p = nullptr;
+  if (cudaMallocAsync(&p, (size_t)want, s) == cudaSuccess) {
+    cudaFreeAsync(p, s);
+    *have = want;
+  } else {
+    cudaGetLastError();   // not enough memory for the reserve: allocate on demand
+  }
 }
 
 // ---- stream/event pool (per device, process-wide, thread-safe)
@@ -187,6 +220,7 @@ int dmk_plan(int dim, int kernel, double eps, int64_t n, const double* points, i
       P->fast_sort = !(pf && pf[0] == '1');
       const char* pt = std::getenv("DMK_PROFILE_TREE");
       P->profile_tree = pt && pt[0] == '1';
+      const int64_t bytes0 = g_alloc_bytes;
       const double* dpts = points;
       DevBuf<double> tmp;
       if (mem == DMK_MEM_HOST) {
@@ -200,6 +234,7 @@ int dmk_plan(int dim, int kernel, double eps, int64_t n, const double* points, i
       P->tab_ref = get_tables(kernel, eps, kernel == DMK_KERNEL_YUKAWA ? P->lambda * P->side : 0.0);
       P->tab = P->tab_ref.get();
       alloc_eval_buffers(P);
+      reserve_pool(g_alloc_bytes - bytes0, P->stream);
       // no synchronisation: the plan's device work is ordered on P->stream before any
       // evaluation or read-back (all of which run on P->stream)
       DMK_CUDA(cudaGetLastError());

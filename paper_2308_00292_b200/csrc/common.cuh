@@ -11,6 +11,7 @@
 
 namespace dmk {
 extern int64_t g_launches, g_cub_launches;
+extern thread_local int64_t g_alloc_bytes;   // bytes requested through DevBuf on this thread
 
 constexpr int NBITS = 21;  // bits per coordinate of the 63-bit Morton key
 constexpr int LMAX = 20;   // deepest level a box may be refined into
@@ -52,6 +53,7 @@ struct DevBuf {
     s = st;
     n = count;
     if (count) DMK_CUDA(cudaMallocAsync((void**)&p, count * sizeof(T), st));
+    g_alloc_bytes += (int64_t)(count * sizeof(T));
   }
   void release() {
     if (p) cudaFreeAsync(p, s);
