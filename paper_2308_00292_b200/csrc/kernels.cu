@@ -652,7 +652,11 @@ __global__ void __launch_bounds__(Ev32<P>::NT) k_eval32(DevTree t, const int32_t
 // 48 p^4 flops per parent.  p2c is the transpose (axis 1 first, expanding 1 -> 2 -> 4
 // -> 8).  A CTA owns a tile of MT rows of the first-contracted axis (c2p: output rows
 // m1 of the parent; p2c: output rows k1 of the children), intermediates in shared
-// memory, each contraction a DMMA GEMM (mma_tiles).
+// memory, each contraction a DMMA GEMM (c2p: grp_tiles, per-lane precomputed operand
+// offsets, A fragments kept across n-tiles, two tiles of global B loads in flight:
+// 0.276 -> 0.235 ms at config 1, 1.49 -> 1.17 ms at eps = 1e-9; p2c: mma_tiles, where
+// the same rewrite measured slower, 0.29 -> 0.33 ms).
+constexpr int cmin(int a, int b) { return a < b ? a : b; }
 template <int P, int MT>
 struct GrpCfg {
   // p = 28: one CTA per SM fits (shared memory), so 16 warps instead of 8 keep more
@@ -662,12 +666,89 @@ struct GrpCfg {
   static constexpr int KS2 = (2 * P + 3) / 4, KS1 = (P + 3) / 4;
   static constexpr size_t smem_c2p = sizeof(double) * ((size_t)2 * P2 + 6 * (size_t)MT * P2);
   static constexpr size_t smem_p2c = sizeof(double) * ((size_t)2 * P2 + 6 * (size_t)MT * P2);
+  // resident CTAs per SM the shared memory allows (registers held to match)
+  static constexpr int MINB_C2P = P > 18 ? 1 : cmin((int)((227 * 1024) / (smem_c2p + 1024)), 4);
 };
+// Warp-level fp64 GEMM on 8x8 output tiles (mma.sync m8n8k4, DMMA) for the group
+// kernels, with the operand addressing precomputed per lane by the caller:
+//   fa(mt, ks) = A[8 mt + g][4 ks + q],  fb(nt, ks) = B[4 ks + q][8 nt + g],
+//   fc(mt, nt, c0, c1) consumes C[8 mt + g][8 nt + 2q + {0, 1}]   (g = lane/4, q = lane%4).
+// Tiles are dealt to the warps round-robin in mt-major order; a warp keeps its A
+// fragments while the m-tile does not change (axis contractions whose M is one or two
+// tiles reuse them over all n-tiles), and loads the next tile's B fragments during the
+// current tile's DMMA chain (NB tiles per step: more loads in flight, for global B).
+// FPRE (accumulating epilogues): fpre(mt, nt, p0, p1) loads the current output values
+// before the chain.
+template <int KS, int NB = 1, class FA, class FB, class FC, class FP>
+__device__ __forceinline__ void grp_tiles(int mtiles, int ntiles, FA fa, FB fb, FC fc, FP fpre) {
+  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int ntot = mtiles * ntiles;
+  int t = warp;
+  if (t >= ntot) return;
+  int cur = -1;
+  double av[KS], bv[NB][KS];
+  // a step takes NB tiles t, t + nw, ..., whose B loads are all in flight together (the
+  // next step's are issued before this step's DMMA chains)
+#pragma unroll
+  for (int j = 0; j < NB; ++j) {
+    const int tj = t + j * nw;
+    const int nt = (tj < ntot ? tj : t) % ntiles;
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) bv[j][ks] = fb(nt, ks);
+  }
+  for (; t < ntot; t += NB * nw) {
+    double bn[NB][KS];
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+      const int tn = t + (NB + j) * nw;
+      if (tn < ntot) {
+        const int ntn = tn % ntiles;
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks) bn[j][ks] = fb(ntn, ks);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+      const int tj = t + j * nw;
+      if (tj < ntot) {
+        const int mt = tj / ntiles, nt = tj - mt * ntiles;
+        if (mt != cur) {
+          cur = mt;
+#pragma unroll
+          for (int ks = 0; ks < KS; ++ks) av[ks] = fa(mt, ks);
+        }
+        double p0 = 0.0, p1 = 0.0;
+        fpre(mt, nt, p0, p1);
+        double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks) dmma(c0, c1, av[ks], bv[j][ks]);
+        fc(mt, nt, c0 + p0, c1 + p1);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < NB; ++j)
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) bv[j][ks] = bn[j][ks];
+  }
+}
+struct NoPre {
+  __device__ __forceinline__ void operator()(int, int, double&, double&) const {}
+};
+// K index k = 4 ks + q of a contraction over both halves o (K = 2p): o = k >= p,
+// k' = k - o p; k >= 2p is padding
+template <int P>
+__device__ __forceinline__ void split_k2(int k, int& o, int& kk, bool& ok) {
+  ok = k < 2 * P;
+  o = k >= P;
+  kk = k - o * P;
+}
 template <int P, int MT>
-__global__ void __launch_bounds__(GrpCfg<P, MT>::NT) k_c2p_grp(DevTree t, const int32_t* __restrict__ parents,
+__global__ void __launch_bounds__(GrpCfg<P, MT>::NT, GrpCfg<P, MT>::MINB_C2P) k_c2p_grp(DevTree t, const int32_t* __restrict__ parents,
                                                  const double* __restrict__ A, double* __restrict__ mom) {
   using C = GrpCfg<P, MT>;
   constexpr int P2 = C::P2, P3 = P2 * P, KS2 = C::KS2;
+  constexpr int NT1 = (P2 + 7) / 8;            // axis-1 n tiles per group
+  constexpr int NT2 = (MT * P + 7) / 8;        // axis-2 n tiles per o3
   extern __shared__ double sm[];
   double* sA = sm;                  // [2][P][P]: A_s[n][k]
   double* xi = sA + 2 * P2;         // [(o2 o3)][MT][P2]
@@ -675,6 +756,7 @@ __global__ void __launch_bounds__(GrpCfg<P, MT>::NT) k_c2p_grp(DevTree t, const 
   __shared__ const double* ch[8];
   // 1D grid, the tiles of a parent adjacent (they read the same children: L2 reuse)
   const int b = parents[blockIdx.x / C::NTILE], tid = threadIdx.x, m0 = (blockIdx.x % C::NTILE) * MT;
+  const int lane = tid & 31, g = lane >> 2, q = lane & 3;
   if (tid < 8) {
     const int c = t.child[8 * (int64_t)b + tid];
     ch[tid] = (c >= 0 && (t.flags[c] & F_OUT)) ? mom + (size_t)t.fout_rank[c] * P3 : nullptr;
@@ -685,71 +767,116 @@ __global__ void __launch_bounds__(GrpCfg<P, MT>::NT) k_c2p_grp(DevTree t, const 
 #pragma unroll
   for (int o = 0; o < 8; ++o) any |= ch[o] != nullptr;
   if (!any) return;
-  // axis 1: xi[g][i][n2n3] = sum_{o1,k1} A_o1[m0+i][k1] mu_(o1 g)[k1][n2n3]
-  for (int g = 0; g < 4; ++g) {
-    const double* c0 = ch[g];
-    const double* c1 = ch[4 + g];
-    mma_tiles<KS2, true>(
-        (MT + 7) / 8, (P2 + 7) / 8,
-        [&](int m, int k) {
-          const int o1 = k >= P, k1 = k - o1 * P;
-          return (m < MT && m0 + m < P && k < 2 * P) ? sA[(o1 * P + m0 + m) * P + k1] : 0.0;
+  // ---- axis 1: xi[gg][i][n2n3] = sum_{o1,k1} A_o1[m0+i][k1] mu_(o1 gg)[k1][n2n3]
+  // M = MT rows (one tile for MT <= 8), K = 2p, N = 4 groups x p^2 columns
+  {
+    int koff[KS2];   // per k step: k1 p^2, or -1 (padding)
+    bool kh[KS2];    // o1 of the k step
+#pragma unroll
+    for (int ks = 0; ks < KS2; ++ks) {
+      int o, kk;
+      bool ok;
+      split_k2<P>(4 * ks + q, o, kk, ok);
+      koff[ks] = ok ? kk * P2 : -1;
+      kh[ks] = o;
+    }
+    grp_tiles<KS2, (P <= 18 ? 2 : 1)>(
+        (MT + 7) / 8, 4 * NT1,
+        [&](int mt, int ks) {
+          int o, kk;
+          bool ok;
+          split_k2<P>(4 * ks + q, o, kk, ok);
+          const int i = mt * 8 + g;
+          return (ok && i < MT && m0 + i < P) ? sA[(o * P + m0 + i) * P + kk] : 0.0;
         },
-        [&](int k, int n) {
-          const int o1 = k >= P, k1 = k - o1 * P;
-          const double* c = o1 ? c1 : c0;
-          return (c && k < 2 * P && n < P2) ? __ldg(c + (size_t)k1 * P2 + n) : 0.0;
+        [&](int nt, int ks) {
+          const int gg = nt / NT1, n = min((nt - gg * NT1) * 8 + g, P2 - 1);
+          const double* c = ch[(kh[ks] ? 4 : 0) + gg];
+          return (c && koff[ks] >= 0) ? __ldg(c + koff[ks] + n) : 0.0;
         },
-        [&](int m, int n, double v0, double v1) {
-          if (m < MT) {
-            if (n < P2) xi[(g * MT + m) * P2 + n] = v0;
-            if (n + 1 < P2) xi[(g * MT + m) * P2 + n + 1] = v1;
+        [&](int mt, int nt, double v0, double v1) {
+          const int gg = nt / NT1, n = (nt - gg * NT1) * 8 + 2 * q, i = mt * 8 + g;
+          if (i < MT) {
+            double* row = xi + (gg * MT + i) * P2;
+            if (n < P2) row[n] = v0;
+            if (n + 1 < P2) row[n + 1] = v1;
           }
-        });
+        },
+        NoPre{});
   }
   __syncthreads();
-  // axis 2: eta[o3][i][m2 n3] = sum_{o2,k2} A_o2[m2][k2] xi[(o2 o3)][i][k2 n3]
-  for (int o3 = 0; o3 < 2; ++o3) {
-    mma_tiles<KS2>(
-        (P + 7) / 8, (MT * P + 7) / 8,
-        [&](int m, int k) {
-          const int o2 = k >= P, k2 = k - o2 * P;
-          return (m < P && k < 2 * P) ? sA[(o2 * P + m) * P + k2] : 0.0;
+  // ---- axis 2: eta[o3][i][m2 n3] = sum_{o2,k2} A_o2[m2][k2] xi[(o2 o3)][i][k2 n3]
+  // M = p rows m2, K = 2p, N = 2 (o3) x MT p columns (i, n3)
+  {
+    int koff[KS2];   // per k step: o2 2 MT p^2 + k2 p, or -1
+#pragma unroll
+    for (int ks = 0; ks < KS2; ++ks) {
+      int o, kk;
+      bool ok;
+      split_k2<P>(4 * ks + q, o, kk, ok);
+      koff[ks] = ok ? o * 2 * MT * P2 + kk * P : -1;
+    }
+    grp_tiles<KS2>(
+        (P + 7) / 8, 2 * NT2,
+        [&](int mt, int ks) {
+          int o, kk;
+          bool ok;
+          split_k2<P>(4 * ks + q, o, kk, ok);
+          const int m2 = mt * 8 + g;
+          return (ok && m2 < P) ? sA[(o * P + m2) * P + kk] : 0.0;
         },
-        [&](int k, int n) {
-          const int o2 = k >= P, k2 = k - o2 * P, i = n / P, n3 = n - i * P;
-          return (k < 2 * P && i < MT) ? xi[((o2 * 2 + o3) * MT + i) * P2 + k2 * P + n3] : 0.0;
+        [&](int nt, int ks) {
+          const int o3 = nt >= NT2, n = (nt - o3 * NT2) * 8 + g, i = n / P, n3 = n - i * P;
+          return (koff[ks] >= 0 && i < MT) ? xi[koff[ks] + (o3 * MT + i) * P2 + n3] : 0.0;
         },
-        [&](int m, int n, double v0, double v1) {
-          if (m >= P) return;
+        [&](int mt, int nt, double v0, double v1) {
+          const int m2 = mt * 8 + g;
+          if (m2 >= P) return;
+          const int o3 = nt >= NT2;
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
-            const int nn = n + e, i = nn / P, n3 = nn - i * P;
-            if (i < MT) eta[(o3 * MT + i) * P2 + m * P + n3] = e ? v1 : v0;
+            const int n = (nt - o3 * NT2) * 8 + 2 * q + e, i = n / P, n3 = n - i * P;
+            if (i < MT) eta[(o3 * MT + i) * P2 + m2 * P + n3] = e ? v1 : v0;
           }
-        });
+        },
+        NoPre{});
   }
   __syncthreads();
-  // axis 3: mu_P[m0+i][m2][m3] += sum_{o3,k3} eta[o3][i][m2][k3] A_o3[m3][k3]
-  double* dst = mom + (size_t)t.fout_rank[b] * P3;
-  mma_tiles<KS2>(
-      (MT * P + 7) / 8, (P + 7) / 8,
-      [&](int m, int k) {
-        const int o3 = k >= P, k3 = k - o3 * P, i = m / P, m2 = m - i * P;
-        return (i < MT && k < 2 * P) ? eta[(o3 * MT + i) * P2 + m2 * P + k3] : 0.0;
-      },
-      [&](int k, int n) {
-        const int o3 = k >= P, k3 = k - o3 * P;
-        return (n < P && k < 2 * P) ? sA[(o3 * P + n) * P + k3] : 0.0;
-      },
-      [&](int m, int n, double v0, double v1) {
-        const int i = m / P, m2 = m - i * P;
-        if (i >= MT || m0 + i >= P) return;
-        // one writer per element: fire-and-forget reductions (RED), no read latency
-        double* row = dst + (size_t)(m0 + i) * P2 + m2 * P;
-        if (n < P) atomicAdd(row + n, v0);
-        if (n + 1 < P) atomicAdd(row + n + 1, v1);
-      });
+  // ---- axis 3: mu_P[m0+i][m2][m3] += sum_{o3,k3} eta[o3][i][m2][k3] A_o3[m3][k3]
+  // M = MT p rows (i, m2), K = 2p, N = p columns m3
+  {
+    int koff[KS2];   // per k step: o3 MT p^2 + k3, or -1
+#pragma unroll
+    for (int ks = 0; ks < KS2; ++ks) {
+      int o, kk;
+      bool ok;
+      split_k2<P>(4 * ks + q, o, kk, ok);
+      koff[ks] = ok ? o * MT * P2 + kk : -1;
+    }
+    double* dst = mom + (size_t)t.fout_rank[b] * P3;
+    grp_tiles<KS2>(
+        (MT * P + 7) / 8, (P + 7) / 8,
+        [&](int mt, int ks) {
+          const int m = mt * 8 + g, i = m / P, m2 = m - i * P;
+          return (koff[ks] >= 0 && i < MT) ? eta[koff[ks] + i * P2 + m2 * P] : 0.0;
+        },
+        [&](int nt, int ks) {
+          int o, kk;
+          bool ok;
+          split_k2<P>(4 * ks + q, o, kk, ok);
+          const int m3 = nt * 8 + g;
+          return (ok && m3 < P) ? sA[(o * P + m3) * P + kk] : 0.0;
+        },
+        [&](int mt, int nt, double v0, double v1) {
+          const int m = mt * 8 + g, i = m / P, m2 = m - i * P, n = nt * 8 + 2 * q;
+          if (i >= MT || m0 + i >= P) return;
+          // one writer per element: fire-and-forget reductions (RED), no read latency
+          double* row = dst + (size_t)(m0 + i) * P2 + m2 * P;
+          if (n < P) atomicAdd(row + n, v0);
+          if (n + 1 < P) atomicAdd(row + n + 1, v1);
+        },
+        NoPre{});
+  }
 }
 
 template <int P, int MT>
