@@ -148,6 +148,8 @@ static void alloc_eval_buffers(dmk_plan_s* P) {
     P->lam.alloc(P->nexp * pd, s);
     // fp32 tier (p <= 18, 3D): weighted incoming plane waves of every local box (k_pwshift)
     if (P->dim == 3 && T.p <= 18) P->pwt.alloc(P->nexp * P->phi_size1, s);
+    // symmetric near field (fp32 tier): one partial sum per same-level entry and target
+    if (P->dim == 3 && T.p <= 18) P->part.alloc(P->npart ? P->npart : 1, s);
     if (P->dim == 3 && T.p > 18 && pw64_group_env() && P->nexp > 1) P->pwt64.alloc(P->nexp * P->phi_size1, s);
   }
 }
@@ -246,6 +248,20 @@ int dmk_plan(int dim, int kernel, double eps, int64_t n, const double* points, i
   });
 }
 
+// Host charges: the H2D copy does not depend on the plan's build, so it goes to the
+// plan's root-box stream (idle between evaluations) and overlaps whatever of the build
+// the plan stream is still running when the caller gets here (dmk_plan returns without
+// a final synchronisation); the plan stream waits for the copy before the gather.
+static void upload_charges(dmk_plan_s* P, const double* charges, DevBuf<double>& dq) {
+  cudaStream_t s = P->stream, cs = P->root_stream ? P->root_stream : s;
+  dq.alloc(P->n, cs);
+  DMK_CUDA(cudaMemcpyAsync(dq.p, charges, P->n * sizeof(double), cudaMemcpyHostToDevice, cs));
+  if (cs != s) {
+    DMK_CUDA(cudaEventRecord(P->ev_fork, cs));
+    DMK_CUDA(cudaStreamWaitEvent(s, P->ev_fork, 0));
+  }
+}
+
 int dmk_eval(dmk_plan_t P, const double* charges, double* potentials, int mem) {
   return guard([&] {
     if (!P) fail(DMK_ERR_ARG, "plan is NULL");
@@ -254,9 +270,8 @@ int dmk_eval(dmk_plan_t P, const double* charges, double* potentials, int mem) {
     cudaStream_t s = P->stream;
     if (mem == DMK_MEM_HOST) {
       DevBuf<double> dq, du;
-      dq.alloc(P->n, s);
       du.alloc(P->n, s);
-      DMK_CUDA(cudaMemcpyAsync(dq.p, charges, P->n * sizeof(double), cudaMemcpyHostToDevice, s));
+      upload_charges(P, charges, dq);
       eval_plan(P, dq.p, du.p);
       DMK_CUDA(cudaMemcpyAsync(potentials, du.p, P->n * sizeof(double), cudaMemcpyDeviceToHost, s));
       DMK_CUDA(cudaStreamSynchronize(s));
@@ -275,8 +290,7 @@ int dmk_upward(dmk_plan_t P, const double* charges, int mem) {
     cudaStream_t s = P->stream;
     if (mem == DMK_MEM_HOST) {
       DevBuf<double> dq;
-      dq.alloc(P->n, s);
-      DMK_CUDA(cudaMemcpyAsync(dq.p, charges, P->n * sizeof(double), cudaMemcpyHostToDevice, s));
+      upload_charges(P, charges, dq);
       eval_upward(P, dq.p);
       DMK_CUDA(cudaStreamSynchronize(s));
     } else {

@@ -64,6 +64,15 @@ struct DevBuf {
   size_t bytes() const { return n * sizeof(T); }
 };
 
+// One same-level leaf pair (B, S) of the symmetric near field (kernels.cu k_p2p32s):
+// point ranges, the partial-sum slots of B's entry for S and S's entry for B (int64),
+// and c_B - c_S (exact fp32) with 1/r_L; S == B (nS < 0 marks it): one-sided
+struct SymTask {
+  int4 rng;         // bB, nB, bS, nS (nS = -nB: the leaf with itself)
+  longlong2 slot;   // slotB, slotS
+  float4 geo;       // c_B - c_S (x, y, z), 1/r_L
+};
+
 // ---------------------------------------------------------------- tables (Step 1)
 // Per-precision tables, computed on the host once and kept on the device.
 struct Tables {
@@ -127,7 +136,7 @@ struct dmk_plan_s {
   bool root_fixed = false;   // lo/side given by the caller (dmk_options.root)
   int min_level = 0;         // levels < min_level fully refined (dmk_options.min_level)
   int64_t n_targets = 0;     // the first n_targets caller points are targets (= n by default)
-  bool fast_sort = true;     // 3D: sort the top 32 key bits first (DMK_FULL_SORT=1: all 63)
+  bool fast_sort = true;     // 3D: sort the top 24 key bits first (DMK_FULL_SORT=1: all 63)
   int sorted_from_bit = 0;   // 0: keys fully sorted; else only bits >= this are ordered
 
   // sorted points (normalised coordinates in [0,1]^3) and permutation
@@ -148,6 +157,20 @@ struct dmk_plan_s {
   // direct lists (CSR over boxes)
   dmk::DevBuf<int32_t> dlist_off, dlist;
   int64_t ndlist = 0;
+  // symmetric near field (3D fp32 tier, kernels.cu k_p2p32s): per box the number of
+  // same-level entries (the list's prefix) and the first of its (entry, target)
+  // partial-sum slots; per entry its owner box; per box the first mixed-level entry
+  // (the queue form's range); the partial sums (fp32, one per same-level entry and
+  // target); the number of mixed-level entries
+  dmk::DevBuf<int32_t> dlist_same, dlist_owner, dlist_mbeg;
+  dmk::DevBuf<int64_t> part_off;
+  dmk::DevBuf<float> part;
+  int64_t npart = 0, nmixed = 0;
+  // the symmetric form's tasks (one per same-level leaf pair, S >= B), appended on the
+  // device (the count stays there: the kernel is persistent), capacity = same-level entries
+  dmk::DevBuf<dmk::SymTask> sym_tasks;
+  dmk::DevBuf<int32_t> sym_ntask;
+  int64_t sym_cap = 0;
   // work list for the P2P kernel: (leaf box, first target) items of <= 32 targets
   dmk::DevBuf<int32_t> p2p_items;
   int64_t np2p = 0;

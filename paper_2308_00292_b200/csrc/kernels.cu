@@ -2210,7 +2210,7 @@ __global__ void __launch_bounds__(32, P2PQ<K, KER, QC>::MINB) k_p2p32q(DevTree t
                                                const float4* __restrict__ boxc, const float4* __restrict__ src,
                                                const float4* __restrict__ srclo, ResPoly32 rp,
                                                const double* __restrict__ lvpoly, float lam, float tc,
-                                               double* __restrict__ unear) {
+                                               double* __restrict__ unear, const int32_t* __restrict__ dbeg) {
   constexpr int CHK = P2PQ<K, KER, QC>::CHK;
   // staged tile as 16 source pairs + slot 16, a permanent pad; slots past the tile's pairs
   // are pads too (a chargeless source at (4, 4, 4) r_L, outside every target's ball)
@@ -2262,8 +2262,9 @@ __global__ void __launch_bounds__(32, P2PQ<K, KER, QC>::MINB) k_p2p32q(DevTree t
     acc += (double)ap.x + (double)ap.y;
     qa = qa0;
   };
-  // ---- the list in batches of 32 entries: lane k holds entry e0 + k
-  const int e_beg = doff[B], e_end = doff[B + 1];
+  // ---- the list in batches of 32 entries: lane k holds entry e0 + k (dbeg: the
+  // list's suffix from dbeg[B], the mixed-level entries beside the symmetric form)
+  const int e_beg = dbeg ? dbeg[B] : doff[B], e_end = doff[B + 1];
   int eb = e_beg;   // first entry of the batch in registers
   int m_start = 0, m_end = 0, m_lev = 0;
   float4 m_c = cB;
@@ -2413,6 +2414,249 @@ __global__ void __launch_bounds__(32, P2PQ<K, KER, QC>::MINB) k_p2p32q(DevTree t
     for (int k = 0; k < f; ++k) u += red[lane + k * nt];
     unear[t0 + lane] = u;
   }
+}
+
+// ---- fp32 tier, symmetric form (the default).  R_L depends only on the source leaf's
+// level, so for two leaves B, S of the SAME level the pair (x, y)
+// contributes R_L(|x - y|) rho_y to u(x) and R_L(|x - y|) rho_x to u(y): one evaluation
+// serves both.  The same-level entries of a leaf's direct list are its colleague leaves
+// (the list's prefix, tree.cu); a warp takes one entry (B, S) with S > B (S < B: S's
+// warp does it) and evaluates every pair of B's and S's points once, densely -- the lanes
+// hold up to 32 points of one leaf, the other leaf's points are broadcast from shared
+// memory two at a time (packed fp32x2), the pairs outside the ball r < r_L weighted 0
+// (~16% of the pairs are inside; culling first costs more on a SIMT
+// machine, profiles/r02_p2p_nbr_experiments.md).  The lanes' side sums stay in registers;
+// the broadcast side's per-point sums are collected in 32 registers per lane and
+// reduced across the warp by a butterfly transpose (31 shuffles).  S == B (the leaf
+// itself) runs one-sided, with the r = 0 pair giving the Step 5 self term
+// -w m_L(-1).  Each (target, same-level entry) sum is an fp32
+// partial in its own slot (part), summed per target in list order by k_p2p_psum (fp64),
+// so the result does not depend on scheduling (bitwise deterministic).  Mixed-level
+// entries (adaptive trees) stay with the queue form k_p2p32q on the list's suffix.
+// Coordinates: the lane leaf's frame in units of r_L (exact scaling), the broadcast
+// points shifted in with TwoSum (double-single); as in the queue form (reading R16) u
+// comes from the high parts and a group of pairs where some pair is closer than
+// sqrt(tc) r_L is re-evaluated on the full double-single difference.
+constexpr int P2PS_NW = 4;
+template <int K, int KER>
+__global__ void __launch_bounds__(P2PS_NW * 32) k_p2p32s(const SymTask* __restrict__ tasks,
+                                                        const int32_t* __restrict__ ntask_p,
+                                                        const float4* __restrict__ src,
+                                                        const float4* __restrict__ srclo, ResPoly32 rp,
+                                                        const double* __restrict__ lvpoly, float lam, float tc,
+                                                        float* __restrict__ part) {
+  // per warp: 16 broadcast pair records (P0 = (x0, x1, y0, y1), P1 = (z0, z1, w0, w1)
+  // high parts, P2 = (x0, x1, y0, y1), P3 = (z0, z1, -, -) low parts; negated)
+  __shared__ float4 sbuf[P2PS_NW][4][16];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ntask = *ntask_p;
+  const int gw = blockIdx.x * P2PS_NW + warp, nwarps = gridDim.x * P2PS_NW;
+  float4* P0 = sbuf[warp][0];
+  float4* P1 = sbuf[warp][1];
+  float4* P2 = sbuf[warp][2];
+  float4* P3 = sbuf[warp][3];
+  float* f0 = reinterpret_cast<float*>(P0);
+  float* f1 = reinterpret_cast<float*>(P1);
+  float* f2 = reinterpret_cast<float*>(P2);
+  float* f3 = reinterpret_cast<float*>(P3);
+  float cf[K + 1];
+  int lev = -1;
+  if constexpr (KER != KER_YUKAWA) {
+#pragma unroll
+    for (int q = 0; q <= K; ++q) cf[q] = rp.a[q];
+  }
+  // persistent: the next task's record is loaded while this one runs
+  SymTask nx{};
+  if (gw < ntask) nx = tasks[gw];
+  for (int ti = gw; ti < ntask; ti += nwarps) {
+    const SymTask tk = nx;
+    if (ti + nwarps < ntask) nx = tasks[ti + nwarps];
+    const bool self = tk.rng.w < 0;
+    const int bB = tk.rng.x, nB = tk.rng.y, bS = tk.rng.z, nS = self ? nB : tk.rng.w;
+    const float irl = tk.geo.w;
+    if constexpr (KER == KER_YUKAWA) {   // the pair's level (both leaves): its residual polynomial
+      const int L = (__float_as_int(irl) >> 23) - 127;
+      if (L != lev) {
+        lev = L;
+#pragma unroll
+        for (int q = 0; q <= K; ++q) cf[q] = (float)__ldg(lvpoly + L * (K + 1) + q);
+      }
+    }
+    const float lamr = lam * __int_as_float(0x7F000000 - __float_as_int(irl));   // Yukawa: lambda r_L
+    const int64_t slotB = tk.slot.x, slotS = tk.slot.y;
+    const int ncB = (nB + 31) >> 5, ncS = (nS + 31) >> 5;
+    for (int cb = 0; cb < ncB; ++cb) {
+      float accS1 = 0.0f;   // one-sided (self): the lane's sum over all of B's chunks
+      for (int cs = 0; cs < ncS; ++cs) {
+        const int nb = min(32, nB - 32 * cb), ns = min(32, nS - 32 * cs);
+        // lanes take the larger chunk (one-sided: always B's targets)
+        const bool swap = !self && ns > nb;
+        const int nxp = swap ? ns : nb, ny = swap ? nb : ns;
+        const int gx = (swap ? bS + 32 * cs : bB + 32 * cb), gy = (swap ? bB + 32 * cb : bS + 32 * cs);
+        // c_X - c_Y
+        const float sgn = swap ? -1.0f : 1.0f;
+        const float dcx = sgn * tk.geo.x, dcy = sgn * tk.geo.y, dcz = sgn * tk.geo.z;
+        // the lane's point (target side), in units of r_L
+        const bool lv = lane < nxp;
+        const float4 th = src[gx + (lv ? lane : 0)], tl = srclo[gx + (lv ? lane : 0)];
+        const float2 xt = make_float2(th.x * irl, th.x * irl), yt = make_float2(th.y * irl, th.y * irl),
+                     zt = make_float2(th.z * irl, th.z * irl);
+        const float2 xtl = make_float2(tl.x * irl, tl.x * irl), ytl = make_float2(tl.y * irl, tl.y * irl),
+                     ztl = make_float2(tl.z * irl, tl.z * irl);
+        const float wi = lv ? th.w * irl : 0.0f;
+        // stage the broadcast chunk: -(y + c_Y - c_X) = (-y) + (c_X - c_Y), TwoSum'd
+        __syncwarp();
+        {
+          const int j = lane, h = j & 1, r = j >> 1;
+          // pads: far away (u > 1e10, never 0) and chargeless
+          float sx = 1e5f, sy = 1e5f, sz = 1e5f, lx = 0.0f, ly = 0.0f, lz = 0.0f, w = 0.0f;
+          if (j < ny) {
+            const float4 hi = src[gy + j], lo = srclo[gy + j];
+            float ex, ey, ez;
+            two_sum(-hi.x, dcx, sx, ex);
+            two_sum(-hi.y, dcy, sy, ey);
+            two_sum(-hi.z, dcz, sz, ez);
+            sx *= irl;
+            sy *= irl;
+            sz *= irl;
+            lx = (ex - lo.x) * irl;
+            ly = (ey - lo.y) * irl;
+            lz = (ez - lo.z) * irl;
+            w = hi.w * irl;
+          }
+          f0[4 * r + h] = sx;
+          f0[4 * r + 2 + h] = sy;
+          f1[4 * r + h] = sz;
+          f1[4 * r + 2 + h] = w;
+          f2[4 * r + h] = lx;
+          f2[4 * r + 2 + h] = ly;
+          f3[4 * r + h] = lz;
+          f3[4 * r + 2 + h] = 0.0f;
+        }
+        __syncwarp();
+        const int npy = (ny + 1) >> 1;
+        float2 accX = make_float2(0.0f, 0.0f);
+        float v[32];
+#pragma unroll
+        for (int k = 0; k < 32; ++k) v[k] = 0.0f;
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {   // groups of 4 pair records (8 points)
+          if (4 * g >= npy) break;
+          float2 u[4];
+          float4 Q[4];
+          bool close = false;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const int r = 4 * g + k;
+            const float4 A = P0[r];
+            Q[k] = P1[r];
+            const float2 dx = __fadd2_rn(xt, make_float2(A.x, A.y));
+            const float2 dy = __fadd2_rn(yt, make_float2(A.z, A.w));
+            const float2 dz = __fadd2_rn(zt, make_float2(Q[k].x, Q[k].y));
+            u[k] = __ffma2_rn(dx, dx, __ffma2_rn(dy, dy, __fmul2_rn(dz, dz)));
+            close |= fminf(u[k].x, u[k].y) < tc;
+          }
+          {   // no pair of the group inside any lane's ball (corner colleagues, mostly): next
+            const float um = fminf(fminf(fminf(u[0].x, u[0].y), fminf(u[1].x, u[1].y)),
+                                   fminf(fminf(u[2].x, u[2].y), fminf(u[3].x, u[3].y)));
+            if (!__any_sync(0xffffffffu, lv && um < 1.0f)) continue;
+          }
+          if (__any_sync(0xffffffffu, close)) {   // rare (always on the self chunk's diagonal)
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const int r = 4 * g + k;
+              const float4 A = P0[r], L = P2[r], Z = P3[r];
+              const float2 dx = __fadd2_rn(__fadd2_rn(xt, make_float2(A.x, A.y)), __fadd2_rn(xtl, make_float2(L.x, L.y)));
+              const float2 dy = __fadd2_rn(__fadd2_rn(yt, make_float2(A.z, A.w)), __fadd2_rn(ytl, make_float2(L.z, L.w)));
+              const float2 dz = __fadd2_rn(__fadd2_rn(zt, make_float2(Q[k].x, Q[k].y)), __fadd2_rn(ztl, make_float2(Z.x, Z.y)));
+              u[k] = __ffma2_rn(dx, dx, __ffma2_rn(dy, dy, __fmul2_rn(dz, dz)));
+            }
+          }
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const int r = 4 * g + k;
+            // R_L outside the ball is 0 (the mask folded into R); the lane's side gets
+            // w_y R, the broadcast side w_x R (pads and idle lanes have w = 0; an idle
+            // lane's own sum is not written)
+            const bool in0 = u[k].x < 1.0f, in1 = u[k].y < 1.0f;
+            const float2 uu = (K > 12) ? make_float2(fminf(u[k].x, 1.0f), fminf(u[k].y, 1.0f)) : u[k];
+            const float2 s2 = __ffma2_rn(uu, make_float2(2.0f, 2.0f), make_float2(-1.0f, -1.0f));
+            float2 pv = make_float2(cf[K], cf[K]);
+#pragma unroll
+            for (int q = K - 1; q >= 0; --q) pv = __ffma2_rn(pv, s2, make_float2(cf[q], cf[q]));
+            float k0v = rsqrt_approx(uu.x), k1v = rsqrt_approx(uu.y);
+            if constexpr (KER == KER_YUKAWA) {
+              k0v *= __expf(-lamr * uu.x * k0v);
+              k1v *= __expf(-lamr * uu.y * k1v);
+            }
+            float2 kv = make_float2(k0v, k1v);
+            // the leaf with itself: u below FLT_MIN (|x - y| < 1e-19 r_L, the r = 0 self
+            // pair) counts as coincident (two different leaves have no coincident pair)
+            if (self) kv = make_float2(uu.x >= 1.17549435e-38f ? k0v : 0.0f, uu.y >= 1.17549435e-38f ? k1v : 0.0f);
+            float2 R = __fadd2_rn(kv, make_float2(-pv.x, -pv.y));
+            R = make_float2(in0 ? R.x : 0.0f, in1 ? R.y : 0.0f);
+            accX = __ffma2_rn(make_float2(Q[k].z, Q[k].w), R, accX);
+            if (!self) {
+              const float2 vb = __fmul2_rn(make_float2(wi, wi), R);
+              v[2 * r] = vb.x;
+              v[2 * r + 1] = vb.y;
+            }
+          }
+        }
+        const float ax = accX.x + accX.y;
+        if (self) {
+          accS1 += ax;
+          continue;
+        }
+        // the broadcast side's sums: butterfly transpose-reduce, lane j gets point j's
+#pragma unroll
+        for (int sft = 16; sft >= 1; sft >>= 1) {
+          const bool up = lane & sft;
+#pragma unroll
+          for (int k = 0; k < sft; ++k) {
+            const float send = up ? v[k] : v[k + sft];
+            const float keep = up ? v[k + sft] : v[k];
+            v[k] = keep + __shfl_xor_sync(0xffffffffu, send, sft);
+          }
+        }
+        // slots: B-chunk cb's targets first written at cs = 0, S-chunk cs's at cb = 0
+        // (later chunk pairs add, in this fixed order)
+        const int64_t sx_ = swap ? slotS + 32 * cs : slotB + 32 * cb;
+        const int64_t sy_ = swap ? slotB + 32 * cb : slotS + 32 * cs;
+        const bool firstX = swap ? cb == 0 : cs == 0, firstY = swap ? cs == 0 : cb == 0;
+        if (lane < nxp) part[sx_ + lane] = firstX ? ax : part[sx_ + lane] + ax;
+        if (lane < ny) part[sy_ + lane] = firstY ? v[0] : part[sy_ + lane] + v[0];
+      }
+      if (self && lane < min(32, nB - 32 * cb)) part[slotB + 32 * cb + lane] = accS1;
+    }
+  }
+}
+
+// near-field sums per target: the same-level entries' partials in list order (fp64),
+// plus the queue form's mixed-level sum (already in unear) when there are mixed entries
+__global__ void k_p2p_psum(DevTree t, const int32_t* __restrict__ items, int64_t nitems,
+                           const int32_t* __restrict__ nsame, const int64_t* __restrict__ part_off,
+                           const float* __restrict__ part, bool mixed, double* __restrict__ unear) {
+  const int64_t it = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (it >= nitems) return;
+  const int B = items[2 * it], t0 = items[2 * it + 1];
+  const int b0 = t.start[B], nB = t.end[B] - b0, i = t0 - b0 + lane;
+  if (i >= nB || lane >= 32) return;
+  const int ns = nsame[B];
+  const float* pp = part + part_off[B] + i;
+  double u = 0.0;
+  int e = 0;
+  for (; e + 8 <= ns; e += 8) {   // 8 loads in flight, summed in list order
+    float v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = __ldg(pp + (int64_t)(e + k) * nB);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) u += (double)v[k];
+  }
+  for (; e < ns; ++e) u += (double)__ldg(pp + (int64_t)e * nB);
+  if (mixed) u += unear[b0 + i];
+  unear[b0 + i] = u;
 }
 
 template <int K, int KER>
@@ -2905,7 +3149,8 @@ static float p2p_tc() {
   return e ? (float)std::atof(e) : 0.0025f;   // r < 0.05 r_L
 }
 template <int KER, int QC>
-static void run_p2p32q_deg(dmk_plan_s* PL, const ResPoly& rp64, int K, cudaStream_t st) {
+static void run_p2p32q_deg(dmk_plan_s* PL, const ResPoly& rp64, int K, cudaStream_t st,
+                           const int32_t* dbeg = nullptr) {
   DevTree dt = dev_tree(PL);
   ResPoly32 rp{};
   for (int k = 0; k < 25; ++k) rp.a[k] = (float)rp64.a[k];
@@ -2916,7 +3161,7 @@ static void run_p2p32q_deg(dmk_plan_s* PL, const ResPoly& rp64, int K, cudaStrea
   case KK:                                                                                                 \
     k_p2p32q<KK, KER, QC><<<(unsigned)nb, 32, 0, st>>>(dt, PL->p2p_items.p, PL->np2p, PL->dlist_off.p,      \
                                                       PL->dlist.p, PL->box_c4.p, PL->xl4.p, PL->xl4lo.p, rp, \
-                                                      T.dRespoly, (float)T.lam, p2p_tc(), PL->unear.p);     \
+                                                      T.dRespoly, (float)T.lam, p2p_tc(), PL->unear.p, dbeg); \
     break;
   switch (K) {
     DMK_P2P_CASE(4) DMK_P2P_CASE(6) DMK_P2P_CASE(8) DMK_P2P_CASE(10) DMK_P2P_CASE(12) DMK_P2P_CASE(14)
@@ -2927,18 +3172,63 @@ static void run_p2p32q_deg(dmk_plan_s* PL, const ResPoly& rp64, int K, cudaStrea
   DMK_LAUNCH_CHECK();
 }
 template <int KER>
-static void run_p2p32q(dmk_plan_s* PL, const ResPoly& rp, int K, cudaStream_t st) {
+static void run_p2p32q(dmk_plan_s* PL, const ResPoly& rp, int K, cudaStream_t st, const int32_t* dbeg = nullptr) {
   const char* e = std::getenv("DMK_P2P_QC");
   const int qc = e ? std::atoi(e) : 32;
-  if (qc == 48) run_p2p32q_deg<KER, 48>(PL, rp, K, st);
-  else if (qc == 24) run_p2p32q_deg<KER, 24>(PL, rp, K, st);
-  else run_p2p32q_deg<KER, 32>(PL, rp, K, st);
+  if (qc == 48) run_p2p32q_deg<KER, 48>(PL, rp, K, st, dbeg);
+  else if (qc == 24) run_p2p32q_deg<KER, 24>(PL, rp, K, st, dbeg);
+  else run_p2p32q_deg<KER, 32>(PL, rp, K, st, dbeg);
 }
-static int p2p_form(const dmk_plan_s* PL) {   // 0 queue (default), 1 leaf (k_p2p32), 2 octant
+// symmetric form (default): same-level pairs once (k_p2p32s, one warp per direct-list
+// entry), the mixed-level suffixes by the queue form into unear, then the per-target
+// sums of the partials (k_p2p_psum)
+template <int KER>
+static void run_p2p32s(dmk_plan_s* PL, const ResPoly& rp64, int K, cudaStream_t st) {
+  DevTree dt = dev_tree(PL);
+  ResPoly32 rp{};
+  for (int k = 0; k < 25; ++k) rp.a[k] = (float)rp64.a[k];
+  if (PL->np2p == 0) return;
+  const Tables& T = *PL->tab;
+  if (PL->nmixed > 0) run_p2p32q<KER>(PL, rp64, K, st, PL->dlist_mbeg.p);
+  if (PL->sym_cap > 0) {
+    // persistent: enough warps to fill the SMs (the task count stays on the device);
+    // the SM count and occupancy are queried once per process and kernel
+    static thread_local int nsm = 0;
+    if (!nsm) {
+      int dev = 0;
+      DMK_CUDA(cudaGetDevice(&dev));
+      DMK_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    }
+#define DMK_P2P_CASE(KK)                                                                                      \
+  case KK: {                                                                                                  \
+    static thread_local int per = 0;                                                                          \
+    if (!per) DMK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_p2p32s<KK, KER>, P2PS_NW * 32, 0)); \
+    k_p2p32s<KK, KER><<<(unsigned)std::min<int64_t>((int64_t)nsm * std::max(per, 1),                        \
+                                                    (PL->sym_cap + P2PS_NW - 1) / P2PS_NW),                   \
+                        P2PS_NW * 32, 0, st>>>(PL->sym_tasks.p, PL->sym_ntask.p, PL->xl4.p, PL->xl4lo.p, rp,   \
+                                               T.dRespoly, (float)T.lam, p2p_tc(), PL->part.p);               \
+    break;                                                                                                    \
+  }
+    switch (K) {
+      DMK_P2P_CASE(4) DMK_P2P_CASE(6) DMK_P2P_CASE(8) DMK_P2P_CASE(10) DMK_P2P_CASE(12) DMK_P2P_CASE(14)
+      DMK_P2P_CASE(16) DMK_P2P_CASE(18) DMK_P2P_CASE(20) DMK_P2P_CASE(22) DMK_P2P_CASE(24)
+      default: fail(DMK_ERR_UNSUPPORTED, "residual polynomial degree out of range");
+    }
+#undef DMK_P2P_CASE
+    DMK_LAUNCH_CHECK();
+  }
+  k_p2p_psum<<<(unsigned)((PL->np2p + 3) / 4), 128, 0, st>>>(dt, PL->p2p_items.p, PL->np2p, PL->dlist_same.p,
+                                                            PL->part_off.p, PL->part.p, PL->nmixed > 0,
+                                                            PL->unear.p);
+  DMK_LAUNCH_CHECK();
+}
+// 0 symmetric (default), 1 leaf (k_p2p32), 2 octant (k_p2p32o), 3 queue (k_p2p32q)
+static int p2p_form(const dmk_plan_s* PL) {
   const char* e = std::getenv("DMK_P2P_FORM");
   if (!e) return 0;
   if (std::strcmp(e, "leaf") == 0) return 1;
   if (std::strcmp(e, "octant") == 0 && PL->np2p_o > 0) return 2;
+  if (std::strcmp(e, "queue") == 0) return 3;
   return 0;
 }
 
@@ -3025,13 +3315,15 @@ void eval_upward(dmk_plan_s* PL, const double* dcharges) {
     K = PL->tab->respoly_deg;
     if (form == 2) run_p2p32o_deg<KER_YUKAWA>(PL, rp, K, slo);
     else if (form == 1) run_p2p32_deg<KER_YUKAWA>(PL, rp, K, slo);
-    else if (form == 0) run_p2p32q<KER_YUKAWA>(PL, rp, K, slo);
+    else if (form == 3) run_p2p32q<KER_YUKAWA>(PL, rp, K, slo);
+    else if (form == 0) run_p2p32s<KER_YUKAWA>(PL, rp, K, slo);
     else if (full) run_p2p_deg<KER_YUKAWA, true>(PL, nullptr, rp, K, slo);
     else run_p2p_deg<KER_YUKAWA, false>(PL, nullptr, rp, K, slo);
   } else {
     if (form == 2) run_p2p32o_deg<KER_LAPLACE>(PL, rp, K, slo);
     else if (form == 1) run_p2p32_deg<KER_LAPLACE>(PL, rp, K, slo);
-    else if (form == 0) run_p2p32q<KER_LAPLACE>(PL, rp, K, slo);
+    else if (form == 3) run_p2p32q<KER_LAPLACE>(PL, rp, K, slo);
+    else if (form == 0) run_p2p32s<KER_LAPLACE>(PL, rp, K, slo);
     else if (full) run_p2p_deg<KER_LAPLACE, true>(PL, nullptr, rp, K, slo);
     else run_p2p_deg<KER_LAPLACE, false>(PL, nullptr, rp, K, slo);
   }

@@ -418,6 +418,7 @@ struct ReadIdx {   // by value
 __global__ void k_read_totals(const int32_t* __restrict__ fscan, const int32_t* __restrict__ escan, ReadIdx ri,
                               const int32_t* __restrict__ doff, const int32_t* __restrict__ poff,
                               const int32_t* __restrict__ poff_o, const unsigned long long* __restrict__ nleaf,
+                              const int64_t* __restrict__ part_off, const unsigned long long* __restrict__ same_tot,
                               int64_t nbox, int64_t* out) {
   const int i = threadIdx.x;
   if (i < ri.m) {
@@ -429,6 +430,8 @@ __global__ void k_read_totals(const int32_t* __restrict__ fscan, const int32_t* 
     out[2 * ri.m + 1] = poff[nbox];
     out[2 * ri.m + 2] = poff_o ? poff_o[nbox] : 0;
     out[2 * ri.m + 3] = nleaf ? (int64_t)*nleaf : 0;
+    out[2 * ri.m + 4] = part_off ? part_off[nbox] : 0;
+    out[2 * ri.m + 5] = same_tot ? (int64_t)*same_tot : 0;
   }
 }
 
@@ -601,17 +604,33 @@ __global__ void k_ranks_lists(const int32_t* __restrict__ fscan, const uint8_t* 
 
 // direct lists: pass 0 counts, pass 1 fills; one warp per box, lanes over the colleague
 // slots (and over the 3^D x 2^D fine-neighbour candidates), ballots for the positions
+// Outputs of the direct-list passes for the symmetric near field (kernels.cu,
+// k_p2p32s): per box the number of same-level entries (the list's prefix) and of
+// (entry, target) partial-sum slots they need (count pass, with the total of
+// same-level entries); per entry its owner box and per box the first mixed-level entry
+// (fill pass).  Null pointers: not wanted.
+struct NearAux {
+  int32_t* same = nullptr;
+  int64_t* slots = nullptr;
+  unsigned long long* same_tot = nullptr;
+  int32_t* owner = nullptr;
+  int32_t* mbeg = nullptr;
+};
 template <int D, bool FILL>
 __global__ void k_dlist(const int32_t* start, const int32_t* end, const int32_t* parent, const int32_t* child,
                         const int32_t* coll, const uint8_t* flags, const uint64_t* code, const int32_t* level,
-                        int64_t nbox, int32_t* cnt, const int32_t* off, int32_t* items) {
+                        int64_t nbox, int32_t* cnt, const int32_t* off, int32_t* items, NearAux aux) {
   constexpr int NCH = Dim<D>::NCH, NCOL = Dim<D>::NCOL;
   const int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (i >= nbox) return;
   const bool is_target = (flags[i] & 1) && end[i] > start[i];
   if (!is_target) {
-    if (!FILL && lane == 0) cnt[i] = 0;
+    if (!FILL && lane == 0) {
+      cnt[i] = 0;
+      if (aux.same) aux.same[i] = 0;
+      if (aux.slots) aux.slots[i] = 0;
+    }
     return;
   }
   const unsigned below = (1u << lane) - 1;
@@ -622,7 +641,22 @@ __global__ void k_dlist(const int32_t* start, const int32_t* end, const int32_t*
     int32_t s = lane < NCOL ? coll[NCOL * a + lane] : -1;
     const bool ok = s >= 0 && (flags[s] & 1) && end[s] > start[s];
     const unsigned m = __ballot_sync(0xffffffffu, ok);
-    if (FILL && ok) items[base + n_ + __popc(m & below)] = s;
+    if (FILL && ok) {
+      items[base + n_ + __popc(m & below)] = s;
+      if (aux.owner) aux.owner[base + n_ + __popc(m & below)] = (int32_t)i;
+    }
+    if (a == i && lane == 0) {
+      // the same-level entries (B's own colleague leaves) are the list's prefix: the
+      // symmetric near field takes them, the queue form the rest (mixed levels)
+      const int ns = __popc(m);
+      if (!FILL) {
+        if (aux.same) aux.same[i] = ns;
+        if (aux.slots) aux.slots[i] = (int64_t)ns * (end[i] - start[i]);
+        if (aux.same_tot) atomicAdd(aux.same_tot, (unsigned long long)ns);
+      } else if (aux.mbeg) {
+        aux.mbeg[i] = (int32_t)(base + ns);
+      }
+    }
     n_ += __popc(m);
     a = parent[a];
   }
@@ -645,10 +679,47 @@ __global__ void k_dlist(const int32_t* start, const int32_t* end, const int32_t*
       }
     }
     const unsigned m = __ballot_sync(0xffffffffu, ok);
-    if (FILL && ok) items[base + n_ + __popc(m & below)] = ch;
+    if (FILL && ok) {
+      items[base + n_ + __popc(m & below)] = ch;
+      if (aux.owner) aux.owner[base + n_ + __popc(m & below)] = (int32_t)i;
+    }
     n_ += __popc(m);
   }
   if (!FILL && lane == 0) cnt[i] = n_;
+}
+
+// Symmetric near-field tasks: one per same-level direct-list entry (B, S) with S >= B
+// (S < B is S's task), with S's entry for B found in S's same-level prefix; appended in
+// any order (each partial-sum slot is written by exactly one task, so the result does
+// not depend on it)
+__global__ void k_sym_tasks(const int32_t* __restrict__ owner, int64_t nent, const int32_t* __restrict__ doff,
+                            const int32_t* __restrict__ dlist, const int32_t* __restrict__ nsame,
+                            const int32_t* __restrict__ start, const int32_t* __restrict__ end,
+                            const int64_t* __restrict__ part_off, const float4* __restrict__ c4,
+                            SymTask* __restrict__ tasks, int32_t* __restrict__ ntask) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= nent) return;
+  const int B = owner[e];
+  const int eB = (int)(e - doff[B]);
+  if (eB >= nsame[B]) return;
+  const int S = dlist[e];
+  if (S < B) return;
+  int eS = eB;
+  if (S != B) {
+    const int32_t* ls = dlist + doff[S];
+    const int ns = nsame[S];
+    eS = -1;
+    for (int k = 0; k < ns; ++k)
+      if (ls[k] == B) eS = k;
+    if (eS < 0) __trap();   // colleague relations are symmetric: never
+  }
+  const int bB = start[B], nB = end[B] - bB, bS = start[S], nS = end[S] - bS;
+  const float4 cB = c4[B], cS = c4[S];
+  SymTask tk;
+  tk.rng = make_int4(bB, nB, bS, S == B ? -nB : nS);
+  tk.slot = make_longlong2(part_off[B] + (int64_t)eB * nB, part_off[S] + (int64_t)eS * nS);
+  tk.geo = make_float4(cB.x - cS.x, cB.y - cS.y, cB.z - cS.z, __int_as_float(0x7F000000 - __float_as_int(cB.w)));
+  tasks[atomicAdd(ntask, 1)] = tk;
 }
 
 // P2P work items: (leaf, first target) for every chunk of 32 targets
@@ -898,11 +969,11 @@ static void build_tree_d(dmk_plan_s* P, const double* dpts) {
     DMK_LAUNCH_CHECK();
     P->keys.alloc(n, s);
     P->perm.alloc(n, s);
-    // 3D: first the top 32 bits (4 radix passes instead of 8): levels <= 10 are sorted,
-    // which is all the tree needs unless a level-9 box must be refined (checked with the
+    // 3D: first the top 24 bits (3 radix passes instead of 8): levels <= 8 are sorted,
+    // which is all the tree needs unless a level-7 box must be refined (checked with the
     // level counts below; then the rest of the key is sorted too, stably, which composes
     // to the full stable sort of reading R5)
-    const int b0 = (D == 3 && P->fast_sort) ? D * NBITS - 32 : 0;
+    const int b0 = (D == 3 && P->fast_sort) ? D * NBITS - 24 : 0;
     P->sorted_from_bit = b0;
     cub_run(s, [&](void* t, size_t& b) {
       return cub::DeviceRadixSort::SortPairs(t, b, k0.p, P->keys.p, i0.p, P->perm.p, (int64_t)n, b0, D * NBITS, s);
@@ -948,9 +1019,9 @@ static void build_tree_d(dmk_plan_s* P, const double* dpts) {
     unsigned long long hc[LMAX];
     DMK_CUDA(cudaMemcpyAsync(hc, dcnt.p, sizeof(hc), cudaMemcpyDeviceToHost, s));
     DMK_CUDA(cudaStreamSynchronize(s));
-    if (P->sorted_from_bit > 0 && hc[9] > 0) {
-      // a level-9 box holds > n_s points: the tree may go below level 10, where the top
-      // 32 bits do not order the keys -- finish the stable sort and recount
+    if (P->sorted_from_bit > 0 && hc[7] > 0) {
+      // a level-7 box holds > n_s points: the tree may go below level 8, where the top
+      // 24 bits do not order the keys -- finish the stable sort and recount
       DevBuf<uint64_t> k1;
       DevBuf<int32_t> i1;
       k1.alloc(n, s);
@@ -1217,10 +1288,30 @@ static void build_tree_d(dmk_plan_s* P, const double* dpts) {
   poff.alloc(nbox + 1, s);
   DMK_CUDA(cudaMemsetAsync(dcnt.p, 0, (nbox + 1) * sizeof(int32_t), s));
   DMK_CUDA(cudaMemsetAsync(pcnt.p, 0, (nbox + 1) * sizeof(int32_t), s));
+  // symmetric near field (3D): same-level counts and partial-sum slots per box
+  DevBuf<int64_t> slots;
+  DevBuf<unsigned long long> same_tot;
+  NearAux aux{};
+  if (D == 3) {
+    P->dlist_same.alloc(nbox, s);
+    slots.alloc(nbox + 1, s);
+    same_tot.alloc(1, s);
+    DMK_CUDA(cudaMemsetAsync(slots.p + nbox, 0, sizeof(int64_t), s));
+    DMK_CUDA(cudaMemsetAsync(same_tot.p, 0, sizeof(unsigned long long), s));
+    aux.same = P->dlist_same.p;
+    aux.slots = slots.p;
+    aux.same_tot = same_tot.p;
+  }
   k_dlist<D, false><<<nblk(32 * nbox), TPB, 0, s>>>(P->box_start.p, P->box_end.p, P->box_parent.p, P->box_child.p,
                                                     P->box_coll.p, P->box_flags.p, P->box_code.p, P->box_level.p,
-                                                    nbox, dcnt.p, nullptr, nullptr);
+                                                    nbox, dcnt.p, nullptr, nullptr, aux);
   DMK_LAUNCH_CHECK();
+  if (D == 3) {
+    P->part_off.alloc(nbox + 1, s);
+    cub_run(s, [&](void* t, size_t& b) {
+      return cub::DeviceScan::ExclusiveSum(t, b, slots.p, P->part_off.p, (int64_t)(nbox + 1), s);
+    });
+  }
   k_p2p_count<<<nblk(nbox), TPB, 0, s>>>(P->box_start.p, P->box_end.p, P->box_flags.p, nbox, pcnt.p);
   DMK_LAUNCH_CHECK();
   P->dlist_off.alloc(nbox + 1, s);
@@ -1253,11 +1344,12 @@ static void build_tree_d(dmk_plan_s* P, const double* dpts) {
     ri.v[nlevels] = nbox;
     ri.m = m;
     DevBuf<int64_t> dout;
-    dout.alloc(2 * m + 4, s);
+    dout.alloc(2 * m + 6, s);
     k_read_totals<<<1, 64, 0, s>>>(fscan.p, escan.p, ri, P->dlist_off.p, poff.p, build_oct ? ooff.p : nullptr,
-                                   build_oct ? nleaf.p : nullptr, nbox, dout.p);
+                                   build_oct ? nleaf.p : nullptr, D == 3 ? P->part_off.p : nullptr,
+                                   D == 3 ? same_tot.p : nullptr, nbox, dout.p);
     DMK_LAUNCH_CHECK();
-    std::vector<int64_t> h(2 * m + 4);
+    std::vector<int64_t> h(2 * m + 6);
     DMK_CUDA(cudaMemcpyAsync(h.data(), dout.p, h.size() * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     DMK_CUDA(cudaStreamSynchronize(s));
     P->nfout = h[nlevels];
@@ -1272,12 +1364,21 @@ static void build_tree_d(dmk_plan_s* P, const double* dpts) {
     P->np2p = h[2 * m + 1];
     P->np2p_o = h[2 * m + 2];
     P->nleaf_t = h[2 * m + 3];
+    P->npart = h[2 * m + 4];
+    P->nmixed = P->ndlist - h[2 * m + 5];
   }
   mark("flags");
   P->dlist.alloc(P->ndlist ? P->ndlist : 1, s);
+  NearAux faux{};
+  if (D == 3) {
+    P->dlist_owner.alloc(P->ndlist ? P->ndlist : 1, s);
+    P->dlist_mbeg.alloc(nbox, s);
+    faux.owner = P->dlist_owner.p;
+    faux.mbeg = P->dlist_mbeg.p;
+  }
   k_dlist<D, true><<<nblk(32 * nbox), TPB, 0, s>>>(P->box_start.p, P->box_end.p, P->box_parent.p, P->box_child.p,
                                                    P->box_coll.p, P->box_flags.p, P->box_code.p, P->box_level.p,
-                                                   nbox, nullptr, P->dlist_off.p, P->dlist.p);
+                                                   nbox, nullptr, P->dlist_off.p, P->dlist.p, faux);
   DMK_LAUNCH_CHECK();
   mark("dlists");
   P->p2p_items.alloc(2 * (P->np2p ? P->np2p : 1), s);
@@ -1292,6 +1393,16 @@ static void build_tree_d(dmk_plan_s* P, const double* dpts) {
     P->box_c4.alloc(nbox, s);
     k_box_c4<<<nblk(nbox), TPB, 0, s>>>(P->box_code.p, P->box_level.p, nbox, P->box_c4.p);
     DMK_LAUNCH_CHECK();
+    P->sym_cap = P->ndlist - P->nmixed;   // the same-level entries
+    P->sym_tasks.alloc(P->sym_cap ? P->sym_cap : 1, s);
+    P->sym_ntask.alloc(1, s);
+    DMK_CUDA(cudaMemsetAsync(P->sym_ntask.p, 0, sizeof(int32_t), s));
+    if (P->ndlist) {
+      k_sym_tasks<<<nblk(P->ndlist), TPB, 0, s>>>(P->dlist_owner.p, P->ndlist, P->dlist_off.p, P->dlist.p,
+                                                  P->dlist_same.p, P->box_start.p, P->box_end.p, P->part_off.p,
+                                                  P->box_c4.p, P->sym_tasks.p, P->sym_ntask.p);
+      DMK_LAUNCH_CHECK();
+    }
     P->xl4.alloc(n ? n : 1, s);
     P->xl4lo.alloc(n ? n : 1, s);
     k_leaf_local4<<<nblk(32 * nbox), TPB, 0, s>>>(P->box_code.p, P->box_level.p, P->box_start.p, P->box_end.p,

@@ -67,7 +67,7 @@ def case(request):
 def same_points_per_leaf(perm, T):
     """The device's point order: a permutation that puts every leaf's points in the
     leaf's range.  Within a leaf the order is free (the paper fixes none; the device
-    sorts by the top 32 Morton bits when the tree ends above level 10, R5)."""
+    sorts by the top 24 Morton bits when the tree ends above level 8, R5)."""
     assert np.array_equal(np.sort(perm), np.arange(len(T.perm)))
     for i in np.nonzero(T.box_leaf)[0]:
         a, b = T.box_start[i], T.box_end[i]
@@ -101,8 +101,8 @@ def test_tree_bit_exact(case):
 
 def test_full_sort_order_bit_exact(monkeypatch):
     """DMK_FULL_SORT=1: the stable sort by the whole 63-bit key (reading R5) -- the device's
-    permutation equals the oracle's element by element; the default (top 32 bits first,
-    the rest only when a level-9 box needs refinement) gives the same tree."""
+    permutation equals the oracle's element by element; the default (top 24 bits first,
+    the rest only when a level-7 box needs refinement) gives the same tree."""
     x, q = dmk_inputs.make("sphere", 8000, seed=21)
     T = Tree(x, 60)
     monkeypatch.setenv("DMK_FULL_SORT", "1")
@@ -310,16 +310,19 @@ def test_linearity():
 
 @pytest.mark.parametrize("kernel", ["laplace", "yukawa"])
 def test_p2p_forms_agree(kernel, monkeypatch):
-    """The three fp32-tier near-field kernels: the queue form (default, k_p2p32q), the
-    per-pair form (k_p2p32, DMK_P2P_FORM=leaf) and the Sec. 3.4 form (octant work items,
-    source octants culled by their distance to the target octant, PAPER.md:1362-1391,
+    """The four fp32-tier near-field kernels: the symmetric form (default, k_p2p32s:
+    same-level leaf pairs evaluated once for both leaves, mixed-level entries by the
+    queue form), the queue form (k_p2p32q, DMK_P2P_FORM=queue), the per-pair form
+    (k_p2p32, DMK_P2P_FORM=leaf) and the Sec. 3.4 form (octant work items, source octants
+    culled by their distance to the target octant, PAPER.md:1362-1391,
     DMK_P2P_FORM=octant) against each other and the direct sum: culled pairs have
     r >= r_L where R_L = 0 (1/r; Yukawa culls r >= r_L in every form, reading R13), so the
-    forms agree to fp32 summation order."""
+    forms agree to fp32 summation order.  The clustered input has leaves at many levels,
+    so every form's mixed-level entries are exercised."""
     x, q = dmk_inputs.clusters(30000, seed=31)
     lam = 10.0 if kernel == "yukawa" else 0.0
     res = {}
-    for form in ("queue", "leaf", "octant"):
+    for form in ("sym", "queue", "leaf", "octant"):
         monkeypatch.setenv("DMK_P2P_FORM", form)
         plan = dmk.dmk_plan(cuda(x), eps=1e-6, leaf_capacity=200, kernel=kernel, lam=lam)
         u = plan.eval(cuda(q)).cpu().numpy()
@@ -327,10 +330,37 @@ def test_p2p_forms_agree(kernel, monkeypatch):
         plan.close()
     ref = direct.yukawa3d(x, q, lam) if kernel == "yukawa" else direct.laplace3d(x, q)
     nl = res["leaf"][1]
-    for form in ("queue", "octant"):
+    for form in ("sym", "queue", "octant"):
         u, nf = res[form]
         assert np.max(np.abs(nf - nl)) <= 1e-6 * np.max(np.abs(nl)), form
         assert direct.rel_l2(u, ref) <= 2e-6, form
+
+
+@pytest.mark.parametrize("kernel", ["laplace", "yukawa"])
+@pytest.mark.parametrize("cap", [20, 50, 300])
+def test_p2p_symmetric_chunks(kernel, cap, monkeypatch):
+    """The symmetric form evaluates the same-level leaf pairs in chunks of 32 points per
+    leaf (the larger chunk on the lanes, the other broadcast): leaf capacities 20, 50 and
+    300 give single chunks, 2-chunk leaves and leaves of up to 10 chunks, on a uniform
+    cloud (all entries same-level) and on clusters (mixed levels: the queue form takes
+    the list suffixes).  The near field equals the per-pair form's to fp32 summation
+    order and the potential is within 2 eps of the direct sum at sampled targets."""
+    lam = 10.0 if kernel == "yukawa" else 0.0
+    for kind in ("uniform", "clusters"):
+        x, q = dmk_inputs.make(kind, 40000, seed=34)
+        res = {}
+        for form in ("sym", "leaf"):
+            monkeypatch.setenv("DMK_P2P_FORM", form)
+            plan = dmk.dmk_plan(cuda(x), eps=1e-6, leaf_capacity=cap, kernel=kernel, lam=lam)
+            u = plan.eval(cuda(q)).cpu().numpy()
+            res[form] = (u, plan.stage("unear"))
+            plan.close()
+        nl = res["leaf"][1]
+        assert np.max(np.abs(res["sym"][1] - nl)) <= 1e-6 * np.max(np.abs(nl)), kind
+        idx = np.random.default_rng(3).choice(x.shape[0], 300, replace=False)
+        ref = (direct.yukawa3d(x, q, lam, targets=x[idx]) if kernel == "yukawa"
+               else direct.laplace3d(x, q, targets=x[idx]))
+        assert direct.rel_l2(res["sym"][0][idx], ref) <= 2e-6, kind
 
 
 @pytest.mark.parametrize("qc", ["24", "32", "48"])
