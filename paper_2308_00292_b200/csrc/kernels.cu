@@ -2471,8 +2471,8 @@ __global__ void __launch_bounds__(P2PS_NW * 32) k_p2p32s(const SymTask* __restri
   for (int ti = gw; ti < ntask; ti += nwarps) {
     const SymTask tk = nx;
     if (ti + nwarps < ntask) nx = tasks[ti + nwarps];
-    const bool self = tk.rng.w < 0;
-    const int bB = tk.rng.x, nB = tk.rng.y, bS = tk.rng.z, nS = self ? nB : tk.rng.w;
+    const bool self_task = tk.rng.w < 0;
+    const int bB = tk.rng.x, nB = tk.rng.y, bS = tk.rng.z, nS = self_task ? nB : tk.rng.w;
     const float irl = tk.geo.w;
     if constexpr (KER == KER_YUKAWA) {   // the pair's level (both leaves): its residual polynomial
       const int L = (__float_as_int(irl) >> 23) - 127;
@@ -2485,9 +2485,10 @@ __global__ void __launch_bounds__(P2PS_NW * 32) k_p2p32s(const SymTask* __restri
     const float lamr = lam * __int_as_float(0x7F000000 - __float_as_int(irl));   // Yukawa: lambda r_L
     const int64_t slotB = tk.slot.x, slotS = tk.slot.y;
     const int ncB = (nB + 31) >> 5, ncS = (nS + 31) >> 5;
-    for (int cb = 0; cb < ncB; ++cb) {
-      float accS1 = 0.0f;   // one-sided (self): the lane's sum over all of B's chunks
-      for (int cs = 0; cs < ncS; ++cs) {
+    // one chunk pair (B chunk cb, S chunk cs); SELF: the leaf with itself, one-sided
+    auto chunk_pair = [&](auto self_, int cb, int cs, float& accS1) {
+      constexpr bool self = decltype(self_)::value;
+      {
         const int nb = min(32, nB - 32 * cb), ns = min(32, nS - 32 * cs);
         // lanes take the larger chunk (one-sided: always B's targets)
         const bool swap = !self && ns > nb;
@@ -2536,9 +2537,9 @@ __global__ void __launch_bounds__(P2PS_NW * 32) k_p2p32s(const SymTask* __restri
         __syncwarp();
         const int npy = (ny + 1) >> 1;
         float2 accX = make_float2(0.0f, 0.0f);
+        // the broadcast points' terms; columns of pads and of records past the chunk are
+        // never read back (a column's butterfly sum lands in its own lane only)
         float v[32];
-#pragma unroll
-        for (int k = 0; k < 32; ++k) v[k] = 0.0f;
 #pragma unroll
         for (int g = 0; g < 4; ++g) {   // groups of 4 pair records (8 points)
           if (4 * g >= npy) break;
@@ -2559,7 +2560,13 @@ __global__ void __launch_bounds__(P2PS_NW * 32) k_p2p32s(const SymTask* __restri
           {   // no pair of the group inside any lane's ball (corner colleagues, mostly): next
             const float um = fminf(fminf(fminf(u[0].x, u[0].y), fminf(u[1].x, u[1].y)),
                                    fminf(fminf(u[2].x, u[2].y), fminf(u[3].x, u[3].y)));
-            if (!__any_sync(0xffffffffu, lv && um < 1.0f)) continue;
+            if (!__any_sync(0xffffffffu, lv && um < 1.0f)) {
+              if (!self) {
+#pragma unroll
+                for (int c = 0; c < 8; ++c) v[8 * g + c] = 0.0f;
+              }
+              continue;
+            }
           }
           if (__any_sync(0xffffffffu, close)) {   // rare (always on the self chunk's diagonal)
 #pragma unroll
@@ -2606,7 +2613,7 @@ __global__ void __launch_bounds__(P2PS_NW * 32) k_p2p32s(const SymTask* __restri
         const float ax = accX.x + accX.y;
         if (self) {
           accS1 += ax;
-          continue;
+          return;
         }
         // the broadcast side's sums: butterfly transpose-reduce, lane j gets point j's
 #pragma unroll
@@ -2627,7 +2634,15 @@ __global__ void __launch_bounds__(P2PS_NW * 32) k_p2p32s(const SymTask* __restri
         if (lane < nxp) part[sx_ + lane] = firstX ? ax : part[sx_ + lane] + ax;
         if (lane < ny) part[sy_ + lane] = firstY ? v[0] : part[sy_ + lane] + v[0];
       }
-      if (self && lane < min(32, nB - 32 * cb)) part[slotB + 32 * cb + lane] = accS1;
+    };
+    for (int cb = 0; cb < ncB; ++cb) {
+      float accS1 = 0.0f;   // one-sided (self): the lane's sum over all of B's chunks
+      if (self_task) {
+        for (int cs = 0; cs < ncS; ++cs) chunk_pair(std::true_type{}, cb, cs, accS1);
+        if (lane < min(32, nB - 32 * cb)) part[slotB + 32 * cb + lane] = accS1;
+      } else {
+        for (int cs = 0; cs < ncS; ++cs) chunk_pair(std::false_type{}, cb, cs, accS1);
+      }
     }
   }
 }
