@@ -159,10 +159,11 @@ struct dmk_plan_s {
   int64_t ndlist = 0;
   // symmetric near field (3D fp32 tier, kernels.cu k_p2p32s): per box the number of
   // same-level entries (the list's prefix) and the first of its (entry, target)
-  // partial-sum slots; per entry its owner box; per box the first mixed-level entry
-  // (the queue form's range); the partial sums (fp32, one per same-level entry and
-  // target); the number of mixed-level entries
-  dmk::DevBuf<int32_t> dlist_same, dlist_owner, dlist_mbeg;
+  // partial-sum slots; per box the first mixed-level entry (the queue form's range);
+  // the partial sums (fp32, one per same-level entry and target); the number of
+  // mixed-level entries
+  dmk::DevBuf<int32_t> dlist_same, dlist_mbeg;
+  dmk::DevBuf<uint32_t> dlist_cmask;   // per box: its non-empty leaf colleagues (bit = slot)
   dmk::DevBuf<int64_t> part_off;
   dmk::DevBuf<float> part;
   int64_t npart = 0, nmixed = 0;

@@ -604,6 +604,12 @@ __global__ void k_ranks_lists(const int32_t* __restrict__ fscan, const uint8_t* 
 
 // direct lists: pass 0 counts, pass 1 fills; one warp per box, lanes over the colleague
 // slots (and over the 3^D x 2^D fine-neighbour candidates), ballots for the positions
+// box centre and side in fp32 (exact: dyadic, level <= 20): (c_x, c_y, c_z, 2^-l)
+__device__ __forceinline__ float4 box_c4f(uint64_t c, int l) {
+  const float sd = ldexpf(1.0f, -l);
+  return make_float4(((float)compact3d(c >> 2) + 0.5f) * sd, ((float)compact3d(c >> 1) + 0.5f) * sd,
+                     ((float)compact3d(c) + 0.5f) * sd, sd);
+}
 // Outputs of the direct-list passes for the symmetric near field (kernels.cu,
 // k_p2p32s): per box the number of same-level entries (the list's prefix) and of
 // (entry, target) partial-sum slots they need (count pass, with the total of
@@ -613,8 +619,12 @@ struct NearAux {
   int32_t* same = nullptr;
   int64_t* slots = nullptr;
   unsigned long long* same_tot = nullptr;
+  uint32_t* cmask = nullptr;        // per box: bit k = colleague k is a non-empty leaf (count pass)
   int32_t* owner = nullptr;
   int32_t* mbeg = nullptr;
+  SymTask* tasks = nullptr;         // fill pass: the symmetric tasks (S >= B), appended
+  int32_t* ntask = nullptr;
+  const int64_t* part_off = nullptr;
 };
 template <int D, bool FILL>
 __global__ void k_dlist(const int32_t* start, const int32_t* end, const int32_t* parent, const int32_t* child,
@@ -645,11 +655,39 @@ __global__ void k_dlist(const int32_t* start, const int32_t* end, const int32_t*
       items[base + n_ + __popc(m & below)] = s;
       if (aux.owner) aux.owner[base + n_ + __popc(m & below)] = (int32_t)i;
     }
+    if constexpr (FILL && D == 3) {
+      if (a == i && aux.tasks) {
+        // symmetric near-field tasks: colleague k = S (a non-empty leaf of B's level)
+        // with S >= B; B is S's colleague 26 - k, so its entry in S's list is the number
+        // of S's leaf colleagues before that slot
+        const bool tk = ok && s >= (int32_t)i;
+        const unsigned tm = __ballot_sync(0xffffffffu, tk);
+        int pos = 0;
+        if (tm) {
+          int b0 = 0;
+          if (lane == __ffs(tm) - 1) b0 = atomicAdd(aux.ntask, __popc(tm));
+          pos = __shfl_sync(0xffffffffu, b0, __ffs(tm) - 1) + __popc(tm & below);
+        }
+        if (tk) {
+          const int eB = __popc(m & below);
+          const int eS = s == (int32_t)i ? eB : __popc(aux.cmask[s] & ((1u << (26 - lane)) - 1u));
+          const int bB = start[i], nB = end[i] - bB, bS = start[s], nS = end[s] - bS;
+          const float4 cB = box_c4f(code[i], level[i]), cS = box_c4f(code[s], level[s]);
+          SymTask t;
+          t.rng = make_int4(bB, nB, bS, s == (int32_t)i ? -nB : nS);
+          t.slot = make_longlong2(aux.part_off[i] + (int64_t)eB * nB, aux.part_off[s] + (int64_t)eS * nS);
+          t.geo = make_float4(cB.x - cS.x, cB.y - cS.y, cB.z - cS.z,
+                              __int_as_float(0x7F000000 - __float_as_int(cB.w)));
+          aux.tasks[pos] = t;
+        }
+      }
+    }
     if (a == i && lane == 0) {
       // the same-level entries (B's own colleague leaves) are the list's prefix: the
       // symmetric near field takes them, the queue form the rest (mixed levels)
       const int ns = __popc(m);
       if (!FILL) {
+        if (aux.cmask) aux.cmask[i] = m;
         if (aux.same) aux.same[i] = ns;
         if (aux.slots) aux.slots[i] = (int64_t)ns * (end[i] - start[i]);
         if (aux.same_tot) atomicAdd(aux.same_tot, (unsigned long long)ns);
@@ -686,40 +724,6 @@ __global__ void k_dlist(const int32_t* start, const int32_t* end, const int32_t*
     n_ += __popc(m);
   }
   if (!FILL && lane == 0) cnt[i] = n_;
-}
-
-// Symmetric near-field tasks: one per same-level direct-list entry (B, S) with S >= B
-// (S < B is S's task), with S's entry for B found in S's same-level prefix; appended in
-// any order (each partial-sum slot is written by exactly one task, so the result does
-// not depend on it)
-__global__ void k_sym_tasks(const int32_t* __restrict__ owner, int64_t nent, const int32_t* __restrict__ doff,
-                            const int32_t* __restrict__ dlist, const int32_t* __restrict__ nsame,
-                            const int32_t* __restrict__ start, const int32_t* __restrict__ end,
-                            const int64_t* __restrict__ part_off, const float4* __restrict__ c4,
-                            SymTask* __restrict__ tasks, int32_t* __restrict__ ntask) {
-  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (e >= nent) return;
-  const int B = owner[e];
-  const int eB = (int)(e - doff[B]);
-  if (eB >= nsame[B]) return;
-  const int S = dlist[e];
-  if (S < B) return;
-  int eS = eB;
-  if (S != B) {
-    const int32_t* ls = dlist + doff[S];
-    const int ns = nsame[S];
-    eS = -1;
-    for (int k = 0; k < ns; ++k)
-      if (ls[k] == B) eS = k;
-    if (eS < 0) __trap();   // colleague relations are symmetric: never
-  }
-  const int bB = start[B], nB = end[B] - bB, bS = start[S], nS = end[S] - bS;
-  const float4 cB = c4[B], cS = c4[S];
-  SymTask tk;
-  tk.rng = make_int4(bB, nB, bS, S == B ? -nB : nS);
-  tk.slot = make_longlong2(part_off[B] + (int64_t)eB * nB, part_off[S] + (int64_t)eS * nS);
-  tk.geo = make_float4(cB.x - cS.x, cB.y - cS.y, cB.z - cS.z, __int_as_float(0x7F000000 - __float_as_int(cB.w)));
-  tasks[atomicAdd(ntask, 1)] = tk;
 }
 
 // P2P work items: (leaf, first target) for every chunk of 32 targets
@@ -1294,11 +1298,13 @@ static void build_tree_d(dmk_plan_s* P, const double* dpts) {
   NearAux aux{};
   if (D == 3) {
     P->dlist_same.alloc(nbox, s);
+    P->dlist_cmask.alloc(nbox, s);
     slots.alloc(nbox + 1, s);
     same_tot.alloc(1, s);
     DMK_CUDA(cudaMemsetAsync(slots.p + nbox, 0, sizeof(int64_t), s));
     DMK_CUDA(cudaMemsetAsync(same_tot.p, 0, sizeof(unsigned long long), s));
     aux.same = P->dlist_same.p;
+    aux.cmask = P->dlist_cmask.p;
     aux.slots = slots.p;
     aux.same_tot = same_tot.p;
   }
@@ -1371,10 +1377,16 @@ static void build_tree_d(dmk_plan_s* P, const double* dpts) {
   P->dlist.alloc(P->ndlist ? P->ndlist : 1, s);
   NearAux faux{};
   if (D == 3) {
-    P->dlist_owner.alloc(P->ndlist ? P->ndlist : 1, s);
     P->dlist_mbeg.alloc(nbox, s);
-    faux.owner = P->dlist_owner.p;
     faux.mbeg = P->dlist_mbeg.p;
+    P->sym_cap = P->ndlist - P->nmixed;   // the same-level entries (tasks: about half)
+    P->sym_tasks.alloc(P->sym_cap ? P->sym_cap : 1, s);
+    P->sym_ntask.alloc(1, s);
+    DMK_CUDA(cudaMemsetAsync(P->sym_ntask.p, 0, sizeof(int32_t), s));
+    faux.cmask = P->dlist_cmask.p;
+    faux.tasks = P->sym_tasks.p;
+    faux.ntask = P->sym_ntask.p;
+    faux.part_off = P->part_off.p;
   }
   k_dlist<D, true><<<nblk(32 * nbox), TPB, 0, s>>>(P->box_start.p, P->box_end.p, P->box_parent.p, P->box_child.p,
                                                    P->box_coll.p, P->box_flags.p, P->box_code.p, P->box_level.p,
@@ -1393,16 +1405,7 @@ static void build_tree_d(dmk_plan_s* P, const double* dpts) {
     P->box_c4.alloc(nbox, s);
     k_box_c4<<<nblk(nbox), TPB, 0, s>>>(P->box_code.p, P->box_level.p, nbox, P->box_c4.p);
     DMK_LAUNCH_CHECK();
-    P->sym_cap = P->ndlist - P->nmixed;   // the same-level entries
-    P->sym_tasks.alloc(P->sym_cap ? P->sym_cap : 1, s);
-    P->sym_ntask.alloc(1, s);
-    DMK_CUDA(cudaMemsetAsync(P->sym_ntask.p, 0, sizeof(int32_t), s));
-    if (P->ndlist) {
-      k_sym_tasks<<<nblk(P->ndlist), TPB, 0, s>>>(P->dlist_owner.p, P->ndlist, P->dlist_off.p, P->dlist.p,
-                                                  P->dlist_same.p, P->box_start.p, P->box_end.p, P->part_off.p,
-                                                  P->box_c4.p, P->sym_tasks.p, P->sym_ntask.p);
-      DMK_LAUNCH_CHECK();
-    }
+
     P->xl4.alloc(n ? n : 1, s);
     P->xl4lo.alloc(n ? n : 1, s);
     k_leaf_local4<<<nblk(32 * nbox), TPB, 0, s>>>(P->box_code.p, P->box_level.p, P->box_start.p, P->box_end.p,

@@ -8,6 +8,6 @@ python scripts/prof_step.py --reps 2 > gpurun_out/r02_plain_$T.log 2>&1
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r02_launches_$T.csv \
     python scripts/prof_step.py --reps 2 > gpurun_out/r02_ncu_launch_$T.log 2>&1
 DMK_SERIAL=1 ncu --set full --clock-control none --import-source on \
-    -k "regex:k_p2p32|k_anterp|k_eval|k_pwshift|k_pw2poly32|k_prox2pw32|k_c2p_grp|k_p2c_grp" -c 24 \
+    -k "regex:k_p2p32|k_p2p_psum|k_anterp|k_eval|k_pwshift|k_pw2poly32|k_prox2pw32|k_c2p_grp|k_p2c_grp" -c 24 \
     -o gpurun_out/r02_prof_$T python scripts/prof_step.py --reps 1 > gpurun_out/r02_ncu_full_$T.log 2>&1
 tail -3 gpurun_out/r02_bench_$T.err
