@@ -56,6 +56,17 @@ __device__ __forceinline__ void cheb_vec(double x, double* T, int P, double scal
   }
 }
 
+// ---------------------------------------------------------------- asynchronous global -> shared copies
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
 // ---------------------------------------------------------------- fp64 tensor-core (DMMA) versions
 // mma.sync.m8n8k4 f64: A[row=lane>>2][col=lane&3], B[row=lane&3][col=lane>>2],
 // C[row=lane>>2][col=2*(lane&3)+{0,1}].  Measured on this B200: 37.2 TFLOP/s, the

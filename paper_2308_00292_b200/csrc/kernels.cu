@@ -1492,6 +1492,340 @@ __global__ void __launch_bounds__(PWS64_NT, 2)
     }
 }
 
+// ---- Parent-group translation staged through shared memory (both tiers; TT = the
+// plane-wave storage type, float for p <= 18, double for p = 28).  The same window sums
+// as k_pwshift / k_pwshift64 (Eq. 3.39, separable per-axis rotations by 2 pi m_d delta_d
+// / 3), over chunks of MC modes of one slab a, in two passes:
+//   ZY: a thread owns (w1, pi1, mode i) and walks w2 = 0..3: it loads the 16 values
+//       F[w1 w2 w3][pi1 pi2 pi3][m] (w3, pi2, pi3), sums the Z taps over w3 for both
+//       children o3 in registers and accumulates the Y taps into Y[o2][o3][pi2 pi3];
+//       the 16 results go to YS[w1 o2 o3][pi][MC] (shared, double buffered by chunk);
+//   X:  a thread owns (child o, pi2 pi3, i): the three w1 taps from YS, the weights,
+//       T (global).
+// One barrier per chunk.  The three taps of an axis combine as  R(+1) g_l + g_m + R(-1) g_r
+// for a child with window rows (l, m, r) = (o, o + 1, o + 2)  (delta = o + 1 - w).
+template <class TT>
+__device__ __forceinline__ void rot3(TT l0, TT l1, TT m0, TT m1, TT r0, TT r1, TT C, TT S, TT& o0, TT& o1) {
+  const TT s0 = l0 + r0, s1 = l1 + r1, d0 = l0 - r0, d1 = l1 - r1;
+  o0 = C * s0 + (m0 - S * d1);
+  o1 = C * s1 + (m1 + S * d0);
+}
+template <int DELTA, class TT>
+__device__ __forceinline__ void racc(TT& a0, TT& a1, TT g0, TT g1, TT C, TT S) {
+  if (DELTA == 0) {
+    a0 += g0;
+    a1 += g1;
+  } else if (DELTA > 0) {
+    a0 += C * g0 - S * g1;
+    a1 += S * g0 + C * g1;
+  } else {
+    a0 += C * g0 + S * g1;
+    a1 += C * g1 - S * g0;
+  }
+}
+template <class TT>
+__device__ __forceinline__ void rcs(int m, TT& C, TT& S) {
+  const int e = m % 3;   // angle 2 pi m / 3
+  C = e == 0 ? TT(1) : TT(-0.5);
+  S = e == 0 ? TT(0) : (e == 1 ? TT(0.86602540378443864676) : TT(-0.86602540378443864676));
+}
+template <int H, class TT>
+struct PwsS {
+  static constexpr int NT = 256, HSQ = H * H, MC = 32, NCH = (HSQ + MC - 1) / MC;
+  static constexpr int YSZ = 16 * 8 * MC;   // one YS buffer
+  static constexpr size_t smem = sizeof(TT) * (size_t)2 * YSZ;
+  static constexpr int MINB = 2;
+  static_assert(8 * MC == NT, "one ZY item per thread");
+};
+template <int H, class TT>
+__global__ void __launch_bounds__(PwsS<H, TT>::NT, PwsS<H, TT>::MINB)
+    k_pwshift_s(DevTree t, const int32_t* __restrict__ parents, const TT* __restrict__ F, size_t base, size_t stride,
+                const double* __restrict__ W, size_t wstride, TT* __restrict__ Tout) {
+  using C = PwsS<H, TT>;
+  constexpr int NT = C::NT, HSQ = H * H, SLAB = 8 * HSQ, MC = C::MC, NCH = C::NCH, YSZ = C::YSZ;
+  extern __shared__ __align__(16) unsigned char pws_raw[];
+  TT* YSb = reinterpret_cast<TT*>(pws_raw);   // [2][(w1 o2) o3][pi][MC]
+  __shared__ const TT* win[64];               // window box (w1 w2 w3), null: absent or not F_out
+  __shared__ int rank[8];                     // exp rank of child o = (o1 o2 o3), -1: none
+  __shared__ int lvl;
+  const int pb = parents[blockIdx.x], tid = threadIdx.x;
+  if (tid < 64) {
+    const int w1 = tid >> 4, w2 = (tid >> 2) & 3, w3 = tid & 3;
+    const int D1 = w1 == 0 ? -1 : (w1 == 3 ? 1 : 0), D2 = w2 == 0 ? -1 : (w2 == 3 ? 1 : 0),
+              D3 = w3 == 0 ? -1 : (w3 == 3 ? 1 : 0);
+    const int c1 = w1 - 2 * D1 - 1, c2 = w2 - 2 * D2 - 1, c3 = w3 - 2 * D3 - 1;
+    const int S = t.coll[27 * (int64_t)pb + (D1 + 1) * 9 + (D2 + 1) * 3 + (D3 + 1)];
+    const TT* ptr = nullptr;
+    if (S >= 0) {
+      const int ch = t.child[8 * (int64_t)S + (c1 << 2) + (c2 << 1) + c3];
+      if (ch >= 0 && (t.flags[ch] & F_OUT)) ptr = F + base + (size_t)(t.fout_rank[ch] - 1) * stride;
+    }
+    win[tid] = ptr;
+  } else if (tid < 72) {
+    const int ch = t.child[8 * (int64_t)pb + (tid - 64)];
+    rank[tid - 64] = (ch >= 0 && (t.flags[ch] & F_EXP)) ? t.exp_rank[ch] : -1;
+    if (tid == 64) lvl = t.level[pb] + 1;
+  }
+  __syncthreads();
+  bool any = false;
+#pragma unroll
+  for (int o = 0; o < 8; ++o) any |= rank[o] >= 0;
+  if (!any) return;
+  const double* Wl = W + (size_t)lvl * wstride;
+  // ZY item of this thread: (w1, pi1) warp-uniform, i = lane
+  const int zi = tid % MC, zg = tid / MC, pi1 = zg & 1, w1 = zg >> 1;
+  int nb = 0;
+  for (int ch = blockIdx.y; ch < H * NCH; ch += gridDim.y, ++nb) {
+    const int a = ch / NCH, m0 = (ch - a * NCH) * MC;
+    const size_t aoff = (size_t)a * SLAB;
+    TT* YS = YSb + (nb & 1) * YSZ;
+    {
+      const int m = m0 + zi;
+      const bool ok = m < HSQ;
+      TT Cc, Sc, Cb, Sb;
+      rcs(m % H, Cc, Sc);
+      rcs(m / H, Cb, Sb);
+      TT Y[2][2][4];   // [o2][o3][pi2 pi3]
+#pragma unroll
+      for (int o2 = 0; o2 < 2; ++o2)
+#pragma unroll
+        for (int o3 = 0; o3 < 2; ++o3)
+#pragma unroll
+          for (int p = 0; p < 4; ++p) Y[o2][o3][p] = TT(0);
+#pragma unroll
+      for (int w2 = 0; w2 < 4; ++w2) {
+        TT g[4][4];   // [w3][pi2 pi3]
+#pragma unroll
+        for (int w3 = 0; w3 < 4; ++w3) {
+          const TT* sp = ok ? win[w1 * 16 + w2 * 4 + w3] : nullptr;
+#pragma unroll
+          for (int p = 0; p < 4; ++p) g[w3][p] = sp ? __ldg(sp + aoff + (pi1 * 4 + p) * HSQ + m) : TT(0);
+        }
+        // Z taps: pairs (pi3 = 0, 1) for pi2 = 0, 1; child o3 from w3 = o3 .. o3 + 2
+        TT Z[2][4];
+#pragma unroll
+        for (int o3 = 0; o3 < 2; ++o3)
+#pragma unroll
+          for (int p2 = 0; p2 < 2; ++p2)
+            rot3(g[o3][2 * p2], g[o3][2 * p2 + 1], g[o3 + 1][2 * p2], g[o3 + 1][2 * p2 + 1], g[o3 + 2][2 * p2],
+                 g[o3 + 2][2 * p2 + 1], Cc, Sc, Z[o3][2 * p2], Z[o3][2 * p2 + 1]);
+        // Y taps: pairs (pi2 = 0, 1) for pi3 = 0, 1; child o2 takes w2 in o2 .. o2 + 2
+#pragma unroll
+        for (int o2 = 0; o2 < 2; ++o2) {
+          if (w2 < o2 || w2 > o2 + 2) continue;
+          constexpr int dummy = 0;
+          (void)dummy;
+#pragma unroll
+          for (int o3 = 0; o3 < 2; ++o3)
+#pragma unroll
+            for (int p3 = 0; p3 < 2; ++p3) {
+              TT& y0 = Y[o2][o3][p3];
+              TT& y1 = Y[o2][o3][2 + p3];
+              const int d = o2 + 1 - w2;
+              if (d > 0) racc<1>(y0, y1, Z[o3][p3], Z[o3][2 + p3], Cb, Sb);
+              else if (d < 0) racc<-1>(y0, y1, Z[o3][p3], Z[o3][2 + p3], Cb, Sb);
+              else racc<0>(y0, y1, Z[o3][p3], Z[o3][2 + p3], Cb, Sb);
+            }
+        }
+      }
+#pragma unroll
+      for (int o2 = 0; o2 < 2; ++o2)
+#pragma unroll
+        for (int o3 = 0; o3 < 2; ++o3)
+#pragma unroll
+          for (int p = 0; p < 4; ++p) YS[(((w1 * 2 + o2) * 2 + o3) * 8 + pi1 * 4 + p) * MC + zi] = Y[o2][o3][p];
+    }
+    __syncthreads();
+    // ---- X: child o1 from w1 = o1 .. o1 + 2 (axis 1, mode a), weights, T; pairs (p, p + 4)
+    TT Ca, Sa;
+    rcs(a, Ca, Sa);
+#pragma unroll
+    for (int u = 0; u < 32 * MC / NT; ++u) {
+      const int it = tid + u * NT, i = it % MC, g = it / MC, p = g & 3, o = g >> 2, m = m0 + i;
+      const int r = rank[o];
+      if (m >= HSQ || r < 0) continue;
+      const TT* yl = YS + ((((o >> 2) * 2 + ((o >> 1) & 1)) * 2 + (o & 1)) * 8 + p) * MC + i;
+      TT x0, x1;
+      rot3(yl[0], yl[4 * MC], yl[32 * MC], yl[36 * MC], yl[64 * MC], yl[68 * MC], Ca, Sa, x0, x1);
+      const TT wt = (TT)__ldg(Wl + (size_t)a * HSQ + m);
+      TT* dst = Tout + (size_t)r * H * SLAB + aoff + m;
+      dst[p * HSQ] = wt * x0;
+      dst[(p + 4) * HSQ] = wt * x1;
+    }
+    // YS is double buffered: the next chunk writes the other buffer, and this buffer
+    // again only after the next chunk's barrier (every thread is past this X pass)
+  }
+}
+
+// eps = 1e-9 tier: T_pw2poly (Eqs. 3.43-3.44) of every non-root local box from the fp64
+// weighted incoming expansion T[a][pi][b][c], all three axis contractions on DMMA
+// (m8n8k4 f64).  The slabs a stream through shared memory AC = 2 at a time (cp.async
+// double buffer): axis 3 (over c, output parity n3 % 2 picks pi3) into U[a][pi12][b][n3],
+// axis 2 (over b) into V[a][pi1][n2 n3] for 4 slabs, then the axis-1 contraction over
+// those 4 slabs as one DMMA k-step into Lambda accumulators that stay in registers for
+// the whole box (each warp owns a fixed set of (n2 n3) column tiles).
+template <int P, int H>
+struct Pw2p64 {
+  static constexpr int NT = 384, NW = NT / 32, AC = 2, HH = (H + 1) & ~1, P2 = P * P;
+  static constexpr int PH = (P + 1) / 2, MT = (PH + 7) / 8;   // tiles of one parity class
+  static constexpr int NT1 = (P2 + 7) / 8, TPW = (NT1 + NW - 1) / NW;
+  static constexpr int TSZ = AC * 8 * H * H;
+  static constexpr size_t smem =
+      sizeof(double) * ((size_t)P * HH + 2 * (size_t)TSZ + (size_t)AC * 4 * H * P + 4 * 2 * (size_t)P2);
+};
+template <int P, int H>
+__global__ void __launch_bounds__(Pw2p64<P, H>::NT, 1)
+    k_pw2poly64(DevTree t, const int32_t* __restrict__ boxes, const double* __restrict__ Gr,
+                const double* __restrict__ Tin, double* __restrict__ lam) {
+  using C = Pw2p64<P, H>;
+  constexpr int NT = C::NT, NW = C::NW, AC = C::AC, HH = C::HH, P2 = C::P2, MT = C::MT, NT1 = C::NT1,
+                TPW = C::TPW, TSZ = C::TSZ, HSQ = H * H, SLAB = 8 * HSQ, NCHUNK = H / AC;
+  constexpr int R3 = AC * 4 * H, MT3 = R3 / 8, KS = (H + 3) / 4, NT3 = (P + 7) / 8;
+  static_assert(H % 4 == 0 && R3 % 8 == 0, "slab chunking");
+  extern __shared__ __align__(16) double sm[];
+  double* sG = sm;                   // [P][HH]
+  double* Tc = sG + P * HH;          // [2][AC][8][H][H]
+  double* U = Tc + 2 * TSZ;          // [AC][4][H][P]
+  double* V = U + AC * 4 * H * P;    // [4][2][P2]
+  const int b = boxes[blockIdx.x], tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2,
+            q = lane & 3;
+  const double* tb = Tin + (size_t)t.exp_rank[b] * H * SLAB;
+  auto load = [&](int k) {
+    const double* src = tb + (size_t)k * TSZ;
+    double* dst = Tc + (k & 1) * TSZ;
+    for (int i = tid; i < TSZ / 2; i += NT) cp_async16(dst + 2 * i, src + 2 * i);
+    cp_async_commit();
+  };
+  load(0);
+  for (int i = tid; i < P * HH; i += NT) sG[i] = Gr[i];
+  double acc[TPW][2][MT][2];
+#pragma unroll
+  for (int s = 0; s < TPW; ++s)
+#pragma unroll
+    for (int par = 0; par < 2; ++par)
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) acc[s][par][mt][0] = acc[s][par][mt][1] = 0.0;
+#pragma unroll 1
+  for (int k = 0; k < NCHUNK; ++k) {
+    if (k + 1 < NCHUNK) {
+      load(k + 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    // ---- axis 3: U[r = (ac pi12 b)][n3] = sum_c Gr[n3][c] T[ac][2 pi12 + n3 % 2][b][c];
+    // a warp takes one row tile and both column tiles of a parity (two DMMA chains)
+    const double* Tk = Tc + (k & 1) * TSZ;
+    static_assert(MT == 2, "two column tiles per parity");
+    for (int u = warp; u < 2 * MT3; u += NW) {
+      const int par = u / MT3, mt = u - par * MT3;
+      const int r = mt * 8 + g, ac = r / (4 * H), pi12 = (r / H) & 3, bb = r % H;
+      const double* arow = Tk + ((ac * 8 + 2 * pi12 + par) * H + bb) * H;
+      const int n3a = 2 * g + par, n3b = 2 * (8 + g) + par;
+      const double* brow0 = sG + n3a * HH;
+      const double* brow1 = sG + (n3b < P ? n3b : 0) * HH;
+      double av[KS], b0[KS], b1[KS];
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) {
+        const int kk = ks * 4 + q;
+        av[ks] = kk < H ? arow[kk] : 0.0;
+        b0[ks] = kk < H ? brow0[kk] : 0.0;
+        b1[ks] = (n3b < P && kk < H) ? brow1[kk] : 0.0;
+      }
+      double c0 = 0.0, c1 = 0.0, d0 = 0.0, d1 = 0.0;
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) {
+        dmma(c0, c1, av[ks], b0[ks]);
+        dmma(d0, d1, av[ks], b1[ks]);
+      }
+      double* urow = U + r * P;
+      const int na = 4 * q + par, nb = 2 * (8 + 2 * q) + par;
+      urow[na] = c0;          // 4q + par + 2 < 16 <= P
+      urow[na + 2] = c1;
+      if (nb < P) urow[nb] = d0;
+      if (nb + 2 < P) urow[nb + 2] = d1;
+    }
+    __syncthreads();
+    // ---- axis 2: V[slot ac][pi1][n2][n3] = sum_b Gr[n2][b] U[ac][2 pi1 + n2 % 2][b][n3];
+    // a warp takes one column tile of a group and both row tiles (two DMMA chains)
+    for (int u = warp; u < AC * 4 * NT3; u += NW) {
+      const int grp = u / NT3, nt = u - grp * NT3;
+      const int ac = grp >> 2, pi1 = (grp >> 1) & 1, par2 = grp & 1;
+      const int n2a = 2 * g + par2, n2b = 2 * (8 + g) + par2, n3 = nt * 8 + g;
+      const double* arow0 = sG + n2a * HH;
+      const double* arow1 = sG + (n2b < P ? n2b : 0) * HH;
+      const double* ucol = U + ((ac * 4 + 2 * pi1 + par2) * H) * P + (n3 < P ? n3 : 0);
+      double a0v[KS], a1v[KS], bv[KS];
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) {
+        const int kk = ks * 4 + q;
+        a0v[ks] = kk < H ? arow0[kk] : 0.0;
+        a1v[ks] = (n2b < P && kk < H) ? arow1[kk] : 0.0;
+        bv[ks] = (n3 < P && kk < H) ? ucol[kk * P] : 0.0;
+      }
+      double c0 = 0.0, c1 = 0.0, d0 = 0.0, d1 = 0.0;
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) {
+        dmma(c0, c1, a0v[ks], bv[ks]);
+        dmma(d0, d1, a1v[ks], bv[ks]);
+      }
+      const int c3 = nt * 8 + 2 * q;
+      double* vb = V + ((size_t)(((k & 1) * AC + ac) * 2 + pi1)) * P2;
+      double* vr0 = vb + n2a * P;
+      if (c3 < P) vr0[c3] = c0;
+      if (c3 + 1 < P) vr0[c3 + 1] = c1;
+      if (n2b < P) {
+        double* vr1 = vb + n2b * P;
+        if (c3 < P) vr1[c3] = d0;
+        if (c3 + 1 < P) vr1[c3 + 1] = d1;
+      }
+    }
+    if (k & 1) {
+      __syncthreads();
+      // ---- axis 1 over the 4 slabs a0 .. a0 + 3 in V: one k-step per (parity, tile)
+      const int a0 = (k >> 1) * 4;
+      double af[2][MT];
+#pragma unroll
+      for (int par = 0; par < 2; ++par)
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+          const int n1 = 2 * (mt * 8 + g) + par;
+          af[par][mt] = n1 < P ? sG[n1 * HH + a0 + q] : 0.0;
+        }
+#pragma unroll
+      for (int s = 0; s < TPW; ++s) {
+        const int nt = warp + s * NW;
+        if (nt < NT1) {
+          const int n = nt * 8 + g;
+#pragma unroll
+          for (int par = 0; par < 2; ++par) {
+            const double bv = n < P2 ? V[(q * 2 + par) * P2 + n] : 0.0;
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt) dmma(acc[s][par][mt][0], acc[s][par][mt][1], af[par][mt], bv);
+          }
+        }
+      }
+    }
+  }
+  double* dst = lam + (size_t)t.exp_rank[b] * P * P2;
+#pragma unroll
+  for (int s = 0; s < TPW; ++s) {
+    const int nt = warp + s * NW;
+    if (nt >= NT1) continue;
+    const int n = nt * 8 + 2 * q;
+#pragma unroll
+    for (int par = 0; par < 2; ++par)
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        const int n1 = 2 * (mt * 8 + g) + par;
+        if (n1 >= P) continue;
+        if (n < P2) dst[(size_t)n1 * P2 + n] = acc[s][par][mt][0];
+        if (n + 1 < P2) dst[(size_t)n1 * P2 + n + 1] = acc[s][par][mt][1];
+      }
+  }
+}
+
 // fp32 tier: T_pw2poly (Eqs. 3.43-3.44) of every non-root local box from the weighted
 // incoming expansion T[a][pi][b][c] written by k_pwshift, as three axis contractions
 // over the whole box (no slab chunking, two barriers): axis 3 rows (a, pi12, b) from
@@ -2889,15 +3223,27 @@ static bool eval_tc() {   // default: tensor cores; DMK_EVAL=ffma selects k_eval
   return !(e && std::strcmp(e, "ffma") == 0);
 }
 
-// eps = 1e-9 translation: the 27-colleague per-box form (default: measured 8.4 ms at
-// config 1) or parent groups + fp64 T + back transforms (DMK_PW64=group: 7.0 + 3.6 ms,
-// k_pwshift64 is latency-bound at 204 registers / 8 warps per SM; profiles/
-// r02_pw64_forms_v1.jsonl); chosen at plan time (the T buffer is sized then)
-bool pw64_group_env() {
+// eps = 1e-9 translation + back transforms, chosen at plan time (the T buffer is sized
+// then): parent groups staged through shared memory (k_pwshift_s<H, double>) into an
+// fp64 T, back transforms on DMMA (k_pw2poly64) -- the default, 1.97 + 1.53 ms at
+// config 1 (profiles/r02_pw64_forms_v3.jsonl); DMK_PW64=box: the 27-colleague per-box
+// form k_pwlocal (8.4 ms); DMK_PW64=group: register window sums k_pwshift64 + k_pwlocal
+// from T (7.0 + 3.6 ms: 204 registers, 8 warps per SM, latency-bound)
+constexpr int PW64_BOX = 0, PW64_GROUP = 1, PW64_STAGED = 2;
+static int pw64_form() {
   const char* e = std::getenv("DMK_PW64");
-  return e && std::strcmp(e, "group") == 0;
+  if (e && std::strcmp(e, "group") == 0) return PW64_GROUP;
+  if (e && std::strcmp(e, "box") == 0) return PW64_BOX;
+  return PW64_STAGED;
 }
+bool pw64_group_env() { return pw64_form() != PW64_BOX; }
 #define pw64_group() (PL->pwt64.n > 0)
+// fp32-tier translation: k_pwshift (register window sums) or k_pwshift_s (DMK_PWS=staged)
+static bool pws_staged() {
+  const char* e = std::getenv("DMK_PWS");
+  return e && std::strcmp(e, "staged") == 0;
+}
+constexpr unsigned PWS_S_GY = 4;   // CTAs per parent (each walks every 4th mode chunk)
 
 // Phases of run_eval: UP = anterpolation + c2p (Step 2), DOWN = Step 3; C2P_ONLY =
 // c2p for the levels above `top` only (after dmk_level_moments injected level `top`).
@@ -3032,9 +3378,18 @@ static void run_eval(dmk_plan_s* PL, int phase = PH_UP | PH_DOWN, int top = 0) {
           tm.end();
           tm.begin("pwshift");
           if (PL->nfout > 0) {
-            const unsigned grid = (unsigned)(PL->nfout * PWS_GY);
-            k_pwshift<H><<<grid, PWS_NT, 0, s>>>(dt, PL->fout_list.p, reinterpret_cast<const float*>(Fp),
-                                                  PL->phi_size0, PL->phi_size1, T.dW, T.wstride, PL->pwt.p);
+            if (pws_staged()) {
+              using KS = PwsS<H, float>;
+              set_smem(k_pwshift_s<H, float>, KS::smem);
+              const dim3 grid((unsigned)PL->nfout, PWS_S_GY);
+              k_pwshift_s<H, float><<<grid, KS::NT, KS::smem, s>>>(dt, PL->fout_list.p,
+                                                                  reinterpret_cast<const float*>(Fp), PL->phi_size0,
+                                                                  PL->phi_size1, T.dW, T.wstride, PL->pwt.p);
+            } else {
+              const unsigned grid = (unsigned)(PL->nfout * PWS_GY);
+              k_pwshift<H><<<grid, PWS_NT, 0, s>>>(dt, PL->fout_list.p, reinterpret_cast<const float*>(Fp),
+                                                    PL->phi_size0, PL->phi_size1, T.dW, T.wstride, PL->pwt.p);
+            }
             DMK_LAUNCH_CHECK();
           }
           tm.end();
@@ -3047,18 +3402,35 @@ static void run_eval(dmk_plan_s* PL, int phase = PH_UP | PH_DOWN, int top = 0) {
           // eps = 1e-9: fp64 parent-group translation into T, then the back transforms
           tm.end();
           tm.begin("pwshift");
+          const bool staged = pw64_form() == PW64_STAGED;
           if (PL->nfout > 0) {
-            const dim3 grid((unsigned)PL->nfout, (unsigned)((H * H * H + PWS64_NT - 1) / PWS64_NT), 2);
-            k_pwshift64<H><<<grid, PWS64_NT, 0, s>>>(dt, PL->fout_list.p, reinterpret_cast<const double*>(Fp),
-                                                     PL->phi_size0, PL->phi_size1, T.dW, T.wstride, PL->pwt64.p);
+            if (staged) {
+              using KS = PwsS<H, double>;
+              set_smem(k_pwshift_s<H, double>, KS::smem);
+              const dim3 grid((unsigned)PL->nfout, PWS_S_GY);
+              k_pwshift_s<H, double><<<grid, KS::NT, KS::smem, s>>>(dt, PL->fout_list.p,
+                                                                   reinterpret_cast<const double*>(Fp), PL->phi_size0,
+                                                                   PL->phi_size1, T.dW, T.wstride, PL->pwt64.p);
+            } else {
+              const dim3 grid((unsigned)PL->nfout, (unsigned)((H * H * H + PWS64_NT - 1) / PWS64_NT), 2);
+              k_pwshift64<H><<<grid, PWS64_NT, 0, s>>>(dt, PL->fout_list.p, reinterpret_cast<const double*>(Fp),
+                                                       PL->phi_size0, PL->phi_size1, T.dW, T.wstride, PL->pwt64.p);
+            }
             DMK_LAUNCH_CHECK();
           }
           tm.end();
           tm.begin("pw2poly");
-          set_smem(k_pwlocal<P, H, AC, false, true, double>, K1::smem);
-          k_pwlocal<P, H, AC, false, true, double><<<(int)(PL->nexp - 1), K1::NT, K1::smem, s>>>(
-              dt, PL->exp_list.p + 1, T.dGr1, T.dW, T.wstride, Fp, PL->phi_size0, PL->phi_size1, PL->lam.p,
-              PL->pwt64.p);
+          if (staged) {
+            using K2 = Pw2p64<P, H>;
+            set_smem(k_pw2poly64<P, H>, K2::smem);
+            k_pw2poly64<P, H><<<(int)(PL->nexp - 1), K2::NT, K2::smem, s>>>(dt, PL->exp_list.p + 1, T.dGr1,
+                                                                             PL->pwt64.p, PL->lam.p);
+          } else {
+            set_smem(k_pwlocal<P, H, AC, false, true, double>, K1::smem);
+            k_pwlocal<P, H, AC, false, true, double><<<(int)(PL->nexp - 1), K1::NT, K1::smem, s>>>(
+                dt, PL->exp_list.p + 1, T.dGr1, T.dW, T.wstride, Fp, PL->phi_size0, PL->phi_size1, PL->lam.p,
+                PL->pwt64.p);
+          }
         } else {
           k_pwlocal<P, H, AC, false><<<(int)(PL->nexp - 1), K1::NT, K1::smem, s>>>(
               dt, PL->exp_list.p + 1, T.dGr1, T.dW, T.wstride, Fp, PL->phi_size0, PL->phi_size1, PL->lam.p);

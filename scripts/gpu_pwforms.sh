@@ -8,3 +8,8 @@ tail -3 gpurun_out/r02_pwforms_test_$T.log
 timeout 600 python scripts/stage_forms.py DMK_PW64 box,group,staged --eps 1e-9 --no-err > gpurun_out/r02_pw64_forms_$T.jsonl 2>&1
 timeout 600 python scripts/stage_forms.py DMK_PWS reg,staged --eps 1e-6,1e-3 --no-err > gpurun_out/r02_pws_forms_$T.jsonl 2>&1
 cat gpurun_out/r02_pw64_forms_$T.jsonl gpurun_out/r02_pws_forms_$T.jsonl | cut -c1-600
+if [ -n "$NCU" ]; then
+  DMK_SERIAL=1 ncu --set full --clock-control none --import-source on -k "regex:k_pwshift_s|k_pw2poly64|k_prox2pw" -c 4 \
+      -o gpurun_out/r02_prof_pw64_$T python scripts/prof_step.py --eps 1e-9 --reps 1 > gpurun_out/r02_ncu_pw64_$T.log 2>&1
+  tail -2 gpurun_out/r02_ncu_pw64_$T.log
+fi

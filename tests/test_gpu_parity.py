@@ -428,7 +428,7 @@ def test_pw64_parent_group_form(monkeypatch):
     x, q = dmk_inputs.make("sphere", 8000, seed=21)
     _, st = dmk_laplace3d(x, q, 1e-9, 60, return_stages=True)
     res = {}
-    for form in ("group", "box"):
+    for form in ("group", "staged", "box"):
         monkeypatch.setenv("DMK_PW64", form)
         plan, u = gpu_run(x, q, 1e-9, 60)
         p = plan.info().p
@@ -439,5 +439,49 @@ def test_pw64_parent_group_form(monkeypatch):
         for i in np.nonzero(ex >= 0)[0]:
             assert np.max(np.abs(lam[ex[i]] - st["local"][i])) <= tol(28, "local") * scale, form
         res[form] = u
-    assert np.max(np.abs(res["group"] - res["box"])) <= 1e-13 * np.max(np.abs(res["box"]))
-    assert direct.rel_l2(res["group"], direct.laplace3d(x, q)) <= 2e-9
+    for form in ("group", "staged"):
+        assert np.max(np.abs(res[form] - res["box"])) <= 1e-13 * np.max(np.abs(res["box"])), form
+        assert direct.rel_l2(res[form], direct.laplace3d(x, q)) <= 2e-9, form
+
+
+@pytest.mark.parametrize("kind,n,ns", [("clusters", 12000, 40), ("uniform", 20000, 60)])
+def test_pw64_staged_deep(monkeypatch, kind, n, ns):
+    """The staged parent-group translation (k_pwshift_s<H, double>: Z, Y, X window passes
+    through shared memory) + DMMA back transforms (k_pw2poly64) on deeper trees (clustered:
+    ~11 levels, missing window boxes; uniform 2e4 at n_s = 60: full 4x4x4 windows) against
+    the oracle's local expansions (Eq. 3.39, Eqs. 3.43-3.44) and the direct sum."""
+    monkeypatch.setenv("DMK_PW64", "staged")
+    x, q = dmk_inputs.make(kind, n, seed=23)
+    _, st = dmk_laplace3d(x, q, 1e-9, ns, return_stages=True)
+    plan, u = gpu_run(x, q, 1e-9, ns)
+    p = plan.info().p
+    lam = plan.stage("local").reshape(-1, p, p, p)
+    ex = plan.tree("exp")
+    plan.close()
+    scale = max(np.max(np.abs(st["local"][i])) for i in st["local"])
+    for i in np.nonzero(ex >= 0)[0]:
+        assert np.max(np.abs(lam[ex[i]] - st["local"][i])) <= tol(28, "local") * scale
+    assert direct.rel_l2(u, direct.laplace3d(x, q)) <= 2e-9
+
+
+@pytest.mark.parametrize("eps", [1e-3, 1e-6])
+@pytest.mark.parametrize("kind,n,ns", [("clusters", 12000, 40), ("sphere", 8000, 60)])
+def test_pws_staged_fp32_tier(monkeypatch, eps, kind, n, ns):
+    """fp32 tier (R16): the staged translation (k_pwshift_s<H, float>, DMK_PWS=staged)
+    against the oracle's local expansions and the register form (k_pwshift)."""
+    x, q = dmk_inputs.make(kind, n, seed=24)
+    _, st = dmk_laplace3d(x, q, eps, ns, return_stages=True)
+    lams = {}
+    for form in ("staged", "reg"):
+        monkeypatch.setenv("DMK_PWS", form)
+        plan, u = gpu_run(x, q, eps, ns)
+        p = plan.info().p
+        lam = plan.stage("local").reshape(-1, p, p, p)
+        ex = plan.tree("exp")
+        plan.close()
+        scale = max(np.max(np.abs(st["local"][i])) for i in st["local"])
+        for i in np.nonzero(ex >= 0)[0]:
+            assert np.max(np.abs(lam[ex[i]] - st["local"][i])) <= tol(p, "local") * scale, form
+        assert direct.rel_l2(u, direct.laplace3d(x, q)) <= 2 * eps, form
+        lams[form] = lam
+    assert np.max(np.abs(lams["staged"] - lams["reg"])) <= 2e-7 * np.max(np.abs(lams["reg"]))
