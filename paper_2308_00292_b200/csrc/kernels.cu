@@ -2772,6 +2772,15 @@ __global__ void __launch_bounds__(32, P2PQ<K, KER, QC>::MINB) k_p2p32q(DevTree t
 // comes from the high parts and a group of pairs where some pair is closer than
 // sqrt(tc) r_L is re-evaluated on the full double-single difference.
 constexpr int P2PS_NW = 4;
+// records past a chunk's tail skip the kernel evaluation (warp-uniform); optionally
+// also records with no pair inside any lane's ball (one vote per record)
+#ifndef DMK_P2PS_TAIL
+#define DMK_P2PS_TAIL 1
+#endif
+#ifndef DMK_P2PS_RSKIP
+#define DMK_P2PS_RSKIP 0
+#endif
+constexpr bool P2PS_TAIL = DMK_P2PS_TAIL, P2PS_RSKIP = DMK_P2PS_RSKIP;
 template <int K, int KER>
 __global__ void __launch_bounds__(P2PS_NW * 32) k_p2p32s(const SymTask* __restrict__ tasks,
                                                         const int32_t* __restrict__ ntask_p,
@@ -2916,6 +2925,14 @@ __global__ void __launch_bounds__(P2PS_NW * 32) k_p2p32s(const SymTask* __restri
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
             const int r = 4 * g + k;
+            if (P2PS_TAIL && r >= npy) {   // records past the chunk's tail (warp-uniform): no pairs
+              if (!self) v[2 * r] = v[2 * r + 1] = 0.0f;
+              continue;
+            }
+            if (P2PS_RSKIP && !__any_sync(0xffffffffu, lv && fminf(u[k].x, u[k].y) < 1.0f)) {
+              if (!self) v[2 * r] = v[2 * r + 1] = 0.0f;
+              continue;
+            }
             // R_L outside the ball is 0 (the mask folded into R); the lane's side gets
             // w_y R, the broadcast side w_x R (pads and idle lanes have w = 0; an idle
             // lane's own sum is not written)
