@@ -2772,15 +2772,17 @@ __global__ void __launch_bounds__(32, P2PQ<K, KER, QC>::MINB) k_p2p32q(DevTree t
 // comes from the high parts and a group of pairs where some pair is closer than
 // sqrt(tc) r_L is re-evaluated on the full double-single difference.
 constexpr int P2PS_NW = 4;
-// records past a chunk's tail skip the kernel evaluation (warp-uniform); optionally
-// also records with no pair inside any lane's ball (one vote per record)
+// compile-time experiments (both measured slower, profiles/r02_p2p_tail_ab.jsonl, off):
+// records past a chunk's tail skip the kernel evaluation (warp-uniform); records with
+// no pair inside any lane's ball skip it (one vote per record)
 #ifndef DMK_P2PS_TAIL
-#define DMK_P2PS_TAIL 1
+#define DMK_P2PS_TAIL 0
 #endif
 #ifndef DMK_P2PS_RSKIP
 #define DMK_P2PS_RSKIP 0
 #endif
 constexpr bool P2PS_TAIL = DMK_P2PS_TAIL, P2PS_RSKIP = DMK_P2PS_RSKIP;
+constexpr int P2PS_PER_DEFAULT = 64;
 template <int K, int KER>
 __global__ void __launch_bounds__(P2PS_NW * 32) k_p2p32s(const SymTask* __restrict__ tasks,
                                                         const int32_t* __restrict__ ntask_p,
@@ -3603,11 +3605,15 @@ static void run_p2p32s(dmk_plan_s* PL, const ResPoly& rp64, int K, cudaStream_t 
       DMK_CUDA(cudaGetDevice(&dev));
       DMK_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
     }
+    // resident CTAs per SM: all that fit by default; DMK_P2PS_PER = k caps them (leaves
+    // registers for the far-field kernels of the other stream), 0 = one task per warp
+    const char* pe = std::getenv("DMK_P2PS_PER");
+    const int per_env = pe ? std::atoi(pe) : P2PS_PER_DEFAULT;
 #define DMK_P2P_CASE(KK)                                                                                      \
   case KK: {                                                                                                  \
     static thread_local int per = 0;                                                                          \
     if (!per) DMK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_p2p32s<KK, KER>, P2PS_NW * 32, 0)); \
-    k_p2p32s<KK, KER><<<(unsigned)std::min<int64_t>((int64_t)nsm * std::max(per, 1),                        \
+    k_p2p32s<KK, KER><<<(unsigned)std::min<int64_t>(per_env == 0 ? INT64_MAX : (int64_t)nsm * std::max(std::min(per, per_env), 1), \
                                                     (PL->sym_cap + P2PS_NW - 1) / P2PS_NW),                   \
                         P2PS_NW * 32, 0, st>>>(PL->sym_tasks.p, PL->sym_ntask.p, PL->xl4.p, PL->xl4lo.p, rp,   \
                                                T.dRespoly, (float)T.lam, p2p_tc(), PL->part.p);               \
