@@ -165,6 +165,73 @@ __device__ __forceinline__ void mma_tiles_acc(int mtiles, int ntiles, FA fa, FB 
   }
 }
 
+// Register-blocked forms for a contraction with one SMALL operand (the 1D transform
+// matrix): its fragments stay in registers, so a tile costs KS loads of the large
+// operand instead of 2 KS (mma_tiles reloads both per 8x8 tile).
+//   mma_sweep_n: A = the small operand (MT m-tiles, all kept), B swept over n-tiles;
+//   mma_sweep_m: B = the small operand (NTL n-tiles, all kept), A swept over m-tiles,
+//                the next tile's A loaded during the DMMA chain (A may come from global).
+template <int KS, int MT, class FA, class FB, class FC>
+__device__ __forceinline__ void mma_sweep_n(int ntiles, FA fa, FB fb, FC fc) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int g = lane >> 2, q = lane & 3;
+  double av[MT][KS];
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) av[mt][ks] = fa(mt * 8 + g, ks * 4 + q);
+  for (int t = warp; t < ntiles; t += nw) {
+    const int n0 = t * 8;
+    double bv[KS];
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) bv[ks] = fb(ks * 4 + q, n0 + g);
+    double c[MT][2];
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) c[mt][0] = c[mt][1] = 0.0;
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) dmma(c[mt][0], c[mt][1], av[mt][ks], bv[ks]);
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) fc(mt * 8 + g, n0 + 2 * q, c[mt][0], c[mt][1]);
+  }
+}
+template <int KS, int NTL, class FA, class FB, class FC>
+__device__ __forceinline__ void mma_sweep_m(int mtiles, FA fa, FB fb, FC fc) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int g = lane >> 2, q = lane & 3;
+  double bv[NTL][KS];
+#pragma unroll
+  for (int nt = 0; nt < NTL; ++nt)
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) bv[nt][ks] = fb(ks * 4 + q, nt * 8 + g);
+  int t = warp;
+  if (t >= mtiles) return;
+  double av[KS];
+#pragma unroll
+  for (int ks = 0; ks < KS; ++ks) av[ks] = fa(t * 8 + g, ks * 4 + q);
+  for (; t < mtiles; t += nw) {
+    double an[KS];
+    if (t + nw < mtiles) {
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) an[ks] = fa((t + nw) * 8 + g, ks * 4 + q);
+    }
+    double c[NTL][2];
+#pragma unroll
+    for (int nt = 0; nt < NTL; ++nt) c[nt][0] = c[nt][1] = 0.0;
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+      for (int nt = 0; nt < NTL; ++nt) dmma(c[nt][0], c[nt][1], av[ks], bv[nt][ks]);
+#pragma unroll
+    for (int nt = 0; nt < NTL; ++nt) fc(t * 8 + g, nt * 8 + 2 * q, c[nt][0], c[nt][1]);
+    if (t + nw < mtiles) {
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) av[ks] = an[ks];
+    }
+  }
+}
+
 // collect the point ranges a box works on:
 //   ANTERP: leaf children with points (F_out box)
 //   EVAL:   own points if the box is a leaf, else leaf children without F_in

@@ -1036,7 +1036,10 @@ struct Prox2pw {
   static constexpr int NT = P > 18 ? 512 : 256, KS = ((P + 1) / 2 + 3) / 4, HP = (H + 7) / 8 * 8;
   static constexpr size_t smem = sizeof(double) * ((size_t)2 * HP * KS * 4 + (size_t)P * P * CH + (size_t)H * P * CH);
 };
-template <int P, int H, int CH>
+// RB: the register-blocked sweeps (device.cuh mma_sweep_m / mma_sweep_n: the 1D transform
+// matrix's fragments stay in registers, one load of the large operand per 8-column tile
+// and HP/8 (or CH/8) DMMA chains on it) instead of independent 8x8 tiles.
+template <int P, int H, int CH, bool RB>
 __global__ void __launch_bounds__(Prox2pw<P, H, CH>::NT) k_prox2pw(DevTree t, const int32_t* __restrict__ boxes,
                                                  const double* __restrict__ Qr, const double* __restrict__ mom,
                                                  FStore<P>* __restrict__ F, size_t base, size_t stride) {
@@ -1062,51 +1065,57 @@ __global__ void __launch_bounds__(Prox2pw<P, H, CH>::NT) k_prox2pw(DevTree t, co
     for (int pi3 = 0; pi3 < 2; ++pi3) {
       const double* q3 = sQ + pi3 * HP * K4;
       // S1: M = P2 rows (n1 n2), N = nc, K = j
-      mma_tiles<KS>(
-          (P2 + 7) / 8, (nc + 7) / 8,
-          [&](int m, int k) { return (m < P2 && 2 * k + pi3 < P) ? __ldg(mu + m * P + 2 * k + pi3) : 0.0; },
-          [&](int k, int n) { return c0 + n < H ? q3[(c0 + n) * K4 + k] : 0.0; },
-          [&](int m, int n, double v0, double v1) {
-            if (m < P2) {
-              if (n < nc) X1[m * CH + n] = v0;
-              if (n + 1 < nc) X1[m * CH + n + 1] = v1;
-            }
-          });
+      {
+        auto fa = [&](int m, int k) { return (m < P2 && 2 * k + pi3 < P) ? __ldg(mu + m * P + 2 * k + pi3) : 0.0; };
+        auto fb = [&](int k, int n) { return (n < nc && c0 + n < H) ? q3[(c0 + n) * K4 + k] : 0.0; };
+        auto fc = [&](int m, int n, double v0, double v1) {
+          if (m < P2) {
+            if (n < nc) X1[m * CH + n] = v0;
+            if (n + 1 < nc) X1[m * CH + n + 1] = v1;
+          }
+        };
+        if constexpr (RB) mma_sweep_m<KS, (CH + 7) / 8>((P2 + 7) / 8, fa, fb, fc);
+        else mma_tiles<KS>((P2 + 7) / 8, (nc + 7) / 8, fa, fb, fc);
+      }
       __syncthreads();
       for (int pi2 = 0; pi2 < 2; ++pi2) {
         const double* q2 = sQ + pi2 * HP * K4;
         // S2: M = H rows b, N = (n1, c) = P CH (c >= nc padded), K = j
-        mma_tiles<KS>(
-            HP / 8, (P * CH + 7) / 8, [&](int m, int k) { return q2[m * K4 + k]; },
-            [&](int k, int n) {
-              const int n1 = n / CH, c = n - n1 * CH;
-              return (n1 < P && c < nc && 2 * k + pi2 < P) ? X1[(n1 * P + 2 * k + pi2) * CH + c] : 0.0;
-            },
-            [&](int m, int n, double v0, double v1) {
-              if (m < H) {
-                if (n < P * CH) X2[m * P * CH + n] = v0;
-                if (n + 1 < P * CH) X2[m * P * CH + n + 1] = v1;
-              }
-            });
+        {
+          auto fa = [&](int m, int k) { return q2[m * K4 + k]; };
+          auto fb = [&](int k, int n) {
+            const int n1 = n / CH, c = n - n1 * CH;
+            return (n1 < P && c < nc && 2 * k + pi2 < P) ? X1[(n1 * P + 2 * k + pi2) * CH + c] : 0.0;
+          };
+          auto fc = [&](int m, int n, double v0, double v1) {
+            if (m < H) {
+              if (n < P * CH) X2[m * P * CH + n] = v0;
+              if (n + 1 < P * CH) X2[m * P * CH + n + 1] = v1;
+            }
+          };
+          if constexpr (RB) mma_sweep_n<KS, HP / 8>((P * CH + 7) / 8, fa, fb, fc);
+          else mma_tiles<KS>(HP / 8, (P * CH + 7) / 8, fa, fb, fc);
+        }
         __syncthreads();
         for (int pi1 = 0; pi1 < 2; ++pi1) {
           const double* q1 = sQ + pi1 * HP * K4;
           TF* o = out + (size_t)(4 * pi1 + 2 * pi2 + pi3) * HSQ + c0;
           // S3: M = H rows a, N = (b, c) = H CH (c >= nc skipped), K = j
-          mma_tiles<KS>(
-              HP / 8, (H * CH + 7) / 8, [&](int m, int k) { return q1[m * K4 + k]; },
-              [&](int k, int n) {
-                const int bb = n / CH, c = n - bb * CH;
-                return (bb < H && 2 * k + pi1 < P) ? X2[(bb * P + 2 * k + pi1) * CH + c] : 0.0;
-              },
-              [&](int m, int n, double v0, double v1) {
-                if (m < H) {
-                  const int bb = n / CH, c = n - bb * CH;   // n even, CH may be odd
-                  if (bb < H && c < nc) o[(size_t)m * G::SLAB + bb * H + c] = (TF)v0;
-                  const int b1 = (n + 1) / CH, c1 = n + 1 - b1 * CH;
-                  if (b1 < H && c1 < nc) o[(size_t)m * G::SLAB + b1 * H + c1] = (TF)v1;
-                }
-              });
+          auto fa = [&](int m, int k) { return q1[m * K4 + k]; };
+          auto fb = [&](int k, int n) {
+            const int bb = n / CH, c = n - bb * CH;
+            return (bb < H && 2 * k + pi1 < P) ? X2[(bb * P + 2 * k + pi1) * CH + c] : 0.0;
+          };
+          auto fc = [&](int m, int n, double v0, double v1) {
+            if (m < H) {
+              const int bb = n / CH, c = n - bb * CH;   // n even, CH may be odd
+              if (bb < H && c < nc) o[(size_t)m * G::SLAB + bb * H + c] = (TF)v0;
+              const int b1 = (n + 1) / CH, c1 = n + 1 - b1 * CH;
+              if (b1 < H && c1 < nc) o[(size_t)m * G::SLAB + b1 * H + c1] = (TF)v1;
+            }
+          };
+          if constexpr (RB) mma_sweep_n<KS, HP / 8>((H * CH + 7) / 8, fa, fb, fc);
+          else mma_tiles<KS>(HP / 8, (H * CH + 7) / 8, fa, fb, fc);
         }
         __syncthreads();   // X2 is rewritten by the next pi2
       }
@@ -3349,9 +3358,13 @@ static void run_eval(dmk_plan_s* PL, int phase = PH_UP | PH_DOWN, int top = 0) {
       constexpr int H = NF + 1, H0 = NF0 + 1, AC = px_ch(P, H), AC0 = px_ch(P, H0);
       using K1 = Prox2pw<P, H, AC>;
       using K0 = Prox2pw<P, H0, AC0>;
+      // DMK_PROX2PW=tiles: the independent-tile form (before the register-blocked sweeps)
+      const char* pxe = std::getenv("DMK_PROX2PW");
+      const bool px_rb = !(pxe && std::strcmp(pxe, "tiles") == 0);
       if constexpr (P > 18) {
-        set_smem(k_prox2pw<P, H0, AC0>, K0::smem);
-        set_smem(k_prox2pw<P, H, AC>, K1::smem);
+        set_smem(k_prox2pw<P, H0, AC0, true>, K0::smem);
+        set_smem(k_prox2pw<P, H, AC, true>, K1::smem);
+        set_smem(k_prox2pw<P, H, AC, false>, K1::smem);
       }
       FStore<P>* Fp = reinterpret_cast<FStore<P>*>(PL->phi.p);
       if constexpr (P <= 18) {   // fp32 tier (R16)
@@ -3367,12 +3380,15 @@ static void run_eval(dmk_plan_s* PL, int phase = PH_UP | PH_DOWN, int top = 0) {
           DMK_LAUNCH_CHECK();
         }
       } else {
-        k_prox2pw<P, H0, AC0><<<1, K0::NT, K0::smem, sr>>>(dt, PL->fout_list.p, T.dQr0, PL->mom.p, Fp, 0, 0);
+        k_prox2pw<P, H0, AC0, true><<<1, K0::NT, K0::smem, sr>>>(dt, PL->fout_list.p, T.dQr0, PL->mom.p, Fp, 0, 0);
         DMK_LAUNCH_CHECK();
         if (PL->nfout > 1) {
-          k_prox2pw<P, H, AC><<<(int)(PL->nfout - 1), K1::NT, K1::smem, s>>>(dt, PL->fout_list.p + 1, T.dQr1,
-                                                                             PL->mom.p, Fp, PL->phi_size0,
-                                                                             PL->phi_size1);
+          if (px_rb)
+            k_prox2pw<P, H, AC, true><<<(int)(PL->nfout - 1), K1::NT, K1::smem, s>>>(
+                dt, PL->fout_list.p + 1, T.dQr1, PL->mom.p, Fp, PL->phi_size0, PL->phi_size1);
+          else
+            k_prox2pw<P, H, AC, false><<<(int)(PL->nfout - 1), K1::NT, K1::smem, s>>>(
+                dt, PL->fout_list.p + 1, T.dQr1, PL->mom.p, Fp, PL->phi_size0, PL->phi_size1);
           DMK_LAUNCH_CHECK();
         }
       }
