@@ -1047,8 +1047,11 @@ __global__ void __launch_bounds__(Prox2pw<P, H, CH>::NT) k_prox2pw(DevTree t, co
   using C = Prox2pw<P, H, CH>;
   using TF = FStore<P>;
   constexpr int NT = C::NT, P2 = G::P2, PP = G::PP, KS = C::KS, K4 = KS * 4, HP = C::HP, HSQ = G::HSQ;
-  extern __shared__ double sm[];
-  double* sQ = sm;                   // [2][HP][K4]: sQ[pi][a][j] = Qr[a][2j+pi], zero padded
+  // H and CH even (the non-root boxes at p = 28): a lane's two outputs (n, n + 1) stay in
+  // one row of c and are stored as one 16-byte word (smem intermediates and F)
+  constexpr bool EV = RB && H % 2 == 0 && CH % 2 == 0;
+  extern __shared__ __align__(16) double sm_px[];
+  double* sQ = sm_px;                  // [2][HP][K4]: sQ[pi][a][j] = Qr[a][2j+pi], zero padded
   double* X1 = sQ + 2 * HP * K4;     // [P2][CH]
   double* X2 = X1 + P2 * CH;         // [H][P][CH]
   const int b = boxes[blockIdx.x], tid = threadIdx.x;
@@ -1070,8 +1073,12 @@ __global__ void __launch_bounds__(Prox2pw<P, H, CH>::NT) k_prox2pw(DevTree t, co
         auto fb = [&](int k, int n) { return (n < nc && c0 + n < H) ? q3[(c0 + n) * K4 + k] : 0.0; };
         auto fc = [&](int m, int n, double v0, double v1) {
           if (m < P2) {
-            if (n < nc) X1[m * CH + n] = v0;
-            if (n + 1 < nc) X1[m * CH + n + 1] = v1;
+            if constexpr (EV) {   // n, nc even: one 16-byte store
+              if (n < nc) *reinterpret_cast<double2*>(X1 + m * CH + n) = make_double2(v0, v1);
+            } else {
+              if (n < nc) X1[m * CH + n] = v0;
+              if (n + 1 < nc) X1[m * CH + n + 1] = v1;
+            }
           }
         };
         if constexpr (RB) mma_sweep_m<KS, (CH + 7) / 8>((P2 + 7) / 8, fa, fb, fc);
@@ -1089,8 +1096,12 @@ __global__ void __launch_bounds__(Prox2pw<P, H, CH>::NT) k_prox2pw(DevTree t, co
           };
           auto fc = [&](int m, int n, double v0, double v1) {
             if (m < H) {
-              if (n < P * CH) X2[m * P * CH + n] = v0;
-              if (n + 1 < P * CH) X2[m * P * CH + n + 1] = v1;
+              if constexpr (EV) {
+                if (n < P * CH) *reinterpret_cast<double2*>(X2 + m * P * CH + n) = make_double2(v0, v1);
+              } else {
+                if (n < P * CH) X2[m * P * CH + n] = v0;
+                if (n + 1 < P * CH) X2[m * P * CH + n + 1] = v1;
+              }
             }
           };
           if constexpr (RB) mma_sweep_n<KS, HP / 8>((P * CH + 7) / 8, fa, fb, fc);
@@ -1109,6 +1120,11 @@ __global__ void __launch_bounds__(Prox2pw<P, H, CH>::NT) k_prox2pw(DevTree t, co
           auto fc = [&](int m, int n, double v0, double v1) {
             if (m < H) {
               const int bb = n / CH, c = n - bb * CH;   // n even, CH may be odd
+              if constexpr (EV && sizeof(TF) == 8) {   // (c, c + 1) in one row, 16-byte aligned
+                if (bb < H && c < nc)
+                  *reinterpret_cast<double2*>(o + (size_t)m * G::SLAB + bb * H + c) = make_double2(v0, v1);
+                return;
+              }
               if (bb < H && c < nc) o[(size_t)m * G::SLAB + bb * H + c] = (TF)v0;
               const int b1 = (n + 1) / CH, c1 = n + 1 - b1 * CH;
               if (b1 < H && c1 < nc) o[(size_t)m * G::SLAB + b1 * H + c1] = (TF)v1;
