@@ -1122,7 +1122,7 @@ __global__ void __launch_bounds__(Prox2pw<P, H, CH>::NT) k_prox2pw(DevTree t, co
               const int bb = n / CH, c = n - bb * CH;   // n even, CH may be odd
               if constexpr (EV && sizeof(TF) == 8) {   // (c, c + 1) in one row, 16-byte aligned
                 if (bb < H && c < nc)
-                  *reinterpret_cast<double2*>(o + (size_t)m * G::SLAB + bb * H + c) = make_double2(v0, v1);
+                  __stcs(reinterpret_cast<double2*>(o + (size_t)m * G::SLAB + bb * H + c), make_double2(v0, v1));
                 return;
               }
               if (bb < H && c < nc) o[(size_t)m * G::SLAB + bb * H + c] = (TF)v0;
