@@ -2808,8 +2808,14 @@ constexpr int P2PS_NW = 4;
 #endif
 constexpr bool P2PS_TAIL = DMK_P2PS_TAIL, P2PS_RSKIP = DMK_P2PS_RSKIP;
 constexpr int P2PS_PER_DEFAULT = 64;
+// -DDMK_P2PS_MINB=5|6 caps the registers at 96|80 (spills; profiles/r02_p2ps_minb.jsonl)
+#ifdef DMK_P2PS_MINB
+#define DMK_P2PS_BOUNDS __launch_bounds__(P2PS_NW * 32, DMK_P2PS_MINB)
+#else
+#define DMK_P2PS_BOUNDS __launch_bounds__(P2PS_NW * 32)
+#endif
 template <int K, int KER>
-__global__ void __launch_bounds__(P2PS_NW * 32) k_p2p32s(const SymTask* __restrict__ tasks,
+__global__ void DMK_P2PS_BOUNDS k_p2p32s(const SymTask* __restrict__ tasks,
                                                         const int32_t* __restrict__ ntask_p,
                                                         const float4* __restrict__ src,
                                                         const float4* __restrict__ srclo, ResPoly32 rp,
