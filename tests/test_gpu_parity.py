@@ -444,6 +444,37 @@ def test_pw64_parent_group_form(monkeypatch):
         assert direct.rel_l2(res[form], direct.laplace3d(x, q)) <= 2e-9, form
 
 
+@pytest.mark.parametrize("kind,n,ns", [("sphere", 8000, 60), ("clusters", 12000, 40)])
+def test_prox2pw64_forms(monkeypatch, kind, n, ns):
+    """eps = 1e-9 (p = 28): T_prox2pw (Eq. 3.42) by the register-blocked DMMA sweeps
+    (default) and by the independent-tile form (DMK_PROX2PW=tiles): both against the
+    oracle's outgoing expansions over the full mode cube, and against each other (the
+    same products in the same k order: the stored parity-split arrays agree to rounding)."""
+    x, q = dmk_inputs.make(kind, n, seed=23)
+    _, st = dmk_laplace3d(x, q, 1e-9, ns, return_stages=True)
+    T = st["tree"]
+    raw = {}
+    for form in ("sweep", "tiles"):
+        monkeypatch.setenv("DMK_PROX2PW", form)
+        plan, u = gpu_run(x, q, 1e-9, ns)
+        inf = plan.info()
+        nf, nf0 = inf.nf, inf.nf0
+        s0, s1 = 8 * (nf0 + 1) ** 3, 8 * (nf + 1) ** 3
+        phi = plan.stage("outgoing")
+        fout = plan.tree("fout")
+        plan.close()
+        assert phi.size == s0 + (inf.nfout - 1) * s1
+        for i in np.nonzero(T.fout)[0][:40]:
+            r = fout[i]
+            got = phi_from_parity_split(phi[:s0], nf0) if r == 0 else \
+                phi_from_parity_split(phi[s0 + (r - 1) * s1: s0 + r * s1], nf)
+            ref = st["Phi"][i]
+            assert np.max(np.abs(got - ref)) <= tol(28, "outgoing") * np.max(np.abs(ref)), form
+        raw[form] = phi
+        assert direct.rel_l2(u, direct.laplace3d(x, q)) <= 2e-9, form
+    assert np.max(np.abs(raw["sweep"] - raw["tiles"])) <= 1e-13 * np.max(np.abs(raw["tiles"]))
+
+
 @pytest.mark.parametrize("kind,n,ns", [("clusters", 12000, 40), ("uniform", 20000, 60)])
 def test_pw64_staged_deep(monkeypatch, kind, n, ns):
     """The staged parent-group translation (k_pwshift_s<H, double>: Z, Y, X window passes
