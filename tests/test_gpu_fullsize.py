@@ -29,7 +29,7 @@ def test_config2_clustered_1e7():
     depth = plan.info().nlevels - 1
     plan.close()
     assert depth >= 12
-    idx = np.random.default_rng(4).choice(len(x), 40, replace=False)
+    idx = np.random.default_rng(4).choice(len(x), 200, replace=False)
     assert direct.rel_l2(u[idx], sampled_direct(x, q, idx, "laplace")) <= 2e-6
 
 
@@ -41,7 +41,7 @@ def test_config4_yukawa_1e8_single_gpu():
     plan = dmk.dmk_plan(X, eps=1e-6, leaf_capacity=200, kernel="yukawa", lam=10.0)
     u = plan.eval(Q).cpu().numpy()
     plan.close()
-    idx = np.random.default_rng(5).choice(len(q), 16, replace=False)
+    idx = np.random.default_rng(5).choice(len(q), 32, replace=False)
     x = X.cpu().numpy()
     del X, Q
     torch.cuda.empty_cache()
