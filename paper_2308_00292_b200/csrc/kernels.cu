@@ -2808,10 +2808,8 @@ constexpr int P2PS_NW = 4;
 #endif
 constexpr bool P2PS_TAIL = DMK_P2PS_TAIL, P2PS_RSKIP = DMK_P2PS_RSKIP;
 constexpr int P2PS_PER_DEFAULT = 64;
-#ifndef DMK_P2PS_BL
-#define DMK_P2PS_BL 1
-#endif
-constexpr int P2PS_BL = DMK_P2PS_BL;
+// (blocks of consecutive tasks per warp visit instead of the round-robin deal measured
+// slower: profiles/r02_p2ps_bl.jsonl, commit 'task-block assignment experiment')
 // -DDMK_P2PS_MINB=5|6 caps the registers at 96|80 (spills; profiles/r02_p2ps_minb.jsonl)
 #ifdef DMK_P2PS_MINB
 #define DMK_P2PS_BOUNDS __launch_bounds__(P2PS_NW * 32, DMK_P2PS_MINB)
@@ -2846,14 +2844,11 @@ __global__ void DMK_P2PS_BOUNDS k_p2p32s(const SymTask* __restrict__ tasks,
     for (int q = 0; q <= K; ++q) cf[q] = rp.a[q];
   }
   // persistent: the next task's record is loaded while this one runs
-  // a warp takes blocks of P2PS_BL consecutive tasks (one leaf's entries are consecutive:
-  // its points and its neighbours' stay in L1), the blocks dealt round-robin
-  auto task_of = [&](int v) { return ((v / P2PS_BL) * nwarps + gw) * P2PS_BL + v % P2PS_BL; };
   SymTask nx{};
-  if (task_of(0) < ntask) nx = tasks[task_of(0)];
-  for (int v = 0, ti = task_of(0); ti < ntask; ++v, ti = task_of(v)) {
+  if (gw < ntask) nx = tasks[gw];
+  for (int ti = gw; ti < ntask; ti += nwarps) {
     const SymTask tk = nx;
-    if (task_of(v + 1) < ntask) nx = tasks[task_of(v + 1)];
+    if (ti + nwarps < ntask) nx = tasks[ti + nwarps];
     const bool self_task = tk.rng.w < 0;
     const int bB = tk.rng.x, nB = tk.rng.y, bS = tk.rng.z, nS = self_task ? nB : tk.rng.w;
     const float irl = tk.geo.w;
